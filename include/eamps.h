@@ -1,0 +1,149 @@
+/* eamps.h -- C ABI of the B200-native entanglement-aware MPS/MPO two-site gate update.
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, the LaTeX of arXiv:2307.16870):
+ *   a two-qubit gate on sites (i, i+1) of an MPS (E2) or of a vectorised MPO
+ *   (E4, local dimension d = 4) is applied by "contracting both tensors
+ *   neighbouring the bond" and "performing its SVD", then truncating to the
+ *   smallest rank whose truncation fidelity (E10 pure / E11 mixed) is "as close
+ *   to but not lower than" a target f_t. The target comes from the input fidelity
+ *   F_min and the number n of two-qubit gates (E14) and is updated after
+ *   every truncation by the chosen strategy (naive / nearest / global). The running
+ *   product of truncation fidelities estimates the final state fidelity (E12/E13,
+ *   PAPER.md:132-139). A bond-dimension cap may force deeper cuts, in which case the guarantee is
+ *   lost.
+ * Readings where the paper is silent or garbled are listed in DESIGN.md ("Readings").
+ *
+ * Memory model. Every device byte the library touches lives inside ONE caller-provided device
+ * slab (cfg.dev_slab, cfg.slab_bytes; e.g. torch.empty(bytes, dtype=uint8, device="cuda")). The
+ * caller keeps it alive until mps_destroy. Site tensors and Schmidt vectors are carved from it by
+ * a device-side pool allocator; per-layer workspace from its top. Host pointers passed in are
+ * read before the call returns (the caller may free them at once); outputs go to caller buffers.
+ * All work is issued on cfg.stream (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream).
+ *
+ * Layouts. Complex numbers are interleaved (re, im) float32 ("c64") unless stated. A site tensor
+ * B_i is row-major (chi_l, d, chi_r). A gate U is row-major d^2 x d^2 with
+ * U[(s*d+t), (s'*d+t')], s the physical index of `site` (the left / more significant one).
+ * For d = 4 the physical index is s = 2*sigma + sigma' (ket, bra) and the "gate" is the 16x16
+ * superoperator S (workloads.mpo_gate). The represented vector is psi = B_0 B_1 ... B_{N-1}
+ * with site 0 the most significant digit.
+ *
+ * Errors. Argument errors are returned synchronously. Device-side errors (Jacobi
+ * non-convergence, non-finite values, pool exhaustion) are sticky and reported by the next
+ * synchronising call (mps_apply_layer's end-of-layer readback, mps_fidelity_estimate,
+ * mps_amplitude, mps_to_statevector, mps_sync). After MPS_E_CUDA the handle is poisoned: only
+ * mps_destroy is legal. One handle is single-writer (not thread-safe).
+ */
+#ifndef EAMPS_H
+#define EAMPS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mps_handle* mps_t;
+typedef int32_t mps_status;
+
+enum {
+  MPS_OK = 0,
+  MPS_E_INVAL = -1,   /* bad argument: overlapping gates, non-finite gate entry, bad dims */
+  MPS_E_RANGE = -2,   /* site / bond index out of range */
+  MPS_E_NOMEM = -3,   /* slab or device pool exhausted */
+  MPS_E_CUDA = -4,    /* CUDA runtime error (handle poisoned) */
+  MPS_E_NCCL = -5,    /* reserved for the multi-GPU boundary exchange */
+  MPS_E_NOCONV = -6,  /* Jacobi SVD did not converge within max_sweeps */
+  MPS_E_NUMERIC = -7, /* non-finite singular value */
+  MPS_E_STATE = -8,   /* more truncations than n_planned, or bad query state */
+  MPS_E_TOOBIG = -9   /* query too large (statevector with d^N > 2^26) */
+};
+/* target-update strategies: PAPER.md:153 (Fig. 1 caption) and 158; FIXED = per-update target
+ * f_fixed with no ledger feedback (the BASELINE config-2 microbench). */
+enum { MPS_STRAT_NAIVE = 0, MPS_STRAT_NEAREST = 1, MPS_STRAT_GLOBAL = 2, MPS_STRAT_FIXED = 3 };
+/* truncation fidelity rule: PURE = E10 read as 1 - T_k/P; WANG = E11 read as sqrt(1 - T_k/P)
+ * (Wang fidelity E9 of rho vs the truncated rho); RATIO = 1 - T_k/P applied to an MPO. */
+enum { MPS_RULE_PURE = 0, MPS_RULE_WANG = 1, MPS_RULE_RATIO = 2 };
+
+typedef struct {
+  double f_min;        /* (0, 1]; 1 = exact mode (E14 with F_min = 1) */
+  int64_t n_planned;   /* number of two-qubit gates to be applied */
+  int32_t strategy;    /* MPS_STRAT_* */
+  int32_t rule;        /* MPS_RULE_* (MPO default: WANG) */
+  int32_t chi_cap;     /* <= 0: no cap; else bond cap */
+  int32_t max_sweeps;  /* Jacobi safety limit (<= 0: 60) -> MPS_E_NOCONV */
+  double f_fixed;      /* per-update target for MPS_STRAT_FIXED */
+  void* stream;        /* cudaStream_t; NULL = legacy default stream */
+  void* dev_slab;      /* device memory owned by the caller */
+  size_t slab_bytes;
+  int32_t rank, world; /* reserved: multi-GPU site-block sharding (world == 1 in this build) */
+  const void* nccl_unique_id;
+} mps_config;
+
+/* One row per truncation (SPEC.md:189-193 TruncationRecord). */
+typedef struct {
+  int64_t gate_index;  /* ledger index j (0-based, canonical order: layer-major, ascending site) */
+  int32_t bond;        /* bond i = the gate's left site */
+  int32_t chi_before;  /* chi_i before the gate */
+  int32_t chi_after;   /* kept rank k */
+  int32_t capped;      /* 1 if chi_cap forced a deeper cut */
+  double target_f;     /* issued target t_j */
+  double achieved_f;   /* f_j */
+  double discarded_weight; /* T_k / P */
+} mps_record;
+
+/* |0...0> (MPO: rho = |0..0><0..0|), every bond extent 1. d in {2, 4}. */
+mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* out);
+mps_status mps_destroy(mps_t);
+
+/* Single-site gate (d x d, row-major c64, host pointer), no truncation. */
+mps_status mps_apply_gate1(mps_t, int32_t site, const float* U);
+/* One two-site gate on (site, site+1): contract -> SVD -> fidelity-driven truncation ->
+ * reabsorb. U host pointer, d^2 x d^2 c64 row-major. */
+mps_status mps_apply_gate2(mps_t, int32_t site, const float* U);
+/* All gates of one layer: sites[g] (host, int32), Us (host, n_gates * d^4 c64). Sites must be
+ * disjoint pairs (|site_a - site_b| >= 2) and in [0, N-1). Truncations are ledgered in
+ * ascending-site order (reading "canonical order"). Synchronises the stream at the end
+ * of the layer (the new bond profile drives the next layer's bucketing). */
+mps_status mps_apply_layer(mps_t, int32_t n_gates, const int32_t* sites, const float* Us);
+
+/* Running estimate (E12/E13): est = exp(log_est); n_done = truncations so far; guarantee_held =
+ * no cap fired; is_lower_bound = 1 for the MPO (noisy) regime (E13). Any pointer may be NULL. */
+mps_status mps_fidelity_estimate(mps_t, double* est, double* log_est, int64_t* n_done,
+                                 int32_t* guarantee_held, int32_t* is_lower_bound);
+/* <digits|psi> (MPO: the vectorised element <<digits|rho>>); digits: N values in [0, d). */
+mps_status mps_amplitude(mps_t, const uint8_t* digits, double* re_im);
+/* Full d^N vector (interleaved complex128), site 0 most significant; d^N <= 2^26. */
+mps_status mps_to_statevector(mps_t, double* out, size_t n_doubles);
+mps_status mps_bond_dims(mps_t, int32_t* out /* N-1 */);
+/* Schmidt vector lambda of `bond` (float32, descending), *len = its length. */
+mps_status mps_schmidt_values(mps_t, int32_t bond, float* out, int32_t cap, int32_t* len);
+mps_status mps_truncation_log(mps_t, mps_record* rows, int64_t cap, int64_t* len);
+/* Sorted singular values (float64, descending, all n of them) of gate g (ascending-site order)
+ * of the most recent layer -- the parity export for the SVD step. */
+mps_status mps_last_spectrum(mps_t, int32_t g, double* out, int32_t cap, int32_t* len);
+/* Site tensors for tests / checkpoints. dims3 = {chi_l, d, chi_r}. B: c64 row-major. The
+ * pointer kind (host or device) is detected with cudaPointerGetAttributes. lam (float32, may be
+ * NULL) = Schmidt vector of the bond right of `site`. Import resets the lambda of a bond whose
+ * extent changed to ones. */
+mps_status mps_export_site(mps_t, int32_t site, float* B, int32_t* dims3);
+mps_status mps_import_site(mps_t, int32_t site, const float* B, const int32_t* dims3);
+/* Bulk import of `count` consecutive sites starting at `first`: B holds the tensors back to back
+ * (c64, row-major each; host -- pinned or pageable -- or device pointer), dims holds count x 3
+ * extents (host). One H2D copy plus one device allocation/scatter launch pair. */
+mps_status mps_import_sites(mps_t, int32_t first, int32_t count, const float* B, const int32_t* dims);
+mps_status mps_set_lambda(mps_t, int32_t bond /* -1..N-1 */, const float* lam, int32_t len);
+/* Device-side snapshot of the whole state (site store, ledger, pool) into a caller device buffer
+ * and back; *bytes_needed reports the size when buf == NULL. */
+mps_status mps_snapshot_save(mps_t, void* dev_buf, size_t buf_bytes, size_t* bytes_needed);
+mps_status mps_snapshot_load(mps_t, const void* dev_buf, size_t buf_bytes);
+/* Kernel launches issued by this handle since creation (the bench's gpu_launches). */
+mps_status mps_launch_count(mps_t, int64_t* count);
+/* Jacobi sweeps of gate g of the last layer. */
+mps_status mps_last_sweeps(mps_t, int32_t g, int32_t* sweeps);
+mps_status mps_sync(mps_t);
+const char* mps_last_error(mps_t);
+const char* mps_status_string(mps_status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

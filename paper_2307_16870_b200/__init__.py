@@ -1,0 +1,278 @@
+"""B200-native entanglement-aware MPS/MPO gate update (arXiv:2307.16870) -- Python binding.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libeamps.so (csrc/), behind the C ABI of include/eamps.h, whose functions this module exposes
+under the same names. PyTorch provides the device slab and the stream -- nothing else. There is
+no CPU fallback: importing this package on a machine without the built library raises, and
+creating a state without a CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libeamps.so")
+
+MPS_OK, MPS_E_INVAL, MPS_E_RANGE, MPS_E_NOMEM, MPS_E_CUDA, MPS_E_NCCL = 0, -1, -2, -3, -4, -5
+MPS_E_NOCONV, MPS_E_NUMERIC, MPS_E_STATE, MPS_E_TOOBIG = -6, -7, -8, -9
+STRATEGIES = {"naive": 0, "nearest": 1, "global": 2, "fixed": 3}
+RULES = {"pure": 0, "wang": 1, "ratio": 2}
+
+ABI_FUNCTIONS = [
+    "mps_create", "mps_destroy", "mps_apply_gate1", "mps_apply_gate2", "mps_apply_layer",
+    "mps_fidelity_estimate", "mps_amplitude", "mps_to_statevector", "mps_bond_dims",
+    "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
+    "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
+    "mps_launch_count", "mps_last_sweeps", "mps_sync", "mps_last_error", "mps_status_string",
+]
+
+
+class EampsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("eamps status %d: %s" % (status, msg))
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("f_min", C.c_double), ("n_planned", C.c_int64), ("strategy", C.c_int32),
+                ("rule", C.c_int32), ("chi_cap", C.c_int32), ("max_sweeps", C.c_int32),
+                ("f_fixed", C.c_double), ("stream", C.c_void_p), ("dev_slab", C.c_void_p),
+                ("slab_bytes", C.c_size_t), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_unique_id", C.c_void_p)]
+
+
+class Record(C.Structure):
+    _fields_ = [("gate_index", C.c_int64), ("bond", C.c_int32), ("chi_before", C.c_int32),
+                ("chi_after", C.c_int32), ("capped", C.c_int32), ("target_f", C.c_double),
+                ("achieved_f", C.c_double), ("discarded_weight", C.c_double)]
+
+
+_P = C.c_void_p
+_lib = None
+
+
+def lib():
+    """Load libeamps.so (fails loudly if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libeamps.so not built: run `python -m paper_2307_16870_b200._build`")
+        L = C.CDLL(LIB_PATH)
+        i32, i64, dbl = C.c_int32, C.c_int64, C.c_double
+        sig = {
+            "mps_create": [i32, i32, C.POINTER(Config), C.POINTER(_P)],
+            "mps_destroy": [_P],
+            "mps_apply_gate1": [_P, i32, _P],
+            "mps_apply_gate2": [_P, i32, _P],
+            "mps_apply_layer": [_P, i32, _P, _P],
+            "mps_fidelity_estimate": [_P, _P, _P, _P, _P, _P],
+            "mps_amplitude": [_P, _P, _P],
+            "mps_to_statevector": [_P, _P, C.c_size_t],
+            "mps_bond_dims": [_P, _P],
+            "mps_schmidt_values": [_P, i32, _P, i32, _P],
+            "mps_truncation_log": [_P, _P, i64, _P],
+            "mps_last_spectrum": [_P, i32, _P, i32, _P],
+            "mps_export_site": [_P, i32, _P, _P],
+            "mps_import_site": [_P, i32, _P, _P],
+            "mps_import_sites": [_P, i32, i32, _P, _P],
+            "mps_set_lambda": [_P, i32, _P, i32],
+            "mps_snapshot_save": [_P, _P, C.c_size_t, _P],
+            "mps_snapshot_load": [_P, _P, C.c_size_t],
+            "mps_launch_count": [_P, _P],
+            "mps_last_sweeps": [_P, i32, _P],
+            "mps_sync": [_P],
+            "mps_last_error": [_P],
+            "mps_status_string": [i32],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_char_p if name in ("mps_last_error", "mps_status_string") else C.c_int32
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _c64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.complex64)
+
+
+class MPS:
+    """One EA-MPS (d=2) or vectorised EA-MPO (d=4) on one GPU.
+
+    slab_bytes of device memory are taken from torch's caching allocator and handed to the
+    library, which owns the layout (site store, device pool, per-layer workspace).
+    """
+
+    def __init__(self, n_sites: int, d: int = 2, f_min: float = 1.0, n_planned: int = 0,
+                 strategy: str = "global", rule: str | None = None, chi_cap: int = 0,
+                 max_sweeps: int = 60, f_fixed: float = 1.0, slab_bytes: int = 1 << 30,
+                 device=None, stream=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2307_16870_b200 needs a CUDA device (no CPU fallback)")
+        L = lib()
+        if rule is None:
+            rule = "wang" if d == 4 else "pure"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.slab = torch.empty(int(slab_bytes), dtype=torch.uint8, device=self.device)
+        self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        cfg = Config(float(f_min), int(n_planned), STRATEGIES[strategy], RULES[rule], int(chi_cap),
+                     int(max_sweeps), float(f_fixed), C.c_void_p(self.stream.cuda_stream),
+                     C.c_void_p(self.slab.data_ptr()), int(slab_bytes), 0, 1, None)
+        h = C.c_void_p()
+        self._check(L.mps_create(int(n_sites), int(d), C.byref(cfg), C.byref(h)), None)
+        self._h = h
+        self.n_sites, self.d, self.rule = n_sites, d, rule
+
+    # -- plumbing ---------------------------------------------------------------------------
+    def _check(self, rc, h="self"):
+        if rc != 0:
+            hh = self._h if h == "self" else h
+            msg = lib().mps_last_error(hh).decode() if hh else lib().mps_status_string(rc).decode()
+            raise EampsError(rc, msg)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mps_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the hot path ---------------------------------------------------------------------------
+    def mps_apply_gate1(self, site: int, U):
+        U = _c64(U)
+        self._check(lib().mps_apply_gate1(self._h, int(site), _ptr(U)))
+
+    def mps_apply_gate2(self, site: int, U):
+        U = _c64(U)
+        self._check(lib().mps_apply_gate2(self._h, int(site), _ptr(U)))
+
+    def mps_apply_layer(self, sites, Us):
+        sites = np.ascontiguousarray(sites, np.int32)
+        Us = _c64(Us)
+        self._check(lib().mps_apply_layer(self._h, int(sites.size), _ptr(sites), _ptr(Us)))
+
+    def run(self, layers):
+        for sites, us in layers:
+            self.mps_apply_layer(sites, us)
+
+    # -- queries -------------------------------------------------------------------------------
+    def mps_fidelity_estimate(self):
+        est, le = C.c_double(0), C.c_double(0)
+        nd, gh, lb = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+        self._check(lib().mps_fidelity_estimate(self._h, C.byref(est), C.byref(le), C.byref(nd), C.byref(gh),
+                                                C.byref(lb)))
+        return dict(est=est.value, log_est=le.value, n_done=nd.value, guarantee_held=bool(gh.value),
+                    is_lower_bound=bool(lb.value))
+
+    def mps_amplitude(self, digits) -> complex:
+        dg = np.ascontiguousarray(digits, np.uint8)
+        out = np.zeros(2)
+        self._check(lib().mps_amplitude(self._h, _ptr(dg), _ptr(out)))
+        return complex(out[0], out[1])
+
+    def mps_to_statevector(self) -> np.ndarray:
+        n = self.d ** self.n_sites
+        out = np.zeros(n, np.complex128)
+        self._check(lib().mps_to_statevector(self._h, _ptr(out), 2 * n))
+        return out
+
+    def mps_bond_dims(self) -> np.ndarray:
+        out = np.zeros(self.n_sites - 1, np.int32)
+        self._check(lib().mps_bond_dims(self._h, _ptr(out)))
+        return out
+
+    def mps_schmidt_values(self, bond: int) -> np.ndarray:
+        ln = C.c_int32(0)
+        self._check(lib().mps_schmidt_values(self._h, int(bond), None, 0, C.byref(ln)))
+        out = np.zeros(ln.value, np.float32)
+        self._check(lib().mps_schmidt_values(self._h, int(bond), _ptr(out), ln.value, C.byref(ln)))
+        return out
+
+    def mps_truncation_log(self):
+        ln = C.c_int64(0)
+        self._check(lib().mps_truncation_log(self._h, None, 0, C.byref(ln)))
+        arr = (Record * max(1, ln.value))()
+        self._check(lib().mps_truncation_log(self._h, arr, ln.value, C.byref(ln)))
+        return [dict(gate_index=r.gate_index, bond=r.bond, chi_before=r.chi_before, chi_after=r.chi_after,
+                     capped=bool(r.capped), target_f=r.target_f, achieved_f=r.achieved_f,
+                     discarded_weight=r.discarded_weight) for r in arr[: ln.value]]
+
+    def mps_last_spectrum(self, g: int) -> np.ndarray:
+        ln = C.c_int32(0)
+        self._check(lib().mps_last_spectrum(self._h, int(g), None, 0, C.byref(ln)))
+        out = np.zeros(ln.value)
+        self._check(lib().mps_last_spectrum(self._h, int(g), _ptr(out), ln.value, C.byref(ln)))
+        return out
+
+    def mps_last_sweeps(self, g: int) -> int:
+        s = C.c_int32(0)
+        self._check(lib().mps_last_sweeps(self._h, int(g), C.byref(s)))
+        return s.value
+
+    def mps_export_site(self, site: int) -> np.ndarray:
+        dims = np.zeros(3, np.int32)
+        self._check(lib().mps_export_site(self._h, int(site), None, _ptr(dims)))
+        B = np.zeros(tuple(int(x) for x in dims), np.complex64)
+        self._check(lib().mps_export_site(self._h, int(site), _ptr(B), _ptr(dims)))
+        return B
+
+    def mps_import_site(self, site: int, B):
+        if hasattr(B, "data_ptr"):  # a torch tensor already on the device
+            dims = np.array(B.shape, np.int32)
+            self._check(lib().mps_import_site(self._h, int(site), _ptr(B), _ptr(dims)))
+            return
+        B = _c64(B)
+        dims = np.array(B.shape, np.int32)
+        self._check(lib().mps_import_site(self._h, int(site), _ptr(B), _ptr(dims)))
+
+    def mps_import_sites(self, first: int, tensors):
+        """Bulk import of consecutive sites (one H2D copy + one device scatter)."""
+        dims = np.array([t.shape for t in tensors], np.int32).reshape(-1, 3)
+        flat = np.concatenate([_c64(t).ravel() for t in tensors])
+        self._check(lib().mps_import_sites(self._h, int(first), len(tensors), _ptr(flat), _ptr(dims)))
+
+    def mps_import_sites_raw(self, first: int, count: int, flat_ptr, dims: np.ndarray):
+        dims = np.ascontiguousarray(dims, np.int32)
+        self._check(lib().mps_import_sites(self._h, int(first), int(count), flat_ptr, _ptr(dims)))
+
+    def mps_set_lambda(self, bond: int, lam):
+        lam = np.ascontiguousarray(lam, np.float32)
+        self._check(lib().mps_set_lambda(self._h, int(bond), _ptr(lam), int(lam.size)))
+
+    def mps_snapshot_save(self, buf=None):
+        import torch
+
+        need = C.c_size_t(0)
+        self._check(lib().mps_snapshot_save(self._h, None, 0, C.byref(need)))
+        if buf is None:
+            buf = torch.empty(need.value, dtype=torch.uint8, device=self.device)
+        self._check(lib().mps_snapshot_save(self._h, _ptr(buf), buf.numel(), C.byref(need)))
+        return buf
+
+    def mps_snapshot_load(self, buf):
+        self._check(lib().mps_snapshot_load(self._h, _ptr(buf), buf.numel()))
+
+    def mps_launch_count(self) -> int:
+        c = C.c_int64(0)
+        self._check(lib().mps_launch_count(self._h, C.byref(c)))
+        return c.value
+
+    def mps_sync(self):
+        self._check(lib().mps_sync(self._h))

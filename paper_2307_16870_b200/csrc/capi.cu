@@ -1,0 +1,883 @@
+// capi.cu -- the C ABI (include/eamps.h) and the host-side layer scheduler (step a0):
+// validate the brickwork layer (disjoint LNN pairs), bucket its gates by SVD regime,
+// plan waves against the slab, stage the gates with one H2D copy, launch the grouped kernels
+//   contract (all) -> SVD small (one CTA per theta) | SVD blocked (large) -> select (one warp,
+//   canonical order) -> reabsorb (all)
+// and read back the new bond profile, ledger and truncation records (one sync per wave).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "eamps.h"
+#include "eamps_internal.cuh"
+
+using namespace eamps;
+
+static_assert(sizeof(Record) == sizeof(mps_record), "record layout");
+
+struct mps_handle {
+  int N = 0, d = 0;
+  mps_config cfg{};
+  cudaStream_t s = nullptr;
+  uint8_t* slab = nullptr;
+  size_t slab_bytes = 0;
+  DevState* dst = nullptr;
+  uint64_t pool_base = 0;
+  std::vector<int32_t> chl, chr, lamlen;  // host mirror of the bond profile
+  DevState hstate{};                       // host copy after the last sync
+  std::vector<mps_record> records;
+  std::vector<GateDesc> last_desc;         // last wave
+  bool poisoned = false;
+  int sticky = 0;
+  std::string err;
+  int64_t launches = 0;
+  void* pinned[2] = {nullptr, nullptr};   // [0] general / readback, [1] layer upload staging
+  size_t pinned_bytes[2] = {0, 0};
+  // host side of a snapshot
+  struct Snap {
+    bool valid = false;
+    std::vector<int32_t> chl, chr, lamlen;
+    DevState hstate{};
+    size_t nrec = 0;
+  } snap;
+};
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+mps_status set_err(mps_t h, mps_status st, const std::string& msg) {
+  if (h) h->err = msg;
+  return st;
+}
+
+mps_status cuda_check(mps_t h, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return MPS_OK;
+  h->poisoned = true;
+  return set_err(h, MPS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                            \
+  do {                                                      \
+    mps_status _st = cuda_check(h, (call), #call);          \
+    if (_st != MPS_OK) return _st;                          \
+  } while (0)
+
+#define CKL(what)                                           \
+  do {                                                      \
+    mps_status _st = cuda_check(h, cudaGetLastError(), what); \
+    if (_st != MPS_OK) return _st;                          \
+  } while (0)
+
+// Pinned staging buffers. Growing one first drains the stream so that no in-flight async copy
+// still reads or writes the old buffer.
+void* pinned_buf(mps_t h, size_t bytes, int which = 0) {
+  if (bytes > h->pinned_bytes[which]) {
+    if (h->s) cudaStreamSynchronize(h->s); else cudaDeviceSynchronize();
+    if (h->pinned[which]) cudaFreeHost(h->pinned[which]);
+    size_t nb = std::max(bytes, h->pinned_bytes[which] * 2);
+    if (cudaHostAlloc(&h->pinned[which], nb, cudaHostAllocDefault) != cudaSuccess) {
+      h->pinned[which] = nullptr;
+      h->pinned_bytes[which] = 0;
+      return nullptr;
+    }
+    h->pinned_bytes[which] = nb;
+  }
+  return h->pinned[which];
+}
+
+mps_status sync_state(mps_t h) {
+  DevState* hs = static_cast<DevState*>(pinned_buf(h, sizeof(DevState)));
+  if (!hs) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  CK(cudaMemcpyAsync(hs, h->dst, sizeof(DevState), cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->hstate = *hs;
+  return MPS_OK;
+}
+
+mps_status check_sticky(mps_t h) {
+  if (h->poisoned) return set_err(h, MPS_E_CUDA, h->err.empty() ? "handle poisoned" : h->err);
+  if (h->sticky) return h->sticky;
+  return MPS_OK;
+}
+
+const char* status_name(mps_status s) {
+  switch (s) {
+    case MPS_OK: return "ok";
+    case MPS_E_INVAL: return "invalid argument";
+    case MPS_E_RANGE: return "index out of range";
+    case MPS_E_NOMEM: return "out of slab / pool memory";
+    case MPS_E_CUDA: return "CUDA error";
+    case MPS_E_NCCL: return "NCCL error";
+    case MPS_E_NOCONV: return "Jacobi SVD did not converge";
+    case MPS_E_NUMERIC: return "non-finite singular value";
+    case MPS_E_STATE: return "ledger/state error";
+    case MPS_E_TOOBIG: return "query too large";
+    default: return "unknown";
+  }
+}
+
+mps_status device_error(mps_t h) {
+  int e = h->hstate.led.error;
+  if (e == 0) return MPS_OK;
+  h->sticky = e;
+  if (e == MPS_E_NOMEM) h->poisoned = true;  // the site table may be half-updated
+  return set_err(h, e, std::string("device: ") + status_name(e));
+}
+
+// ---- device pool helpers for host-side operations (not on the hot path) -------------------
+mps_status dev_alloc(mps_t h, uint64_t bytes, int64_t* off, int* cls) {
+  // scratch: the last 256 bytes of the slab
+  int64_t* dout = reinterpret_cast<int64_t*>(h->slab + h->slab_bytes - kAlign);
+  launch_pool_alloc(h->slab, h->dst, bytes, dout, h->s);
+  ++h->launches;
+  CKL("pool_alloc");
+  int64_t* hb = static_cast<int64_t*>(pinned_buf(h, 16));
+  CK(cudaMemcpyAsync(hb, dout, 16, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  *off = hb[0];
+  *cls = (int)hb[1];
+  if (*off == 0) {
+    mps_status st = sync_state(h);
+    if (st != MPS_OK) return st;
+    return device_error(h) != MPS_OK ? h->sticky : set_err(h, MPS_E_NOMEM, "pool exhausted");
+  }
+  return MPS_OK;
+}
+
+mps_status read_site(mps_t h, int site, SiteEntry* e) {
+  SiteEntry* hb = static_cast<SiteEntry*>(pinned_buf(h, sizeof(SiteEntry)));
+  CK(cudaMemcpyAsync(hb, h->slab + h->hstate.sites_off + sizeof(SiteEntry) * site, sizeof(SiteEntry),
+                     cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  *e = *hb;
+  return MPS_OK;
+}
+
+mps_status read_bond(mps_t h, int bond, BondEntry* e) {
+  BondEntry* hb = static_cast<BondEntry*>(pinned_buf(h, sizeof(BondEntry)));
+  CK(cudaMemcpyAsync(hb, h->slab + h->hstate.bonds_off + sizeof(BondEntry) * (bond + 1), sizeof(BondEntry),
+                     cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  *e = *hb;
+  return MPS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// write `len` floats (lambda) for bond b into a fresh pool block
+mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
+  int64_t off;
+  int cls;
+  mps_status st = dev_alloc(h, (uint64_t)len * 4, &off, &cls);
+  if (st != MPS_OK) return st;
+  BondEntry old;
+  st = read_bond(h, bond, &old);
+  if (st != MPS_OK) return st;
+  float* hb = static_cast<float*>(pinned_buf(h, (size_t)len * 4 + sizeof(BondEntry) + 64));
+  for (int x = 0; x < len; ++x) hb[x] = ones ? 1.f : lam[x];
+  BondEntry* ne = reinterpret_cast<BondEntry*>(reinterpret_cast<uint8_t*>(hb) + align_up((size_t)len * 4, 16));
+  ne->off = off;
+  ne->len = len;
+  ne->cls = cls;
+  CK(cudaMemcpyAsync(h->slab + off, hb, (size_t)len * 4, cudaMemcpyHostToDevice, h->s));
+  CK(cudaMemcpyAsync(h->slab + h->hstate.bonds_off + sizeof(BondEntry) * (bond + 1), ne, sizeof(BondEntry),
+                     cudaMemcpyHostToDevice, h->s));
+  if (old.off) {
+    launch_pool_free(h->slab, h->dst, old.off, old.cls, h->s);
+    ++h->launches;
+  }
+  CK(cudaStreamSynchronize(h->s));
+  h->lamlen[bond + 1] = len;
+  return MPS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mps_status_string(mps_status s) { return status_name(s); }
+
+const char* mps_last_error(mps_t h) { return h ? h->err.c_str() : "null handle"; }
+
+mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* out) {
+  if (!out || !cfg) return MPS_E_INVAL;
+  *out = nullptr;
+  if (n_sites < 2 || (d != 2 && d != 4)) return MPS_E_INVAL;
+  if (!(cfg->f_min > 0.0 && cfg->f_min <= 1.0)) return MPS_E_INVAL;
+  if (cfg->strategy < 0 || cfg->strategy > 3 || cfg->rule < 0 || cfg->rule > 2) return MPS_E_INVAL;
+  if (cfg->strategy == MPS_STRAT_FIXED && !(cfg->f_fixed > 0.0 && cfg->f_fixed <= 1.0)) return MPS_E_INVAL;
+  if (!cfg->dev_slab || cfg->slab_bytes < (1u << 20)) return MPS_E_INVAL;
+  if (cfg->world > 1) return MPS_E_INVAL;  // this build shards above the ABI (independent handles)
+  mps_t h = new mps_handle();
+  h->N = n_sites;
+  h->d = d;
+  h->cfg = *cfg;
+  if (h->cfg.max_sweeps <= 0) h->cfg.max_sweeps = 60;
+  h->s = static_cast<cudaStream_t>(cfg->stream);
+  h->slab = static_cast<uint8_t*>(cfg->dev_slab);
+  h->slab_bytes = cfg->slab_bytes;
+  h->dst = reinterpret_cast<DevState*>(h->slab);
+  h->chl.assign(n_sites, 1);
+  h->chr.assign(n_sites, 1);
+  h->lamlen.assign(n_sites + 1, 1);
+
+  // slab layout: DevState | SiteEntry[N] | BondEntry[N+1] | pending frees | pool ...
+  const size_t sites_off = align_up(sizeof(DevState));
+  const size_t bonds_off = align_up(sites_off + sizeof(SiteEntry) * n_sites);
+  const int64_t pend_cap = 3 * (int64_t)n_sites + 64;
+  const size_t pend_off = align_up(bonds_off + sizeof(BondEntry) * (n_sites + 1));
+  const size_t pool_base = align_up(pend_off + 16 * pend_cap);
+  const size_t init_end = pool_base + kAlign * (2 * (size_t)n_sites + 1);
+  if (init_end + (1u << 16) > h->slab_bytes) {
+    delete h;
+    return MPS_E_NOMEM;
+  }
+  h->pool_base = pool_base;
+  std::vector<uint8_t> img(init_end, 0);
+  DevState& S = *reinterpret_cast<DevState*>(img.data());
+  S.led.logE = 0.0;
+  S.led.j = 0;
+  S.led.guarantee = 1;
+  S.led.error = 0;
+  S.led.log_fmin = std::log(cfg->f_min);
+  S.led.log_ffixed = cfg->strategy == MPS_STRAT_FIXED ? std::log(cfg->f_fixed) : 0.0;
+  S.led.n_planned = cfg->n_planned;
+  S.led.strategy = cfg->strategy;
+  S.led.rule = cfg->rule;
+  S.led.chi_cap = cfg->chi_cap;
+  S.led.d = d;
+  S.pool.bump = init_end;
+  S.pool.ceiling = h->slab_bytes - kAlign;
+  S.pool.npending = 0;
+  S.pool.pending_cap = pend_cap;
+  S.pool.pending_off = (int64_t)pend_off;
+  S.n_sites = n_sites;
+  S.d = d;
+  S.sites_off = (int64_t)sites_off;
+  S.bonds_off = (int64_t)bonds_off;
+  SiteEntry* se = reinterpret_cast<SiteEntry*>(img.data() + sites_off);
+  BondEntry* be = reinterpret_cast<BondEntry*>(img.data() + bonds_off);
+  // |0...0>: B_i[0,0,0] = 1 (MPO: s = 2 sigma + sigma' = 0), lambda = [1]
+  for (int i = 0; i < n_sites; ++i) {
+    size_t off = pool_base + kAlign * i;
+    se[i].off = (int64_t)off;
+    se[i].chl = se[i].chr = 1;
+    se[i].cls = kMinClass;
+    reinterpret_cast<float*>(img.data() + off)[0] = 1.f;
+  }
+  for (int b = 0; b <= n_sites; ++b) {
+    size_t off = pool_base + kAlign * (n_sites + b);
+    be[b].off = (int64_t)off;
+    be[b].len = 1;
+    be[b].cls = kMinClass;
+    reinterpret_cast<float*>(img.data() + off)[0] = 1.f;
+  }
+  void* pb = pinned_buf(h, img.size());
+  if (!pb) {
+    delete h;
+    return MPS_E_NOMEM;
+  }
+  std::memcpy(pb, img.data(), img.size());
+  if (cudaMemcpyAsync(h->slab, pb, img.size(), cudaMemcpyHostToDevice, h->s) != cudaSuccess ||
+      cudaStreamSynchronize(h->s) != cudaSuccess) {
+    cudaFreeHost(h->pinned[0]);
+    delete h;
+    return MPS_E_CUDA;
+  }
+  h->hstate = S;
+  *out = h;
+  return MPS_OK;
+}
+
+mps_status mps_destroy(mps_t h) {
+  if (!h) return MPS_E_INVAL;
+  if (h->s) cudaStreamSynchronize(h->s);
+  for (int w = 0; w < 2; ++w)
+    if (h->pinned[w]) cudaFreeHost(h->pinned[w]);
+  delete h;
+  return MPS_OK;
+}
+
+mps_status mps_sync(mps_t h) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  return device_error(h);
+}
+
+mps_status mps_launch_count(mps_t h, int64_t* c) {
+  if (!h || !c) return MPS_E_INVAL;
+  *c = h->launches;
+  return MPS_OK;
+}
+
+mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
+  if (!h || !U) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
+  const int dd = h->d * h->d;
+  for (int x = 0; x < 2 * dd; ++x)
+    if (!std::isfinite(U[x])) return set_err(h, MPS_E_INVAL, "non-finite gate entry");
+  float* hb = static_cast<float*>(pinned_buf(h, 8 * dd));
+  std::memcpy(hb, U, 8 * dd);
+  float2* du = reinterpret_cast<float2*>(h->slab + h->slab_bytes - 2 * kAlign);  // 2 KB scratch below the top
+  CK(cudaMemcpyAsync(du, hb, 8 * dd, cudaMemcpyHostToDevice, h->s));
+  launch_gate1(h->slab, h->dst, site, h->d, du, h->s);
+  ++h->launches;
+  CKL("gate1");
+  CK(cudaStreamSynchronize(h->s));
+  return MPS_OK;
+}
+
+mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float* Us) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (G < 0 || (G > 0 && (!sites || !Us))) return set_err(h, MPS_E_INVAL, "bad arguments");
+  if (G == 0) return MPS_OK;
+  const int d = h->d, d4 = d * d * d * d;
+  // ---- a0: validate (in range, disjoint pairs), canonical order = ascending site
+  std::vector<std::pair<int, int>> ord(G);
+  for (int g = 0; g < G; ++g) {
+    if (sites[g] < 0 || sites[g] >= h->N - 1) return set_err(h, MPS_E_RANGE, "gate site out of range");
+    ord[g] = {sites[g], g};
+  }
+  std::sort(ord.begin(), ord.end());
+  for (int g = 1; g < G; ++g)
+    if (ord[g].first < ord[g - 1].first + 2) return set_err(h, MPS_E_INVAL, "overlapping gates in a layer");
+  for (int64_t x = 0; x < (int64_t)G * d4 * 2; ++x)
+    if (!std::isfinite(Us[x])) return set_err(h, MPS_E_INVAL, "non-finite gate entry");
+  if (h->cfg.strategy != MPS_STRAT_FIXED && h->hstate.led.j + G > h->cfg.n_planned)
+    return set_err(h, MPS_E_STATE, "more truncations than n_planned");
+  for (int g = 0; g < G; ++g) {
+    int i = ord[g].first;
+    if (h->chr[i] != h->chl[i + 1] || h->lamlen[i] != h->chl[i])
+      return set_err(h, MPS_E_INVAL, "inconsistent bond extents at the gate");
+  }
+
+  // ---- per-gate shapes, regimes and workspace sizes
+  struct Plan {
+    GateDesc gd;
+    size_t ws, reserve;
+    int ctiles, rtiles;
+  };
+  std::vector<Plan> plan(G);
+  const int TA = 64 / d;
+  for (int g = 0; g < G; ++g) {
+    Plan& p = plan[g];
+    GateDesc& gd = p.gd;
+    std::memset(&gd, 0, sizeof(gd));
+    int i = ord[g].first;
+    gd.site = i;
+    gd.l = h->chl[i];
+    gd.mid = h->chr[i];
+    gd.r = h->chr[i + 1];
+    gd.m = gd.l * d;
+    gd.n = d * gd.r;
+    gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : 1;
+    gd.n_pad = gd.regime == 0 ? gd.n : (int)align_up(gd.n, 32);
+    gd.u_index = ord[g].second;
+    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+    p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
+           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4);
+    int kmax = std::min(gd.m, gd.n);
+    if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);
+    p.reserve = ((size_t)1 << size_class((uint64_t)gd.l * d * kmax * 8)) +
+                ((size_t)1 << size_class((uint64_t)kmax * d * gd.r * 8)) + ((size_t)1 << size_class((uint64_t)kmax * 4)) +
+                3 * kAlign;
+    p.ctiles = ((gd.l + TA - 1) / TA) * ((gd.r + TA - 1) / TA);
+    const int km = std::min(gd.m, gd.n);
+    p.rtiles = ((gd.m + 63) / 64) * ((km + 63) / 64) + km;
+  }
+
+  // ---- waves (gates in canonical order; each wave's workspace + worst-case new blocks fit)
+  const size_t top = h->slab_bytes - 4 * kAlign;  // the top 1 KB is scratch for small host ops
+  int g0 = 0;
+  h->last_desc.clear();
+  while (g0 < G) {
+    const uint64_t bump = h->hstate.pool.bump;
+    size_t fixed = 0, ws = 0, reserve = 0;
+    int g1 = g0;
+    while (g1 < G) {
+      const int cnt = g1 - g0 + 1;
+      size_t fx = align_up(sizeof(GateDesc) * cnt) + 2 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
+                  align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
+      size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
+      if (bump + r2 + fx + w2 + kAlign > top) break;
+      fixed = fx;
+      ws = w2;
+      reserve = r2;
+      ++g1;
+    }
+    if (g1 == g0) return set_err(h, MPS_E_NOMEM, "one gate's workspace does not fit the slab");
+    const int Gw = g1 - g0;
+    // device addresses of the wave's staging block (just below `top`)
+    const size_t base = align_up(top - fixed - ws - kAlign) - 0;
+    size_t cur = base;
+    auto take = [&](size_t bytes) {
+      size_t o = cur;
+      cur = align_up(cur + bytes);
+      return o;
+    };
+    const size_t o_desc = take(sizeof(GateDesc) * Gw);
+    const size_t o_cpre = take(4 * (Gw + 1));
+    const size_t o_rpre = take(4 * (Gw + 1));
+    const size_t o_small = take(4 * Gw);
+    const size_t o_large = take(4 * Gw);
+    const size_t o_us = take((size_t)Gw * d4 * 8);
+    const size_t o_rec = take(sizeof(Record) * Gw);
+    const size_t o_scr = take(32 * (size_t)Gw + 64);
+    const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
+    std::vector<int32_t> cpre(Gw + 1, 0), rpre(Gw + 1, 0), small, large;
+    std::vector<GateDesc> hd(Gw);
+    size_t smem_small = 0;
+    for (int x = 0; x < Gw; ++x) {
+      Plan& p = plan[g0 + x];
+      GateDesc gd = p.gd;
+      gd.u_index = x;
+      const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+      gd.ws_theta = (int64_t)take(mnp);
+      gd.ws_thetap = (int64_t)take(mn);
+      gd.ws_V = (int64_t)take((size_t)gd.n_pad * gd.n_pad * 8);
+      gd.ws_sig2 = (int64_t)take((size_t)gd.n_pad * 8);
+      gd.ws_T = (int64_t)take((size_t)(gd.n_pad + 1) * 8);
+      gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
+      hd[x] = gd;
+      cpre[x + 1] = cpre[x] + p.ctiles;
+      rpre[x + 1] = rpre[x] + p.rtiles;
+      if (gd.regime == 0) {
+        small.push_back(x);
+        smem_small = std::max(smem_small, svd_small_smem(gd.m, gd.n));
+      } else {
+        large.push_back(x);
+      }
+    }
+    if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
+    // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
+    const size_t tail = align_up(staged_bytes, 64);  // 3 small pinned slots after the staged block
+    uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));
+    if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+    std::memset(hb, 0, staged_bytes);
+    std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
+    std::memcpy(hb + (o_cpre - base), cpre.data(), 4 * (Gw + 1));
+    std::memcpy(hb + (o_rpre - base), rpre.data(), 4 * (Gw + 1));
+    if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
+    if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
+    for (int x = 0; x < Gw; ++x)
+      std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, Us + (size_t)ord[g0 + x].second * d4 * 2, (size_t)d4 * 8);
+    CK(cudaMemcpyAsync(h->slab + base, hb, staged_bytes, cudaMemcpyHostToDevice, h->s));
+    // the pool may not grow into the workspace
+    uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + tail);
+    *hceil = base;
+    CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
+
+    GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + o_desc);
+    const int32_t* d_cpre = reinterpret_cast<const int32_t*>(h->slab + o_cpre);
+    const int32_t* d_rpre = reinterpret_cast<const int32_t*>(h->slab + o_rpre);
+    const int32_t* d_small = reinterpret_cast<const int32_t*>(h->slab + o_small);
+    const int32_t* d_large = reinterpret_cast<const int32_t*>(h->slab + o_large);
+    const float2* d_us = reinterpret_cast<const float2*>(h->slab + o_us);
+    Record* d_rec = reinterpret_cast<Record*>(h->slab + o_rec);
+
+    // a1 contract (all gates of the wave)
+    launch_contract(d_desc, d_cpre, Gw, cpre[Gw], d, h->slab, h->dst, d_us, h->s);
+    ++h->launches;
+    CKL("contract");
+    // a2 + a3 SVD, small regime: one CTA per theta
+    if (!small.empty()) {
+      launch_svd_small(d_desc, d_small, (int)small.size(), smem_small, h->cfg.max_sweeps, h->slab, h->dst, h->s);
+      ++h->launches;
+      CKL("svd_small");
+    }
+    // a2 + a3 SVD, large regime: blocked Jacobi
+    if (!large.empty()) {
+      int err = 0;
+      int32_t* hflag = reinterpret_cast<int32_t*>(hb + tail + 64);
+      h->launches += run_svd_blocked(d_desc, hd.data(), d_large, large.data(), (int)large.size(), h->cfg.max_sweeps,
+                                     h->slab, h->dst, reinterpret_cast<int32_t*>(h->slab + o_scr), hflag, h->s, &err);
+      CKL("svd_blocked");
+      if (err) {
+        // record on device so that it is sticky like the small-path error
+        int32_t* he = reinterpret_cast<int32_t*>(hb + tail + 128);
+        *he = err;
+        CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
+      }
+    }
+    // a4 select + ledger + pool
+    launch_select(d_desc, Gw, h->slab, h->dst, d_rec, h->s);
+    ++h->launches;
+    CKL("select");
+    // a5 reabsorb
+    launch_reabsorb(d_desc, d_rpre, Gw, rpre[Gw], d, h->slab, h->dst, h->s);
+    ++h->launches;
+    CKL("reabsorb");
+    // read back: descriptors (k, sweeps), records, device state
+    const size_t back = sizeof(GateDesc) * Gw + sizeof(Record) * Gw + sizeof(DevState);
+    uint8_t* rb = static_cast<uint8_t*>(pinned_buf(h, back + 64));
+    CK(cudaMemcpyAsync(rb, d_desc, sizeof(GateDesc) * Gw, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw, d_rec, sizeof(Record) * Gw, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, h->dst, sizeof(DevState),
+                       cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    std::memcpy(hd.data(), rb, sizeof(GateDesc) * Gw);
+    const Record* rr = reinterpret_cast<const Record*>(rb + sizeof(GateDesc) * Gw);
+    std::memcpy(&h->hstate, rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, sizeof(DevState));
+    mps_status de = device_error(h);
+    for (int x = 0; x < Gw; ++x) {
+      const GateDesc& gd = hd[x];
+      if (gd.k <= 0) continue;
+      h->chr[gd.site] = gd.k;
+      h->chl[gd.site + 1] = gd.k;
+      h->lamlen[gd.site + 1] = gd.k;
+      mps_record rec;
+      std::memcpy(&rec, &rr[x], sizeof(rec));
+      h->records.push_back(rec);
+    }
+    h->last_desc = hd;
+    if (de != MPS_OK) return de;
+    g0 = g1;
+  }
+  return MPS_OK;
+}
+
+mps_status mps_apply_gate2(mps_t h, int32_t site, const float* U) { return mps_apply_layer(h, 1, &site, U); }
+
+mps_status mps_fidelity_estimate(mps_t h, double* est, double* log_est, int64_t* n_done, int32_t* guarantee_held,
+                                 int32_t* is_lower_bound) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  st = device_error(h);
+  if (st != MPS_OK) return st;
+  if (est) *est = std::exp(h->hstate.led.logE);
+  if (log_est) *log_est = h->hstate.led.logE;
+  if (n_done) *n_done = h->hstate.led.j;
+  if (guarantee_held) *guarantee_held = h->hstate.led.guarantee;
+  if (is_lower_bound) *is_lower_bound = h->d == 4 ? 1 : 0;
+  return MPS_OK;
+}
+
+mps_status mps_bond_dims(mps_t h, int32_t* out) {
+  if (!h || !out) return MPS_E_INVAL;
+  for (int i = 0; i < h->N - 1; ++i) out[i] = h->chr[i];
+  return MPS_OK;
+}
+
+mps_status mps_schmidt_values(mps_t h, int32_t bond, float* out, int32_t cap, int32_t* len) {
+  if (!h || !len) return MPS_E_INVAL;
+  if (bond < -1 || bond > h->N - 1) return set_err(h, MPS_E_RANGE, "bond out of range");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  BondEntry e;
+  st = read_bond(h, bond, &e);
+  if (st != MPS_OK) return st;
+  *len = e.len;
+  if (out && cap > 0) {
+    int nc = std::min(cap, e.len);
+    CK(cudaMemcpyAsync(out, h->slab + e.off, 4 * (size_t)nc, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+  }
+  return MPS_OK;
+}
+
+mps_status mps_truncation_log(mps_t h, mps_record* rows, int64_t cap, int64_t* len) {
+  if (!h || !len) return MPS_E_INVAL;
+  *len = (int64_t)h->records.size();
+  if (rows)
+    for (int64_t r = 0; r < *len && r < cap; ++r) rows[r] = h->records[r];
+  return MPS_OK;
+}
+
+mps_status mps_last_spectrum(mps_t h, int32_t g, double* out, int32_t cap, int32_t* len) {
+  if (!h || !len) return MPS_E_INVAL;
+  if (g < 0 || g >= (int)h->last_desc.size()) return set_err(h, MPS_E_RANGE, "gate index out of range");
+  const GateDesc& gd = h->last_desc[g];
+  *len = gd.n;
+  if (out && cap > 0) {
+    CK(cudaMemcpyAsync(out, h->slab + gd.ws_sig2, 8 * (size_t)std::min(cap, gd.n), cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    for (int j = 0; j < std::min(cap, gd.n); ++j) out[j] = std::sqrt(std::max(out[j], 0.0));
+  }
+  return MPS_OK;
+}
+
+mps_status mps_last_sweeps(mps_t h, int32_t g, int32_t* sweeps) {
+  if (!h || !sweeps) return MPS_E_INVAL;
+  if (g < 0 || g >= (int)h->last_desc.size()) return MPS_E_RANGE;
+  *sweeps = h->last_desc[g].sweeps;
+  return MPS_OK;
+}
+
+mps_status mps_export_site(mps_t h, int32_t site, float* B, int32_t* dims3) {
+  if (!h || !dims3) return MPS_E_INVAL;
+  if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  SiteEntry e;
+  st = read_site(h, site, &e);
+  if (st != MPS_OK) return st;
+  dims3[0] = e.chl;
+  dims3[1] = h->d;
+  dims3[2] = e.chr;
+  if (B) {
+    CK(cudaMemcpyAsync(B, h->slab + e.off, (size_t)e.chl * h->d * e.chr * 8, cudaMemcpyDefault, h->s));
+    CK(cudaStreamSynchronize(h->s));
+  }
+  return MPS_OK;
+}
+
+mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t* dims3) {
+  if (!h || !B || !dims3) return MPS_E_INVAL;
+  if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
+  if (dims3[1] != h->d || dims3[0] < 1 || dims3[2] < 1) return set_err(h, MPS_E_INVAL, "bad dims");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  const size_t bytes = (size_t)dims3[0] * h->d * dims3[2] * 8;
+  int64_t off;
+  int cls;
+  st = dev_alloc(h, bytes, &off, &cls);
+  if (st != MPS_OK) return st;
+  SiteEntry old;
+  st = read_site(h, site, &old);
+  if (st != MPS_OK) return st;
+  CK(cudaMemcpyAsync(h->slab + off, B, bytes, is_device_ptr(B) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     h->s));
+  SiteEntry* ne = static_cast<SiteEntry*>(pinned_buf(h, sizeof(SiteEntry)));
+  ne->off = off;
+  ne->chl = dims3[0];
+  ne->chr = dims3[2];
+  ne->cls = cls;
+  ne->pad = 0;
+  CK(cudaMemcpyAsync(h->slab + h->hstate.sites_off + sizeof(SiteEntry) * site, ne, sizeof(SiteEntry),
+                     cudaMemcpyHostToDevice, h->s));
+  if (old.off) {
+    launch_pool_free(h->slab, h->dst, old.off, old.cls, h->s);
+    ++h->launches;
+  }
+  CK(cudaStreamSynchronize(h->s));
+  h->chl[site] = dims3[0];
+  h->chr[site] = dims3[2];
+  if (h->lamlen[site] != dims3[0]) {
+    st = put_lambda(h, site - 1, nullptr, dims3[0], true);
+    if (st != MPS_OK) return st;
+  }
+  if (h->lamlen[site + 1] != dims3[2]) {
+    st = put_lambda(h, site, nullptr, dims3[2], true);
+    if (st != MPS_OK) return st;
+  }
+  return sync_state(h);
+}
+
+mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* B, const int32_t* dims) {
+  if (!h || !B || !dims || count < 1) return MPS_E_INVAL;
+  if (first < 0 || first + count > h->N) return set_err(h, MPS_E_RANGE, "sites out of range");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  std::vector<ImportEntry> ent(count);
+  std::vector<int32_t> lamlen = h->lamlen;
+  int64_t elems = 0;
+  for (int x = 0; x < count; ++x) {
+    const int32_t* dm = dims + 3 * x;
+    if (dm[1] != h->d || dm[0] < 1 || dm[2] < 1) return set_err(h, MPS_E_INVAL, "bad dims");
+    ImportEntry& e = ent[x];
+    std::memset(&e, 0, sizeof(e));
+    e.site = first + x;
+    e.chl = dm[0];
+    e.chr = dm[2];
+    e.src_elem = elems;
+    elems += (int64_t)dm[0] * h->d * dm[2];
+    if (lamlen[e.site] != e.chl) { e.resetL = e.chl; lamlen[e.site] = e.chl; }
+    if (lamlen[e.site + 1] != e.chr) { e.resetR = e.chr; lamlen[e.site + 1] = e.chr; }
+  }
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const bool dev = is_device_ptr(B);
+  const size_t ent_bytes = align_up(sizeof(ImportEntry) * count);
+  const size_t data_bytes = dev ? 0 : align_up((size_t)elems * 8);
+  const size_t top = h->slab_bytes - 4 * kAlign;
+  // worst case the new blocks take fresh pool memory: keep the staging area above that
+  size_t reserve = 0;
+  for (const ImportEntry& e : ent)
+    reserve += ((size_t)1 << size_class((uint64_t)e.chl * h->d * e.chr * 8)) + 2 * kAlign +
+               (e.resetL ? ((size_t)1 << size_class((uint64_t)e.resetL * 4)) : 0) +
+               (e.resetR ? ((size_t)1 << size_class((uint64_t)e.resetR * 4)) : 0);
+  if (h->hstate.pool.bump + reserve + ent_bytes + data_bytes + kAlign > top)
+    return set_err(h, MPS_E_NOMEM, "no room to stage the import");
+  const size_t base = align_up(top - ent_bytes - data_bytes - kAlign);
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, ent_bytes + 64, 1));
+  std::memcpy(hb, ent.data(), sizeof(ImportEntry) * count);
+  uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + ent_bytes);
+  *hceil = base;
+  CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
+  CK(cudaMemcpyAsync(h->slab + base, hb, sizeof(ImportEntry) * count, cudaMemcpyHostToDevice, h->s));
+  const float2* src = reinterpret_cast<const float2*>(B);
+  if (!dev) {
+    CK(cudaMemcpyAsync(h->slab + base + ent_bytes, B, (size_t)elems * 8, cudaMemcpyHostToDevice, h->s));
+    src = reinterpret_cast<const float2*>(h->slab + base + ent_bytes);
+  }
+  launch_import(h->slab, h->dst, reinterpret_cast<ImportEntry*>(h->slab + base), count, src, h->d, h->s);
+  h->launches += 2;
+  CKL("import");
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  st = device_error(h);
+  if (st != MPS_OK) return st;
+  for (const ImportEntry& e : ent) {
+    h->chl[e.site] = e.chl;
+    h->chr[e.site] = e.chr;
+  }
+  h->lamlen = lamlen;
+  return MPS_OK;
+}
+
+mps_status mps_set_lambda(mps_t h, int32_t bond, const float* lam, int32_t len) {
+  if (!h || !lam || len < 1) return MPS_E_INVAL;
+  if (bond < -1 || bond > h->N - 1) return set_err(h, MPS_E_RANGE, "bond out of range");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  std::vector<float> tmp(len);
+  if (is_device_ptr(lam)) {
+    CK(cudaMemcpy(tmp.data(), lam, 4 * (size_t)len, cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(tmp.data(), lam, 4 * (size_t)len);
+  }
+  st = put_lambda(h, bond, tmp.data(), len, false);
+  if (st != MPS_OK) return st;
+  return sync_state(h);
+}
+
+mps_status mps_amplitude(mps_t h, const uint8_t* digits, double* re_im) {
+  if (!h || !digits || !re_im) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (h->chl[0] != 1 || h->chr[h->N - 1] != 1) return set_err(h, MPS_E_STATE, "open boundary legs");
+  int maxchi = 1;
+  for (int i = 0; i < h->N; ++i) {
+    if (digits[i] >= h->d) return set_err(h, MPS_E_INVAL, "digit out of range");
+    maxchi = std::max(maxchi, h->chr[i]);
+  }
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const size_t need = 2 * align_up((size_t)maxchi * 16) + kAlign;
+  if (h->hstate.pool.bump + need + 4 * kAlign > h->slab_bytes) return set_err(h, MPS_E_NOMEM, "no room for query");
+  const size_t base = align_up(h->slab_bytes - 4 * kAlign - need);
+  double2* v0 = reinterpret_cast<double2*>(h->slab + base);
+  double2* v1 = reinterpret_cast<double2*>(h->slab + base + align_up((size_t)maxchi * 16));
+  double2* one = static_cast<double2*>(pinned_buf(h, 16));
+  *one = make_double2(1.0, 0.0);
+  CK(cudaMemcpyAsync(v0, one, 16, cudaMemcpyHostToDevice, h->s));
+  for (int i = 0; i < h->N; ++i) {
+    launch_amplitude_step(h->slab, h->dst, i, digits[i], v0, v1, h->s);
+    ++h->launches;
+    std::swap(v0, v1);
+  }
+  CKL("amplitude");
+  CK(cudaMemcpyAsync(one, v0, 16, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  re_im[0] = one->x;
+  re_im[1] = one->y;
+  return device_error(h);
+}
+
+mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
+  if (!h || !out) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (h->chl[0] != 1 || h->chr[h->N - 1] != 1) return set_err(h, MPS_E_STATE, "open boundary legs");
+  double total = std::pow((double)h->d, h->N);
+  if (total > (double)(1 << 26)) return set_err(h, MPS_E_TOOBIG, "d^N > 2^26");
+  const int64_t tot = (int64_t)total;
+  if (n_doubles < 2 * (size_t)tot) return set_err(h, MPS_E_RANGE, "output buffer too small");
+  // largest intermediate: rows * chi <= d^N (chi_i <= d^(N-i-1)); allow slack
+  size_t maxel = 1;
+  {
+    double rows = 1;
+    for (int i = 0; i < h->N; ++i) {
+      rows *= h->d;
+      maxel = std::max(maxel, (size_t)(rows * h->chr[i]));
+    }
+  }
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const size_t need = 2 * align_up(maxel * 16) + kAlign;
+  if (h->hstate.pool.bump + need + 4 * kAlign > h->slab_bytes) return set_err(h, MPS_E_NOMEM, "no room for query");
+  const size_t base = align_up(h->slab_bytes - 4 * kAlign - need);
+  double2* S0 = reinterpret_cast<double2*>(h->slab + base);
+  double2* S1 = reinterpret_cast<double2*>(h->slab + base + align_up(maxel * 16));
+  double2* one = static_cast<double2*>(pinned_buf(h, 16));
+  *one = make_double2(1.0, 0.0);
+  CK(cudaMemcpyAsync(S0, one, 16, cudaMemcpyHostToDevice, h->s));
+  int64_t rows = 1;
+  int cols = 1;
+  for (int i = 0; i < h->N; ++i) {
+    launch_statevector_step(h->slab, h->dst, i, rows, cols, S0, S1, h->s);
+    ++h->launches;
+    rows *= h->d;
+    cols = h->chr[i];
+    std::swap(S0, S1);
+  }
+  CKL("statevector");
+  CK(cudaMemcpyAsync(out, S0, (size_t)tot * 16, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  return device_error(h);
+}
+
+mps_status mps_snapshot_save(mps_t h, void* buf, size_t buf_bytes, size_t* bytes_needed) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const size_t need = h->hstate.pool.bump;
+  if (bytes_needed) *bytes_needed = need;
+  if (!buf) return MPS_OK;
+  if (buf_bytes < need) return set_err(h, MPS_E_RANGE, "snapshot buffer too small");
+  CK(cudaMemcpyAsync(buf, h->slab, need, cudaMemcpyDeviceToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->snap.valid = true;
+  h->snap.chl = h->chl;
+  h->snap.chr = h->chr;
+  h->snap.lamlen = h->lamlen;
+  h->snap.hstate = h->hstate;
+  h->snap.nrec = h->records.size();
+  return MPS_OK;
+}
+
+mps_status mps_snapshot_load(mps_t h, const void* buf, size_t buf_bytes) {
+  if (!h || !buf) return MPS_E_INVAL;
+  if (!h->snap.valid) return set_err(h, MPS_E_STATE, "no snapshot saved by this handle");
+  const size_t need = h->snap.hstate.pool.bump;
+  if (buf_bytes < need) return set_err(h, MPS_E_RANGE, "snapshot buffer too small");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  CK(cudaMemcpyAsync(h->slab, buf, need, cudaMemcpyDeviceToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->chl = h->snap.chl;
+  h->chr = h->snap.chr;
+  h->lamlen = h->snap.lamlen;
+  h->hstate = h->snap.hstate;
+  h->records.resize(h->snap.nrec);
+  h->last_desc.clear();
+  return MPS_OK;
+}
+
+}  // extern "C"

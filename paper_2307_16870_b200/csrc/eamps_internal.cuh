@@ -1,0 +1,111 @@
+// eamps_internal.cuh -- device-side data structures and kernel entry points of the B200 path.
+//
+// Product code. It shares nothing with oracle/ (no headers, constants or helpers).
+// Layouts:
+//   * site tensor B_i: row-major (chi_l, d, chi_r) complex64 in a pool block of the slab
+//   * Schmidt vector lambda_b: float32 in a pool block
+//   * per-gate workspace (top of the slab): theta, Theta' column-major (m x n, ld m),
+//     V column-major (n_pad x n_pad), sigma^2 (f64, n_pad), tails T (f64, n_pad+1), pi (i32)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eamps {
+
+constexpr int kMaxClasses = 48;     // pool size classes 2^0 .. 2^47 bytes (blocks >= 256 B)
+constexpr int kMinClass = 8;
+
+struct SiteEntry {                  // B_i
+  int64_t off;                      // byte offset in the slab (0 = none)
+  int32_t chl, chr;
+  int32_t cls, pad;
+};
+struct BondEntry {                  // lambda of bond b, stored at index b+1 (b = -1 .. N-1)
+  int64_t off;
+  int32_t len, cls;
+};
+
+struct DevLedger {                  // E12/E14 ledger, log space (reading 10)
+  double logE;
+  int64_t j;
+  int32_t guarantee;                // 1 until a cap fires
+  int32_t error;                    // sticky device error (MPS_E_*), 0 = none
+  double log_fmin, log_ffixed;
+  int64_t n_planned;
+  int32_t strategy, rule, chi_cap, d;
+};
+
+struct DevPool {
+  uint64_t bump;                    // next never-used byte (absolute slab offset)
+  uint64_t ceiling;                 // host-set upper limit of pool allocations
+  uint64_t free_head[kMaxClasses];  // singly linked free lists (next offset in block's first 8 B)
+  int64_t npending;                 // deferred frees (released at the next selector launch)
+  int64_t pending_cap;
+  int64_t pending_off;              // slab offset of the pending array (int64 pairs: off, cls)
+};
+
+// One per gate of a wave (device array, built by the host).
+struct GateDesc {
+  int32_t site, l, mid, r;          // chi_l, chi_m, chi_r
+  int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large
+  int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
+  int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
+  int32_t k, capped;                // outputs of the selector
+  int64_t off_newL, off_newR, off_newLam;                    // outputs of the selector
+  double nu;                        // sqrt(kept weight)
+  double f, t;                      // achieved / target truncation fidelity
+};
+
+struct Record {                     // == mps_record
+  int64_t gate_index;
+  int32_t bond, chi_before, chi_after, capped;
+  double target_f, achieved_f, discarded_weight;
+};
+
+struct ImportEntry {                // bulk site import (mps_import_sites)
+  int32_t site, chl, chr, resetL, resetR, pad;   // reset*: lambda extents to set to ones (0 = keep)
+  int64_t src_elem;                 // first complex element of this site in the source buffer
+  int64_t dst_off, lamL_off, lamR_off;           // written by the device allocator
+};
+
+struct DevState {                   // lives at slab offset 0
+  DevLedger led;
+  DevPool pool;
+  int32_t n_sites, d;
+  int64_t sites_off, bonds_off;     // SiteEntry[N], BondEntry[N+1]
+};
+
+__host__ __device__ inline int size_class(uint64_t bytes) {
+  int c = kMinClass;
+  while ((1ull << c) < bytes) ++c;
+  return c;
+}
+
+template <typename T>
+__host__ __device__ inline T* at(uint8_t* slab, int64_t off) { return reinterpret_cast<T*>(slab + off); }
+
+// ---- kernels (launched by capi.cu) -------------------------------------------------------------
+void launch_contract(const GateDesc* d_desc, const int32_t* d_tile_prefix, int G, int total_tiles, int d,
+                     uint8_t* slab, const DevState* st, const float2* d_us, cudaStream_t s);
+size_t svd_small_smem(int m, int n);
+bool svd_small_fits(int m, int n);
+void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps,
+                      uint8_t* slab, DevState* st, cudaStream_t s);
+// blocked (large) path: returns launches issued
+int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
+                    int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,
+                    cudaStream_t s, int* error_out);
+void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, cudaStream_t s);
+void launch_reabsorb(const GateDesc* d_desc, const int32_t* d_tile_prefix, int G, int total_tiles, int d,
+                     uint8_t* slab, DevState* st, cudaStream_t s);
+void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
+                   cudaStream_t s);
+void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s);
+void launch_pool_free(uint8_t* slab, DevState* st, int64_t off, int cls, cudaStream_t s);
+void launch_gate1(uint8_t* slab, DevState* st, int site, int d, const float2* d_u, cudaStream_t s);
+void launch_amplitude_step(uint8_t* slab, const DevState* st, int site, int digit, const double2* vin, double2* vout,
+                           cudaStream_t s);
+void launch_statevector_step(uint8_t* slab, const DevState* st, int site, int64_t rows, int cols_in,
+                             const double2* Sin, double2* Sout, cudaStream_t s);
+
+}  // namespace eamps
