@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json metric on BASELINE.json configs[1] (the isolated batched gate-update
+microbench): 4096 independent two-site updates per step, chi_l = chi_r = chi (d = 2), theta with
+a sigma_k ~ k^-1.5 spectrum, per-update target fidelity 0.9999 (rule pure), contract-inclusive
+(B_left, B_right, Haar U -> contract -> SVD -> select -> reabsorb), all through the C ABI.
+
+  python bench.py [--gpus N --steps K --warmup W] [--chi 64] [--count 4096] [--impl reference]
+
+One JSON line on rank 0 (see DESIGN.md "Measurement" for every field). A step = one
+mps_apply_layer over the 4096-gate layer (all §8(a) rows a0-a5); the state is restored from a
+device snapshot and L2 is flushed between steps (both untimed). Multi-GPU (torchrun): each rank
+runs its own 4096 updates (independent problems, no collective on the data path: weak scaling),
+time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "2-qubit MPS gate updates/s (contract+SVD+truncate); TFLOP/s as % of FP32 peak"
+UNIT = "gate updates/s"
+F_TRUNC = 0.9999
+# FP32 SIMT peak derived from the guide's unit counts: 148 SMs x 128 FP32
+# lanes x 2 flop/FMA x 1.965 GHz (clocks.max.sm)
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="eamps", choices=["eamps", "reference"])
+    ap.add_argument("--chi", type=int, default=int(os.environ.get("BENCH_CHI", "64")))
+    ap.add_argument("--count", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def svd_flops(m, n, sweeps):
+    """algorithmic flops of the scalar one-sided Jacobi: (20 m n^2 + 12 n^3) per sweep."""
+    return sweeps * (20.0 * m * n * n + 12.0 * n ** 3)
+
+
+def update_flops(chi, sweeps, k):
+    """contract + SVD + reabsorb for one config-2 theta (m = n = 2 chi, chi_m = 2 chi, d = 2)."""
+    d, l, mid, r = 2, chi, 2 * chi, chi
+    m, n = d * l, d * r
+    contract = 8 * d * d * l * mid * r + 8 * d ** 4 * l * r
+    return contract + svd_flops(m, n, sweeps) + 8.0 * m * n * k
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.gpu = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), mx=float(parts[2]), pw=float(parts[3]), reasons=parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        loaded = [r for r in rows if r["sm"] > 300] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        seen = sorted({names[i] for r in rows for i, v in enumerate(r["reasons"]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r["sm"] for r in loaded])), "sm_max_mhz": rows[0]["mx"],
+                "reasons": seen, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_sample(chi, budget_s, first=0):
+    """Time the oracle (as it stands) on the first G_s updates of the same workload."""
+    import workloads
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    import oracle
+
+    def run(G):
+        tensors, gates = workloads.micro_chain(chi, G, first=first)
+        o = oracle.OracleMPS(2 * G, strategy="fixed", f_fixed=F_TRUNC)
+        for i, B in enumerate(tensors):
+            o.import_site(i, B)
+        sites = np.arange(0, 2 * G, 2, dtype=np.int32)
+        t0 = time.perf_counter()
+        o.apply_layer(sites, gates)
+        return time.perf_counter() - t0
+
+    t1 = run(1)  # one update, one thread
+    G = int(max(1, min(4096, budget_s * cores / max(t1, 1e-4))))
+    dt = run(G) if G > 1 else t1
+    return dict(value=G / dt, unit=UNIT, cores=int(os.environ.get("OMP_NUM_THREADS", cores)), kind="oracle",
+                sample="%d of the %d chi=%d updates (first seeds), OpenMP over gates, %.1f s" % (G, 4096, chi, dt))
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import workloads  # noqa: F401
+    per_step = max(2.0, 150.0 / (args.steps + args.warmup))
+    cb = cpu_sample(args.chi, per_step)
+    G = int(round(cb["value"] * per_step)) or 1
+    import oracle
+    times = []
+    for step in range(args.warmup + args.steps):
+        tensors, gates = workloads.micro_chain(args.chi, G, first=step * G)
+        o = oracle.OracleMPS(2 * G, strategy="fixed", f_fixed=F_TRUNC)
+        for i, B in enumerate(tensors):
+            o.import_site(i, B)
+        t0 = time.perf_counter()
+        o.apply_layer(np.arange(0, 2 * G, 2, dtype=np.int32), gates)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = G / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, BASELINE configs[1] recipe)",
+            "impl": "reference",
+            "config": {"workload": "config2_microbench chi=%d contract-inclusive, oracle sample of %d updates/step"
+                       % (args.chi, G), "chi": args.chi, "count": G, "f_trunc": F_TRUNC},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
+                             "sample": "%d updates per step (of 4096), %d steps" % (G, args.steps)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2307_16870_b200 as pk
+    import workloads
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    chi, G = args.chi, args.count
+    n = 2 * chi
+    # ---- inputs: this rank's 4096 updates (seeds b = rank*G .. rank*G + G - 1)
+    left, right, gates = workloads.micro_chain_torch(chi, G, first=rank * G, device=dev)
+    site_bytes = (left.numel() + right.numel()) * 8
+    ws_bytes = G * (3 * n * n * 8 + 64 * n + 4096) + 2 * G * (chi * 2 * n * 8) * 2
+    slab_bytes = int(1.25 * (2 * site_bytes + ws_bytes)) + (256 << 20)
+    mps = pk.MPS(2 * G, strategy="fixed", f_fixed=F_TRUNC, slab_bytes=slab_bytes, device=dev)
+    inter = torch.cat([left.reshape(G, -1), right.reshape(G, -1)], dim=1).reshape(-1)  # L0 R0 L1 R1 ...
+    dims = np.array([[chi, 2, n], [n, 2, chi]] * G, np.int32)
+    mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(inter.data_ptr()), dims)
+    snap = mps.mps_snapshot_save()
+    sites = np.arange(0, 2 * G, 2, dtype=np.int32)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step_timed():
+        mps.mps_snapshot_load(snap)
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        mps.mps_apply_layer(sites, gates)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        step_timed()
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    mps.mps_set_profiling(True)
+    l0 = mps.mps_launch_count()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        total_ms += step_timed()
+    launches = mps.mps_launch_count() - l0
+    phases = mps.mps_phase_times()
+    mps.mps_set_profiling(False)
+    clocks = clk.stop()
+    sweeps = np.array([mps.mps_last_sweeps(g) for g in range(G)])
+    ks = np.array([r["chi_after"] for r in mps.mps_truncation_log()[-G:]])
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * G / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (the SVD phase)
+    svd_key = "svd_small" if phases["svd_small"][1] else "svd_blocked"
+    svd_ms, svd_n = phases[svd_key]
+    svd_ms_per_launch = svd_ms / max(1, svd_n)
+    alg_svd = float(sum(svd_flops(n, n, s) for s in sweeps))  # per launch (one wave = the layer)
+    achieved = alg_svd / (svd_ms_per_launch / 1e3) / 1e12
+    traffic = None
+    tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tj):
+        try:
+            traffic = json.load(open(tj)).get("chi%d" % chi, {}).get(svd_key)
+        except Exception:
+            traffic = None
+    total_flops = float(sum(update_flops(chi, s, k) for s, k in zip(sweeps, ks)))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 norms/Rayleigh)",
+        "data": "synthetic (seeded BASELINE configs[1] recipe: theta = X diag(k^-1.5) Y^H, Haar X/Y/U)",
+        "config": {"workload": "config2_microbench chi=%d x%d contract-inclusive (configs[1])" % (chi, G),
+                   "chi": chi, "count": G, "theta": "%dx%d" % (n, n), "f_trunc": F_TRUNC, "rule": "pure",
+                   "parallelism": "independent updates per rank" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (256 MB write)"},
+        "tflops_algorithmic": total_flops / (ms_step / 1e3) / 1e12 * world,
+        "pct_fp32_simt_peak": 100.0 * total_flops / (ms_step / 1e3) / 1e12 / FP32_SIMT_PEAK_TFLOPS,
+        "sweeps_mean": float(sweeps.mean()), "k_mean": float(ks.mean()),
+        "phase_ms_per_step": {p: v[0] / max(1, args.steps) for p, v in phases.items()},
+        "roofline": {"bound": "alu", "kernel": svd_key, "achieved": achieved, "peak": FP32_SIMT_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP32_SIMT_PEAK_TFLOPS, "traffic": traffic,
+                     "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    # ---- e2e: host (pinned) inputs -> H2D -> update -> D2H of the step's records, through the ABI
+    if not args.no_e2e:
+        host = torch.empty(inter.numel(), dtype=torch.complex64, pin_memory=True)
+        host.copy_(inter.cpu())
+        reps = max(1, min(args.steps, 3))
+        t_e2e = 0.0
+        for rep in range(reps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(host.data_ptr()), dims)
+            mps.mps_apply_layer(sites, gates)
+            recs = mps.mps_truncation_log()[-G:]
+            torch.cuda.synchronize()
+            if rep > 0:
+                t_e2e += time.perf_counter() - t0
+        assert len(recs) == G
+        line["e2e"] = {"value": world * G / (t_e2e / reps), "unit": UNIT,
+                       "h2d_bytes_per_step": int(site_bytes + gates.nbytes),
+                       "d2h_bytes_per_step": int(G * (48 + 160) + 512)}
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_sample(chi, args.cpu_seconds)
+        except Exception as e:  # the baseline never blocks the GPU line
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

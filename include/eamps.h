@@ -139,6 +139,12 @@ mps_status mps_snapshot_load(mps_t, const void* dev_buf, size_t buf_bytes);
 mps_status mps_launch_count(mps_t, int64_t* count);
 /* Jacobi sweeps of gate g of the last layer. */
 mps_status mps_last_sweeps(mps_t, int32_t g, int32_t* sweeps);
+/* Phase timers: with profiling on, apply_layer records CUDA events on cfg.stream around each
+ * phase and accumulates device milliseconds: ms[0] contract, ms[1] SVD (small regime),
+ * ms[2] SVD (blocked regime), ms[3] select, ms[4] reabsorb; counts[p] = waves timed.
+ * mps_set_profiling resets the accumulators. */
+mps_status mps_set_profiling(mps_t, int32_t on);
+mps_status mps_phase_times(mps_t, double* ms /* [5] */, int64_t* counts /* [5], may be NULL */);
 mps_status mps_sync(mps_t);
 const char* mps_last_error(mps_t);
 const char* mps_status_string(mps_status);

@@ -26,7 +26,7 @@ ABI_FUNCTIONS = [
     "mps_fidelity_estimate", "mps_amplitude", "mps_to_statevector", "mps_bond_dims",
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
-    "mps_launch_count", "mps_last_sweeps", "mps_sync", "mps_last_error", "mps_status_string",
+    "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
 ]
 
 
@@ -82,6 +82,8 @@ def lib():
             "mps_snapshot_save": [_P, _P, C.c_size_t, _P],
             "mps_snapshot_load": [_P, _P, C.c_size_t],
             "mps_launch_count": [_P, _P],
+            "mps_set_profiling": [_P, i32],
+            "mps_phase_times": [_P, _P, _P],
             "mps_last_sweeps": [_P, i32, _P],
             "mps_sync": [_P],
             "mps_last_error": [_P],
@@ -273,6 +275,17 @@ class MPS:
         c = C.c_int64(0)
         self._check(lib().mps_launch_count(self._h, C.byref(c)))
         return c.value
+
+    def mps_set_profiling(self, on: bool = True):
+        self._check(lib().mps_set_profiling(self._h, int(bool(on))))
+
+    PHASES = ("contract", "svd_small", "svd_blocked", "select", "reabsorb")
+
+    def mps_phase_times(self):
+        ms = np.zeros(5)
+        cnt = np.zeros(5, np.int64)
+        self._check(lib().mps_phase_times(self._h, _ptr(ms), _ptr(cnt)))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
 
     def mps_sync(self):
         self._check(lib().mps_sync(self._h))

@@ -38,6 +38,11 @@ struct mps_handle {
   int64_t launches = 0;
   void* pinned[2] = {nullptr, nullptr};   // [0] general / readback, [1] layer upload staging
   size_t pinned_bytes[2] = {0, 0};
+  // phase timers (mps_set_profiling): CUDA events recorded on the launch stream around each phase
+  bool profiling = false;
+  double phase_ms[5] = {0, 0, 0, 0, 0};      // contract, svd_small, svd_blocked, select, reabsorb
+  int64_t phase_n[5] = {0, 0, 0, 0, 0};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // host side of a snapshot
   struct Snap {
     bool valid = false;
@@ -308,6 +313,8 @@ mps_status mps_destroy(mps_t h) {
   if (h->s) cudaStreamSynchronize(h->s);
   for (int w = 0; w < 2; ++w)
     if (h->pinned[w]) cudaFreeHost(h->pinned[w]);
+  for (int e = 0; e < 6; ++e)
+    if (h->ev[e]) cudaEventDestroy(h->ev[e]);
   delete h;
   return MPS_OK;
 }
@@ -319,6 +326,24 @@ mps_status mps_sync(mps_t h) {
   st = sync_state(h);
   if (st != MPS_OK) return st;
   return device_error(h);
+}
+
+mps_status mps_set_profiling(mps_t h, int32_t on) {
+  if (!h) return MPS_E_INVAL;
+  if (on && !h->ev[0])
+    for (int e = 0; e < 6; ++e) CK(cudaEventCreate(&h->ev[e]));
+  h->profiling = on != 0;
+  for (int p = 0; p < 5; ++p) { h->phase_ms[p] = 0; h->phase_n[p] = 0; }
+  return MPS_OK;
+}
+
+mps_status mps_phase_times(mps_t h, double* ms, int64_t* counts) {
+  if (!h || !ms) return MPS_E_INVAL;
+  for (int p = 0; p < 5; ++p) {
+    ms[p] = h->phase_ms[p];
+    if (counts) counts[p] = h->phase_n[p];
+  }
+  return MPS_OK;
 }
 
 mps_status mps_launch_count(mps_t h, int64_t* c) {
@@ -496,16 +521,21 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     const float2* d_us = reinterpret_cast<const float2*>(h->slab + o_us);
     Record* d_rec = reinterpret_cast<Record*>(h->slab + o_rec);
 
+    const bool prof = h->profiling;
+    bool ran[5] = {true, !small.empty(), !large.empty(), true, true};
+    if (prof) CK(cudaEventRecord(h->ev[0], h->s));
     // a1 contract (all gates of the wave)
     launch_contract(d_desc, d_cpre, Gw, cpre[Gw], d, h->slab, h->dst, d_us, h->s);
     ++h->launches;
     CKL("contract");
+    if (prof) CK(cudaEventRecord(h->ev[1], h->s));
     // a2 + a3 SVD, small regime: one CTA per theta
     if (!small.empty()) {
       launch_svd_small(d_desc, d_small, (int)small.size(), smem_small, h->cfg.max_sweeps, h->slab, h->dst, h->s);
       ++h->launches;
       CKL("svd_small");
     }
+    if (prof) CK(cudaEventRecord(h->ev[2], h->s));
     // a2 + a3 SVD, large regime: blocked Jacobi
     if (!large.empty()) {
       int err = 0;
@@ -520,14 +550,17 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
         CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
       }
     }
+    if (prof) CK(cudaEventRecord(h->ev[3], h->s));
     // a4 select + ledger + pool
     launch_select(d_desc, Gw, h->slab, h->dst, d_rec, h->s);
     ++h->launches;
     CKL("select");
+    if (prof) CK(cudaEventRecord(h->ev[4], h->s));
     // a5 reabsorb
     launch_reabsorb(d_desc, d_rpre, Gw, rpre[Gw], d, h->slab, h->dst, h->s);
     ++h->launches;
     CKL("reabsorb");
+    if (prof) CK(cudaEventRecord(h->ev[5], h->s));
     // read back: descriptors (k, sweeps), records, device state
     const size_t back = sizeof(GateDesc) * Gw + sizeof(Record) * Gw + sizeof(DevState);
     uint8_t* rb = static_cast<uint8_t*>(pinned_buf(h, back + 64));
@@ -539,6 +572,15 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     std::memcpy(hd.data(), rb, sizeof(GateDesc) * Gw);
     const Record* rr = reinterpret_cast<const Record*>(rb + sizeof(GateDesc) * Gw);
     std::memcpy(&h->hstate, rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, sizeof(DevState));
+    if (prof) {
+      for (int p = 0; p < 5; ++p) {
+        if (!ran[p]) continue;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev[p], h->ev[p + 1]));
+        h->phase_ms[p] += ms;
+        h->phase_n[p] += 1;
+      }
+    }
     mps_status de = device_error(h);
     for (int x = 0; x < Gw; ++x) {
       const GateDesc& gd = hd[x];

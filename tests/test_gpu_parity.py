@@ -58,7 +58,7 @@ def compare_layer(gpu, orc, n_gates, rule="pure"):
             assert near_tie(so, ro["target_f"], ro["chi_after"], rule), (g, rg, ro)
             return worst, False
         assert abs(rg["achieved_f"] - ro["achieved_f"]) < 1e-6
-        assert abs(rg["target_f"] - ro["target_f"]) < 1e-9
+        assert abs(rg["target_f"] - ro["target_f"]) < 1e-6  # t_j depends on E_{j-1} (global)
     return worst, True
 
 

@@ -192,3 +192,39 @@ def micro_chain(chi: int, count: int, first: int = 0, with_gate: bool = True):
         tensors += [L, R]
         gates.append(U)
     return tensors, np.stack(gates)
+
+
+def micro_chain_torch(chi: int, count: int, first: int = 0, device="cuda"):
+    """Same recipe as micro_chain (seeds [.., 2, chi, b]), with the QRs / products batched in
+    torch (complex128, on `device`) for bench-sized batches. Haar(Z) = Q diag(R_ii/|R_ii|) is
+    unique for a given Z, so this equals micro_chain up to FP64 rounding before the complex64
+    rounding. Returns (site tensors as one complex64 torch tensor per side, gates complex64 np)."""
+    import torch
+
+    n = 2 * chi
+    Zx = np.empty((count, n, n), np.complex128)
+    Zy = np.empty((count, n, n), np.complex128)
+    Zu = np.empty((count, 4, 4), np.complex128)
+    for x, b in enumerate(range(first, first + count)):
+        rng = rng_for(2, chi, b)
+        Zx[x] = ginibre(rng, n)
+        Zy[x] = ginibre(rng, n)
+        Zu[x] = ginibre(rng_for(2, chi, b, 1 << 20), 4)
+    U = haar_from_ginibre(Zu).astype(np.complex64).astype(np.complex128)  # as micro_pair
+    sig = torch.as_tensor(powerlaw_sigma(n), device=device, dtype=torch.float64)
+
+    def haar_t(Z):
+        q, r = torch.linalg.qr(Z)
+        dg = torch.diagonal(r, dim1=-2, dim2=-1)
+        return q * (dg / dg.abs()).unsqueeze(-2)
+
+    X = haar_t(torch.as_tensor(Zx, device=device))
+    Y = haar_t(torch.as_tensor(Zy, device=device))
+    th = (X * sig.to(X.dtype)) @ Y.conj().transpose(-1, -2)
+    th = th.to(torch.complex64).to(torch.complex128)
+    T = th.reshape(count, chi, 2, 2, chi)
+    Ud = torch.as_tensor(np.conj(U), device=device).reshape(count, 2, 2, 2, 2)
+    C = torch.einsum("gstuv,gastc->gauvc", Ud, T)
+    left = C.reshape(count, chi, 2, n).to(torch.complex64)
+    right = torch.eye(n, dtype=torch.complex64, device=device).reshape(n, 2, chi).expand(count, n, 2, chi)
+    return left, right.contiguous(), U.astype(np.complex64)
