@@ -245,7 +245,9 @@ mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* 
   const size_t bonds_off = align_up(sites_off + sizeof(SiteEntry) * n_sites);
   const int64_t pend_cap = 3 * (int64_t)n_sites + 64;
   const size_t pend_off = align_up(bonds_off + sizeof(BondEntry) * (n_sites + 1));
-  const size_t pool_base = align_up(pend_off + 16 * pend_cap);
+  const int64_t stack_cap = 3 * (int64_t)n_sites + 64;  // >= live + pending blocks of any class
+  const size_t stack_off = align_up(pend_off + 16 * pend_cap);
+  const size_t pool_base = align_up(stack_off + 8 * (size_t)kMaxClasses * stack_cap);
   const size_t init_end = pool_base + kAlign * (2 * (size_t)n_sites + 1);
   if (init_end + (1u << 16) > h->slab_bytes) {
     delete h;
@@ -268,6 +270,8 @@ mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* 
   S.pool.bump = init_end;
   S.pool.ceiling = h->slab_bytes - kAlign;
   S.pool.npending = 0;
+  S.pool.stack_off = (int64_t)stack_off;
+  S.pool.stack_cap = stack_cap;
   S.pool.pending_cap = pend_cap;
   S.pool.pending_off = (int64_t)pend_off;
   S.n_sites = n_sites;
@@ -401,7 +405,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
   struct Plan {
     GateDesc gd;
     size_t ws, reserve;
-    int ctiles, rtiles;
+    int ctiles, rtiles, gtiles, atiles;
   };
   std::vector<Plan> plan(G);
   const int TA = 64 / d;
@@ -420,8 +424,9 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     gd.n_pad = gd.regime == 0 ? gd.n : (int)align_up(gd.n, 32);
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+    const int kmn = std::min(gd.m, gd.n);
     p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
-           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4);
+           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) + align_up((size_t)kmn * kmn * 8);
     int kmax = std::min(gd.m, gd.n);
     if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);
     p.reserve = ((size_t)1 << size_class((uint64_t)gd.l * d * kmax * 8)) +
@@ -430,6 +435,8 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     p.ctiles = ((gd.l + TA - 1) / TA) * ((gd.r + TA - 1) / TA);
     const int km = std::min(gd.m, gd.n);
     p.rtiles = ((gd.m + 63) / 64) * ((km + 63) / 64) + km;
+    p.gtiles = ((km + 31) / 32) * ((km + 31) / 32);
+    p.atiles = ((gd.n + 63) / 64) * ((km + 63) / 64);
   }
 
   // ---- waves (gates in canonical order; each wave's workspace + worst-case new blocks fit)
@@ -442,7 +449,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     int g1 = g0;
     while (g1 < G) {
       const int cnt = g1 - g0 + 1;
-      size_t fx = align_up(sizeof(GateDesc) * cnt) + 2 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
+      size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
                   align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
       size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
       if (bump + r2 + fx + w2 + kAlign > top) break;
@@ -464,13 +471,15 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     const size_t o_desc = take(sizeof(GateDesc) * Gw);
     const size_t o_cpre = take(4 * (Gw + 1));
     const size_t o_rpre = take(4 * (Gw + 1));
+    const size_t o_gpre = take(4 * (Gw + 1));
+    const size_t o_apre = take(4 * (Gw + 1));
     const size_t o_small = take(4 * Gw);
     const size_t o_large = take(4 * Gw);
     const size_t o_us = take((size_t)Gw * d4 * 8);
     const size_t o_rec = take(sizeof(Record) * Gw);
     const size_t o_scr = take(32 * (size_t)Gw + 64);
     const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
-    std::vector<int32_t> cpre(Gw + 1, 0), rpre(Gw + 1, 0), small, large;
+    std::vector<int32_t> cpre(Gw + 1, 0), rpre(Gw + 1, 0), gpre(Gw + 1, 0), apre(Gw + 1, 0), small, large;
     std::vector<GateDesc> hd(Gw);
     size_t smem_small = 0;
     for (int x = 0; x < Gw; ++x) {
@@ -484,9 +493,13 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
       gd.ws_sig2 = (int64_t)take((size_t)gd.n_pad * 8);
       gd.ws_T = (int64_t)take((size_t)(gd.n_pad + 1) * 8);
       gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
+      const size_t kmn = (size_t)std::min(gd.m, gd.n);
+      gd.ws_E = (int64_t)take(kmn * kmn * 8);
       hd[x] = gd;
       cpre[x + 1] = cpre[x] + p.ctiles;
       rpre[x + 1] = rpre[x] + p.rtiles;
+      gpre[x + 1] = gpre[x] + p.gtiles;
+      apre[x + 1] = apre[x] + p.atiles;
       if (gd.regime == 0) {
         small.push_back(x);
         smem_small = std::max(smem_small, svd_small_smem(gd.m, gd.n));
@@ -503,6 +516,8 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
     std::memcpy(hb + (o_cpre - base), cpre.data(), 4 * (Gw + 1));
     std::memcpy(hb + (o_rpre - base), rpre.data(), 4 * (Gw + 1));
+    std::memcpy(hb + (o_gpre - base), gpre.data(), 4 * (Gw + 1));
+    std::memcpy(hb + (o_apre - base), apre.data(), 4 * (Gw + 1));
     if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
     if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
     for (int x = 0; x < Gw; ++x)
@@ -516,6 +531,8 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + o_desc);
     const int32_t* d_cpre = reinterpret_cast<const int32_t*>(h->slab + o_cpre);
     const int32_t* d_rpre = reinterpret_cast<const int32_t*>(h->slab + o_rpre);
+    const int32_t* d_gpre = reinterpret_cast<const int32_t*>(h->slab + o_gpre);
+    const int32_t* d_apre = reinterpret_cast<const int32_t*>(h->slab + o_apre);
     const int32_t* d_small = reinterpret_cast<const int32_t*>(h->slab + o_small);
     const int32_t* d_large = reinterpret_cast<const int32_t*>(h->slab + o_large);
     const float2* d_us = reinterpret_cast<const float2*>(h->slab + o_us);
@@ -552,13 +569,14 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     }
     if (prof) CK(cudaEventRecord(h->ev[3], h->s));
     // a4 select + ledger + pool
-    launch_select(d_desc, Gw, h->slab, h->dst, d_rec, h->s);
-    ++h->launches;
+    const int par = (h->cfg.strategy == MPS_STRAT_FIXED || h->cfg.strategy == MPS_STRAT_NAIVE) ? 1 : 0;
+    launch_select(d_desc, Gw, h->slab, h->dst, d_rec, par, h->s);
+    h->launches += 2;
     CKL("select");
     if (prof) CK(cudaEventRecord(h->ev[4], h->s));
     // a5 reabsorb
-    launch_reabsorb(d_desc, d_rpre, Gw, rpre[Gw], d, h->slab, h->dst, h->s);
-    ++h->launches;
+    launch_reabsorb(d_desc, d_gpre, gpre[Gw], d_apre, apre[Gw], d_rpre, rpre[Gw], Gw, h->slab, h->s);
+    h->launches += 3;
     CKL("reabsorb");
     if (prof) CK(cudaEventRecord(h->ev[5], h->s));
     // read back: descriptors (k, sweeps), records, device state

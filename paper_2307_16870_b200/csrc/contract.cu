@@ -57,11 +57,13 @@ __global__ void __launch_bounds__(256) k_contract(const GateDesc* __restrict__ d
   for (int x = tid; x < D * D * D * D; x += 256) Us[x] = us[(int64_t)gd.u_index * D * D * D * D + x];
 
   const int ty = tid >> 4, tx = tid & 15;
-  float2 acc[4][4];
+  // FP32 products accumulated per KC-chunk, chunk sums accumulated in FP64: the rounding of a
+  // chi_m-long dot product drops from ~sqrt(chi_m) eps32 to ~sqrt(KC) eps32 (DESIGN "Precision")
+  double2 dacc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < 4; ++j) dacc[i][j] = make_double2(0.0, 0.0);
 
   for (int b0 = 0; b0 < mid; b0 += KC) {
     // A chunk: rows rho = (a_local, s') of B_i as (l d) x mid, columns b0..b0+KC (contiguous)
@@ -86,6 +88,11 @@ __global__ void __launch_bounds__(256) k_contract(const GateDesc* __restrict__ d
       Bs[kk][tp * TC + cc] = v;
     }
     __syncthreads();
+    float2 acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       float2 av[4], bv[4];
@@ -103,12 +110,16 @@ __global__ void __launch_bounds__(256) k_contract(const GateDesc* __restrict__ d
           acc[i][j].y = fmaf(av[i].y, bv[j].x, acc[i][j].y);
         }
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { dacc[i][j].x += acc[i][j].x; dacc[i][j].y += acc[i][j].y; }
     __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) Cs[ty + 16 * i][tx + 16 * j] = acc[i][j];
+    for (int j = 0; j < 4; ++j) Cs[ty + 16 * i][tx + 16 * j] = make_float2((float)dacc[i][j].x, (float)dacc[i][j].y);
   __syncthreads();
 
   // epilogue: gate mixing over (s', t') and the lambda row scale; coalesced along a

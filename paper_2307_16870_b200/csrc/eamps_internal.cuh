@@ -38,8 +38,10 @@ struct DevLedger {                  // E12/E14 ledger, log space (DESIGN.md read
 struct DevPool {
   uint64_t bump;                    // next never-used byte (absolute slab offset)
   uint64_t ceiling;                 // host-set upper limit of pool allocations
-  uint64_t free_head[kMaxClasses];  // singly linked free lists (next offset in block's first 8 B)
-  int64_t npending;                 // deferred frees (released at the next selector launch)
+  int32_t count[kMaxClasses];       // free-stack depth per size class
+  int64_t stack_off;                // slab offset of the free stacks: kMaxClasses x stack_cap int64
+  int64_t stack_cap;
+  int64_t npending;                 // deferred frees (released at the next commit launch)
   int64_t pending_cap;
   int64_t pending_off;              // slab offset of the pending array (int64 pairs: off, cls)
 };
@@ -49,11 +51,13 @@ struct GateDesc {
   int32_t site, l, mid, r;          // chi_l, chi_m, chi_r
   int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large
   int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
+  int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
   int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
   int32_t k, capped;                // outputs of the selector
   int64_t off_newL, off_newR, off_newLam;                    // outputs of the selector
   double nu;                        // sqrt(kept weight)
   double f, t;                      // achieved / target truncation fidelity
+  double dlogE, disc;               // log f, discarded weight T_k / P
 };
 
 struct Record {                     // == mps_record
@@ -95,9 +99,11 @@ void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t
 int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                     int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,
                     cudaStream_t s, int* error_out);
-void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, cudaStream_t s);
-void launch_reabsorb(const GateDesc* d_desc, const int32_t* d_tile_prefix, int G, int total_tiles, int d,
-                     uint8_t* slab, DevState* st, cudaStream_t s);
+// parallel = 1: FIXED / NAIVE (target independent of the ledger): one warp per gate;
+// parallel = 0: GLOBAL / NEAREST: one warp walks the gates in canonical order.
+void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s);
+void launch_reabsorb(const GateDesc* d_desc, const int32_t* d_pre_gram, int tiles_gram, const int32_t* d_pre_apply,
+                     int tiles_apply, const int32_t* d_pre_reab, int tiles_reab, int G, uint8_t* slab, cudaStream_t s);
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s);
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s);

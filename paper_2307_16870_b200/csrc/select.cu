@@ -2,7 +2,7 @@
 // pool allocator of the site store (north-star: "a per-site HBM tensor store with variable chi
 // and a device-side pool allocator").
 //
-// One warp walks the wave's gates in canonical order (ascending site; reading 5):
+// Rank selection, per gate (one warp):
 //   log t_j  (E14; strategies PAPER.md:153/158 in log space, DESIGN reading 6)
 //     naive   : log F_min / n
 //     global  : min(0, (log F_min - log E) / R)                R = n - j
@@ -12,25 +12,29 @@
 //   k = min{k >= 1 : T_k <= tau P}  ("as close to but not lower than f_t")
 //       -- a 32-ary warp search over the non-increasing tails T
 //   k <= min(m, n); k > chi_cap -> k = chi_cap, guarantee lost
-//   f = 1 - T_k/P (pure/ratio) or sqrt(1 - T_k/P) (wang); log E += log f   (E12)
-// then frees the old blocks of B_i, B_{i+1}, lambda_i (deferred to the next launch, when the
-// reabsorb that reads the workspace -- never the old blocks -- has finished) and allocates the
-// new ones from power-of-two size classes (free lists threaded through the free blocks + bump).
+//   f = 1 - T_k/P (pure/ratio) or sqrt(1 - T_k/P) (wang)
+// FIXED / NAIVE targets do not depend on the ledger: one warp per gate, all gates in parallel.
+// GLOBAL / NEAREST: t_j depends on E_{j-1}, so one warp walks the wave in canonical order.
+//
+// Commit (one CTA): log E += log f_j in canonical order (E12), the truncation records, and the
+// pool: the old blocks of B_i, B_{i+1}, lambda_i are deferred-freed (released at the next commit,
+// after the reabsorb that never reads them has finished); the new blocks come from per-class
+// free stacks (power-of-two classes) or the bump pointer. One thread plans every request with
+// shared-memory counters only (no global loads on the sequential path); all threads then resolve
+// the stack pops and write the site tables in parallel.
 #include "eamps_internal.cuh"
 
 namespace eamps {
 
 namespace {
 
+// ---- single-threaded pool ops (host-side helpers and import; not on the layer hot path) ----
 __device__ uint64_t pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int* cls_out) {
   DevPool& P = st->pool;
   int c = size_class(bytes);
   *cls_out = c;
-  uint64_t off = P.free_head[c];
-  if (off) {
-    P.free_head[c] = *reinterpret_cast<uint64_t*>(slab + off);
-    return off;
-  }
+  int64_t* stk = reinterpret_cast<int64_t*>(slab + P.stack_off);
+  if (P.count[c] > 0) return (uint64_t)stk[(int64_t)c * P.stack_cap + (--P.count[c])];
   uint64_t o = (P.bump + 255ull) & ~255ull;
   uint64_t sz = 1ull << c;
   if (o + sz > P.ceiling) {
@@ -43,142 +47,235 @@ __device__ uint64_t pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int*
 
 __device__ void pool_free_now(uint8_t* slab, DevState* st, uint64_t off, int cls) {
   if (!off) return;
-  *reinterpret_cast<uint64_t*>(slab + off) = st->pool.free_head[cls];
-  st->pool.free_head[cls] = off;
-}
-
-__device__ void pool_defer(uint8_t* slab, DevState* st, uint64_t off, int cls) {
-  if (!off) return;
   DevPool& P = st->pool;
-  int64_t* pend = reinterpret_cast<int64_t*>(slab + P.pending_off);
-  if (P.npending < P.pending_cap) {
-    pend[2 * P.npending] = (int64_t)off;
-    pend[2 * P.npending + 1] = cls;
-    ++P.npending;
-  } else {
+  if (P.count[cls] >= P.stack_cap) {  // cannot happen with stack_cap >= live + pending blocks
     if (st->led.error == 0) st->led.error = -3;
+    return;
   }
+  int64_t* stk = reinterpret_cast<int64_t*>(slab + P.stack_off);
+  stk[(int64_t)cls * P.stack_cap + (P.count[cls]++)] = (int64_t)off;
 }
 
-__device__ double target_log(const DevLedger& L, bool* bad) {
+__device__ __forceinline__ double target_log(int strategy, double log_fmin, double log_ffixed, int64_t n_planned,
+                                             double logE, int64_t j, bool* bad) {
   *bad = false;
   double lt;
-  if (L.strategy == 3) {
-    lt = L.log_ffixed;
+  if (strategy == 3) {
+    lt = log_ffixed;
   } else {
-    if (L.j >= L.n_planned) { *bad = true; return 0.0; }
-    double R = (double)(L.n_planned - L.j);
-    if (L.strategy == 0) lt = L.log_fmin / (double)L.n_planned;
-    else if (L.strategy == 2) lt = (L.log_fmin - L.logE) / R;
-    else lt = L.log_fmin - L.logE - (R - 1.0) * L.log_fmin / (double)L.n_planned;
+    if (j >= n_planned) { *bad = true; return 0.0; }
+    double R = (double)(n_planned - j);
+    if (strategy == 0) lt = log_fmin / (double)n_planned;
+    else if (strategy == 2) lt = (log_fmin - logE) / R;
+    else lt = log_fmin - logE - (R - 1.0) * log_fmin / (double)n_planned;
   }
   return lt < 0.0 ? lt : 0.0;
 }
 
-__global__ void k_select(GateDesc* desc, int G, uint8_t* slab, DevState* st, Record* rec) {
-  const int lane = threadIdx.x;
+// Rank search for one gate by one warp; writes k, capped, f, t, nu, dlogE, disc into gd.
+__device__ void rank_one(GateDesc& gd, const uint8_t* slab, int rule, int chi_cap, double lt) {
+  const int lane = threadIdx.x & 31;
+  const double* T = reinterpret_cast<const double*>(slab + gd.ws_T);
+  const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
+  const int n = gd.n;
+  const double P = T[0];
+  const double tau = rule == 1 ? -expm1(2.0 * lt) : -expm1(lt);
+  int k;
+  if (!(P > 0.0)) {
+    k = 1;
+  } else if (tau <= 0.0) {
+    // exact mode: keep sigma > 1e-6 sigma_0 (the FP32 noise floor; reading 8)
+    const double thr = 1e-12 * s2[0];
+    int cnt = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      int j = j0 + lane;
+      unsigned b = __ballot_sync(0xffffffffu, j < n && s2[j] > thr);
+      cnt += __popc(b);
+    }
+    k = max(1, cnt);
+  } else {
+    const double thr = tau * P;
+    int lo = 1, hi = n;  // invariant: answer in [lo, hi] and T[hi] <= thr (T[n] = 0)
+    while (lo < hi) {
+      const int step = (hi - lo + 31) / 32;
+      const int cand = lo + lane * step;
+      const bool pred = cand < hi ? (T[cand] <= thr) : true;
+      const unsigned b = __ballot_sync(0xffffffffu, pred);
+      if (b == 0u) {
+        lo = lo + 31 * step + 1;
+      } else {
+        const int f = __ffs(b) - 1;
+        hi = min(hi, lo + f * step);
+        if (f > 0) lo = lo + (f - 1) * step + 1;
+      }
+    }
+    k = lo;
+  }
+  const int kmax = min(gd.m, n);
+  if (k > kmax) k = kmax;
+  int capped = 0;
+  if (chi_cap > 0 && k > chi_cap) { k = chi_cap; capped = 1; }
+  double kw = 0.0;  // nu^2 = kept weight: lane-strided FP64 sum + xor tree (deterministic)
+  for (int j = lane; j < k; j += 32) kw += s2[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kw += __shfl_xor_sync(0xffffffffu, kw, o);
   if (lane == 0) {
-    DevPool& P = st->pool;
-    const int64_t* pend = reinterpret_cast<const int64_t*>(slab + P.pending_off);
-    for (int64_t x = 0; x < P.npending; ++x) pool_free_now(slab, st, (uint64_t)pend[2 * x], (int)pend[2 * x + 1]);
-    P.npending = 0;
+    const double r = P > 0.0 ? T[k] / P : 0.0;
+    if (rule == 1) { gd.f = sqrt(1.0 - r); gd.dlogE = 0.5 * log1p(-r); }
+    else { gd.f = 1.0 - r; gd.dlogE = log1p(-r); }
+    gd.k = k; gd.capped = capped; gd.t = exp(lt); gd.nu = sqrt(kw); gd.disc = r;
   }
   __syncwarp();
+}
+
+__global__ void k_select_parallel(GateDesc* desc, int G, const uint8_t* slab, const DevState* st) {
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= G) return;
+  const DevLedger& L = st->led;
+  bool bad;
+  // the target does not depend on the ledger here: j only guards n_planned (checked on the host)
+  double lt = target_log(L.strategy, L.log_fmin, L.log_ffixed, L.n_planned, 0.0, 0, &bad);
+  rank_one(desc[g], slab, L.rule, L.chi_cap, lt);
+}
+
+__global__ void k_select_sequential(GateDesc* desc, int G, const uint8_t* slab, DevState* st) {
+  const int lane = threadIdx.x;
+  const DevLedger L = st->led;
+  double logE = L.logE;
+  int64_t j = L.j;
+  for (int g = 0; g < G; ++g) {
+    bool bad;
+    double lt = target_log(L.strategy, L.log_fmin, L.log_ffixed, L.n_planned, logE, j, &bad);
+    if (bad) {
+      if (lane == 0) { st->led.error = -8; for (int x = g; x < G; ++x) desc[x].k = 0; }
+      return;
+    }
+    rank_one(desc[g], slab, L.rule, L.chi_cap, lt);
+    logE += desc[g].dlogE;  // the same summation order as the commit kernel
+    ++j;
+  }
+}
+
+constexpr int kCommitThreads = 1024;
+constexpr int kChunk = 2048;  // gates planned per shared-memory chunk
+
+__global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G, uint8_t* slab, DevState* st,
+                                                            Record* rec) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  // chunk scratch: plan[3*kChunk] (uint64: offset, or stack slot with the top bit set), cls[3*kChunk]
+  uint64_t* plan = reinterpret_cast<uint64_t*>(sm);
+  int32_t* pcls = reinterpret_cast<int32_t*>(plan + 3 * kChunk);
+  int64_t* ordv = reinterpret_cast<int64_t*>(pcls + 3 * kChunk);  // ledger index per gate of the chunk
+  __shared__ int32_t cnt[kMaxClasses];
+  __shared__ uint64_t s_bump;
+  __shared__ int s_err;
+  const int tid = threadIdx.x;
+  DevPool& P = st->pool;
+  int64_t* stk = reinterpret_cast<int64_t*>(slab + P.stack_off);
+  int64_t* pend = reinterpret_cast<int64_t*>(slab + P.pending_off);
   SiteEntry* sites = reinterpret_cast<SiteEntry*>(slab + st->sites_off);
   BondEntry* bonds = reinterpret_cast<BondEntry*>(slab + st->bonds_off);
   const int d = st->d;
-  for (int g = 0; g < G; ++g) {
-    GateDesc& gd = desc[g];
-    if (st->led.error != 0) {  // sticky error: leave the rest of the wave untouched
-      if (lane == 0) gd.k = 0;
-      continue;
+  const int64_t cap = P.stack_cap;
+  const uint64_t ceiling = P.ceiling;
+  if (tid < kMaxClasses) cnt[tid] = P.count[tid];
+  if (tid == 0) { s_bump = P.bump; s_err = st->led.error; }
+  __syncthreads();
+
+  // A. release the previous wave's deferred frees onto the class stacks
+  const int64_t npend = P.npending;
+  for (int64_t c0 = 0; c0 < npend; c0 += 3 * kChunk) {
+    const int64_t cn = min((int64_t)3 * kChunk, npend - c0);
+    for (int64_t x = tid; x < cn; x += kCommitThreads) {
+      plan[x] = (uint64_t)pend[2 * (c0 + x)];
+      pcls[x] = (int32_t)pend[2 * (c0 + x) + 1];
     }
-    const double* T = reinterpret_cast<const double*>(slab + gd.ws_T);
-    const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
-    const int n = gd.n;
-    const double P = T[0];
-    bool bad = false;
-    const double lt = target_log(st->led, &bad);
-    if (bad) {
-      if (lane == 0) { st->led.error = -8; gd.k = 0; }
-      __syncwarp();
-      continue;
-    }
-    const int rule = st->led.rule;
-    const double tau = rule == 1 ? -expm1(2.0 * lt) : -expm1(lt);
-    int k;
-    if (!(P > 0.0)) {
-      k = 1;
-    } else if (tau <= 0.0) {
-      // exact mode: keep sigma > 1e-6 sigma_0 (the FP32 noise floor; reading 8)
-      const double thr = 1e-12 * s2[0];
-      int cnt = 0;
-      for (int j0 = 0; j0 < n; j0 += 32) {
-        int j = j0 + lane;
-        unsigned b = __ballot_sync(0xffffffffu, j < n && s2[j] > thr);
-        cnt += __popc(b);
+    __syncthreads();
+    if (tid == 0) {
+      for (int64_t x = 0; x < cn; ++x) {
+        if (!plan[x]) continue;
+        int c = pcls[x];
+        if (cnt[c] >= cap) { s_err = -3; plan[x] = 0; continue; }
+        pcls[x] = c | (cnt[c]++ << 6);  // class (6 bits) + stack slot
       }
-      k = max(1, cnt);
-    } else {
-      const double thr = tau * P;
-      int lo = 1, hi = n;  // invariant: answer in [lo, hi] and T[hi] <= thr (T[n] = 0)
-      while (lo < hi) {
-        const int step = (hi - lo + 31) / 32;
-        const int cand = lo + lane * step;
-        const bool pred = cand < hi ? (T[cand] <= thr) : true;
-        const unsigned b = __ballot_sync(0xffffffffu, pred);
-        if (b == 0u) {
-          lo = lo + 31 * step + 1;
-        } else {
-          const int f = __ffs(b) - 1;
-          hi = min(hi, lo + f * step);
-          if (f > 0) lo = lo + (f - 1) * step + 1;
+    }
+    __syncthreads();
+    for (int64_t x = tid; x < cn; x += kCommitThreads) {
+      if (!plan[x]) continue;
+      int c = pcls[x] & 63, slot = pcls[x] >> 6;
+      stk[(int64_t)c * cap + slot] = (int64_t)plan[x];
+    }
+    __syncthreads();
+  }
+
+  // B/C. per chunk of gates: sequential plan (ledger + allocation) then parallel resolve
+  double logE = st->led.logE;
+  int64_t j = st->led.j;
+  int guarantee = st->led.guarantee;
+  for (int g0 = 0; g0 < G; g0 += kChunk) {
+    const int gn = min(kChunk, G - g0);
+    if (tid == 0) {
+      for (int x = 0; x < gn; ++x) {
+        const GateDesc& gd = desc[g0 + x];
+        ordv[x] = -1;
+        if (gd.k <= 0 || s_err) { plan[3 * x] = plan[3 * x + 1] = plan[3 * x + 2] = 0; continue; }
+        logE += gd.dlogE;
+        ordv[x] = j++;
+        if (gd.capped) guarantee = 0;
+        const uint64_t bytes[3] = {(uint64_t)gd.l * d * gd.k * 8, (uint64_t)gd.k * d * gd.r * 8, (uint64_t)gd.k * 4};
+        for (int q = 0; q < 3; ++q) {
+          int c = size_class(bytes[q]);
+          pcls[3 * x + q] = c;
+          if (cnt[c] > 0) {
+            plan[3 * x + q] = (1ull << 63) | (uint64_t)(--cnt[c]);
+          } else {
+            uint64_t o = (s_bump + 255ull) & ~255ull;
+            if (o + (1ull << c) > ceiling) { s_err = -3; plan[3 * x + q] = 0; continue; }
+            s_bump = o + (1ull << c);
+            plan[3 * x + q] = o;
+          }
         }
       }
-      k = lo;
     }
-    const int kmax = min(gd.m, n);
-    if (k > kmax) k = kmax;
-    int capped = 0;
-    if (st->led.chi_cap > 0 && k > st->led.chi_cap) { k = st->led.chi_cap; capped = 1; }
-    // nu^2 = kept weight, deterministic lane-strided FP64 sum + xor tree
-    double kw = 0.0;
-    for (int j = lane; j < k; j += 32) kw += s2[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kw += __shfl_xor_sync(0xffffffffu, kw, o);
-    if (lane == 0) {
-      const double r = P > 0.0 ? T[k] / P : 0.0;
-      double f, dl;
-      if (rule == 1) { f = sqrt(1.0 - r); dl = 0.5 * log1p(-r); }
-      else { f = 1.0 - r; dl = log1p(-r); }
-      DevLedger& L = st->led;
-      Record& R = rec[g];
-      R.gate_index = L.j; R.bond = gd.site; R.chi_before = gd.mid; R.chi_after = k; R.capped = capped;
-      R.target_f = exp(lt); R.achieved_f = f; R.discarded_weight = r;
-      L.logE += dl;
-      L.j += 1;
-      if (capped) L.guarantee = 0;
-      // site store: defer-free the old blocks, allocate the new ones
+    __syncthreads();
+    for (int x = tid; x < gn; x += kCommitThreads) {
+      GateDesc& gd = desc[g0 + x];
       const int i = gd.site;
-      pool_defer(slab, st, (uint64_t)sites[i].off, sites[i].cls);
-      pool_defer(slab, st, (uint64_t)sites[i + 1].off, sites[i + 1].cls);
-      pool_defer(slab, st, (uint64_t)bonds[i + 1].off, bonds[i + 1].cls);
-      int cL, cR, cLam;
-      uint64_t oL = pool_alloc(slab, st, (uint64_t)gd.l * d * k * 8, &cL);
-      uint64_t oR = pool_alloc(slab, st, (uint64_t)k * d * gd.r * 8, &cR);
-      uint64_t oLam = pool_alloc(slab, st, (uint64_t)k * 4, &cLam);
-      if (!oL || !oR || !oLam) {
-        gd.k = 0;
-      } else {
-        sites[i].off = (int64_t)oL; sites[i].chr = k; sites[i].cls = cL;
-        sites[i + 1].off = (int64_t)oR; sites[i + 1].chl = k; sites[i + 1].cls = cR;
-        bonds[i + 1].off = (int64_t)oLam; bonds[i + 1].len = k; bonds[i + 1].cls = cLam;
-        gd.k = k; gd.capped = capped;
-        gd.off_newL = (int64_t)oL; gd.off_newR = (int64_t)oR; gd.off_newLam = (int64_t)oLam;
-        gd.nu = sqrt(kw); gd.f = f; gd.t = exp(lt);
+      uint64_t off[3] = {0, 0, 0};
+      bool ok = ordv[x] >= 0;
+      for (int q = 0; q < 3 && ok; ++q) {
+        uint64_t p = plan[3 * x + q];
+        if (!p) { ok = false; break; }
+        off[q] = (p >> 63) ? (uint64_t)stk[(int64_t)pcls[3 * x + q] * cap + (int64_t)(p & ~(1ull << 63))] : p;
       }
+      const int64_t pb = 3 * (int64_t)(g0 + x);
+      if (!ok) {
+        gd.k = 0;
+        pend[2 * pb] = pend[2 * pb + 2] = pend[2 * pb + 4] = 0;
+        continue;
+      }
+      // deferred frees of the old blocks
+      pend[2 * pb] = sites[i].off; pend[2 * pb + 1] = sites[i].cls;
+      pend[2 * pb + 2] = sites[i + 1].off; pend[2 * pb + 3] = sites[i + 1].cls;
+      pend[2 * pb + 4] = bonds[i + 1].off; pend[2 * pb + 5] = bonds[i + 1].cls;
+      sites[i].off = (int64_t)off[0]; sites[i].chr = gd.k; sites[i].cls = pcls[3 * x];
+      sites[i + 1].off = (int64_t)off[1]; sites[i + 1].chl = gd.k; sites[i + 1].cls = pcls[3 * x + 1];
+      bonds[i + 1].off = (int64_t)off[2]; bonds[i + 1].len = gd.k; bonds[i + 1].cls = pcls[3 * x + 2];
+      gd.off_newL = (int64_t)off[0]; gd.off_newR = (int64_t)off[1]; gd.off_newLam = (int64_t)off[2];
+      Record& R = rec[g0 + x];
+      R.gate_index = ordv[x]; R.bond = i; R.chi_before = gd.mid; R.chi_after = gd.k; R.capped = gd.capped;
+      R.target_f = gd.t; R.achieved_f = gd.f; R.discarded_weight = gd.disc;
     }
-    __syncwarp();
+    __syncthreads();
+  }
+  if (tid < kMaxClasses) P.count[tid] = cnt[tid];
+  if (tid == 0) {
+    P.bump = s_bump;
+    P.npending = 3 * (int64_t)G;
+    st->led.logE = logE;
+    st->led.j = j;
+    st->led.guarantee = guarantee;
+    if (s_err && !st->led.error) st->led.error = s_err;
   }
 }
 
@@ -265,9 +362,19 @@ void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, c
   k_import_scatter<<<count, 256, 0, s>>>(slab, d_ent, src, d);
 }
 
-void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, cudaStream_t s) {
+void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s) {
   if (G <= 0) return;
-  k_select<<<1, 32, 0, s>>>(d_desc, G, slab, st, d_rec);
+  if (parallel)
+    k_select_parallel<<<(G + 7) / 8, 256, 0, s>>>(d_desc, G, slab, st);
+  else
+    k_select_sequential<<<1, 32, 0, s>>>(d_desc, G, slab, st);
+  const size_t smem = (size_t)3 * kChunk * 8 + (size_t)3 * kChunk * 4 + (size_t)kChunk * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_commit<<<1, kCommitThreads, smem, s>>>(d_desc, G, slab, st, d_rec);
 }
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s) {
   k_pool_alloc<<<1, 1, 0, s>>>(slab, st, bytes, d_out);

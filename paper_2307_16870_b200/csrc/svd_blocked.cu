@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(256) k_block_round(const GateDesc* __restrict_
       }
       __syncthreads();
     }
-    if (!s_inner) break;
+    const bool again = s_inner != 0;
+    __syncthreads();  // every thread has read s_inner before thread 0 resets it
+    if (!again) break;
   }
   for (int x = tid; x < PW * PW; x += 256) {
     int a = x / PW, b = x % PW;
