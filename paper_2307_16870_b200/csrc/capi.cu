@@ -434,7 +434,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
                 3 * kAlign;
     p.ctiles = ((gd.l + TA - 1) / TA) * ((gd.r + TA - 1) / TA);
     const int km = std::min(gd.m, gd.n);
-    p.rtiles = ((gd.m + 63) / 64) * ((km + 63) / 64) + km;
+    p.rtiles = ((gd.m + 63) / 64) * ((km + 63) / 64) + (km + 63) / 64;
     p.gtiles = ((km + 31) / 32) * ((km + 31) / 32);
     p.atiles = ((gd.n + 63) / 64) * ((km + 63) / 64);
   }

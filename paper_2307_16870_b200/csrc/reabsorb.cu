@@ -172,18 +172,20 @@ __global__ void __launch_bounds__(256) k_reabsorb(const GateDesc* __restrict__ d
   const int tid = threadIdx.x;
 
   if (local >= gemm_tiles) {
-    // row j of B_{i+1}' = conj(V_k[:, j]) and lambda_i[j]
-    const int j = local - gemm_tiles;
-    if (j >= k) return;
-    const float2* vj = Vk + (int64_t)j * n;
-    float2* Br = reinterpret_cast<float2*>(slab + gd.off_newR) + (int64_t)j * n;
-    for (int c = tid; c < n; c += 256) {
-      float2 v = vj[c];
-      Br[c] = make_float2(v.x, -v.y);
+    // rows j0 .. j0+63 of B_{i+1}' = conj(V_k[:, j]) (contiguous copy) and lambda_i[j]
+    const int j0 = (local - gemm_tiles) * 64;
+    if (j0 >= k) return;
+    const int j1 = min(k, j0 + 64);
+    const float2* src = Vk + (int64_t)j0 * n;
+    float2* dst = reinterpret_cast<float2*>(slab + gd.off_newR) + (int64_t)j0 * n;
+    const int64_t cnt = (int64_t)(j1 - j0) * n;
+    for (int64_t x = tid; x < cnt; x += 256) {
+      float2 v = src[x];
+      dst[x] = make_float2(v.x, -v.y);
     }
-    if (tid == 0) {
+    if (tid < j1 - j0) {
       const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
-      reinterpret_cast<float*>(slab + gd.off_newLam)[j] = (float)(sqrt(s2[j]) / gd.nu);
+      reinterpret_cast<float*>(slab + gd.off_newLam)[j0 + tid] = (float)(sqrt(s2[j0 + tid]) / gd.nu);
     }
     return;
   }

@@ -166,6 +166,11 @@ __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G
   uint64_t* plan = reinterpret_cast<uint64_t*>(sm);
   int32_t* pcls = reinterpret_cast<int32_t*>(plan + 3 * kChunk);
   int64_t* ordv = reinterpret_cast<int64_t*>(pcls + 3 * kChunk);  // ledger index per gate of the chunk
+  double* gdl = reinterpret_cast<double*>(ordv + kChunk);             // per-gate fields, preloaded in parallel
+  int32_t* gk = reinterpret_cast<int32_t*>(gdl + kChunk);
+  int32_t* gl = gk + kChunk;
+  int32_t* gr = gl + kChunk;
+  int32_t* gc = gr + kChunk;
   __shared__ int32_t cnt[kMaxClasses];
   __shared__ uint64_t s_bump;
   __shared__ int s_err;
@@ -214,15 +219,20 @@ __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G
   int guarantee = st->led.guarantee;
   for (int g0 = 0; g0 < G; g0 += kChunk) {
     const int gn = min(kChunk, G - g0);
+    for (int x = tid; x < gn; x += kCommitThreads) {  // parallel preload: no global loads below
+      const GateDesc& gd = desc[g0 + x];
+      gk[x] = gd.k; gl[x] = gd.l; gr[x] = gd.r; gc[x] = gd.capped; gdl[x] = gd.dlogE;
+    }
+    __syncthreads();
     if (tid == 0) {
       for (int x = 0; x < gn; ++x) {
-        const GateDesc& gd = desc[g0 + x];
         ordv[x] = -1;
-        if (gd.k <= 0 || s_err) { plan[3 * x] = plan[3 * x + 1] = plan[3 * x + 2] = 0; continue; }
-        logE += gd.dlogE;
+        const int kk = gk[x];
+        if (kk <= 0 || s_err) { plan[3 * x] = plan[3 * x + 1] = plan[3 * x + 2] = 0; continue; }
+        logE += gdl[x];
         ordv[x] = j++;
-        if (gd.capped) guarantee = 0;
-        const uint64_t bytes[3] = {(uint64_t)gd.l * d * gd.k * 8, (uint64_t)gd.k * d * gd.r * 8, (uint64_t)gd.k * 4};
+        if (gc[x]) guarantee = 0;
+        const uint64_t bytes[3] = {(uint64_t)gl[x] * d * kk * 8, (uint64_t)kk * d * gr[x] * 8, (uint64_t)kk * 4};
         for (int q = 0; q < 3; ++q) {
           int c = size_class(bytes[q]);
           pcls[3 * x + q] = c;
@@ -368,7 +378,8 @@ void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record*
     k_select_parallel<<<(G + 7) / 8, 256, 0, s>>>(d_desc, G, slab, st);
   else
     k_select_sequential<<<1, 32, 0, s>>>(d_desc, G, slab, st);
-  const size_t smem = (size_t)3 * kChunk * 8 + (size_t)3 * kChunk * 4 + (size_t)kChunk * 8;
+  const size_t smem = (size_t)3 * kChunk * 8 + (size_t)3 * kChunk * 4 + (size_t)kChunk * 8 + (size_t)kChunk * 8 +
+                      (size_t)4 * kChunk * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
