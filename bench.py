@@ -62,6 +62,22 @@ def update_flops(chi, sweeps, k):
     return contract + svd_flops(m, n, sweeps) + 8.0 * m * n * k
 
 
+# ------------------------------------------------------------------------------ multi-rank
+def rank_seed_range(rank, count):
+    """Each rank runs its own `count` config-2 updates (weak scaling, no data-path collective):
+    seeds b in [rank*count, (rank+1)*count)."""
+    return rank * count, (rank + 1) * count
+
+
+def max_over_ranks(value, device=None):
+    """Device-timed totals are reduced with MAX over ranks (the slowest rank defines the step)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -188,7 +204,7 @@ def main():
     chi, G = args.chi, args.count
     n = 2 * chi
     # ---- inputs: this rank's 4096 updates (seeds b = rank*G .. rank*G + G - 1)
-    left, right, gates = workloads.micro_chain_torch(chi, G, first=rank * G, device=dev)
+    left, right, gates = workloads.micro_chain_torch(chi, G, first=rank_seed_range(rank, G)[0], device=dev)
     site_bytes = (left.numel() + right.numel()) * 8
     ws_bytes = G * (3 * n * n * 8 + 64 * n + 4096) + 2 * G * (chi * 2 * n * 8) * 2
     slab_bytes = int(1.25 * (2 * site_bytes + ws_bytes)) + (256 << 20)
@@ -230,9 +246,7 @@ def main():
     sweeps = np.array([mps.mps_last_sweeps(g) for g in range(G)])
     ks = np.array([r["chi_after"] for r in mps.mps_truncation_log()[-G:]])
     if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms, dev)
     ms_step = total_ms / args.steps
     value = world * G / (ms_step / 1e3)
 

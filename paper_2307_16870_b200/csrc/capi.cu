@@ -420,13 +420,18 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     gd.r = h->chr[i + 1];
     gd.m = gd.l * d;
     gd.n = d * gd.r;
-    gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : 1;
-    gd.n_pad = gd.regime == 0 ? gd.n : (int)align_up(gd.n, 32);
+    // SVD regime: 0 small (theta + V in one CTA), 2 medium (theta in one CTA, V replayed from a
+    // rotation log), 1 large (blocked, HBM-resident)
+    gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
+    gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 32);
+    gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
+    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16 : 0;
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
     const int kmn = std::min(gd.m, gd.n);
     p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
-           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) + align_up((size_t)kmn * kmn * 8);
+           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) + align_up((size_t)kmn * kmn * 8) +
+           align_up(logb);
     int kmax = std::min(gd.m, gd.n);
     if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);
     p.reserve = ((size_t)1 << size_class((uint64_t)gd.l * d * kmax * 8)) +
@@ -481,7 +486,13 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
     std::vector<int32_t> cpre(Gw + 1, 0), rpre(Gw + 1, 0), gpre(Gw + 1, 0), apre(Gw + 1, 0), small, large;
     std::vector<GateDesc> hd(Gw);
-    size_t smem_small = 0;
+    // small / medium buckets by lane-group size GT (one launch per bucket); `small` holds them
+    // back to back, [bstart, bend) per bucket
+    struct Bucket {
+      int regime, gt, begin, end, threads, tile_rows;
+      size_t smem, smem2;
+    };
+    std::vector<Bucket> buckets;
     for (int x = 0; x < Gw; ++x) {
       Plan& p = plan[g0 + x];
       GateDesc gd = p.gd;
@@ -495,16 +506,40 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
       gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
       const size_t kmn = (size_t)std::min(gd.m, gd.n);
       gd.ws_E = (int64_t)take(kmn * kmn * 8);
+      gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16) : 0;
       hd[x] = gd;
       cpre[x + 1] = cpre[x] + p.ctiles;
       rpre[x + 1] = rpre[x] + p.rtiles;
       gpre[x + 1] = gpre[x] + p.gtiles;
       apre[x + 1] = apre[x] + p.atiles;
-      if (gd.regime == 0) {
-        small.push_back(x);
-        smem_small = std::max(smem_small, svd_small_smem(gd.m, gd.n));
-      } else {
-        large.push_back(x);
+      if (gd.regime == 1) large.push_back(x);
+    }
+    for (int reg : {0, 2}) {
+      for (int gt : {4, 8, 16, 32}) {
+        Bucket b{reg, gt, (int)small.size(), 0, 64, 64, 0, 0};
+        int maxn = 2;
+        for (int x = 0; x < Gw; ++x) {
+          const GateDesc& gd = hd[x];
+          if (gd.regime != reg) continue;
+          const int g_gt = std::min(small_group(gd.m), std::max(4, 2048 / gd.n));
+          if (g_gt != gt) continue;
+          small.push_back(x);
+          maxn = std::max(maxn, gd.n);
+          if (reg == 0) {
+            b.smem = std::max(b.smem, svd_small_smem(gd.m, gd.n));
+          } else {
+            const int tr = vrep_tile_rows(gd.m, gd.n);
+            b.tile_rows = std::min(b.tile_rows, tr);
+            b.smem = std::max(b.smem, svd_theta_smem(gd.m, gd.n));
+          }
+        }
+        b.end = (int)small.size();
+        if (b.end == b.begin) continue;
+        if (reg == 2) {
+          for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
+        }
+        b.threads = (int)std::min<size_t>(1024, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
+        buckets.push_back(b);
       }
     }
     if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
@@ -539,7 +574,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     Record* d_rec = reinterpret_cast<Record*>(h->slab + o_rec);
 
     const bool prof = h->profiling;
-    bool ran[5] = {true, !small.empty(), !large.empty(), true, true};
+    bool ran[5] = {true, !buckets.empty(), !large.empty(), true, true};
     if (prof) CK(cudaEventRecord(h->ev[0], h->s));
     // a1 contract (all gates of the wave)
     launch_contract(d_desc, d_cpre, Gw, cpre[Gw], d, h->slab, h->dst, d_us, h->s);
@@ -547,10 +582,17 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     CKL("contract");
     if (prof) CK(cudaEventRecord(h->ev[1], h->s));
     // a2 + a3 SVD, small regime: one CTA per theta
-    if (!small.empty()) {
-      launch_svd_small(d_desc, d_small, (int)small.size(), smem_small, h->cfg.max_sweeps, h->slab, h->dst, h->s);
-      ++h->launches;
-      CKL("svd_small");
+    for (const Bucket& b : buckets) {
+      if (b.regime == 0) {
+        launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.threads,
+                         h->slab, h->dst, h->s);
+        ++h->launches;
+      } else {
+        launch_svd_medium(d_desc, d_small + b.begin, b.end - b.begin, b.smem, b.smem2, b.tile_rows, h->cfg.max_sweeps,
+                          b.gt, b.threads, h->slab, h->dst, h->s);
+        h->launches += 2;
+      }
+      CKL("svd_small/medium");
     }
     if (prof) CK(cudaEventRecord(h->ev[2], h->s));
     // a2 + a3 SVD, large regime: blocked Jacobi

@@ -1,0 +1,114 @@
+// jacobi_common.cuh -- pieces shared by the shared-memory Jacobi kernels (svd_small.cu,
+// svd_medium.cu): the circle-method pairing, the 2x2 rotation, and the CTA epilogue
+// (Rayleigh-quotient sigma^2 in FP64, V to global, bitonic sort, FP64 tails).
+#pragma once
+#include "eamps_internal.cuh"
+#include "sort_tails.cuh"
+
+namespace eamps {
+
+// pair (p, q) of slot i in round rnd of the circle method over n (even) players
+__device__ __forceinline__ void circle_pair_n(int i, int rnd, int n, int& p, int& q) {
+  auto pos = [&](int j) { return j == 0 ? 0 : ((j - 1 + rnd) % (n - 1)) + 1; };
+  p = pos(i);
+  q = pos(n - 1 - i);
+}
+
+struct Rot {
+  float c, s, er, ei;  // (a_p, a_q) <- (c a_p - s conj(e) a_q, s a_p + c conj(e) a_q)
+};
+
+// The 2x2 one-sided Jacobi rotation from alpha = |a_p|^2, beta = |a_q|^2, gamma = a_p^H a_q:
+// e = gamma/|gamma|, zeta = (beta - alpha)/(2|gamma|), t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+// c = 1/sqrt(1 + t^2), s = c t (SURVEY §8(c) algorithm item 3). Returns false (identity) when the
+// pair is already orthogonal to tol or a column is below the rounding floor.
+__device__ __forceinline__ bool jacobi_rot(float al, float be, float gr, float gi, float skip, float tol, Rot& R) {
+  R.c = 1.f; R.s = 0.f; R.er = 1.f; R.ei = 0.f;
+  if (fminf(al, be) <= skip) return false;
+  const float g = sqrtf(gr * gr + gi * gi);
+  if (!(g > tol * sqrtf(al) * sqrtf(be))) return false;
+  R.er = gr / g;
+  R.ei = gi / g;
+  const float zeta = (be - al) / (2.f * g);
+  const float az = fabsf(zeta);
+  const float hyp = az > 1.f ? az * sqrtf(1.f + 1.f / (az * az)) : sqrtf(1.f + az * az);
+  const float t = (zeta >= 0.f ? 1.f : -1.f) / (az + hyp);
+  R.c = rsqrtf(1.f + t * t);
+  R.s = R.c * t;
+  return true;
+}
+
+__device__ __forceinline__ void apply_rot(float2& x, float2& y, const Rot& R) {
+  const float2 ey = make_float2(R.er * y.x + R.ei * y.y, R.er * y.y - R.ei * y.x);  // conj(e) y
+  const float2 nx = make_float2(R.c * x.x - R.s * ey.x, R.c * x.y - R.s * ey.y);
+  const float2 ny = make_float2(R.s * x.x + R.c * ey.x, R.s * x.y + R.c * ey.y);
+  x = nx;
+  y = ny;
+}
+
+__device__ __forceinline__ double warp_sum_d32(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ inline void jacobi_finish(const GateDesc& gd, uint8_t* slab, const float2* V, double* s2, int32_t* six,
+                                     double* part);
+
+// Epilogue: A (m x n, ld m, shared) must hold the ORIGINAL theta, V (n x n, ld n, shared) the
+// accumulated rotations. sigma_j^2 = ||theta v_j||^2 / ||v_j||^2 with FP64 products of the FP32
+// inputs (second order in V's rounding); V -> global (ld n); sort (sigma^2,
+// index) descending; tails T in FP64. `s2`/`six` are npow2-long shared scratch, `part` has
+// blockDim.x doubles.
+__device__ inline void jacobi_epilogue(const GateDesc& gd, uint8_t* slab, DevState* st, const float2* A,
+                                       const float2* V, double* s2, int32_t* six, double* part) {
+  const int m = gd.m, n = gd.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int npow2 = 1;
+  while (npow2 < n) npow2 <<= 1;
+  for (int j = warp; j < n; j += nw) {
+    const float2* vj = V + (size_t)j * n;
+    double num = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      double wr = 0.0, wi = 0.0;
+      for (int k = 0; k < n; ++k) {
+        float2 a = A[(size_t)k * m + i];
+        float2 v = vj[k];
+        wr = fma((double)a.x, (double)v.x, fma(-(double)a.y, (double)v.y, wr));
+        wi = fma((double)a.x, (double)v.y, fma((double)a.y, (double)v.x, wi));
+      }
+      num += wr * wr + wi * wi;
+    }
+    double den = 0.0;
+    for (int k = lane; k < n; k += 32) den += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
+    num = warp_sum_d32(num);
+    den = warp_sum_d32(den);
+    if (lane == 0) {
+      double v = den > 0.0 ? num / den : 0.0;
+      if (!isfinite(v)) atomicCAS(&st->led.error, 0, -7 /* MPS_E_NUMERIC */);
+      s2[j] = v;
+    }
+  }
+  __syncthreads();
+  jacobi_finish(gd, slab, V, s2, six, part);
+}
+
+// Shared tail of the epilogues: s2[j] = sigma_j^2 (j < n) already in shared memory.
+__device__ inline void jacobi_finish(const GateDesc& gd, uint8_t* slab, const float2* V, double* s2, int32_t* six,
+                                     double* part) {
+  const int n = gd.n, tid = threadIdx.x;
+  int npow2 = 1;
+  while (npow2 < n) npow2 <<= 1;
+  for (int j = tid; j < n; j += blockDim.x) six[j] = j;
+  for (int j = n + tid; j < npow2; j += blockDim.x) { s2[j] = -1.0; six[j] = j; }
+  float2* gV = reinterpret_cast<float2*>(slab + gd.ws_V);
+  for (int x = tid; x < n * n; x += blockDim.x) gV[x] = V[x];
+  __syncthreads();
+  cta_sort_desc(s2, six, npow2);
+  double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  int32_t* gP = reinterpret_cast<int32_t*>(slab + gd.ws_pi);
+  for (int j = tid; j < n; j += blockDim.x) { gS[j] = s2[j]; gP[j] = six[j]; }
+  cta_tails(s2, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
+}
+
+}  // namespace eamps

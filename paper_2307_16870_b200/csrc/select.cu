@@ -23,6 +23,7 @@
 // shared-memory counters only (no global loads on the sequential path); all threads then resolve
 // the stack pops and write the site tables in parallel.
 #include "eamps_internal.cuh"
+#include "pool.cuh"
 
 namespace eamps {
 
@@ -157,135 +158,187 @@ __global__ void k_select_sequential(GateDesc* desc, int G, const uint8_t* slab, 
 }
 
 constexpr int kCommitThreads = 1024;
-constexpr int kChunk = 2048;  // gates planned per shared-memory chunk
+constexpr int kChunk = 1024;  // gates per shared-memory chunk (3 pool requests each)
+constexpr int kReq = 3 * kChunk;
+
+struct CommitSmem {
+  int32_t cls[kReq], rank[kReq];
+  uint64_t val[kReq], tmp[kReq];
+  double gdl[kChunk];
+  int32_t gk[kChunk], gl[kChunk], gr[kChunk], gc[kChunk], ord[kChunk];
+  int32_t cnt[kMaxClasses], present[kMaxClasses], iws[32];
+  uint64_t uws[32];
+  uint64_t bump;
+  int err;
+};
+
+__device__ inline PoolBatch make_batch(CommitSmem& S) {
+  return PoolBatch{S.cls, S.rank, S.val, S.tmp, S.cnt, S.iws, S.uws};
+}
 
 __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G, uint8_t* slab, DevState* st,
                                                             Record* rec) {
   extern __shared__ __align__(16) uint8_t sm[];
-  // chunk scratch: plan[3*kChunk] (uint64: offset, or stack slot with the top bit set), cls[3*kChunk]
-  uint64_t* plan = reinterpret_cast<uint64_t*>(sm);
-  int32_t* pcls = reinterpret_cast<int32_t*>(plan + 3 * kChunk);
-  int64_t* ordv = reinterpret_cast<int64_t*>(pcls + 3 * kChunk);  // ledger index per gate of the chunk
-  double* gdl = reinterpret_cast<double*>(ordv + kChunk);             // per-gate fields, preloaded in parallel
-  int32_t* gk = reinterpret_cast<int32_t*>(gdl + kChunk);
-  int32_t* gl = gk + kChunk;
-  int32_t* gr = gl + kChunk;
-  int32_t* gc = gr + kChunk;
-  __shared__ int32_t cnt[kMaxClasses];
-  __shared__ uint64_t s_bump;
-  __shared__ int s_err;
+  CommitSmem& S = *reinterpret_cast<CommitSmem*>(sm);
+  PoolBatch B = make_batch(S);
   const int tid = threadIdx.x;
   DevPool& P = st->pool;
-  int64_t* stk = reinterpret_cast<int64_t*>(slab + P.stack_off);
   int64_t* pend = reinterpret_cast<int64_t*>(slab + P.pending_off);
   SiteEntry* sites = reinterpret_cast<SiteEntry*>(slab + st->sites_off);
   BondEntry* bonds = reinterpret_cast<BondEntry*>(slab + st->bonds_off);
   const int d = st->d;
-  const int64_t cap = P.stack_cap;
-  const uint64_t ceiling = P.ceiling;
-  if (tid < kMaxClasses) cnt[tid] = P.count[tid];
-  if (tid == 0) { s_bump = P.bump; s_err = st->led.error; }
+  if (tid < kMaxClasses) S.cnt[tid] = P.count[tid];
+  if (tid == 0) { S.bump = P.bump; S.err = st->led.error; }
   __syncthreads();
 
-  // A. release the previous wave's deferred frees onto the class stacks
+  // A. release the previous wave's deferred frees onto the class stacks (canonical order)
   const int64_t npend = P.npending;
-  for (int64_t c0 = 0; c0 < npend; c0 += 3 * kChunk) {
-    const int64_t cn = min((int64_t)3 * kChunk, npend - c0);
-    for (int64_t x = tid; x < cn; x += kCommitThreads) {
-      plan[x] = (uint64_t)pend[2 * (c0 + x)];
-      pcls[x] = (int32_t)pend[2 * (c0 + x) + 1];
+  for (int64_t c0 = 0; c0 < npend; c0 += kReq) {
+    const int cn = (int)min((int64_t)kReq, npend - c0);
+    for (int i = tid; i < cn; i += kCommitThreads) {
+      S.val[i] = (uint64_t)pend[2 * (c0 + i)];
+      S.cls[i] = (int32_t)pend[2 * (c0 + i) + 1];
     }
     __syncthreads();
-    if (tid == 0) {
-      for (int64_t x = 0; x < cn; ++x) {
-        if (!plan[x]) continue;
-        int c = pcls[x];
-        if (cnt[c] >= cap) { s_err = -3; plan[x] = 0; continue; }
-        pcls[x] = c | (cnt[c]++ << 6);  // class (6 bits) + stack slot
-      }
-    }
-    __syncthreads();
-    for (int64_t x = tid; x < cn; x += kCommitThreads) {
-      if (!plan[x]) continue;
-      int c = pcls[x] & 63, slot = pcls[x] >> 6;
-      stk[(int64_t)c * cap + slot] = (int64_t)plan[x];
-    }
-    __syncthreads();
+    if (!pool_batch_free(B, cn, slab, P, S.present) && tid == 0) S.err = -3;
   }
+  __syncthreads();
 
-  // B/C. per chunk of gates: sequential plan (ledger + allocation) then parallel resolve
-  double logE = st->led.logE;
-  int64_t j = st->led.j;
+  // B. per chunk of gates: ledger, batched allocation, table updates, records
+  double logE = st->led.logE;   // meaningful in thread 0 only
+  int64_t j0 = st->led.j;
   int guarantee = st->led.guarantee;
   for (int g0 = 0; g0 < G; g0 += kChunk) {
     const int gn = min(kChunk, G - g0);
-    for (int x = tid; x < gn; x += kCommitThreads) {  // parallel preload: no global loads below
-      const GateDesc& gd = desc[g0 + x];
-      gk[x] = gd.k; gl[x] = gd.l; gr[x] = gd.r; gc[x] = gd.capped; gdl[x] = gd.dlogE;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int x = 0; x < gn; ++x) {
-        ordv[x] = -1;
-        const int kk = gk[x];
-        if (kk <= 0 || s_err) { plan[3 * x] = plan[3 * x + 1] = plan[3 * x + 2] = 0; continue; }
-        logE += gdl[x];
-        ordv[x] = j++;
-        if (gc[x]) guarantee = 0;
-        const uint64_t bytes[3] = {(uint64_t)gl[x] * d * kk * 8, (uint64_t)kk * d * gr[x] * 8, (uint64_t)kk * 4};
-        for (int q = 0; q < 3; ++q) {
-          int c = size_class(bytes[q]);
-          pcls[3 * x + q] = c;
-          if (cnt[c] > 0) {
-            plan[3 * x + q] = (1ull << 63) | (uint64_t)(--cnt[c]);
-          } else {
-            uint64_t o = (s_bump + 255ull) & ~255ull;
-            if (o + (1ull << c) > ceiling) { s_err = -3; plan[3 * x + q] = 0; continue; }
-            s_bump = o + (1ull << c);
-            plan[3 * x + q] = o;
-          }
-        }
-      }
-    }
-    __syncthreads();
     for (int x = tid; x < gn; x += kCommitThreads) {
-      GateDesc& gd = desc[g0 + x];
-      const int i = gd.site;
-      uint64_t off[3] = {0, 0, 0};
-      bool ok = ordv[x] >= 0;
-      for (int q = 0; q < 3 && ok; ++q) {
-        uint64_t p = plan[3 * x + q];
-        if (!p) { ok = false; break; }
-        off[q] = (p >> 63) ? (uint64_t)stk[(int64_t)pcls[3 * x + q] * cap + (int64_t)(p & ~(1ull << 63))] : p;
+      const GateDesc& gd = desc[g0 + x];
+      S.gk[x] = gd.k; S.gl[x] = gd.l; S.gr[x] = gd.r; S.gc[x] = gd.capped; S.gdl[x] = gd.dlogE;
+    }
+    __syncthreads();
+    const bool err0 = S.err != 0;
+    // ledger indices = exclusive count of valid gates (canonical order)
+    {
+      const int per = (gn + kCommitThreads - 1) / kCommitThreads;
+      const int b = tid * per, e = min(gn, b + per);
+      int32_t cnt = 0;
+      for (int x = b; x < e; ++x) cnt += (S.gk[x] > 0 && !err0);
+      int32_t tot;
+      int32_t pre = cta_exclusive_scan<int32_t>(cnt, S.iws, &tot);
+      for (int x = b; x < e; ++x) S.ord[x] = (S.gk[x] > 0 && !err0) ? pre++ : -1;
+      if (tid == 0) {
+        for (int x = 0; x < gn; ++x)
+          if (S.ord[x] >= 0) {  // sequential in canonical order: the same summation as the sequential selector
+            logE += S.gdl[x];
+            if (S.gc[x]) guarantee = 0;
+          }
       }
-      const int64_t pb = 3 * (int64_t)(g0 + x);
-      if (!ok) {
-        gd.k = 0;
-        pend[2 * pb] = pend[2 * pb + 2] = pend[2 * pb + 4] = 0;
-        continue;
+      __syncthreads();
+      // requests: new B_i, new B_{i+1}, new lambda_i
+      for (int x = tid; x < gn; x += kCommitThreads) {
+        const int k = S.gk[x];
+        const bool v = S.ord[x] >= 0;
+        S.val[3 * x] = v ? (uint64_t)S.gl[x] * d * k * 8 : 0;
+        S.val[3 * x + 1] = v ? (uint64_t)k * d * S.gr[x] * 8 : 0;
+        S.val[3 * x + 2] = v ? (uint64_t)k * 4 : 0;
       }
-      // deferred frees of the old blocks
-      pend[2 * pb] = sites[i].off; pend[2 * pb + 1] = sites[i].cls;
-      pend[2 * pb + 2] = sites[i + 1].off; pend[2 * pb + 3] = sites[i + 1].cls;
-      pend[2 * pb + 4] = bonds[i + 1].off; pend[2 * pb + 5] = bonds[i + 1].cls;
-      sites[i].off = (int64_t)off[0]; sites[i].chr = gd.k; sites[i].cls = pcls[3 * x];
-      sites[i + 1].off = (int64_t)off[1]; sites[i + 1].chl = gd.k; sites[i + 1].cls = pcls[3 * x + 1];
-      bonds[i + 1].off = (int64_t)off[2]; bonds[i + 1].len = gd.k; bonds[i + 1].cls = pcls[3 * x + 2];
-      gd.off_newL = (int64_t)off[0]; gd.off_newR = (int64_t)off[1]; gd.off_newLam = (int64_t)off[2];
-      Record& R = rec[g0 + x];
-      R.gate_index = ordv[x]; R.bond = i; R.chi_before = gd.mid; R.chi_after = gd.k; R.capped = gd.capped;
-      R.target_f = gd.t; R.achieved_f = gd.f; R.discarded_weight = gd.disc;
+      __syncthreads();
+      const bool ok = pool_batch_alloc(B, 3 * gn, slab, P, &S.bump, P.ceiling, S.present);
+      if (!ok && tid == 0) S.err = -3;
+      __syncthreads();
+      for (int x = tid; x < gn; x += kCommitThreads) {
+        GateDesc& gd = desc[g0 + x];
+        const int64_t pb = 3 * (int64_t)(g0 + x);
+        if (!ok || S.ord[x] < 0) {
+          gd.k = 0;
+          pend[2 * pb] = pend[2 * pb + 2] = pend[2 * pb + 4] = 0;
+          continue;
+        }
+        const int i = gd.site, k = S.gk[x];
+        // deferred frees of the old blocks (released at the next commit)
+        pend[2 * pb] = sites[i].off; pend[2 * pb + 1] = sites[i].cls;
+        pend[2 * pb + 2] = sites[i + 1].off; pend[2 * pb + 3] = sites[i + 1].cls;
+        pend[2 * pb + 4] = bonds[i + 1].off; pend[2 * pb + 5] = bonds[i + 1].cls;
+        const uint64_t oL = S.val[3 * x], oR = S.val[3 * x + 1], oLam = S.val[3 * x + 2];
+        sites[i].off = (int64_t)oL; sites[i].chr = k; sites[i].cls = S.cls[3 * x];
+        sites[i + 1].off = (int64_t)oR; sites[i + 1].chl = k; sites[i + 1].cls = S.cls[3 * x + 1];
+        bonds[i + 1].off = (int64_t)oLam; bonds[i + 1].len = k; bonds[i + 1].cls = S.cls[3 * x + 2];
+        gd.off_newL = (int64_t)oL; gd.off_newR = (int64_t)oR; gd.off_newLam = (int64_t)oLam;
+        Record& R = rec[g0 + x];
+        R.gate_index = j0 + S.ord[x]; R.bond = i; R.chi_before = gd.mid; R.chi_after = k; R.capped = gd.capped;
+        R.target_f = gd.t; R.achieved_f = gd.f; R.discarded_weight = gd.disc;
+      }
+      j0 += tot;
+      __syncthreads();
+    }
+  }
+  if (tid < kMaxClasses) P.count[tid] = S.cnt[tid];
+  if (tid == 0) {
+    P.bump = S.bump;
+    P.npending = 3 * (int64_t)G;
+    st->led.logE = logE;
+    st->led.j = j0;
+    st->led.guarantee = guarantee;
+    if (S.err && !st->led.error) st->led.error = S.err;
+  }
+}
+
+// Bulk import: free the replaced blocks, allocate the new ones (one batch each), fill tables.
+__global__ void __launch_bounds__(kCommitThreads) k_import_batch(uint8_t* slab, DevState* st, ImportEntry* ent,
+                                                                  int count) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  CommitSmem& S = *reinterpret_cast<CommitSmem*>(sm);
+  PoolBatch B = make_batch(S);
+  const int tid = threadIdx.x;
+  DevPool& P = st->pool;
+  SiteEntry* sites = reinterpret_cast<SiteEntry*>(slab + st->sites_off);
+  BondEntry* bonds = reinterpret_cast<BondEntry*>(slab + st->bonds_off);
+  const int d = st->d;
+  if (tid < kMaxClasses) S.cnt[tid] = P.count[tid];
+  if (tid == 0) { S.bump = P.bump; S.err = st->led.error; }
+  __syncthreads();
+  for (int e0 = 0; e0 < count; e0 += kChunk) {
+    const int en = min(kChunk, count - e0);
+    // frees of the replaced site blocks and reset lambdas
+    for (int x = tid; x < en; x += kCommitThreads) {
+      const ImportEntry& e = ent[e0 + x];
+      S.val[3 * x] = (uint64_t)sites[e.site].off; S.cls[3 * x] = sites[e.site].cls;
+      S.val[3 * x + 1] = e.resetL > 0 ? (uint64_t)bonds[e.site].off : 0; S.cls[3 * x + 1] = bonds[e.site].cls;
+      S.val[3 * x + 2] = e.resetR > 0 ? (uint64_t)bonds[e.site + 1].off : 0; S.cls[3 * x + 2] = bonds[e.site + 1].cls;
+    }
+    __syncthreads();
+    if (!pool_batch_free(B, 3 * en, slab, P, S.present) && tid == 0) S.err = -3;
+    for (int x = tid; x < en; x += kCommitThreads) {
+      const ImportEntry& e = ent[e0 + x];
+      S.val[3 * x] = (uint64_t)e.chl * d * e.chr * 8;
+      S.val[3 * x + 1] = e.resetL > 0 ? (uint64_t)e.resetL * 4 : 0;
+      S.val[3 * x + 2] = e.resetR > 0 ? (uint64_t)e.resetR * 4 : 0;
+    }
+    __syncthreads();
+    const bool ok = pool_batch_alloc(B, 3 * en, slab, P, &S.bump, P.ceiling, S.present);
+    if (!ok) {
+      if (tid == 0) S.err = -3;
+      break;
+    }
+    for (int x = tid; x < en; x += kCommitThreads) {
+      ImportEntry& e = ent[e0 + x];
+      const int i = e.site;
+      sites[i].off = (int64_t)S.val[3 * x]; sites[i].chl = e.chl; sites[i].chr = e.chr; sites[i].cls = S.cls[3 * x];
+      e.dst_off = (int64_t)S.val[3 * x];
+      if (e.resetL > 0) {
+        bonds[i].off = (int64_t)S.val[3 * x + 1]; bonds[i].len = e.resetL; bonds[i].cls = S.cls[3 * x + 1];
+        e.lamL_off = (int64_t)S.val[3 * x + 1];
+      }
+      if (e.resetR > 0) {
+        bonds[i + 1].off = (int64_t)S.val[3 * x + 2]; bonds[i + 1].len = e.resetR; bonds[i + 1].cls = S.cls[3 * x + 2];
+        e.lamR_off = (int64_t)S.val[3 * x + 2];
+      }
     }
     __syncthreads();
   }
-  if (tid < kMaxClasses) P.count[tid] = cnt[tid];
+  if (tid < kMaxClasses) P.count[tid] = S.cnt[tid];
   if (tid == 0) {
-    P.bump = s_bump;
-    P.npending = 3 * (int64_t)G;
-    st->led.logE = logE;
-    st->led.j = j;
-    st->led.guarantee = guarantee;
-    if (s_err && !st->led.error) st->led.error = s_err;
+    P.bump = S.bump;
+    if (S.err && !st->led.error) st->led.error = S.err;
   }
 }
 
@@ -324,32 +377,6 @@ __global__ void k_gate1(uint8_t* slab, DevState* st, int site, const float2* U) 
   }
 }
 
-__global__ void k_import_alloc(uint8_t* slab, DevState* st, ImportEntry* ent, int count) {
-  SiteEntry* sites = reinterpret_cast<SiteEntry*>(slab + st->sites_off);
-  BondEntry* bonds = reinterpret_cast<BondEntry*>(slab + st->bonds_off);
-  const int d = st->d;
-  for (int x = 0; x < count; ++x) {
-    ImportEntry& e = ent[x];
-    const int i = e.site;
-    pool_free_now(slab, st, (uint64_t)sites[i].off, sites[i].cls);
-    int c;
-    uint64_t o = pool_alloc(slab, st, (uint64_t)e.chl * d * e.chr * 8, &c);
-    if (!o) return;
-    sites[i].off = (int64_t)o; sites[i].chl = e.chl; sites[i].chr = e.chr; sites[i].cls = c;
-    e.dst_off = (int64_t)o;
-    for (int side = 0; side < 2; ++side) {
-      const int len = side == 0 ? e.resetL : e.resetR;
-      const int b = side == 0 ? i : i + 1;  // bond index + 1
-      if (len <= 0) continue;
-      pool_free_now(slab, st, (uint64_t)bonds[b].off, bonds[b].cls);
-      uint64_t ol = pool_alloc(slab, st, (uint64_t)len * 4, &c);
-      if (!ol) return;
-      bonds[b].off = (int64_t)ol; bonds[b].len = len; bonds[b].cls = c;
-      if (side == 0) e.lamL_off = (int64_t)ol; else e.lamR_off = (int64_t)ol;
-    }
-  }
-}
-
 __global__ void k_import_scatter(uint8_t* slab, const ImportEntry* ent, const float2* src, int d) {
   const ImportEntry e = ent[blockIdx.x];
   if (!e.dst_off) return;
@@ -368,7 +395,12 @@ __global__ void k_import_scatter(uint8_t* slab, const ImportEntry* ent, const fl
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s) {
   if (count <= 0) return;
-  k_import_alloc<<<1, 1, 0, s>>>(slab, st, d_ent, count);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_import_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CommitSmem));
+    attr = true;
+  }
+  k_import_batch<<<1, kCommitThreads, sizeof(CommitSmem), s>>>(slab, st, d_ent, count);
   k_import_scatter<<<count, 256, 0, s>>>(slab, d_ent, src, d);
 }
 
@@ -378,14 +410,12 @@ void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record*
     k_select_parallel<<<(G + 7) / 8, 256, 0, s>>>(d_desc, G, slab, st);
   else
     k_select_sequential<<<1, 32, 0, s>>>(d_desc, G, slab, st);
-  const size_t smem = (size_t)3 * kChunk * 8 + (size_t)3 * kChunk * 4 + (size_t)kChunk * 8 + (size_t)kChunk * 8 +
-                      (size_t)4 * kChunk * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CommitSmem));
     attr = true;
   }
-  k_commit<<<1, kCommitThreads, smem, s>>>(d_desc, G, slab, st, d_rec);
+  k_commit<<<1, kCommitThreads, sizeof(CommitSmem), s>>>(d_desc, G, slab, st, d_rec);
 }
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s) {
   k_pool_alloc<<<1, 1, 0, s>>>(slab, st, bytes, d_out);

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_block_round(const GateDesc* __restrict_
 
   // inner FP64 Hermitian Jacobi on G, accumulating W
   const int grp = tid >> 4, t16 = tid & 15;
-  for (int isw = 0; isw < 12; ++isw) {
+  for (int isw = 0; isw < 3; ++isw) {  // partial diagonalisation: the outer sweeps re-check fresh Grams
     if (tid == 0) s_inner = 0;
     __syncthreads();
     for (int rr = 0; rr < PW - 1; ++rr) {
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_block_round(const GateDesc* __restrict_
         double2 gm = Gs[p][q];
         double g = sqrt(gm.x * gm.x + gm.y * gm.y);
         double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
-        if (fmin(al, be) > skip && g > 1e-15 * sqrt(al * be)) {
+        if (fmin(al, be) > skip && g > 1e-12 * sqrt(al * be)) {
           er = gm.x / g; ei = gm.y / g;
           double zeta = (be - al) / (2.0 * g);
           double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
