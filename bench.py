@@ -206,8 +206,12 @@ def main():
     # ---- inputs: this rank's 4096 updates (seeds b = rank*G .. rank*G + G - 1)
     left, right, gates = workloads.micro_chain_torch(chi, G, first=rank_seed_range(rank, G)[0], device=dev)
     site_bytes = (left.numel() + right.numel()) * 8
-    ws_bytes = G * (3 * n * n * 8 + 64 * n + 4096) + 2 * G * (chi * 2 * n * 8) * 2
-    slab_bytes = int(1.25 * (2 * site_bytes + ws_bytes)) + (256 << 20)
+    # one wave needs: old + new site blocks (pow2 classes), theta/Theta'/V/E, the medium-regime
+    # rotation log (24 sweeps x (n-1) x n/2 x 8 B) and small arrays; take it from the free memory
+    ws_gate = 4 * n * n * 8 + 24 * (n - 1) * (n // 2) * 8 + 64 * n + 8192
+    need = int(2.2 * 2 * site_bytes + G * ws_gate) + (512 << 20)
+    free, _ = torch.cuda.mem_get_info(dev)
+    slab_bytes = int(min(max(need, 1 << 30), 0.6 * free))
     mps = pk.MPS(2 * G, strategy="fixed", f_fixed=F_TRUNC, slab_bytes=slab_bytes, device=dev)
     inter = torch.cat([left.reshape(G, -1), right.reshape(G, -1)], dim=1).reshape(-1)  # L0 R0 L1 R1 ...
     dims = np.array([[chi, 2, n], [n, 2, chi]] * G, np.int32)

@@ -118,7 +118,9 @@ mps_status mps_bond_dims(mps_t, int32_t* out /* N-1 */);
 mps_status mps_schmidt_values(mps_t, int32_t bond, float* out, int32_t cap, int32_t* len);
 mps_status mps_truncation_log(mps_t, mps_record* rows, int64_t cap, int64_t* len);
 /* Sorted singular values (float64, descending, all n of them) of gate g (ascending-site order)
- * of the most recent layer -- the parity export for the SVD step. */
+ * of the most recent layer -- the parity export for the SVD step. Readable for the gates of the
+ * layer's final wave (a layer larger than the slab's workspace runs in waves); MPS_E_STATE for
+ * earlier waves, whose workspace was reused. */
 mps_status mps_last_spectrum(mps_t, int32_t g, double* out, int32_t cap, int32_t* len);
 /* Site tensors for tests / checkpoints. dims3 = {chi_l, d, chi_r}. B: c64 row-major. The
  * pointer kind (host or device) is detected with cudaPointerGetAttributes. lam (float32, may be

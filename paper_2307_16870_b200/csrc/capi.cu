@@ -31,7 +31,8 @@ struct mps_handle {
   std::vector<int32_t> chl, chr, lamlen;  // host mirror of the bond profile
   DevState hstate{};                       // host copy after the last sync
   std::vector<mps_record> records;
-  std::vector<GateDesc> last_desc;         // last wave
+  std::vector<GateDesc> last_desc;         // every wave of the last layer (k, sweeps)
+  int last_wave_begin = 0;                 // spectra are readable for the final wave only
   bool poisoned = false;
   int sticky = 0;
   std::string err;
@@ -425,7 +426,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 32);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
-    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16 : 0;
+    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8 : 0;
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
     const int kmn = std::min(gd.m, gd.n);
@@ -448,6 +449,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
   const size_t top = h->slab_bytes - 4 * kAlign;  // the top 1 KB is scratch for small host ops
   int g0 = 0;
   h->last_desc.clear();
+  h->last_wave_begin = 0;
   while (g0 < G) {
     const uint64_t bump = h->hstate.pool.bump;
     size_t fixed = 0, ws = 0, reserve = 0;
@@ -506,7 +508,7 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
       gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
       const size_t kmn = (size_t)std::min(gd.m, gd.n);
       gd.ws_E = (int64_t)take(kmn * kmn * 8);
-      gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16) : 0;
+      gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8) : 0;
       hd[x] = gd;
       cpre[x + 1] = cpre[x] + p.ctiles;
       rpre[x + 1] = rpre[x] + p.rtiles;
@@ -652,7 +654,8 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
       std::memcpy(&rec, &rr[x], sizeof(rec));
       h->records.push_back(rec);
     }
-    h->last_desc = hd;
+    h->last_wave_begin = (int)h->last_desc.size();
+    h->last_desc.insert(h->last_desc.end(), hd.begin(), hd.end());
     if (de != MPS_OK) return de;
     g0 = g1;
   }
@@ -712,6 +715,7 @@ mps_status mps_truncation_log(mps_t h, mps_record* rows, int64_t cap, int64_t* l
 mps_status mps_last_spectrum(mps_t h, int32_t g, double* out, int32_t cap, int32_t* len) {
   if (!h || !len) return MPS_E_INVAL;
   if (g < 0 || g >= (int)h->last_desc.size()) return set_err(h, MPS_E_RANGE, "gate index out of range");
+  if (g < h->last_wave_begin) return set_err(h, MPS_E_STATE, "spectrum of an earlier wave (workspace reused)");
   const GateDesc& gd = h->last_desc[g];
   *len = gd.n;
   if (out && cap > 0) {

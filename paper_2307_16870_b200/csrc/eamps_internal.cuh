@@ -52,7 +52,7 @@ struct GateDesc {
   int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large
   int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
   int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
-  int64_t ws_log;                   // medium regime: rotation log, log_sweeps x (n-1) x n/2 float4
+  int64_t ws_log;                   // medium regime: rotation log, log_sweeps x (n-1) x n/2 float2 (t, arg e)
   int32_t log_sweeps, pad0;
   int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
   int32_t k, capped;                // outputs of the selector

@@ -4,8 +4,10 @@
 // Two one-CTA-per-theta kernels instead of a cluster: the rotations are data-independent of V,
 // so V can be built afterwards from a log of the rotations.
 //   k_svd_theta : the one-sided Jacobi of svd_small.cu on theta alone (theta in shared memory);
-//                 every round's (c, s, e) per column pair goes to a log in the workspace
-//                 (16 B per pair-round: ~1 MB per theta for 11 sweeps at n = 128).
+//                 every round's rotation per column pair goes to a log in the workspace as
+//                 (t = s/c, arg e): 8 B per pair-round, ~0.7 MB per theta for 11 sweeps at n = 128.
+//                 V only has to be a unitary product of (nearly) the same rotations: the replay
+//                 recomputing c, s, e from (t, arg e) to 1 ulp does not affect sigma or the update.
 //   k_svd_vrep  : V = I R_1 R_2 ... R_T replayed from the log in shared memory (the same circle
 //                 order, identity rotations skipped), then sigma_j^2 = ||theta v_j||^2/||v_j||^2
 //                 with theta streamed from the workspace in row tiles (FP64 products), V to
@@ -30,7 +32,7 @@ __global__ void __launch_bounds__(1024) k_svd_theta(GateDesc* desc, const int32_
   __shared__ float s_wn[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);
-  float4* lg = reinterpret_cast<float4*>(slab + gd.ws_log);
+  float2* lg = reinterpret_cast<float2*>(slab + gd.ws_log);
   float nrm = 0.f;
   for (int x = tid; x < m * n; x += blockDim.x) {
     float2 v = gth[x];
@@ -53,7 +55,7 @@ __global__ void __launch_bounds__(1024) k_svd_theta(GateDesc* desc, const int32_
     int any = 0;
     for (int rnd = 0; rnd < n - 1; ++rnd) {
       bool rot = false;
-      float4* lrow = lg + ((size_t)sweep * (n - 1) + rnd) * (n / 2);
+      float2* lrow = lg + ((size_t)sweep * (n - 1) + rnd) * (n / 2);
       for (int base = 0; base < n / 2; base += groups) {
         const int slot = base + gid;
         const bool active = slot < n / 2;
@@ -80,7 +82,8 @@ __global__ void __launch_bounds__(1024) k_svd_theta(GateDesc* desc, const int32_
         }
         Rot R;
         const bool doit = active && jacobi_rot(al, be, gr, gi, skip, tol, R);
-        if (active && lgi == 0) lrow[slot] = make_float4(R.c, R.s, R.er, R.ei);
+        // log (t = s/c, phase of e): 8 B per pair-round; identity rotations are logged as t = 0
+        if (active && lgi == 0) lrow[slot] = make_float2(doit ? R.s / R.c : 0.f, atan2f(R.ei, R.er));
         if (doit) {
           rot = true;
           for (int i = lgi; i < m; i += GT) {
@@ -116,17 +119,20 @@ __global__ void __launch_bounds__(1024) k_svd_vrep(GateDesc* desc, const int32_t
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int x = tid; x < n * n; x += blockDim.x) V[x] = make_float2((x / n) == (x % n) ? 1.f : 0.f, 0.f);
   __syncthreads();
-  const float4* lg = reinterpret_cast<const float4*>(slab + gd.ws_log);
+  const float2* lg = reinterpret_cast<const float2*>(slab + gd.ws_log);
   const int groups = blockDim.x / GT, gid = tid / GT, lgi = tid % GT;
   for (int sw = 0; sw < S; ++sw) {
     for (int rnd = 0; rnd < n - 1; ++rnd) {
-      const float4* lrow = lg + ((size_t)sw * (n - 1) + rnd) * (n / 2);
+      const float2* lrow = lg + ((size_t)sw * (n - 1) + rnd) * (n / 2);
       for (int slot = gid; slot < n / 2; slot += groups) {
-        const float4 r = lrow[slot];
-        if (r.y == 0.f) continue;  // identity rotation (uniform within the group)
+        const float2 r = lrow[slot];
+        if (r.x == 0.f) continue;  // identity rotation (uniform within the group)
         int p, q;
         circle_pair_n(slot, rnd, n, p, q);
-        const Rot R{r.x, r.y, r.z, r.w};
+        Rot R;
+        R.c = rsqrtf(1.f + r.x * r.x);
+        R.s = R.c * r.x;
+        sincosf(r.y, &R.ei, &R.er);
         float2* vp = V + (size_t)p * n;
         float2* vq = V + (size_t)q * n;
         for (int i = lgi; i < n; i += GT) {
