@@ -826,8 +826,17 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
     reserve += ((size_t)1 << size_class((uint64_t)e.chl * h->d * e.chr * 8)) + 2 * kAlign +
                (e.resetL ? ((size_t)1 << size_class((uint64_t)e.resetL * 4)) : 0) +
                (e.resetR ? ((size_t)1 << size_class((uint64_t)e.resetR * 4)) : 0);
-  if (h->hstate.pool.bump + reserve + ent_bytes + data_bytes + kAlign > top)
+  if (h->hstate.pool.bump + reserve + ent_bytes + data_bytes + kAlign > top) {
+    // host data is staged through the top of the slab: import it in two halves (each half's
+    // blocks land in the pool before the next half is staged)
+    if (!dev && count > 1) {
+      const int c0 = count / 2;
+      st = mps_import_sites(h, first, c0, B, dims);
+      if (st != MPS_OK) return st;
+      return mps_import_sites(h, first + c0, count - c0, B + 2 * ent[c0].src_elem, dims + 3 * c0);
+    }
     return set_err(h, MPS_E_NOMEM, "no room to stage the import");
+  }
   const size_t base = align_up(top - ent_bytes - data_bytes - kAlign);
   uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, ent_bytes + 64, 1));
   std::memcpy(hb, ent.data(), sizeof(ImportEntry) * count);

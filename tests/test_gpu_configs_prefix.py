@@ -47,7 +47,10 @@ def _run_prefix(cfg_id, n_prefix, slab=4 << 30):
 def test_config3_prefix():
     """N = 50, Haar brickwork depth 20, F_min = 0.9, cap 4096: layers 0-5 (chi <= 64)."""
     gpu, orc = _run_prefix(3, 6)
-    assert max(gpu.mps_bond_dims()) >= 32
+    # the per-gate budget (t = 0.99978) already truncates at layer 3: the bulk settles near
+    # chi ~ 20 (measured on the oracle), so the prefix exercises real cuts, not the exact regime
+    assert max(gpu.mps_bond_dims()) >= 16
+    assert sum(r["discarded_weight"] > 0 for r in gpu.mps_truncation_log()) > 0
 
 
 def test_config4_mpo_prefix():
