@@ -74,7 +74,8 @@ typedef struct {
   void* stream;        /* cudaStream_t; NULL = legacy default stream */
   void* dev_slab;      /* device memory owned by the caller */
   size_t slab_bytes;
-  int32_t rank, world; /* reserved: multi-GPU site-block sharding (world == 1 in this build) */
+  int32_t rank, world; /* must be 0, 1: the site-block sharding of §8(e) runs ABOVE this ABI, one
+                        * world-1 handle per rank for its block (paper_2307_16870_b200/sharded.py) */
   const void* nccl_unique_id;
 } mps_config;
 
@@ -104,6 +105,21 @@ mps_status mps_apply_gate2(mps_t, int32_t site, const float* U);
  * ascending-site order (reading "canonical order"). Synchronises the stream at the end
  * of the layer (the new bond profile drives the next layer's bucketing). */
 mps_status mps_apply_layer(mps_t, int32_t n_gates, const int32_t* sites, const float* Us);
+
+/* The same layer in two halves, so that a caller can pass the ledger between calls (the
+ * multi-rank token chain of SURVEY §8(e)): mps_layer_begin validates and
+ * plans exactly like mps_apply_layer and issues the first wave's contract + SVD (steps a0-a3)
+ * without waiting for them; *n_waves = 1 if work was issued (0 for an empty layer).
+ * mps_layer_step runs the current wave's select + ledger + reabsorb (a4-a5, reading the ledger
+ * as it stands on the device), synchronises, and issues the next wave's a0-a3 if any;
+ * *remaining = gates not yet committed (0 = layer done). While a layer is in flight, imports,
+ * set_lambda and snapshot_load return MPS_E_STATE. mps_apply_layer == begin + step until 0. */
+mps_status mps_layer_begin(mps_t, int32_t n_gates, const int32_t* sites, const float* Us, int32_t* n_waves);
+mps_status mps_layer_step(mps_t, int32_t* remaining);
+/* Ledger token (E12 running product in log space, next truncation index j, guarantee flag).
+ * get synchronises; set writes the device ledger (MPS_E_INVAL if log_E is not finite or > 0). */
+mps_status mps_ledger_get(mps_t, double* log_E, int64_t* j, int32_t* guarantee);
+mps_status mps_ledger_set(mps_t, double log_E, int64_t j, int32_t guarantee);
 
 /* Running estimate (E12/E13): est = exp(log_est); n_done = truncations so far; guarantee_held =
  * no cap fired; is_lower_bound = 1 for the MPO (noisy) regime (E13). Any pointer may be NULL. */

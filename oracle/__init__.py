@@ -78,6 +78,7 @@ def _declare(L):
     L.orc_set_lambda.argtypes = [_P, C.c_int, _P, C.c_int]
     L.orc_export_site.argtypes = [_P, C.c_int, _P, _P]
     L.orc_apply_gate1.argtypes = [_P, C.c_int, _P]
+    L.orc_set_ledger.argtypes = [_P, C.c_double, C.c_int64, C.c_int]
     L.orc_apply_gate2.argtypes = [_P, C.c_int, _P]
     L.orc_apply_layer.argtypes = [_P, C.c_int, _P, _P]
     L.orc_bond_dims.argtypes = [_P, _P]
@@ -227,6 +228,10 @@ class OracleMPS:
         _ck(lib().orc_estimate(self._h, C.byref(le), C.byref(nd), C.byref(gh)))
         return dict(log_est=le.value, est=float(np.exp(le.value)), n_done=nd.value,
                     guarantee_held=bool(gh.value), is_lower_bound=(self.d == 4))
+
+    def set_ledger(self, log_E: float, j: int, guarantee_held: int):
+        """Ledger token plumbing (multi-rank tests): no arithmetic."""
+        _ck(lib().orc_set_ledger(self._h, float(log_E), int(j), int(guarantee_held)))
 
     def records(self):
         ln = C.c_int64(0)

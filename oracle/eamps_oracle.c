@@ -477,7 +477,8 @@ int orc_bond_dims(orc_mps* s, int32_t* out) {
 }
 
 int orc_schmidt_values(orc_mps* s, int bond, double* out, int cap, int* len) {
-  if (bond < 0 || bond >= s->N - 1) return ORC_E_RANGE;
+  /* bonds -1 and N-1 are the trivial boundary vectors [1] (readable like set_lambda's range) */
+  if (bond < -1 || bond > s->N - 1) return ORC_E_RANGE;
   int L = s->lamlen[bond + 1];
   *len = L;
   for (int j = 0; j < L && j < cap; ++j) out[j] = s->lam[bond + 1][j];
@@ -486,6 +487,14 @@ int orc_schmidt_values(orc_mps* s, int bond, double* out, int cap, int* len) {
 
 int orc_estimate(orc_mps* s, double* log_est, int64_t* n_done, int* guarantee_held) {
   *log_est = s->logE; *n_done = s->j; *guarantee_held = s->guarantee_held;
+  return ORC_OK;
+}
+
+/* Ledger token plumbing for the multi-rank tests: replace (log E, j, guarantee).
+ * No arithmetic: the next truncation reads these exactly as if the preceding gates had run here. */
+int orc_set_ledger(orc_mps* s, double log_E, int64_t j, int guarantee_held) {
+  if (!(log_E <= 0.0) || j < 0) return ORC_E_INVAL;
+  s->logE = log_E; s->j = j; s->guarantee_held = guarantee_held;
   return ORC_OK;
 }
 

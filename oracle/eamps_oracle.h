@@ -71,6 +71,7 @@ int  orc_bond_dims(orc_mps*, int32_t* out /* N-1 */);
 int  orc_schmidt_values(orc_mps*, int bond, double* out, int cap, int* len);
 int  orc_estimate(orc_mps*, double* log_est, int64_t* n_done, int* guarantee_held);
 int  orc_records(orc_mps*, orc_record* out, int64_t cap, int64_t* len);
+int  orc_set_ledger(orc_mps*, double log_E, int64_t j, int guarantee_held);
 int  orc_amplitude(orc_mps*, const uint8_t* digits, double* re_im);
 int  orc_statevector(orc_mps*, double* out, int64_t n_complex);
 /* the last gate's sorted spectrum (for parity on isolated updates) */

@@ -27,6 +27,7 @@ ABI_FUNCTIONS = [
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
+    "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set",
 ]
 
 
@@ -88,6 +89,10 @@ def lib():
             "mps_sync": [_P],
             "mps_last_error": [_P],
             "mps_status_string": [i32],
+            "mps_layer_begin": [_P, i32, _P, _P, _P],
+            "mps_layer_step": [_P, _P],
+            "mps_ledger_get": [_P, _P, _P, _P],
+            "mps_ledger_set": [_P, dbl, i64, i32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -169,6 +174,28 @@ class MPS:
         sites = np.ascontiguousarray(sites, np.int32)
         Us = _c64(Us)
         self._check(lib().mps_apply_layer(self._h, int(sites.size), _ptr(sites), _ptr(Us)))
+
+    def mps_layer_begin(self, sites, Us) -> int:
+        """a0-a3 of the layer's first wave, issued without waiting (returns the waves issued)."""
+        sites = np.ascontiguousarray(sites, np.int32)
+        Us = _c64(Us)
+        w = C.c_int32(0)
+        self._check(lib().mps_layer_begin(self._h, int(sites.size), _ptr(sites), _ptr(Us), C.byref(w)))
+        return w.value
+
+    def mps_layer_step(self) -> int:
+        """a4-a5 of the wave in flight (+ a0-a3 of the next); returns the gates still pending."""
+        r = C.c_int32(0)
+        self._check(lib().mps_layer_step(self._h, C.byref(r)))
+        return r.value
+
+    def mps_ledger_get(self):
+        le, j, g = C.c_double(0), C.c_int64(0), C.c_int32(0)
+        self._check(lib().mps_ledger_get(self._h, C.byref(le), C.byref(j), C.byref(g)))
+        return le.value, j.value, g.value
+
+    def mps_ledger_set(self, log_E: float, j: int, guarantee: int):
+        self._check(lib().mps_ledger_set(self._h, float(log_E), int(j), int(guarantee)))
 
     def run(self, layers):
         for sites, us in layers:

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +21,24 @@ using namespace eamps;
 
 static_assert(sizeof(Record) == sizeof(mps_record), "record layout");
 
+struct LayerPlan {                 // per gate of a layer (a0 planning)
+  GateDesc gd;
+  size_t ws, reserve;
+  int ctiles, rtiles, gtiles, atiles;
+};
+
+struct LayerJob {                  // the layer in flight (mps_layer_begin / mps_layer_step)
+  bool active = false, front = false;
+  int G = 0, d4 = 0, g0 = 0, g1 = 0, Gw = 0;
+  std::vector<std::pair<int, int>> ord;
+  std::vector<LayerPlan> plan;
+  std::vector<float> us;             // the caller's gates, copied at begin
+  std::vector<GateDesc> hd;          // the current wave
+  std::vector<int32_t> rpre, gpre, apre;
+  size_t o_desc = 0, o_rec = 0, o_gpre = 0, o_apre = 0, o_rpre = 0, tail = 0;
+  bool ran[5] = {false, false, false, false, false};
+};
+
 struct mps_handle {
   int N = 0, d = 0;
   mps_config cfg{};
@@ -32,6 +51,7 @@ struct mps_handle {
   DevState hstate{};                       // host copy after the last sync
   std::vector<mps_record> records;
   std::vector<GateDesc> last_desc;         // every wave of the last layer (k, sweeps)
+  LayerJob job;
   int last_wave_begin = 0;                 // spectra are readable for the final wave only
   bool poisoned = false;
   int sticky = 0;
@@ -211,6 +231,254 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
   return MPS_OK;
 }
 
+// ---- one wave of a layer: the front half (a0 staging, a1 contract, a2+a3 SVD) is issued by
+// wave_front; the back half (a4 select + ledger, a5 reabsorb, readback) by wave_back. Between the
+// two the caller may replace the ledger (mps_ledger_set): the multi-rank token chain of §8(e).
+mps_status wave_front(mps_t h) {
+  LayerJob& J = h->job;
+  std::vector<LayerPlan>& plan = J.plan;
+  const int G = J.G, d = h->d, d4 = J.d4;
+  const int g0 = J.g0;
+  const size_t top = h->slab_bytes - 4 * kAlign;  // the top 1 KB is scratch for small host ops
+  const uint64_t bump = h->hstate.pool.bump;
+  size_t fixed = 0, ws = 0, reserve = 0;
+  int g1 = g0;
+  while (g1 < G) {
+    const int cnt = g1 - g0 + 1;
+    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
+                align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
+    size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
+    if (bump + r2 + fx + w2 + kAlign > top) break;
+    fixed = fx;
+    ws = w2;
+    reserve = r2;
+    ++g1;
+  }
+  if (g1 == g0) return set_err(h, MPS_E_NOMEM, "one gate's workspace does not fit the slab");
+  const int Gw = g1 - g0;
+  J.g1 = g1;
+  J.Gw = Gw;
+  // device addresses of the wave's staging block (just below `top`)
+  const size_t base = align_up(top - fixed - ws - kAlign);
+  size_t cur = base;
+  auto take = [&](size_t bytes) {
+    size_t o = cur;
+    cur = align_up(cur + bytes);
+    return o;
+  };
+  const size_t o_desc = take(sizeof(GateDesc) * Gw);
+  const size_t o_cpre = take(4 * (Gw + 1));
+  const size_t o_rpre = take(4 * (Gw + 1));
+  const size_t o_gpre = take(4 * (Gw + 1));
+  const size_t o_apre = take(4 * (Gw + 1));
+  const size_t o_small = take(4 * Gw);
+  const size_t o_large = take(4 * Gw);
+  const size_t o_us = take((size_t)Gw * d4 * 8);
+  const size_t o_rec = take(sizeof(Record) * Gw);
+  const size_t o_scr = take(32 * (size_t)Gw + 64);
+  const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
+  std::vector<int32_t> cpre(Gw + 1, 0), small, large;
+  J.rpre.assign(Gw + 1, 0);
+  J.gpre.assign(Gw + 1, 0);
+  J.apre.assign(Gw + 1, 0);
+  std::vector<int32_t>&rpre = J.rpre, &gpre = J.gpre, &apre = J.apre;
+  J.hd.assign(Gw, GateDesc{});
+  std::vector<GateDesc>& hd = J.hd;
+  // small / medium buckets by lane-group size GT (one launch per bucket); `small` holds them
+  // back to back, [bstart, bend) per bucket
+  struct Bucket {
+    int regime, gt, begin, end, threads, tile_rows;
+    size_t smem, smem2;
+  };
+  std::vector<Bucket> buckets;
+  for (int x = 0; x < Gw; ++x) {
+    LayerPlan& p = plan[g0 + x];
+    GateDesc gd = p.gd;
+    gd.u_index = x;
+    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+    gd.ws_theta = (int64_t)take(mnp);
+    gd.ws_thetap = (int64_t)take(mn);
+    gd.ws_V = (int64_t)take((size_t)gd.n_pad * gd.n_pad * 8);
+    gd.ws_sig2 = (int64_t)take((size_t)gd.n_pad * 8);
+    gd.ws_T = (int64_t)take((size_t)(gd.n_pad + 1) * 8);
+    gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
+    const size_t kmn = (size_t)std::min(gd.m, gd.n);
+    gd.ws_E = (int64_t)take(kmn * kmn * 8);
+    gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8) : 0;
+    hd[x] = gd;
+    cpre[x + 1] = cpre[x] + p.ctiles;
+    rpre[x + 1] = rpre[x] + p.rtiles;
+    gpre[x + 1] = gpre[x] + p.gtiles;
+    apre[x + 1] = apre[x] + p.atiles;
+    if (gd.regime == 1) large.push_back(x);
+  }
+  for (int reg : {0, 2}) {
+    for (int gt : {4, 8, 16, 32}) {
+      Bucket b{reg, gt, (int)small.size(), 0, 64, 64, 0, 0};
+      int maxn = 2;
+      for (int x = 0; x < Gw; ++x) {
+        const GateDesc& gd = hd[x];
+        if (gd.regime != reg) continue;
+        const int g_gt = std::min(small_group(gd.m), std::max(4, 2048 / gd.n));
+        if (g_gt != gt) continue;
+        small.push_back(x);
+        maxn = std::max(maxn, gd.n);
+        if (reg == 0) {
+          b.smem = std::max(b.smem, svd_small_smem(gd.m, gd.n));
+        } else {
+          const int tr = vrep_tile_rows(gd.m, gd.n);
+          b.tile_rows = std::min(b.tile_rows, tr);
+          b.smem = std::max(b.smem, svd_theta_smem(gd.m, gd.n));
+        }
+      }
+      b.end = (int)small.size();
+      if (b.end == b.begin) continue;
+      if (reg == 2) {
+        for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
+      }
+      b.threads = (int)std::min<size_t>(1024, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
+      buckets.push_back(b);
+    }
+  }
+  if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
+  // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
+  const size_t tail = align_up(staged_bytes, 64);  // 3 small pinned slots after the staged block
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));
+  if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  J.tail = tail;
+  std::memset(hb, 0, staged_bytes);
+  std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
+  std::memcpy(hb + (o_cpre - base), cpre.data(), 4 * (Gw + 1));
+  std::memcpy(hb + (o_rpre - base), rpre.data(), 4 * (Gw + 1));
+  std::memcpy(hb + (o_gpre - base), gpre.data(), 4 * (Gw + 1));
+  std::memcpy(hb + (o_apre - base), apre.data(), 4 * (Gw + 1));
+  if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
+  if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
+  for (int x = 0; x < Gw; ++x)
+    std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, J.us.data() + (size_t)J.ord[g0 + x].second * d4 * 2,
+                (size_t)d4 * 8);
+  CK(cudaMemcpyAsync(h->slab + base, hb, staged_bytes, cudaMemcpyHostToDevice, h->s));
+  // the pool may not grow into the workspace
+  uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + tail);
+  *hceil = base;
+  CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
+
+  GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + o_desc);
+  J.o_desc = o_desc;
+  J.o_rec = o_rec;
+  J.o_gpre = o_gpre;
+  J.o_apre = o_apre;
+  J.o_rpre = o_rpre;
+  const int32_t* d_cpre = reinterpret_cast<const int32_t*>(h->slab + o_cpre);
+  const int32_t* d_small = reinterpret_cast<const int32_t*>(h->slab + o_small);
+  const int32_t* d_large = reinterpret_cast<const int32_t*>(h->slab + o_large);
+  const float2* d_us = reinterpret_cast<const float2*>(h->slab + o_us);
+
+  const bool prof = h->profiling;
+  J.ran[0] = true;
+  J.ran[1] = !buckets.empty();
+  J.ran[2] = !large.empty();
+  J.ran[3] = J.ran[4] = true;
+  if (prof) CK(cudaEventRecord(h->ev[0], h->s));
+  // a1 contract (all gates of the wave)
+  launch_contract(d_desc, d_cpre, Gw, cpre[Gw], d, h->slab, h->dst, d_us, h->s);
+  ++h->launches;
+  CKL("contract");
+  if (prof) CK(cudaEventRecord(h->ev[1], h->s));
+  // a2 + a3 SVD, small regime: one CTA per theta
+  for (const Bucket& b : buckets) {
+    if (b.regime == 0) {
+      launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.threads,
+                       h->slab, h->dst, h->s);
+      ++h->launches;
+    } else {
+      launch_svd_medium(d_desc, d_small + b.begin, b.end - b.begin, b.smem, b.smem2, b.tile_rows, h->cfg.max_sweeps,
+                        b.gt, b.threads, h->slab, h->dst, h->s);
+      h->launches += 2;
+    }
+    CKL("svd_small/medium");
+  }
+  if (prof) CK(cudaEventRecord(h->ev[2], h->s));
+  // a2 + a3 SVD, large regime: blocked Jacobi
+  if (!large.empty()) {
+    int err = 0;
+    int32_t* hflag = reinterpret_cast<int32_t*>(hb + tail + 64);
+    h->launches += run_svd_blocked(d_desc, hd.data(), d_large, large.data(), (int)large.size(), h->cfg.max_sweeps,
+                                   h->slab, h->dst, reinterpret_cast<int32_t*>(h->slab + o_scr), hflag, h->s, &err);
+    CKL("svd_blocked");
+    if (err) {
+      // record on device so that it is sticky like the small-path error
+      int32_t* he = reinterpret_cast<int32_t*>(hb + tail + 128);
+      *he = err;
+      CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
+    }
+  }
+  if (prof) CK(cudaEventRecord(h->ev[3], h->s));
+  J.front = true;
+  return MPS_OK;
+}
+
+mps_status wave_back(mps_t h) {
+  LayerJob& J = h->job;
+  if (!J.front) return set_err(h, MPS_E_STATE, "no wave in flight");
+  J.front = false;
+  const int Gw = J.Gw;
+  std::vector<GateDesc>& hd = J.hd;
+  GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + J.o_desc);
+  Record* d_rec = reinterpret_cast<Record*>(h->slab + J.o_rec);
+  const int32_t* d_gpre = reinterpret_cast<const int32_t*>(h->slab + J.o_gpre);
+  const int32_t* d_apre = reinterpret_cast<const int32_t*>(h->slab + J.o_apre);
+  const int32_t* d_rpre = reinterpret_cast<const int32_t*>(h->slab + J.o_rpre);
+  const bool prof = h->profiling;
+  // a4 select + ledger + pool
+  const int par = (h->cfg.strategy == MPS_STRAT_FIXED || h->cfg.strategy == MPS_STRAT_NAIVE) ? 1 : 0;
+  launch_select(d_desc, Gw, h->slab, h->dst, d_rec, par, h->s);
+  h->launches += 2;
+  CKL("select");
+  if (prof) CK(cudaEventRecord(h->ev[4], h->s));
+  // a5 reabsorb
+  launch_reabsorb(d_desc, d_gpre, J.gpre[Gw], d_apre, J.apre[Gw], d_rpre, J.rpre[Gw], Gw, h->slab, h->s);
+  h->launches += 3;
+  CKL("reabsorb");
+  if (prof) CK(cudaEventRecord(h->ev[5], h->s));
+  // read back: descriptors (k, sweeps), records, device state
+  const size_t back = sizeof(GateDesc) * Gw + sizeof(Record) * Gw + sizeof(DevState);
+  uint8_t* rb = static_cast<uint8_t*>(pinned_buf(h, back + 64));
+  CK(cudaMemcpyAsync(rb, d_desc, sizeof(GateDesc) * Gw, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw, d_rec, sizeof(Record) * Gw, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, h->dst, sizeof(DevState),
+                     cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  std::memcpy(hd.data(), rb, sizeof(GateDesc) * Gw);
+  const Record* rr = reinterpret_cast<const Record*>(rb + sizeof(GateDesc) * Gw);
+  std::memcpy(&h->hstate, rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, sizeof(DevState));
+  if (prof) {
+    for (int p = 0; p < 5; ++p) {
+      if (!J.ran[p]) continue;
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h->ev[p], h->ev[p + 1]));
+      h->phase_ms[p] += ms;
+      h->phase_n[p] += 1;
+    }
+  }
+  mps_status de = device_error(h);
+  for (int x = 0; x < Gw; ++x) {
+    const GateDesc& gd = hd[x];
+    if (gd.k <= 0) continue;
+    h->chr[gd.site] = gd.k;
+    h->chl[gd.site + 1] = gd.k;
+    h->lamlen[gd.site + 1] = gd.k;
+    mps_record rec;
+    std::memcpy(&rec, &rr[x], sizeof(rec));
+    h->records.push_back(rec);
+  }
+  h->last_wave_begin = (int)h->last_desc.size();
+  h->last_desc.insert(h->last_desc.end(), hd.begin(), hd.end());
+  if (de != MPS_OK) return de;
+  J.g0 = J.g1;
+  return MPS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -376,11 +644,13 @@ mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
   return MPS_OK;
 }
 
-mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float* Us) {
+mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float* Us, int32_t* n_waves) {
+  if (n_waves) *n_waves = 0;
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
   if (G < 0 || (G > 0 && (!sites || !Us))) return set_err(h, MPS_E_INVAL, "bad arguments");
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is still in progress (mps_layer_step)");
   if (G == 0) return MPS_OK;
   const int d = h->d, d4 = d * d * d * d;
   // ---- a0: validate (in range, disjoint pairs), canonical order = ascending site
@@ -403,15 +673,12 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
   }
 
   // ---- per-gate shapes, regimes and workspace sizes
-  struct Plan {
-    GateDesc gd;
-    size_t ws, reserve;
-    int ctiles, rtiles, gtiles, atiles;
-  };
-  std::vector<Plan> plan(G);
+  LayerJob& J = h->job;
+  J.plan.assign(G, LayerPlan{});
+  std::vector<LayerPlan>& plan = J.plan;
   const int TA = 64 / d;
   for (int g = 0; g < G; ++g) {
-    Plan& p = plan[g];
+    LayerPlan& p = plan[g];
     GateDesc& gd = p.gd;
     std::memset(&gd, 0, sizeof(gd));
     int i = ord[g].first;
@@ -445,219 +712,51 @@ mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float
     p.atiles = ((gd.n + 63) / 64) * ((km + 63) / 64);
   }
 
-  // ---- waves (gates in canonical order; each wave's workspace + worst-case new blocks fit)
-  const size_t top = h->slab_bytes - 4 * kAlign;  // the top 1 KB is scratch for small host ops
-  int g0 = 0;
+  J.G = G;
+  J.d4 = d4;
+  J.ord = ord;
+  J.us.assign(Us, Us + (size_t)G * d4 * 2);
+  J.g0 = 0;
+  J.front = false;
+  J.active = true;
   h->last_desc.clear();
   h->last_wave_begin = 0;
-  while (g0 < G) {
-    const uint64_t bump = h->hstate.pool.bump;
-    size_t fixed = 0, ws = 0, reserve = 0;
-    int g1 = g0;
-    while (g1 < G) {
-      const int cnt = g1 - g0 + 1;
-      size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
-                  align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
-      size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
-      if (bump + r2 + fx + w2 + kAlign > top) break;
-      fixed = fx;
-      ws = w2;
-      reserve = r2;
-      ++g1;
-    }
-    if (g1 == g0) return set_err(h, MPS_E_NOMEM, "one gate's workspace does not fit the slab");
-    const int Gw = g1 - g0;
-    // device addresses of the wave's staging block (just below `top`)
-    const size_t base = align_up(top - fixed - ws - kAlign) - 0;
-    size_t cur = base;
-    auto take = [&](size_t bytes) {
-      size_t o = cur;
-      cur = align_up(cur + bytes);
-      return o;
-    };
-    const size_t o_desc = take(sizeof(GateDesc) * Gw);
-    const size_t o_cpre = take(4 * (Gw + 1));
-    const size_t o_rpre = take(4 * (Gw + 1));
-    const size_t o_gpre = take(4 * (Gw + 1));
-    const size_t o_apre = take(4 * (Gw + 1));
-    const size_t o_small = take(4 * Gw);
-    const size_t o_large = take(4 * Gw);
-    const size_t o_us = take((size_t)Gw * d4 * 8);
-    const size_t o_rec = take(sizeof(Record) * Gw);
-    const size_t o_scr = take(32 * (size_t)Gw + 64);
-    const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
-    std::vector<int32_t> cpre(Gw + 1, 0), rpre(Gw + 1, 0), gpre(Gw + 1, 0), apre(Gw + 1, 0), small, large;
-    std::vector<GateDesc> hd(Gw);
-    // small / medium buckets by lane-group size GT (one launch per bucket); `small` holds them
-    // back to back, [bstart, bend) per bucket
-    struct Bucket {
-      int regime, gt, begin, end, threads, tile_rows;
-      size_t smem, smem2;
-    };
-    std::vector<Bucket> buckets;
-    for (int x = 0; x < Gw; ++x) {
-      Plan& p = plan[g0 + x];
-      GateDesc gd = p.gd;
-      gd.u_index = x;
-      const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
-      gd.ws_theta = (int64_t)take(mnp);
-      gd.ws_thetap = (int64_t)take(mn);
-      gd.ws_V = (int64_t)take((size_t)gd.n_pad * gd.n_pad * 8);
-      gd.ws_sig2 = (int64_t)take((size_t)gd.n_pad * 8);
-      gd.ws_T = (int64_t)take((size_t)(gd.n_pad + 1) * 8);
-      gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
-      const size_t kmn = (size_t)std::min(gd.m, gd.n);
-      gd.ws_E = (int64_t)take(kmn * kmn * 8);
-      gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8) : 0;
-      hd[x] = gd;
-      cpre[x + 1] = cpre[x] + p.ctiles;
-      rpre[x + 1] = rpre[x] + p.rtiles;
-      gpre[x + 1] = gpre[x] + p.gtiles;
-      apre[x + 1] = apre[x] + p.atiles;
-      if (gd.regime == 1) large.push_back(x);
-    }
-    for (int reg : {0, 2}) {
-      for (int gt : {4, 8, 16, 32}) {
-        Bucket b{reg, gt, (int)small.size(), 0, 64, 64, 0, 0};
-        int maxn = 2;
-        for (int x = 0; x < Gw; ++x) {
-          const GateDesc& gd = hd[x];
-          if (gd.regime != reg) continue;
-          const int g_gt = std::min(small_group(gd.m), std::max(4, 2048 / gd.n));
-          if (g_gt != gt) continue;
-          small.push_back(x);
-          maxn = std::max(maxn, gd.n);
-          if (reg == 0) {
-            b.smem = std::max(b.smem, svd_small_smem(gd.m, gd.n));
-          } else {
-            const int tr = vrep_tile_rows(gd.m, gd.n);
-            b.tile_rows = std::min(b.tile_rows, tr);
-            b.smem = std::max(b.smem, svd_theta_smem(gd.m, gd.n));
-          }
-        }
-        b.end = (int)small.size();
-        if (b.end == b.begin) continue;
-        if (reg == 2) {
-          for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
-        }
-        b.threads = (int)std::min<size_t>(1024, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
-        buckets.push_back(b);
-      }
-    }
-    if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
-    // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
-    const size_t tail = align_up(staged_bytes, 64);  // 3 small pinned slots after the staged block
-    uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));
-    if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
-    std::memset(hb, 0, staged_bytes);
-    std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
-    std::memcpy(hb + (o_cpre - base), cpre.data(), 4 * (Gw + 1));
-    std::memcpy(hb + (o_rpre - base), rpre.data(), 4 * (Gw + 1));
-    std::memcpy(hb + (o_gpre - base), gpre.data(), 4 * (Gw + 1));
-    std::memcpy(hb + (o_apre - base), apre.data(), 4 * (Gw + 1));
-    if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
-    if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
-    for (int x = 0; x < Gw; ++x)
-      std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, Us + (size_t)ord[g0 + x].second * d4 * 2, (size_t)d4 * 8);
-    CK(cudaMemcpyAsync(h->slab + base, hb, staged_bytes, cudaMemcpyHostToDevice, h->s));
-    // the pool may not grow into the workspace
-    uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + tail);
-    *hceil = base;
-    CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
+  mps_status fs = wave_front(h);
+  if (fs != MPS_OK) {
+    J.active = false;
+    return fs;
+  }
+  if (n_waves) *n_waves = 1;
+  return MPS_OK;
+}
 
-    GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + o_desc);
-    const int32_t* d_cpre = reinterpret_cast<const int32_t*>(h->slab + o_cpre);
-    const int32_t* d_rpre = reinterpret_cast<const int32_t*>(h->slab + o_rpre);
-    const int32_t* d_gpre = reinterpret_cast<const int32_t*>(h->slab + o_gpre);
-    const int32_t* d_apre = reinterpret_cast<const int32_t*>(h->slab + o_apre);
-    const int32_t* d_small = reinterpret_cast<const int32_t*>(h->slab + o_small);
-    const int32_t* d_large = reinterpret_cast<const int32_t*>(h->slab + o_large);
-    const float2* d_us = reinterpret_cast<const float2*>(h->slab + o_us);
-    Record* d_rec = reinterpret_cast<Record*>(h->slab + o_rec);
+mps_status mps_layer_step(mps_t h, int32_t* remaining) {
+  if (!h) return MPS_E_INVAL;
+  if (remaining) *remaining = 0;
+  LayerJob& J = h->job;
+  if (!J.active) return MPS_OK;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) { J.active = false; return st; }
+  st = wave_back(h);
+  if (st != MPS_OK) { J.active = false; return st; }
+  if (J.g0 >= J.G) {
+    J.active = false;
+    return MPS_OK;
+  }
+  st = wave_front(h);
+  if (st != MPS_OK) { J.active = false; return st; }
+  if (remaining) *remaining = J.G - J.g0;
+  return MPS_OK;
+}
 
-    const bool prof = h->profiling;
-    bool ran[5] = {true, !buckets.empty(), !large.empty(), true, true};
-    if (prof) CK(cudaEventRecord(h->ev[0], h->s));
-    // a1 contract (all gates of the wave)
-    launch_contract(d_desc, d_cpre, Gw, cpre[Gw], d, h->slab, h->dst, d_us, h->s);
-    ++h->launches;
-    CKL("contract");
-    if (prof) CK(cudaEventRecord(h->ev[1], h->s));
-    // a2 + a3 SVD, small regime: one CTA per theta
-    for (const Bucket& b : buckets) {
-      if (b.regime == 0) {
-        launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.threads,
-                         h->slab, h->dst, h->s);
-        ++h->launches;
-      } else {
-        launch_svd_medium(d_desc, d_small + b.begin, b.end - b.begin, b.smem, b.smem2, b.tile_rows, h->cfg.max_sweeps,
-                          b.gt, b.threads, h->slab, h->dst, h->s);
-        h->launches += 2;
-      }
-      CKL("svd_small/medium");
-    }
-    if (prof) CK(cudaEventRecord(h->ev[2], h->s));
-    // a2 + a3 SVD, large regime: blocked Jacobi
-    if (!large.empty()) {
-      int err = 0;
-      int32_t* hflag = reinterpret_cast<int32_t*>(hb + tail + 64);
-      h->launches += run_svd_blocked(d_desc, hd.data(), d_large, large.data(), (int)large.size(), h->cfg.max_sweeps,
-                                     h->slab, h->dst, reinterpret_cast<int32_t*>(h->slab + o_scr), hflag, h->s, &err);
-      CKL("svd_blocked");
-      if (err) {
-        // record on device so that it is sticky like the small-path error
-        int32_t* he = reinterpret_cast<int32_t*>(hb + tail + 128);
-        *he = err;
-        CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
-      }
-    }
-    if (prof) CK(cudaEventRecord(h->ev[3], h->s));
-    // a4 select + ledger + pool
-    const int par = (h->cfg.strategy == MPS_STRAT_FIXED || h->cfg.strategy == MPS_STRAT_NAIVE) ? 1 : 0;
-    launch_select(d_desc, Gw, h->slab, h->dst, d_rec, par, h->s);
-    h->launches += 2;
-    CKL("select");
-    if (prof) CK(cudaEventRecord(h->ev[4], h->s));
-    // a5 reabsorb
-    launch_reabsorb(d_desc, d_gpre, gpre[Gw], d_apre, apre[Gw], d_rpre, rpre[Gw], Gw, h->slab, h->s);
-    h->launches += 3;
-    CKL("reabsorb");
-    if (prof) CK(cudaEventRecord(h->ev[5], h->s));
-    // read back: descriptors (k, sweeps), records, device state
-    const size_t back = sizeof(GateDesc) * Gw + sizeof(Record) * Gw + sizeof(DevState);
-    uint8_t* rb = static_cast<uint8_t*>(pinned_buf(h, back + 64));
-    CK(cudaMemcpyAsync(rb, d_desc, sizeof(GateDesc) * Gw, cudaMemcpyDeviceToHost, h->s));
-    CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw, d_rec, sizeof(Record) * Gw, cudaMemcpyDeviceToHost, h->s));
-    CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, h->dst, sizeof(DevState),
-                       cudaMemcpyDeviceToHost, h->s));
-    CK(cudaStreamSynchronize(h->s));
-    std::memcpy(hd.data(), rb, sizeof(GateDesc) * Gw);
-    const Record* rr = reinterpret_cast<const Record*>(rb + sizeof(GateDesc) * Gw);
-    std::memcpy(&h->hstate, rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, sizeof(DevState));
-    if (prof) {
-      for (int p = 0; p < 5; ++p) {
-        if (!ran[p]) continue;
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, h->ev[p], h->ev[p + 1]));
-        h->phase_ms[p] += ms;
-        h->phase_n[p] += 1;
-      }
-    }
-    mps_status de = device_error(h);
-    for (int x = 0; x < Gw; ++x) {
-      const GateDesc& gd = hd[x];
-      if (gd.k <= 0) continue;
-      h->chr[gd.site] = gd.k;
-      h->chl[gd.site + 1] = gd.k;
-      h->lamlen[gd.site + 1] = gd.k;
-      mps_record rec;
-      std::memcpy(&rec, &rr[x], sizeof(rec));
-      h->records.push_back(rec);
-    }
-    h->last_wave_begin = (int)h->last_desc.size();
-    h->last_desc.insert(h->last_desc.end(), hd.begin(), hd.end());
-    if (de != MPS_OK) return de;
-    g0 = g1;
+mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float* Us) {
+  int32_t w = 0;
+  mps_status st = mps_layer_begin(h, G, sites, Us, &w);
+  if (st != MPS_OK || w == 0) return st;
+  int32_t rem = 1;
+  while (rem > 0) {
+    st = mps_layer_step(h, &rem);
+    if (st != MPS_OK) return st;
   }
   return MPS_OK;
 }
@@ -681,6 +780,44 @@ mps_status mps_fidelity_estimate(mps_t h, double* est, double* log_est, int64_t*
   return MPS_OK;
 }
 
+// The ledger token of the multi-rank chain (§8(e)): (log E, j, guarantee). get synchronises;
+// set is stream-ordered (it lands before the next wave's select).
+mps_status mps_ledger_get(mps_t h, double* log_E, int64_t* j, int32_t* guarantee) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  st = device_error(h);
+  if (st != MPS_OK) return st;
+  if (log_E) *log_E = h->hstate.led.logE;
+  if (j) *j = h->hstate.led.j;
+  if (guarantee) *guarantee = h->hstate.led.guarantee;
+  return MPS_OK;
+}
+
+mps_status mps_ledger_set(mps_t h, double log_E, int64_t j, int32_t guarantee) {
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (!std::isfinite(log_E) || log_E > 0.0 || j < 0) return set_err(h, MPS_E_INVAL, "bad ledger token");
+  if (h->cfg.strategy != MPS_STRAT_FIXED && j > h->cfg.n_planned) return set_err(h, MPS_E_STATE, "j > n_planned");
+  // logE (8) | j (8) | guarantee (4): the first 20 bytes of DevLedger; staged in its own pinned slot
+  static_assert(offsetof(DevLedger, logE) == 0 && offsetof(DevLedger, j) == 8 && offsetof(DevLedger, guarantee) == 16,
+                "ledger layout");
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, 64));
+  // the general pinned slot may be reused by the next call before this copy runs: drain first
+  std::memcpy(hb, &log_E, 8);
+  std::memcpy(hb + 8, &j, 8);
+  std::memcpy(hb + 16, &guarantee, 4);
+  CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(h->dst), hb, 20, cudaMemcpyHostToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->hstate.led.logE = log_E;
+  h->hstate.led.j = j;
+  h->hstate.led.guarantee = guarantee;
+  return MPS_OK;
+}
+
 mps_status mps_bond_dims(mps_t h, int32_t* out) {
   if (!h || !out) return MPS_E_INVAL;
   for (int i = 0; i < h->N - 1; ++i) out[i] = h->chr[i];
@@ -698,7 +835,7 @@ mps_status mps_schmidt_values(mps_t h, int32_t bond, float* out, int32_t cap, in
   *len = e.len;
   if (out && cap > 0) {
     int nc = std::min(cap, e.len);
-    CK(cudaMemcpyAsync(out, h->slab + e.off, 4 * (size_t)nc, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaMemcpyAsync(out, h->slab + e.off, 4 * (size_t)nc, cudaMemcpyDefault, h->s));  // host or device out
     CK(cudaStreamSynchronize(h->s));
   }
   return MPS_OK;
@@ -753,6 +890,7 @@ mps_status mps_export_site(mps_t h, int32_t site, float* B, int32_t* dims3) {
 
 mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t* dims3) {
   if (!h || !B || !dims3) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
   if (dims3[1] != h->d || dims3[0] < 1 || dims3[2] < 1) return set_err(h, MPS_E_INVAL, "bad dims");
   mps_status st = check_sticky(h);
@@ -795,6 +933,7 @@ mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t*
 
 mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* B, const int32_t* dims) {
   if (!h || !B || !dims || count < 1) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (first < 0 || first + count > h->N) return set_err(h, MPS_E_RANGE, "sites out of range");
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -866,6 +1005,7 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
 
 mps_status mps_set_lambda(mps_t h, int32_t bond, const float* lam, int32_t len) {
   if (!h || !lam || len < 1) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (bond < -1 || bond > h->N - 1) return set_err(h, MPS_E_RANGE, "bond out of range");
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -979,6 +1119,7 @@ mps_status mps_snapshot_save(mps_t h, void* buf, size_t buf_bytes, size_t* bytes
 
 mps_status mps_snapshot_load(mps_t h, const void* buf, size_t buf_bytes) {
   if (!h || !buf) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (!h->snap.valid) return set_err(h, MPS_E_STATE, "no snapshot saved by this handle");
   const size_t need = h->snap.hstate.pool.bump;
   if (buf_bytes < need) return set_err(h, MPS_E_RANGE, "snapshot buffer too small");
