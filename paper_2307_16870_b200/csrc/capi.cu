@@ -10,6 +10,7 @@
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -303,8 +304,11 @@ mps_status wave_front(mps_t h) {
     gd.ws_T = (int64_t)take((size_t)(gd.n_pad + 1) * 8);
     gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
     const size_t kmn = (size_t)std::min(gd.m, gd.n);
-    gd.ws_E = (int64_t)take(kmn * kmn * 8);
-    gd.ws_log = gd.regime == 2 ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8) : 0;
+    // E (k x k, reabsorb); the large regime's polish also keeps shift | den (2 n_pad doubles) there
+    gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, gd.regime == 1 ? (size_t)16 * gd.n_pad : (size_t)0));
+    gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8)
+                : gd.regime == 1 ? (int64_t)take(svd_tc_scratch_bytes(gd.n_pad))
+                                 : 0;
     hd[x] = gd;
     cpre[x + 1] = cpre[x] + p.ctiles;
     rpre[x + 1] = rpre[x] + p.rtiles;
@@ -403,8 +407,10 @@ mps_status wave_front(mps_t h) {
   if (!large.empty()) {
     int err = 0;
     int32_t* hflag = reinterpret_cast<int32_t*>(hb + tail + 64);
-    h->launches += run_svd_blocked(d_desc, hd.data(), d_large, large.data(), (int)large.size(), h->cfg.max_sweeps,
-                                   h->slab, h->dst, reinterpret_cast<int32_t*>(h->slab + o_scr), hflag, h->s, &err);
+    static const bool simt = getenv("EAMPS_LARGE_SIMT") != nullptr;   // dev A/B switch: SIMT blocked path
+    h->launches += (simt ? run_svd_blocked : run_svd_tc)(d_desc, hd.data(), d_large, large.data(), (int)large.size(),
+                                                         h->cfg.max_sweeps, h->slab, h->dst,
+                                                         reinterpret_cast<int32_t*>(h->slab + o_scr), hflag, h->s, &err);
     CKL("svd_blocked");
     if (err) {
       // record on device so that it is sticky like the small-path error
@@ -691,14 +697,17 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // SVD regime: 0 small (theta + V in one CTA), 2 medium (theta in one CTA, V replayed from a
     // rotation log), 1 large (blocked, HBM-resident)
     gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
-    gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 32);
+    gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
-    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8 : 0;
+    // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)
+    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8
+                                       : (gd.regime == 1 ? svd_tc_scratch_bytes(gd.n_pad) : 0);
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
     const int kmn = std::min(gd.m, gd.n);
     p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
-           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) + align_up((size_t)kmn * kmn * 8) +
+           align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) +
+           align_up(std::max((size_t)kmn * kmn * 8, gd.regime == 1 ? (size_t)16 * gd.n_pad : (size_t)0)) +
            align_up(logb);
     int kmax = std::min(gd.m, gd.n);
     if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);

@@ -15,6 +15,7 @@
 // Then sigma_j^2 = ||theta v_j||^2/||v_j||^2 (Rayleigh, FP64 accumulation) and sort + tails.
 #include "eamps_internal.cuh"
 #include "sort_tails.cuh"
+#include "tc_common.cuh"
 
 namespace eamps {
 
@@ -267,7 +268,7 @@ __global__ void k_block_check(GateDesc* desc, const int32_t* list, int count, La
 // sigma_j^2 = ||theta v_j||^2 / ||v_j||^2 with theta = lambda (x) Theta' (the FP32 theta the
 // Jacobi started from), FP64 accumulation. One CTA per (32-column block, gate).
 __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ desc, const int32_t* list, uint8_t* slab,
-                                                  const DevState* st) {
+                                                  const DevState* st, int write_b = 0) {
   const GateDesc gd = desc[list[blockIdx.y]];
   const int j0 = blockIdx.x * 32;
   if (j0 >= gd.n) return;
@@ -325,6 +326,15 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) num[j] += w[j].x * w[j].x + w[j].y * w[j].y;
+    if (write_b) {   // B = theta V for the FP64-anchored polish (the Jacobi's working theta is dead now)
+      float2* Bw = reinterpret_cast<float2*>(slab + gd.ws_theta);
+      const int row = r0 + oi;
+      if (row < m) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j0 + oj + j < n) Bw[(int64_t)(j0 + oj + j) * m + row] = make_float2((float)w[j].x, (float)w[j].y);
+      }
+    }
   }
   // reduce num over the 64 row-threads of each column group (fixed order -> deterministic)
   __shared__ double colsum[32];
@@ -347,11 +357,16 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
       for (int k = 0; k < n; ++k) den += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
       double v = den > 0.0 ? colsum[tid] / den : 0.0;
       reinterpret_cast<double*>(slab + gd.ws_sig2)[j] = v;
+      if (write_b) {   // polish scratch at ws_E: shift[n_pad] | den[n_pad]
+        double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
+        shift[j] = 0.0;
+        shift[np + j] = den;
+      }
     }
   }
 }
 
-__global__ void k_sort_tails_large(GateDesc* desc, const int32_t* list, uint8_t* slab, DevState* st) {
+__global__ void k_sort_tails_large(GateDesc* desc, const int32_t* list, uint8_t* slab, DevState* st, int polish = 0) {
   extern __shared__ __align__(16) uint8_t sm[];
   const GateDesc gd = desc[list[blockIdx.x]];
   const int n = gd.n;
@@ -361,8 +376,10 @@ __global__ void k_sort_tails_large(GateDesc* desc, const int32_t* list, uint8_t*
   int32_t* idx = reinterpret_cast<int32_t*>(keys + npow2);
   double* part = reinterpret_cast<double*>(idx + npow2 + (npow2 & 1));
   double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  const double* shift = reinterpret_cast<const double*>(slab + gd.ws_E);
   for (int j = threadIdx.x; j < npow2; j += blockDim.x) {
-    double v = j < n ? gS[j] : -1.0;
+    double v = j < n ? gS[j] + (polish ? shift[j] : 0.0) : -1.0;
+    if (j < n && v < 0.0) v = 0.0;
     if (j < n && !isfinite(v)) atomicCAS(&st->led.error, 0, -7);
     keys[j] = v;
     idx[j] = j;
@@ -373,6 +390,569 @@ __global__ void k_sort_tails_large(GateDesc* desc, const int32_t* list, uint8_t*
   for (int j = threadIdx.x; j < n; j += blockDim.x) { gS[j] = keys[j]; gP[j] = idx[j]; }
   cta_tails(keys, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
 }
+
+
+// =================================================================================================
+// Tensor-core (tcgen05, 3xTF32) blocked one-sided Jacobi -- the large regime on sm_100a.
+//
+// Columns in blocks of TB = 32; a round pairs blocks (I, J) by the circle method; the panel
+// P = [A_I A_J] (m x 64 complex) is handled by three kernels per round (all gates, all pairs):
+//   k_tc_gram  : G = P^H P on the tensor core. With Q = [Re P | Im P] (m x 128 real, staged
+//                K-major from theta's columns), D = Q^T Q (128 x 128, K = m) and
+//                G_re = D[p][q] + D[64+p][64+q], G_im = D[p][64+q] - D[64+p][q]. 3xTF32 by the
+//                symmetric form D'' = hi^T hi + hi^T (2 lo), D = (D'' + D''^T)/2 (2 MMAs / k-step).
+//   k_tc_inner : the one-sided Jacobi criterion on G (as the SIMT path), then cyclic two-sided
+//                Jacobi on G in FP64 (the scalar 2x2 rotation), W = prod J, E = W - I split into
+//                TF32 hi + lo images laid out for the rotation's B operand.
+//   k_tc_rot   : P <- P + P E (identity split: the tensor-core error scales with |E|, which goes
+//                to 0 as the sweep converges) for the theta panel (m rows) and the V panel
+//                (n_pad rows), 128-row tiles, [Re' Im'] = [Re Im] [[E_re, E_im], [-E_im, E_re]]
+//                as 4 K=64 x N=64 MMA groups per tile (b_negate for -E_im), 3xTF32.
+// =================================================================================================
+namespace tcj {
+
+constexpr int TB = 32;          // complex columns per block
+constexpr int PWC = 2 * TB;     // panel width (complex) = 64
+constexpr int GKC = 32;         // rows per Gram K-chunk
+constexpr uint32_t G_SBO = 128, G_LBO = (128 / 8) * 128;   // Gram operand image: 128 rows (panel re/im cols)
+constexpr uint32_t E_SBO = 128, E_LBO = (64 / 8) * 128;    // E image: 64 rows (output cols) x 64 k
+constexpr uint32_t R_SBO = 128, R_LBO = (128 / 8) * 128;   // rotation A image: 128 rows x 16 k
+constexpr int EIMG_FLOATS = 6 * 64 * 64;                   // Re hi|mid|lo, Im hi|mid|lo
+constexpr size_t kGramStage = (size_t)128 * GKC * 4;        // one image (hi or lo2) of a chunk: 16 KB
+constexpr size_t kGramSmem = (size_t)128 * 129 * 4 + 1024;  // >= 2 stages x 2 images (64 KB); D staging
+constexpr size_t kRotStage = (size_t)128 * 16 * 4;          // one image of a 128 x 16 chunk: 8 KB
+constexpr size_t kRotSmem = (size_t)EIMG_FLOATS * 4 + (size_t)64 * 128 * 8 + 2 * 3 * kRotStage + 1024;
+constexpr size_t kInnerSmem = (sizeof(double2) + sizeof(float2)) * 64 * 65;
+
+struct Scratch {                  // per gate: slab offset of its TC scratch (GateDesc::ws_log)
+  static __host__ __device__ size_t gram_bytes(int pairs) { return (size_t)pairs * 64 * 64 * 8; }
+  static __host__ __device__ size_t eimg_bytes(int pairs) { return (size_t)pairs * EIMG_FLOATS * 4; }
+  static __host__ __device__ size_t total(int pairs) { return gram_bytes(pairs) + eimg_bytes(pairs) + (size_t)pairs * 4 + 256; }
+};
+
+__device__ __forceinline__ int colof(int c, int I, int J) { return c < TB ? I * TB + c : J * TB + (c - TB); }
+
+// ---- G = P^H P on the tensor core. grid (n_pad/64 pairs max, count); 128 threads.
+__global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                 int rnd, uint8_t* slab, const LargeCtl* ctl) {
+  const int gi = blockIdx.y;
+  if (ctl[gi].conv) return;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  int I, J;
+  circle_pair(pair, rnd, nb, I, J);
+  const int m = gd.m;
+  const float2* __restrict__ th = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tc::tmem_alloc(&tbase, 128);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_barrier_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tbase;
+  const uint32_t idesc = tc::make_idesc_tf32(128, 128, false, false);
+  const int nchunks = (m + GKC - 1) / GKC;
+  for (int q = 0; q < nchunks; ++q) {
+    const int b = q & 1;
+    if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);   // MMAs of chunk q-2 released this buffer
+    uint8_t* hi = base + (size_t)b * 2 * kGramStage;
+    uint8_t* lo2 = hi + kGramStage;
+    const int r0 = q * GKC;
+    // 64 panel columns x 8 groups of 4 rows = 512 items; thread: column c (lane-consecutive), 4 groups
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int c = lane + 32 * (warp & 1);
+      const int rg = (warp >> 1) + 2 * it;
+      const int r = r0 + 4 * rg;
+      const float2* src = th + (int64_t)colof(c, I, J) * m + r;
+      float re[4], im[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float2 v = (r + u < m) ? src[u] : make_float2(0.f, 0.f);
+        re[u] = v.x;
+        im[u] = v.y;
+      }
+      float4 rh, rl, ih, il;
+      tc::split_tf32(re[0], rh.x, rl.x); tc::split_tf32(re[1], rh.y, rl.y);
+      tc::split_tf32(re[2], rh.z, rl.z); tc::split_tf32(re[3], rh.w, rl.w);
+      tc::split_tf32(im[0], ih.x, il.x); tc::split_tf32(im[1], ih.y, il.y);
+      tc::split_tf32(im[2], ih.z, il.z); tc::split_tf32(im[3], ih.w, il.w);
+      rl.x *= 2.f; rl.y *= 2.f; rl.z *= 2.f; rl.w *= 2.f;
+      il.x *= 2.f; il.y *= 2.f; il.z *= 2.f; il.w *= 2.f;
+      const uint32_t oR = tc::kmaj_off(c, 4 * rg, G_LBO, G_SBO), oI = tc::kmaj_off(64 + c, 4 * rg, G_LBO, G_SBO);
+      *reinterpret_cast<float4*>(hi + oR) = rh;
+      *reinterpret_cast<float4*>(lo2 + oR) = rl;
+      *reinterpret_cast<float4*>(hi + oI) = ih;
+      *reinterpret_cast<float4*>(lo2 + oI) = il;
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+      const uint32_t ah = tc::smem_u32(hi), al = tc::smem_u32(lo2);
+#pragma unroll
+      for (int s = 0; s < GKC / 8; ++s) {
+        const uint32_t off = 2 * s * G_LBO;
+        const uint64_t dh = tc::make_desc(ah + off, G_LBO, G_SBO), dl = tc::make_desc(al + off, G_LBO, G_SBO);
+        tc::mma_tf32(tmem, dh, dh, idesc, (q > 0 || s > 0) ? 1u : 0u);
+        tc::mma_tf32(tmem, dh, dl, idesc, 1u);
+      }
+      tc::mma_commit(&mbar[b]);
+    }
+    __syncwarp();
+  }
+  // all MMAs done (the last commit tracks every earlier MMA of the issuing thread)
+  tc::mbar_wait(&mbar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+  tc::fence_after_sync();
+  float* Ds = reinterpret_cast<float*>(base);  // [128][129]
+  const int row = warp * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 8) {
+    float v[8];
+    tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Ds[row * 129 + c + i] = v[i];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+  float2* Gout = reinterpret_cast<float2*>(slab + gd.ws_log) + (size_t)pair * 64 * 64;
+  auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
+  for (int x = tid; x < 64 * 64; x += 128) {
+    const int p = x >> 6, qq = x & 63;
+    Gout[x] = make_float2(sym(p, qq) + sym(64 + p, 64 + qq), sym(p, 64 + qq) - sym(64 + p, qq));
+  }
+}
+
+// ---- inner Jacobi on G -> E = W - I images. grid (pairs max, count); 256 threads.
+// G is rotated in FP32 (it only steers the rotations); every 2x2 rotation is renormalised in
+// FP64 (c = 1/sqrt(1+t^2), s = c t, |e| = 1) and accumulated into W in FP64, so W is unitary to
+// ~1e-15 whatever the FP32 rounding of G (the applied block rotation must not drift from
+// unitarity: DESIGN.md "Precision").
+__global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                  int rnd, uint8_t* slab, LargeCtl* ctl, const double* norm2,
+                                                  int inner_sweeps) {
+  const int gi = blockIdx.y;
+  if (ctl[gi].conv) return;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  const int pairs = gd.n_pad / PWC;
+  const float2* Gin = reinterpret_cast<const float2*>(slab + gd.ws_log) + (size_t)pair * 64 * 64;
+  float* Eimg = reinterpret_cast<float*>(slab + gd.ws_log + Scratch::gram_bytes(pairs)) + (size_t)pair * EIMG_FLOATS;
+  int32_t* rflag = reinterpret_cast<int32_t*>(slab + gd.ws_log + Scratch::gram_bytes(pairs) + Scratch::eimg_bytes(pairs));
+  extern __shared__ __align__(16) uint8_t dsm[];
+  double2(*Ws)[65] = reinterpret_cast<double2(*)[65]>(dsm);
+  float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(dsm + sizeof(double2) * 64 * 65);
+  __shared__ double rcd[32][4];
+  __shared__ float rcf[32][4];
+  __shared__ int s_any, s_inner;
+  const int tid = threadIdx.x;
+  for (int x = tid; x < 64 * 64; x += 256) {
+    const int a = x >> 6, b = x & 63;
+    Gs[a][b] = Gin[x];
+    Ws[a][b] = make_double2(a == b ? 1.0 : 0.0, 0.0);
+  }
+  if (tid == 0) s_any = 0;
+  __syncthreads();
+  const float skip = (float)(norm2[gi] * 3.552713678800501e-15);  // (2^-24)^2 ||theta||^2
+  const float tol = fmaxf(7.62939453125e-6f, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
+  for (int x = tid; x < 64 * 64; x += 256) {
+    const int p = x >> 6, q = x & 63;
+    if (p < q) {
+      const float al = Gs[p][p].x, be = Gs[q][q].x;
+      const float g = sqrtf(Gs[p][q].x * Gs[p][q].x + Gs[p][q].y * Gs[p][q].y);
+      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) s_any = 1;
+    }
+  }
+  __syncthreads();
+  if (!s_any) {
+    if (tid == 0) rflag[pair] = 0;
+    return;
+  }
+  if (tid == 0) {
+    rflag[pair] = 1;
+    atomicAdd(&ctl[gi].rot, 1);
+  }
+  const int grp = tid >> 3, t8 = tid & 7;
+  for (int isw = 0; isw < inner_sweeps; ++isw) {
+    if (tid == 0) s_inner = 0;
+    __syncthreads();
+    for (int rr = 0; rr < 63; ++rr) {
+      int p, q;
+      circle_pair(grp, rr, 64, p, q);
+      if (t8 == 0) {
+        const float al = Gs[p][p].x, be = Gs[q][q].x;
+        const float2 gm = Gs[p][q];
+        const float g = sqrtf(gm.x * gm.x + gm.y * gm.y);
+        double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
+        if (fminf(al, be) > skip && g > 3e-7f * sqrtf(al) * sqrtf(be)) {
+          const float zeta = (be - al) / (2.f * g);
+          const float az = fabsf(zeta);
+          const float hyp = az > 1.f ? az * sqrtf(1.f + 1.f / (az * az)) : sqrtf(1.f + az * az);
+          const double t = (double)((zeta >= 0.f ? 1.f : -1.f) / (az + hyp));
+          c = rsqrt(1.0 + t * t);
+          s = c * t;
+          const double gr = gm.x, gi2 = gm.y, ginv = rsqrt(gr * gr + gi2 * gi2);
+          er = gr * ginv;
+          ei = gi2 * ginv;
+          s_inner = 1;
+        }
+        rcd[grp][0] = c; rcd[grp][1] = s; rcd[grp][2] = er; rcd[grp][3] = ei;
+        rcf[grp][0] = (float)c; rcf[grp][1] = (float)s; rcf[grp][2] = (float)er; rcf[grp][3] = (float)ei;
+      }
+      __syncthreads();
+      if (rcf[grp][1] != 0.f) {
+        const float c = rcf[grp][0], s = rcf[grp][1], er = rcf[grp][2], ei = rcf[grp][3];
+        const double cd = rcd[grp][0], sd = rcd[grp][1], erd = rcd[grp][2], eid = rcd[grp][3];
+#pragma unroll 2
+        for (int x = t8; x < 64; x += 8) {   // columns: G J (FP32) and W J (FP64)
+          float2 a = Gs[x][p], b = Gs[x][q];
+          float2 eb = make_float2(er * b.x + ei * b.y, er * b.y - ei * b.x);
+          Gs[x][p] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
+          Gs[x][q] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
+          double2 ad = Ws[x][p], bd = Ws[x][q];
+          double2 ebd = make_double2(erd * bd.x + eid * bd.y, erd * bd.y - eid * bd.x);
+          Ws[x][p] = make_double2(cd * ad.x - sd * ebd.x, cd * ad.y - sd * ebd.y);
+          Ws[x][q] = make_double2(sd * ad.x + cd * ebd.x, sd * ad.y + cd * ebd.y);
+        }
+      }
+      __syncthreads();
+      if (rcf[grp][1] != 0.f) {
+        const float c = rcf[grp][0], s = rcf[grp][1], er = rcf[grp][2], ei = rcf[grp][3];
+#pragma unroll 2
+        for (int x = t8; x < 64; x += 8) {   // rows: J^H G
+          float2 a = Gs[p][x], b = Gs[q][x];
+          float2 eb = make_float2(er * b.x - ei * b.y, er * b.y + ei * b.x);
+          Gs[p][x] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
+          Gs[q][x] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
+        }
+      }
+      __syncthreads();
+    }
+    const bool again = s_inner != 0;
+    __syncthreads();
+    if (!again) break;
+  }
+  // E = W - I as the rotation's B images, 3-way TF32 split (hi, mid, lo), Re then Im:
+  // element (n = output col, k = input col) = E[k][n]
+  for (int x = tid; x < 64 * 64; x += 256) {
+    const int k = x >> 6, n = x & 63;
+    double2 w = Ws[k][n];
+    if (k == n) w.x -= 1.0;
+    const uint32_t o = tc::kmaj_off(n, k, E_LBO, E_SBO) >> 2;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const double v = part ? w.y : w.x;
+      const float h = tc::tf32_trunc((float)v);
+      const double r1 = v - (double)h;
+      const float md = tc::tf32_trunc((float)r1);
+      const float lo = (float)(r1 - (double)md);
+      Eimg[(3 * part + 0) * 4096 + o] = h;
+      Eimg[(3 * part + 1) * 4096 + o] = md;
+      Eimg[(3 * part + 2) * 4096 + o] = lo;
+    }
+  }
+}
+
+// ---- P <- P + P E for theta (m rows) and V (n_pad rows) panels. grid (pairs max, count); 128 threads.
+// The 128-row tile (64 complex columns, 64 KB) arrives in shared memory by cp.async (all of it in
+// flight at once); its 8-column chunks are split into TF32 hi/mid/lo images (double-buffered) for
+// the MMAs, and the epilogue adds D to the raw tile (no second global read).
+__global__ void __launch_bounds__(128) k_tc_rot(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                int rnd, uint8_t* slab, const LargeCtl* ctl) {
+  const int gi = blockIdx.y;
+  if (ctl[gi].conv) return;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  const int pairs = gd.n_pad / PWC;
+  const int32_t* rflag =
+      reinterpret_cast<const int32_t*>(slab + gd.ws_log + Scratch::gram_bytes(pairs) + Scratch::eimg_bytes(pairs));
+  if (!rflag[pair]) return;
+  int I, J;
+  circle_pair(pair, rnd, nb, I, J);
+  const float* Eg = reinterpret_cast<const float*>(slab + gd.ws_log + Scratch::gram_bytes(pairs)) + (size_t)pair * EIMG_FLOATS;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  float* Es = reinterpret_cast<float*>(base);                           // 96 KB: Re h|m|l, Im h|m|l
+  float2* raw = reinterpret_cast<float2*>(base + (size_t)EIMG_FLOATS * 4);   // [64 cols][128 rows]
+  uint8_t* stg = reinterpret_cast<uint8_t*>(raw + 64 * 128);            // 2 stages x 3 images x 8 KB
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int m = gd.m, np = gd.n_pad;
+  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128;
+  // stage E (cp.async, 16 B each) and the first tile
+  for (int x = tid; x < EIMG_FLOATS / 4; x += 128) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
+  auto issue_tile = [&](int tile) {
+    const bool isV = tile >= tiles_th;
+    const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+    const int rows = isV ? np : m;
+    const int r0 = (isV ? tile - tiles_th : tile) * 128;
+    // 64 columns x 128 rows x 8 B = 4096 x 16 B; 16 B = 2 rows of one column
+    for (int x = tid; x < 64 * 64; x += 128) {
+      const int c = x >> 6, rp = (x & 63) * 2;
+      float2* dst = raw + c * 128 + rp;
+      if (r0 + rp + 1 < rows) {
+        tc::cp_async16(dst, M + (int64_t)colof(c, I, J) * rows + r0 + rp);
+      } else {
+        dst[0] = (r0 + rp < rows) ? M[(int64_t)colof(c, I, J) * rows + r0 + rp] : make_float2(0.f, 0.f);
+        dst[1] = make_float2(0.f, 0.f);
+      }
+    }
+    tc::cp_async_commit();
+  };
+  issue_tile(0);
+  if (warp == 0) tc::tmem_alloc(&tbase, 128);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_barrier_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tbase;
+  const uint32_t id_p = tc::make_idesc_tf32(128, 64, false, false);
+  const uint32_t id_n = id_p | (1u << 14);   // negate B (-E_im)
+  const uint32_t e0 = tc::smem_u32(Es);
+  constexpr uint32_t EI = 16384;             // bytes per E image
+  int chunk_ctr = 0;
+  for (int tile = 0; tile < tiles_th + tiles_v; ++tile) {
+    const bool isV = tile >= tiles_th;
+    float2* M = reinterpret_cast<float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+    const int rows = isV ? np : m;
+    const int r0 = (isV ? tile - tiles_th : tile) * 128;
+    const int r = r0 + tid;
+    tc::cp_async_wait_all();
+    __syncthreads();   // the raw tile (and E) are visible to every thread
+    for (int q = 0; q < PWC / 8; ++q, ++chunk_ctr) {
+      const int b = chunk_ctr & 1;
+      if (chunk_ctr >= 2) tc::mbar_wait(&mbar[b], ((chunk_ctr - 2) >> 1) & 1);
+      uint8_t* im0 = stg + (size_t)b * 3 * kRotStage;
+      // thread = row; complex columns 8q..8q+7 -> K 0..7 (Re) and 8..15 (Im), 3-way split
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 v[2][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 z = raw[(8 * q + 4 * h + u) * 128 + tid];
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const float x = part ? z.y : z.x;
+            const float hi = tc::tf32_trunc(x);
+            const float md = tc::tf32_trunc(x - hi);
+            const float lo = (x - hi) - md;
+            reinterpret_cast<float*>(&v[part][0])[u] = hi;
+            reinterpret_cast<float*>(&v[part][1])[u] = md;
+            reinterpret_cast<float*>(&v[part][2])[u] = lo;
+          }
+        }
+        const uint32_t oR = tc::kmaj_off(tid, 4 * h, R_LBO, R_SBO), oI = tc::kmaj_off(tid, 8 + 4 * h, R_LBO, R_SBO);
+#pragma unroll
+        for (int lvl = 0; lvl < 3; ++lvl) {
+          *reinterpret_cast<float4*>(im0 + lvl * kRotStage + oR) = v[0][lvl];
+          *reinterpret_cast<float4*>(im0 + lvl * kRotStage + oI) = v[1][lvl];
+        }
+      }
+      tc::fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t a0 = tc::smem_u32(im0);
+        uint64_t aR[3], aI[3], bR[3], bI[3];
+        const uint32_t eoff = 2 * q * E_LBO;   // input columns 8q..8q+7
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          aR[l] = tc::make_desc(a0 + l * kRotStage, R_LBO, R_SBO);
+          aI[l] = tc::make_desc(a0 + l * kRotStage + 2 * R_LBO, R_LBO, R_SBO);
+          bR[l] = tc::make_desc(e0 + l * EI + eoff, E_LBO, E_SBO);
+          bI[l] = tc::make_desc(e0 + (3 + l) * EI + eoff, E_LBO, E_SBO);
+        }
+        const uint32_t dRe = tmem, dIm = tmem + 64;
+        // products of total split order <= 2: (h,h) (h,m) (m,h) (h,l) (m,m) (l,h)
+        const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
+        // D_re += Re E_re - Im E_im ; D_im += Re E_im + Im E_re
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          const uint32_t acc = (q > 0 || t > 0) ? 1u : 0u;
+          tc::mma_tf32(dRe, aR[pa[t]], bR[pb[t]], id_p, acc);
+          tc::mma_tf32(dIm, aR[pa[t]], bI[pb[t]], id_p, acc);
+        }
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          tc::mma_tf32(dRe, aI[pa[t]], bI[pb[t]], id_n, 1u);
+          tc::mma_tf32(dIm, aI[pa[t]], bR[pb[t]], id_p, 1u);
+        }
+        tc::mma_commit(&mbar[b]);
+      }
+      __syncwarp();
+    }
+    // wait for this tile's MMAs, then P' = P + D (thread = row), P from the raw tile
+    tc::mbar_wait(&mbar[(chunk_ctr - 1) & 1], ((chunk_ctr - 1) >> 1) & 1);
+    tc::fence_after_sync();
+#pragma unroll 1
+    for (int c = 0; c < PWC; c += 8) {
+      float dr[8], di[8];
+      tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, dr);
+      tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 64 + c, di);
+      if (r < rows) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float2 v = raw[(c + u) * 128 + tid];
+          M[(int64_t)colof(c + u, I, J) * rows + r] = make_float2(v.x + dr[u], v.y + di[u]);
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();   // TMEM and raw reads done before the next tile overwrites them
+    if (tile + 1 < tiles_th + tiles_v) issue_tile(tile + 1);
+  }
+  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+}
+
+// ---- FP64-anchored polish of the spectrum (after convergence). With B = theta V (FP64-accumulated,
+// stored FP32 in the theta workspace) and C = B^H B, the Rayleigh values c_j = C_jj / |v_j|^2 are
+// exact eigenvalues of C only if the off-diagonal C_lj vanish; the FP32 accumulation of V leaves
+// |C_lj| ~ 1e-6 sigma_l sigma_j, which contaminates a small sigma_j^2 by ~|C_lj|^2 / sigma_l^2.
+// Every pair (l, j) contributes the exact 2x2 eigenvalue shift
+//   delta_j = sgn(c_j - c_l) g^2 / (|c_j - c_l|/2 + sqrt((c_j - c_l)^2/4 + g^2)),
+//   g^2 = |C_lj|^2 / (|v_l|^2 |v_j|^2)
+// (second-order perturbation, bounded for near-degenerate pairs), summed over l. C_lj comes from the
+// tensor core (3xTF32: ~2^-22 |b_l||b_j|, far below the |C_lj| it measures); c_j from the FP64
+// Rayleigh quotient. Grid (n_pad/64 pairs, count, n_pad/32 - 1 rounds): the circle method's rounds
+// enumerate every block pair once; round 0 also covers the pairs inside each block.
+__global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                   uint8_t* slab) {
+  const int gi = blockIdx.y, rnd = blockIdx.z;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  int I, J;
+  circle_pair(pair, rnd, nb, I, J);
+  const int m = gd.m, n = gd.n, np = gd.n_pad;
+  if (I * TB >= n && J * TB >= n) return;
+  const float2* __restrict__ th = reinterpret_cast<const float2*>(slab + gd.ws_theta);   // B (m x n)
+  const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
+  double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
+  const double* den = shift + np;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tc::tmem_alloc(&tbase, 128);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_barrier_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tbase;
+  const uint32_t idesc = tc::make_idesc_tf32(128, 128, false, false);
+  const int nchunks = (m + GKC - 1) / GKC;
+  for (int q = 0; q < nchunks; ++q) {
+    const int b = q & 1;
+    if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);
+    uint8_t* hi = base + (size_t)b * 2 * kGramStage;
+    uint8_t* lo2 = hi + kGramStage;
+    const int r0 = q * GKC;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int c = lane + 32 * (warp & 1);
+      const int rg = (warp >> 1) + 2 * it;
+      const int r = r0 + 4 * rg;
+      const int col = colof(c, I, J);
+      float re[4], im[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float2 v = (r + u < m && col < n) ? th[(int64_t)col * m + r + u] : make_float2(0.f, 0.f);
+        re[u] = v.x;
+        im[u] = v.y;
+      }
+      float4 rh, rl, ih, il;
+      tc::split_tf32(re[0], rh.x, rl.x); tc::split_tf32(re[1], rh.y, rl.y);
+      tc::split_tf32(re[2], rh.z, rl.z); tc::split_tf32(re[3], rh.w, rl.w);
+      tc::split_tf32(im[0], ih.x, il.x); tc::split_tf32(im[1], ih.y, il.y);
+      tc::split_tf32(im[2], ih.z, il.z); tc::split_tf32(im[3], ih.w, il.w);
+      rl.x *= 2.f; rl.y *= 2.f; rl.z *= 2.f; rl.w *= 2.f;
+      il.x *= 2.f; il.y *= 2.f; il.z *= 2.f; il.w *= 2.f;
+      const uint32_t oR = tc::kmaj_off(c, 4 * rg, G_LBO, G_SBO), oI = tc::kmaj_off(64 + c, 4 * rg, G_LBO, G_SBO);
+      *reinterpret_cast<float4*>(hi + oR) = rh;
+      *reinterpret_cast<float4*>(lo2 + oR) = rl;
+      *reinterpret_cast<float4*>(hi + oI) = ih;
+      *reinterpret_cast<float4*>(lo2 + oI) = il;
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+      const uint32_t ah = tc::smem_u32(hi), al = tc::smem_u32(lo2);
+#pragma unroll
+      for (int st2 = 0; st2 < GKC / 8; ++st2) {
+        const uint32_t off = 2 * st2 * G_LBO;
+        const uint64_t dh = tc::make_desc(ah + off, G_LBO, G_SBO), dl = tc::make_desc(al + off, G_LBO, G_SBO);
+        tc::mma_tf32(tmem, dh, dh, idesc, (q > 0 || st2 > 0) ? 1u : 0u);
+        tc::mma_tf32(tmem, dh, dl, idesc, 1u);
+      }
+      tc::mma_commit(&mbar[b]);
+    }
+    __syncwarp();
+  }
+  tc::mbar_wait(&mbar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+  tc::fence_after_sync();
+  float* Ds = reinterpret_cast<float*>(base);  // [128][129]
+  const int row = warp * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 8) {
+    float v[8];
+    tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Ds[row * 129 + c + i] = v[i];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+  // thread j (< 64) = panel column j; partners: the other block (always) and its own block (round 0)
+  if (tid < 64) {
+    const int j = tid, cj = colof(j, I, J);
+    if (cj < n) {
+      const double aj = s2[cj], dj = den[cj];
+      auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
+      double acc = 0.0;
+      const int other0 = j < TB ? TB : 0;
+      const int own0 = j < TB ? 0 : TB;
+      for (int pass = 0; pass < (rnd == 0 ? 2 : 1); ++pass) {
+        const int l0 = pass == 0 ? other0 : own0;
+        for (int l = l0; l < l0 + TB; ++l) {
+          const int cl = colof(l, I, J);
+          if (l == j || cl >= n) continue;
+          const double gr = sym(l, j) + sym(64 + l, 64 + j), gim = sym(l, 64 + j) - sym(64 + l, j);
+          const double g2 = (gr * gr + gim * gim) / (dj * den[cl]);
+          const double dlt = aj - s2[cl];
+          const double h = 0.5 * fabs(dlt);
+          const double sh = g2 / (h + sqrt(h * h + g2));
+          acc += dlt >= 0.0 ? sh : -sh;
+        }
+      }
+      atomicAdd(&shift[cj], acc);
+    }
+  }
+}
+
+}  // namespace tcj
 
 }  // namespace
 
@@ -423,6 +1003,67 @@ int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_l
   cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st);
   launches += 2;
+  return launches;
+}
+
+size_t svd_tc_scratch_bytes(int n_pad) { return tcj::Scratch::total(n_pad / tcj::PWC); }
+
+int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
+               int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_scratch, int32_t* h_pinned_flag, cudaStream_t s,
+               int* error_out) {
+  *error_out = 0;
+  if (count <= 0) return 0;
+  int launches = 0;
+  int max_np = 0, max_n = 0;
+  for (int g = 0; g < count; ++g) {
+    max_np = max(max_np, h_desc[h_list[g]].n_pad);
+    max_n = max(max_n, h_desc[h_list[g]].n);
+  }
+  LargeCtl* ctl = reinterpret_cast<LargeCtl*>(d_scratch);
+  double* norm2 = reinterpret_cast<double*>(d_scratch + 2 * ((count + 1) & ~1));
+  int32_t* unconv = reinterpret_cast<int32_t*>(norm2 + count);
+  cudaMemsetAsync(ctl, 0, sizeof(LargeCtl) * count, s);
+  k_large_init<<<dim3(256, count), 256, 0, s>>>(d_desc, d_list, slab);
+  k_large_norm<<<count, 256, 0, s>>>(d_desc, d_list, slab, norm2);
+  launches += 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
+    cudaFuncSetAttribute(tcj::k_tc_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kInnerSmem);
+    cudaFuncSetAttribute(tcj::k_tc_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotSmem);
+    attr = true;
+  }
+  const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
+  const dim3 grid(pairs_max, count);
+  int sweep = 0;
+  bool done = false;
+  for (; sweep < max_sweeps && !done; ++sweep) {
+    for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
+      tcj::k_tc_gram<<<grid, 128, tcj::kGramSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, 2);
+      tcj::k_tc_rot<<<grid, 128, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      launches += 3;
+    }
+    k_block_check<<<1, 256, 0, s>>>(d_desc, d_list, count, ctl, unconv, 0);
+    ++launches;
+    cudaMemcpyAsync(h_pinned_flag, unconv, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    done = (*h_pinned_flag == 0);
+  }
+  if (!done) *error_out = -6;
+  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
+  static bool pattr = false;
+  if (!pattr) {
+    cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
+    pattr = true;
+  }
+  tcj::k_tc_polish<<<dim3(pairs_max, count, nb_max - 1), 128, tcj::kGramSmem, s>>>(d_desc, d_list, slab);
+  int npow2 = 1;
+  while (npow2 < max_n) npow2 <<= 1;
+  size_t smem = (size_t)npow2 * 12 + 16 + 1024 * 8;
+  cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
+  launches += 3;
   return launches;
 }
 
