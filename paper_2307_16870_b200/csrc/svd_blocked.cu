@@ -13,6 +13,9 @@
 // the same fixed point as the scalar method (all column pairs orthogonal to tol); the block
 // rotation is the GEMM-shaped step that the tensor-core path will take over.
 // Then sigma_j^2 = ||theta v_j||^2/||v_j||^2 (Rayleigh, FP64 accumulation) and sort + tails.
+#include <cstdio>
+#include <cstdlib>
+
 #include "eamps_internal.cuh"
 #include "sort_tails.cuh"
 #include "tc_common.cuh"
@@ -249,8 +252,8 @@ __global__ void __launch_bounds__(256) k_block_round(const GateDesc* __restrict_
 
 __global__ void k_block_check(GateDesc* desc, const int32_t* list, int count, LargeCtl* ctl, int32_t* unconv,
                               int final_sweep) {
-  __shared__ int cnt;
-  if (threadIdx.x == 0) cnt = 0;
+  __shared__ int cnt, tot;
+  if (threadIdx.x == 0) cnt = tot = 0;
   __syncthreads();
   for (int g = threadIdx.x; g < count; g += blockDim.x) {
     if (ctl[g].conv) continue;
@@ -258,10 +261,14 @@ __global__ void k_block_check(GateDesc* desc, const int32_t* list, int count, La
     gd.sweeps += 1;
     if (ctl[g].rot == 0) ctl[g].conv = 1;
     else atomicAdd(&cnt, 1);
+    atomicAdd(&tot, ctl[g].rot);
     ctl[g].rot = 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) *unconv = cnt;
+  if (threadIdx.x == 0) {
+    unconv[0] = cnt;
+    unconv[1] = tot;   // rotated block pairs this sweep (diagnostics)
+  }
   (void)final_sweep;
 }
 
@@ -417,12 +424,12 @@ constexpr int GKC = 32;         // rows per Gram K-chunk
 constexpr uint32_t G_SBO = 128, G_LBO = (128 / 8) * 128;   // Gram operand image: 128 rows (panel re/im cols)
 constexpr uint32_t E_SBO = 128, E_LBO = (64 / 8) * 128;    // E image: 64 rows (output cols) x 64 k
 constexpr uint32_t R_SBO = 128, R_LBO = (128 / 8) * 128;   // rotation A image: 128 rows x 16 k
-constexpr int EIMG_FLOATS = 6 * 64 * 64;                   // Re hi|mid|lo, Im hi|mid|lo
+constexpr int EIMG_FLOATS = 4 * 64 * 64;                   // Re hi|lo, Im hi|lo
 constexpr size_t kGramStage = (size_t)128 * GKC * 4;        // one image (hi or lo2) of a chunk: 16 KB
-constexpr size_t kGramSmem = (size_t)128 * 129 * 4 + 1024;  // >= 2 stages x 2 images (64 KB); D staging
+constexpr size_t kGramSmem = 4 * (size_t)128 * 32 * 4 + 2 * (size_t)64 * 288 + 1024;  // images | raw ring (>= D staging)
 constexpr size_t kRotStage = (size_t)128 * 16 * 4;          // one image of a 128 x 16 chunk: 8 KB
-constexpr size_t kRotSmem = (size_t)EIMG_FLOATS * 4 + (size_t)64 * 128 * 8 + 2 * 3 * kRotStage + 1024;
-constexpr size_t kInnerSmem = (sizeof(double2) + sizeof(float2)) * 64 * 65;
+constexpr size_t kRotSmem = (size_t)EIMG_FLOATS * 4 + 2 * (size_t)64 * 128 * 8 + 2 * 2 * kRotStage + 1024;
+constexpr size_t kInnerSmem = 2 * sizeof(float2) * 64 * 65;
 
 struct Scratch {                  // per gate: slab offset of its TC scratch (GateDesc::ws_log)
   static __host__ __device__ size_t gram_bytes(int pairs) { return (size_t)pairs * 64 * 64 * 8; }
@@ -432,60 +439,61 @@ struct Scratch {                  // per gate: slab offset of its TC scratch (Ga
 
 __device__ __forceinline__ int colof(int c, int I, int J) { return c < TB ? I * TB + c : J * TB + (c - TB); }
 
-// ---- G = P^H P on the tensor core. grid (n_pad/64 pairs max, count); 128 threads.
-__global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
-                                                 int rnd, uint8_t* slab, const LargeCtl* ctl) {
-  const int gi = blockIdx.y;
-  if (ctl[gi].conv) return;
-  const GateDesc& gd = desc[list[gi]];
-  const int nb = gd.n_pad / TB, pair = blockIdx.x;
-  if (pair >= nb / 2 || rnd >= nb - 1) return;
-  int I, J;
-  circle_pair(pair, rnd, nb, I, J);
-  const int m = gd.m;
-  const float2* __restrict__ th = reinterpret_cast<const float2*>(slab + gd.ws_theta);
-  extern __shared__ __align__(1024) uint8_t dsm[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t mbar[2];
-  __shared__ uint32_t tbase;
+// ---- panel Gram on the tensor core: D (128 x 128 real, in shared memory Ds[128][129]) = Q^T Q,
+// Q = [Re P | Im P] of the 64 complex columns colof(0..63) of M (m rows, ld m; columns >= ncols read
+// as zero). Raw 32-row chunks arrive by cp.async through a GR-deep ring (pitch 288 B per column),
+// are split into TF32 hi / 2*lo images (double-buffered) and fed to 2 MMAs per k-step
+// (symmetric 3xTF32: D = sym(hi^T hi + hi^T 2lo)). 128 threads. Shared memory: kGramSmem.
+constexpr int GR = 2;                                   // raw ring depth
+constexpr uint32_t GRAW_PITCH = 288;                    // bytes per column of a raw chunk (32 rows + pad)
+constexpr size_t kGramRaw = (size_t)64 * GRAW_PITCH;    // 18 KB
+__device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, int ncols, int I, int J,
+                                           uint8_t* base, uint64_t* mbar, uint32_t tmem, float* Ds) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tc::tmem_alloc(&tbase, 128);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-    tc::fence_barrier_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = tbase;
-  const uint32_t idesc = tc::make_idesc_tf32(128, 128, false, false);
+  uint8_t* img = base;                                   // 2 x (hi, lo2) x 16 KB
+  uint8_t* ring = base + 4 * kGramStage;                 // GR x 18 KB
   const int nchunks = (m + GKC - 1) / GKC;
+  auto issue = [&](int q) {
+    if (q < nchunks) {
+      uint8_t* dst = ring + (size_t)(q % GR) * kGramRaw;
+      const int r0 = q * GKC;
+      // 64 columns x 32 rows x 8 B = 1024 x 16 B; 16 consecutive copies per column
+      for (int x = tid; x < 1024; x += 128) {
+        const int c = x >> 4, rp = (x & 15) * 2;
+        const int col = colof(c, I, J), r = r0 + rp;
+        float2* d = reinterpret_cast<float2*>(dst + c * GRAW_PITCH) + rp;
+        if (col < ncols && r + 1 < m) {
+          tc::cp_async16(d, M + (int64_t)col * m + r);
+        } else {
+          d[0] = (col < ncols && r < m) ? M[(int64_t)col * m + r] : make_float2(0.f, 0.f);
+          d[1] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    tc::cp_async_commit();   // (possibly empty) group: keeps the wait_group count uniform
+  };
+  for (int q = 0; q < GR - 1; ++q) issue(q);
+  const uint32_t idesc = tc::make_idesc_tf32(128, 128, false, false);
   for (int q = 0; q < nchunks; ++q) {
+    issue(q + GR - 1);
+    tc::cp_async_wait<GR - 1>();
+    __syncthreads();                                     // raw chunk q visible to all
     const int b = q & 1;
-    if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);   // MMAs of chunk q-2 released this buffer
-    uint8_t* hi = base + (size_t)b * 2 * kGramStage;
+    if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);
+    uint8_t* hi = img + (size_t)b * 2 * kGramStage;
     uint8_t* lo2 = hi + kGramStage;
-    const int r0 = q * GKC;
-    // 64 panel columns x 8 groups of 4 rows = 512 items; thread: column c (lane-consecutive), 4 groups
+    const uint8_t* raw = ring + (size_t)(q % GR) * kGramRaw;
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int c = lane + 32 * (warp & 1);
       const int rg = (warp >> 1) + 2 * it;
-      const int r = r0 + 4 * rg;
-      const float2* src = th + (int64_t)colof(c, I, J) * m + r;
-      float re[4], im[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float2 v = (r + u < m) ? src[u] : make_float2(0.f, 0.f);
-        re[u] = v.x;
-        im[u] = v.y;
-      }
+      const float4 v0 = *reinterpret_cast<const float4*>(raw + c * GRAW_PITCH + 32 * rg);
+      const float4 v1 = *reinterpret_cast<const float4*>(raw + c * GRAW_PITCH + 32 * rg + 16);
       float4 rh, rl, ih, il;
-      tc::split_tf32(re[0], rh.x, rl.x); tc::split_tf32(re[1], rh.y, rl.y);
-      tc::split_tf32(re[2], rh.z, rl.z); tc::split_tf32(re[3], rh.w, rl.w);
-      tc::split_tf32(im[0], ih.x, il.x); tc::split_tf32(im[1], ih.y, il.y);
-      tc::split_tf32(im[2], ih.z, il.z); tc::split_tf32(im[3], ih.w, il.w);
+      tc::split_tf32(v0.x, rh.x, rl.x); tc::split_tf32(v0.z, rh.y, rl.y);
+      tc::split_tf32(v1.x, rh.z, rl.z); tc::split_tf32(v1.z, rh.w, rl.w);
+      tc::split_tf32(v0.y, ih.x, il.x); tc::split_tf32(v0.w, ih.y, il.y);
+      tc::split_tf32(v1.y, ih.z, il.z); tc::split_tf32(v1.w, ih.w, il.w);
       rl.x *= 2.f; rl.y *= 2.f; rl.z *= 2.f; rl.w *= 2.f;
       il.x *= 2.f; il.y *= 2.f; il.z *= 2.f; il.w *= 2.f;
       const uint32_t oR = tc::kmaj_off(c, 4 * rg, G_LBO, G_SBO), oI = tc::kmaj_off(64 + c, 4 * rg, G_LBO, G_SBO);
@@ -495,7 +503,7 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
       *reinterpret_cast<float4*>(lo2 + oI) = il;
     }
     tc::fence_async_smem();
-    __syncthreads();
+    __syncthreads();                                     // images written; raw slot q%GR free
     if (tid == 0) {
       tc::fence_after_sync();
       const uint32_t ah = tc::smem_u32(hi), al = tc::smem_u32(lo2);
@@ -510,10 +518,10 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
     }
     __syncwarp();
   }
-  // all MMAs done (the last commit tracks every earlier MMA of the issuing thread)
+  tc::cp_async_wait<0>();
   tc::mbar_wait(&mbar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
   tc::fence_after_sync();
-  float* Ds = reinterpret_cast<float*>(base);  // [128][129]
+  __syncthreads();                                       // every thread past its last smem read
   const int row = warp * 32 + lane;
 #pragma unroll 1
   for (int c = 0; c < 128; c += 8) {
@@ -524,20 +532,52 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+}
+
+__device__ __forceinline__ void tc_setup(uint64_t* mbar, uint32_t* tbase) {
+  if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(tbase, 128);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_barrier_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// ---- G = P^H P of the round's panel. grid (n_pad/64 pairs max, count); 128 threads.
+__global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                 int rnd, uint8_t* slab, const LargeCtl* ctl) {
+  const int gi = blockIdx.y;
+  if (ctl[gi].conv) return;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  int I, J;
+  circle_pair(pair, rnd, nb, I, J);
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  tc_setup(mbar, &tbase);
+  float* Ds = reinterpret_cast<float*>(base);
+  gram_panel(reinterpret_cast<const float2*>(slab + gd.ws_theta), gd.m, gd.n_pad, I, J, base, mbar, tbase, Ds);
+  if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(tbase, 128);
   float2* Gout = reinterpret_cast<float2*>(slab + gd.ws_log) + (size_t)pair * 64 * 64;
   auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
-  for (int x = tid; x < 64 * 64; x += 128) {
+  for (int x = threadIdx.x; x < 64 * 64; x += 128) {
     const int p = x >> 6, qq = x & 63;
     Gout[x] = make_float2(sym(p, qq) + sym(64 + p, 64 + qq), sym(p, 64 + qq) - sym(64 + p, qq));
   }
 }
 
-// ---- inner Jacobi on G -> E = W - I images. grid (pairs max, count); 256 threads.
-// G is rotated in FP32 (it only steers the rotations); every 2x2 rotation is renormalised in
-// FP64 (c = 1/sqrt(1+t^2), s = c t, |e| = 1) and accumulated into W in FP64, so W is unitary to
-// ~1e-15 whatever the FP32 rounding of G (the applied block rotation must not drift from
-// unitarity: DESIGN.md "Precision").
+// ---- inner Jacobi on G -> E = W - I images. grid (pairs max, count); 256 threads, FP32.
+// One cyclic sweep (tournament order) of two-sided Jacobi on the 64 x 64 Hermitian G, the
+// rotations accumulated into W; each rotation is computed redundantly by the 8 threads of its
+// group (no broadcast round trip). W's FP32 drift from unitarity (~1e-6) is consistent between
+// theta and V (the same E rotates both) and is absorbed by the Rayleigh normalisation and the
+// FP64-anchored polish.
 __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                   int rnd, uint8_t* slab, LargeCtl* ctl, const double* norm2,
                                                   int inner_sweeps) {
@@ -551,31 +591,27 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   float* Eimg = reinterpret_cast<float*>(slab + gd.ws_log + Scratch::gram_bytes(pairs)) + (size_t)pair * EIMG_FLOATS;
   int32_t* rflag = reinterpret_cast<int32_t*>(slab + gd.ws_log + Scratch::gram_bytes(pairs) + Scratch::eimg_bytes(pairs));
   extern __shared__ __align__(16) uint8_t dsm[];
-  double2(*Ws)[65] = reinterpret_cast<double2(*)[65]>(dsm);
-  float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(dsm + sizeof(double2) * 64 * 65);
-  __shared__ double rcd[32][4];
-  __shared__ float rcf[32][4];
-  __shared__ int s_any, s_inner;
+  float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(dsm);
+  float2(*Ws)[65] = Gs + 64;
   const int tid = threadIdx.x;
   for (int x = tid; x < 64 * 64; x += 256) {
     const int a = x >> 6, b = x & 63;
     Gs[a][b] = Gin[x];
-    Ws[a][b] = make_double2(a == b ? 1.0 : 0.0, 0.0);
+    Ws[a][b] = make_float2(a == b ? 1.f : 0.f, 0.f);
   }
-  if (tid == 0) s_any = 0;
   __syncthreads();
   const float skip = (float)(norm2[gi] * 3.552713678800501e-15);  // (2^-24)^2 ||theta||^2
   const float tol = fmaxf(7.62939453125e-6f, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
+  int any = 0;
   for (int x = tid; x < 64 * 64; x += 256) {
     const int p = x >> 6, q = x & 63;
     if (p < q) {
       const float al = Gs[p][p].x, be = Gs[q][q].x;
       const float g = sqrtf(Gs[p][q].x * Gs[p][q].x + Gs[p][q].y * Gs[p][q].y);
-      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) s_any = 1;
+      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) any = 1;
     }
   }
-  __syncthreads();
-  if (!s_any) {
+  if (!__syncthreads_or(any)) {
     if (tid == 0) rflag[pair] = 0;
     return;
   }
@@ -585,51 +621,42 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   }
   const int grp = tid >> 3, t8 = tid & 7;
   for (int isw = 0; isw < inner_sweeps; ++isw) {
-    if (tid == 0) s_inner = 0;
-    __syncthreads();
+    int rot = 0;
     for (int rr = 0; rr < 63; ++rr) {
       int p, q;
       circle_pair(grp, rr, 64, p, q);
-      if (t8 == 0) {
-        const float al = Gs[p][p].x, be = Gs[q][q].x;
-        const float2 gm = Gs[p][q];
-        const float g = sqrtf(gm.x * gm.x + gm.y * gm.y);
-        double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
-        if (fminf(al, be) > skip && g > 3e-7f * sqrtf(al) * sqrtf(be)) {
-          const float zeta = (be - al) / (2.f * g);
-          const float az = fabsf(zeta);
-          const float hyp = az > 1.f ? az * sqrtf(1.f + 1.f / (az * az)) : sqrtf(1.f + az * az);
-          const double t = (double)((zeta >= 0.f ? 1.f : -1.f) / (az + hyp));
-          c = rsqrt(1.0 + t * t);
-          s = c * t;
-          const double gr = gm.x, gi2 = gm.y, ginv = rsqrt(gr * gr + gi2 * gi2);
-          er = gr * ginv;
-          ei = gi2 * ginv;
-          s_inner = 1;
-        }
-        rcd[grp][0] = c; rcd[grp][1] = s; rcd[grp][2] = er; rcd[grp][3] = ei;
-        rcf[grp][0] = (float)c; rcf[grp][1] = (float)s; rcf[grp][2] = (float)er; rcf[grp][3] = (float)ei;
+      const float al = Gs[p][p].x, be = Gs[q][q].x;
+      const float2 gm = Gs[p][q];
+      const float g2 = gm.x * gm.x + gm.y * gm.y;
+      float c = 1.f, s = 0.f, er = 1.f, ei = 0.f;
+      if (fminf(al, be) > skip && g2 > 1e-13f * al * be) {
+        const float ig = rsqrtf(g2);
+        er = gm.x * ig;
+        ei = gm.y * ig;
+        const float zeta = 0.5f * (be - al) * ig;
+        const float az = fabsf(zeta);
+        const float t = copysignf(1.f, zeta) / (az + sqrtf(fmaf(az, az, 1.f)));
+        c = rsqrtf(fmaf(t, t, 1.f));
+        s = c * t;
+        rot = 1;
       }
-      __syncthreads();
-      if (rcf[grp][1] != 0.f) {
-        const float c = rcf[grp][0], s = rcf[grp][1], er = rcf[grp][2], ei = rcf[grp][3];
-        const double cd = rcd[grp][0], sd = rcd[grp][1], erd = rcd[grp][2], eid = rcd[grp][3];
-#pragma unroll 2
-        for (int x = t8; x < 64; x += 8) {   // columns: G J (FP32) and W J (FP64)
+      __syncthreads();   // every group has read its 2x2 block before any column is rotated
+      if (s != 0.f) {
+#pragma unroll 4
+        for (int x = t8; x < 64; x += 8) {   // columns: G J and W J
           float2 a = Gs[x][p], b = Gs[x][q];
           float2 eb = make_float2(er * b.x + ei * b.y, er * b.y - ei * b.x);
           Gs[x][p] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
           Gs[x][q] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
-          double2 ad = Ws[x][p], bd = Ws[x][q];
-          double2 ebd = make_double2(erd * bd.x + eid * bd.y, erd * bd.y - eid * bd.x);
-          Ws[x][p] = make_double2(cd * ad.x - sd * ebd.x, cd * ad.y - sd * ebd.y);
-          Ws[x][q] = make_double2(sd * ad.x + cd * ebd.x, sd * ad.y + cd * ebd.y);
+          a = Ws[x][p]; b = Ws[x][q];
+          eb = make_float2(er * b.x + ei * b.y, er * b.y - ei * b.x);
+          Ws[x][p] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
+          Ws[x][q] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
         }
       }
       __syncthreads();
-      if (rcf[grp][1] != 0.f) {
-        const float c = rcf[grp][0], s = rcf[grp][1], er = rcf[grp][2], ei = rcf[grp][3];
-#pragma unroll 2
+      if (s != 0.f) {
+#pragma unroll 4
         for (int x = t8; x < 64; x += 8) {   // rows: J^H G
           float2 a = Gs[p][x], b = Gs[q][x];
           float2 eb = make_float2(er * b.x - ei * b.y, er * b.y + ei * b.x);
@@ -637,38 +664,32 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
           Gs[q][x] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
         }
       }
-      __syncthreads();
+      __syncthreads();   // rows written before the next round reads its 2x2 blocks
     }
-    const bool again = s_inner != 0;
-    __syncthreads();
-    if (!again) break;
+    if (!__syncthreads_or(rot)) break;
   }
-  // E = W - I as the rotation's B images, 3-way TF32 split (hi, mid, lo), Re then Im:
-  // element (n = output col, k = input col) = E[k][n]
+  __syncthreads();
+  // E = W - I as the rotation's B images (hi, lo), Re then Im: element (n = out col, k = in col) = E[k][n]
   for (int x = tid; x < 64 * 64; x += 256) {
     const int k = x >> 6, n = x & 63;
-    double2 w = Ws[k][n];
-    if (k == n) w.x -= 1.0;
+    float2 w = Ws[k][n];
+    if (k == n) w.x -= 1.f;
     const uint32_t o = tc::kmaj_off(n, k, E_LBO, E_SBO) >> 2;
-#pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      const double v = part ? w.y : w.x;
-      const float h = tc::tf32_trunc((float)v);
-      const double r1 = v - (double)h;
-      const float md = tc::tf32_trunc((float)r1);
-      const float lo = (float)(r1 - (double)md);
-      Eimg[(3 * part + 0) * 4096 + o] = h;
-      Eimg[(3 * part + 1) * 4096 + o] = md;
-      Eimg[(3 * part + 2) * 4096 + o] = lo;
-    }
+    float h, l;
+    tc::split_tf32(w.x, h, l);
+    Eimg[o] = h;
+    Eimg[4096 + o] = l;
+    tc::split_tf32(w.y, h, l);
+    Eimg[8192 + o] = h;
+    Eimg[12288 + o] = l;
   }
 }
 
-// ---- P <- P + P E for theta (m rows) and V (n_pad rows) panels. grid (pairs max, count); 128 threads.
-// The 128-row tile (64 complex columns, 64 KB) arrives in shared memory by cp.async (all of it in
-// flight at once); its 8-column chunks are split into TF32 hi/mid/lo images (double-buffered) for
-// the MMAs, and the epilogue adds D to the raw tile (no second global read).
-__global__ void __launch_bounds__(128) k_tc_rot(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+// ---- P <- P + P E for theta (m rows) and V (n_pad rows) panels. grid (pairs max, count); 256 threads.
+// Double-buffered raw 128-row tiles (64 KB each, cp.async: tile t+1 loads while tile t computes);
+// thread (row, half) splits 4 of each 8-column chunk into TF32 hi/lo images; 3xTF32 MMAs
+// (hi hi + hi lo + lo hi) for D_re/D_im with N = 64; epilogue P' = P + D from the raw tile.
+__global__ void __launch_bounds__(256) k_tc_rot(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                 int rnd, uint8_t* slab, const LargeCtl* ctl) {
   const int gi = blockIdx.y;
   if (ctl[gi].conv) return;
@@ -684,140 +705,123 @@ __global__ void __launch_bounds__(128) k_tc_rot(const GateDesc* __restrict__ des
   const float* Eg = reinterpret_cast<const float*>(slab + gd.ws_log + Scratch::gram_bytes(pairs)) + (size_t)pair * EIMG_FLOATS;
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
-  float* Es = reinterpret_cast<float*>(base);                           // 96 KB: Re h|m|l, Im h|m|l
-  float2* raw = reinterpret_cast<float2*>(base + (size_t)EIMG_FLOATS * 4);   // [64 cols][128 rows]
-  uint8_t* stg = reinterpret_cast<uint8_t*>(raw + 64 * 128);            // 2 stages x 3 images x 8 KB
+  float* Es = reinterpret_cast<float*>(base);                            // 64 KB: Re h|l, Im h|l
+  float2* rawb = reinterpret_cast<float2*>(base + (size_t)EIMG_FLOATS * 4);   // 2 x [64 cols][128 rows]
+  uint8_t* stg = reinterpret_cast<uint8_t*>(rawb + 2 * 64 * 128);       // 2 stages x (hi, lo) x 8 KB
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tbase;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, row_l = tid & 127, half = tid >> 7;
   const int m = gd.m, np = gd.n_pad;
-  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128;
-  // stage E (cp.async, 16 B each) and the first tile
-  for (int x = tid; x < EIMG_FLOATS / 4; x += 128) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
+  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128, ntiles = tiles_th + tiles_v;
+  for (int x = tid; x < EIMG_FLOATS / 4; x += 256) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
   auto issue_tile = [&](int tile) {
-    const bool isV = tile >= tiles_th;
-    const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
-    const int rows = isV ? np : m;
-    const int r0 = (isV ? tile - tiles_th : tile) * 128;
-    // 64 columns x 128 rows x 8 B = 4096 x 16 B; 16 B = 2 rows of one column
-    for (int x = tid; x < 64 * 64; x += 128) {
-      const int c = x >> 6, rp = (x & 63) * 2;
-      float2* dst = raw + c * 128 + rp;
-      if (r0 + rp + 1 < rows) {
-        tc::cp_async16(dst, M + (int64_t)colof(c, I, J) * rows + r0 + rp);
-      } else {
-        dst[0] = (r0 + rp < rows) ? M[(int64_t)colof(c, I, J) * rows + r0 + rp] : make_float2(0.f, 0.f);
-        dst[1] = make_float2(0.f, 0.f);
+    if (tile < ntiles) {
+      const bool isV = tile >= tiles_th;
+      const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+      const int rows = isV ? np : m;
+      const int r0 = (isV ? tile - tiles_th : tile) * 128;
+      float2* raw = rawb + (tile & 1) * 64 * 128;
+      for (int x = tid; x < 64 * 64; x += 256) {
+        const int c = x >> 6, rp = (x & 63) * 2;
+        float2* dst = raw + c * 128 + rp;
+        if (r0 + rp + 1 < rows) {
+          tc::cp_async16(dst, M + (int64_t)colof(c, I, J) * rows + r0 + rp);
+        } else {
+          dst[0] = (r0 + rp < rows) ? M[(int64_t)colof(c, I, J) * rows + r0 + rp] : make_float2(0.f, 0.f);
+          dst[1] = make_float2(0.f, 0.f);
+        }
       }
     }
     tc::cp_async_commit();
   };
   issue_tile(0);
-  if (warp == 0) tc::tmem_alloc(&tbase, 128);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-    tc::fence_barrier_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
+  tc_setup(mbar, &tbase);
   const uint32_t tmem = tbase;
   const uint32_t id_p = tc::make_idesc_tf32(128, 64, false, false);
   const uint32_t id_n = id_p | (1u << 14);   // negate B (-E_im)
   const uint32_t e0 = tc::smem_u32(Es);
   constexpr uint32_t EI = 16384;             // bytes per E image
   int chunk_ctr = 0;
-  for (int tile = 0; tile < tiles_th + tiles_v; ++tile) {
+  for (int tile = 0; tile < ntiles; ++tile) {
     const bool isV = tile >= tiles_th;
     float2* M = reinterpret_cast<float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
     const int rows = isV ? np : m;
     const int r0 = (isV ? tile - tiles_th : tile) * 128;
-    const int r = r0 + tid;
-    tc::cp_async_wait_all();
-    __syncthreads();   // the raw tile (and E) are visible to every thread
+    const float2* raw = rawb + (tile & 1) * 64 * 128;
+    issue_tile(tile + 1);                    // its buffer was released by tile - 1's epilogue
+    tc::cp_async_wait<1>();
+    __syncthreads();                         // raw tile (and E) visible to every thread
     for (int q = 0; q < PWC / 8; ++q, ++chunk_ctr) {
       const int b = chunk_ctr & 1;
       if (chunk_ctr >= 2) tc::mbar_wait(&mbar[b], ((chunk_ctr - 2) >> 1) & 1);
-      uint8_t* im0 = stg + (size_t)b * 3 * kRotStage;
-      // thread = row; complex columns 8q..8q+7 -> K 0..7 (Re) and 8..15 (Im), 3-way split
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float4 v[2][3];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 z = raw[(8 * q + 4 * h + u) * 128 + tid];
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            const float x = part ? z.y : z.x;
-            const float hi = tc::tf32_trunc(x);
-            const float md = tc::tf32_trunc(x - hi);
-            const float lo = (x - hi) - md;
-            reinterpret_cast<float*>(&v[part][0])[u] = hi;
-            reinterpret_cast<float*>(&v[part][1])[u] = md;
-            reinterpret_cast<float*>(&v[part][2])[u] = lo;
-          }
-        }
-        const uint32_t oR = tc::kmaj_off(tid, 4 * h, R_LBO, R_SBO), oI = tc::kmaj_off(tid, 8 + 4 * h, R_LBO, R_SBO);
-#pragma unroll
-        for (int lvl = 0; lvl < 3; ++lvl) {
-          *reinterpret_cast<float4*>(im0 + lvl * kRotStage + oR) = v[0][lvl];
-          *reinterpret_cast<float4*>(im0 + lvl * kRotStage + oI) = v[1][lvl];
-        }
+      uint8_t* im0 = stg + (size_t)b * 2 * kRotStage;
+      // thread (row, half): complex columns 8q + 4 half .. +3 -> K 4half..4half+3 (Re), 8+4half.. (Im)
+      float4 rh, rl, ih, il;
+      {
+        const float2 z0 = raw[(8 * q + 4 * half + 0) * 128 + row_l], z1 = raw[(8 * q + 4 * half + 1) * 128 + row_l];
+        const float2 z2 = raw[(8 * q + 4 * half + 2) * 128 + row_l], z3 = raw[(8 * q + 4 * half + 3) * 128 + row_l];
+        tc::split_tf32(z0.x, rh.x, rl.x); tc::split_tf32(z1.x, rh.y, rl.y);
+        tc::split_tf32(z2.x, rh.z, rl.z); tc::split_tf32(z3.x, rh.w, rl.w);
+        tc::split_tf32(z0.y, ih.x, il.x); tc::split_tf32(z1.y, ih.y, il.y);
+        tc::split_tf32(z2.y, ih.z, il.z); tc::split_tf32(z3.y, ih.w, il.w);
       }
+      const uint32_t oR = tc::kmaj_off(row_l, 4 * half, R_LBO, R_SBO), oI = tc::kmaj_off(row_l, 8 + 4 * half, R_LBO, R_SBO);
+      *reinterpret_cast<float4*>(im0 + oR) = rh;
+      *reinterpret_cast<float4*>(im0 + kRotStage + oR) = rl;
+      *reinterpret_cast<float4*>(im0 + oI) = ih;
+      *reinterpret_cast<float4*>(im0 + kRotStage + oI) = il;
       tc::fence_async_smem();
       __syncthreads();
       if (tid == 0) {
         tc::fence_after_sync();
         const uint32_t a0 = tc::smem_u32(im0);
-        uint64_t aR[3], aI[3], bR[3], bI[3];
         const uint32_t eoff = 2 * q * E_LBO;   // input columns 8q..8q+7
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          aR[l] = tc::make_desc(a0 + l * kRotStage, R_LBO, R_SBO);
-          aI[l] = tc::make_desc(a0 + l * kRotStage + 2 * R_LBO, R_LBO, R_SBO);
-          bR[l] = tc::make_desc(e0 + l * EI + eoff, E_LBO, E_SBO);
-          bI[l] = tc::make_desc(e0 + (3 + l) * EI + eoff, E_LBO, E_SBO);
-        }
+        const uint64_t aRh = tc::make_desc(a0, R_LBO, R_SBO), aRl = tc::make_desc(a0 + kRotStage, R_LBO, R_SBO);
+        const uint64_t aIh = tc::make_desc(a0 + 2 * R_LBO, R_LBO, R_SBO);
+        const uint64_t aIl = tc::make_desc(a0 + kRotStage + 2 * R_LBO, R_LBO, R_SBO);
+        const uint64_t bRh = tc::make_desc(e0 + eoff, E_LBO, E_SBO), bRl = tc::make_desc(e0 + EI + eoff, E_LBO, E_SBO);
+        const uint64_t bIh = tc::make_desc(e0 + 2 * EI + eoff, E_LBO, E_SBO);
+        const uint64_t bIl = tc::make_desc(e0 + 3 * EI + eoff, E_LBO, E_SBO);
         const uint32_t dRe = tmem, dIm = tmem + 64;
-        // products of total split order <= 2: (h,h) (h,m) (m,h) (h,l) (m,m) (l,h)
-        const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
-        // D_re += Re E_re - Im E_im ; D_im += Re E_im + Im E_re
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          const uint32_t acc = (q > 0 || t > 0) ? 1u : 0u;
-          tc::mma_tf32(dRe, aR[pa[t]], bR[pb[t]], id_p, acc);
-          tc::mma_tf32(dIm, aR[pa[t]], bI[pb[t]], id_p, acc);
-        }
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          tc::mma_tf32(dRe, aI[pa[t]], bI[pb[t]], id_n, 1u);
-          tc::mma_tf32(dIm, aI[pa[t]], bR[pb[t]], id_p, 1u);
-        }
+        const uint32_t acc0 = q > 0 ? 1u : 0u;
+        // D_re += Re E_re - Im E_im ; D_im += Re E_im + Im E_re   (3xTF32 each)
+        tc::mma_tf32(dRe, aRh, bRh, id_p, acc0);
+        tc::mma_tf32(dRe, aRh, bRl, id_p, 1u);
+        tc::mma_tf32(dRe, aRl, bRh, id_p, 1u);
+        tc::mma_tf32(dRe, aIh, bIh, id_n, 1u);
+        tc::mma_tf32(dRe, aIh, bIl, id_n, 1u);
+        tc::mma_tf32(dRe, aIl, bIh, id_n, 1u);
+        tc::mma_tf32(dIm, aRh, bIh, id_p, acc0);
+        tc::mma_tf32(dIm, aRh, bIl, id_p, 1u);
+        tc::mma_tf32(dIm, aRl, bIh, id_p, 1u);
+        tc::mma_tf32(dIm, aIh, bRh, id_p, 1u);
+        tc::mma_tf32(dIm, aIh, bRl, id_p, 1u);
+        tc::mma_tf32(dIm, aIl, bRh, id_p, 1u);
         tc::mma_commit(&mbar[b]);
       }
       __syncwarp();
     }
-    // wait for this tile's MMAs, then P' = P + D (thread = row), P from the raw tile
+    // this tile's MMAs done -> P' = P + D; warp w reads TMEM lanes 32 (w % 4); half 0: D_re, half 1: D_im
     tc::mbar_wait(&mbar[(chunk_ctr - 1) & 1], ((chunk_ctr - 1) >> 1) & 1);
     tc::fence_after_sync();
+    const int r = r0 + row_l;
 #pragma unroll 1
     for (int c = 0; c < PWC; c += 8) {
-      float dr[8], di[8];
-      tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, dr);
-      tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 64 + c, di);
+      float d[8];
+      tc::tmem_ld8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + 64 * half + c, d);
       if (r < rows) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const float2 v = raw[(c + u) * 128 + tid];
-          M[(int64_t)colof(c + u, I, J) * rows + r] = make_float2(v.x + dr[u], v.y + di[u]);
+          const float2 v = raw[(c + u) * 128 + row_l];
+          float* pp = reinterpret_cast<float*>(M + (int64_t)colof(c + u, I, J) * rows + r) + half;
+          *pp = (half ? v.y : v.x) + d[u];
         }
       }
     }
     tc::fence_before_sync();
-    __syncthreads();   // TMEM and raw reads done before the next tile overwrites them
-    if (tile + 1 < tiles_th + tiles_v) issue_tile(tile + 1);
+    __syncthreads();   // TMEM and raw reads done before they are overwritten
   }
+  tc::cp_async_wait<0>();
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
@@ -840,9 +844,8 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
   if (pair >= nb / 2 || rnd >= nb - 1) return;
   int I, J;
   circle_pair(pair, rnd, nb, I, J);
-  const int m = gd.m, n = gd.n, np = gd.n_pad;
+  const int n = gd.n, np = gd.n_pad;
   if (I * TB >= n && J * TB >= n) return;
-  const float2* __restrict__ th = reinterpret_cast<const float2*>(slab + gd.ws_theta);   // B (m x n)
   const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
   double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
   const double* den = shift + np;
@@ -850,81 +853,11 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tbase;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tc::tmem_alloc(&tbase, 128);
-  if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-    tc::fence_barrier_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = tbase;
-  const uint32_t idesc = tc::make_idesc_tf32(128, 128, false, false);
-  const int nchunks = (m + GKC - 1) / GKC;
-  for (int q = 0; q < nchunks; ++q) {
-    const int b = q & 1;
-    if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);
-    uint8_t* hi = base + (size_t)b * 2 * kGramStage;
-    uint8_t* lo2 = hi + kGramStage;
-    const int r0 = q * GKC;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int c = lane + 32 * (warp & 1);
-      const int rg = (warp >> 1) + 2 * it;
-      const int r = r0 + 4 * rg;
-      const int col = colof(c, I, J);
-      float re[4], im[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float2 v = (r + u < m && col < n) ? th[(int64_t)col * m + r + u] : make_float2(0.f, 0.f);
-        re[u] = v.x;
-        im[u] = v.y;
-      }
-      float4 rh, rl, ih, il;
-      tc::split_tf32(re[0], rh.x, rl.x); tc::split_tf32(re[1], rh.y, rl.y);
-      tc::split_tf32(re[2], rh.z, rl.z); tc::split_tf32(re[3], rh.w, rl.w);
-      tc::split_tf32(im[0], ih.x, il.x); tc::split_tf32(im[1], ih.y, il.y);
-      tc::split_tf32(im[2], ih.z, il.z); tc::split_tf32(im[3], ih.w, il.w);
-      rl.x *= 2.f; rl.y *= 2.f; rl.z *= 2.f; rl.w *= 2.f;
-      il.x *= 2.f; il.y *= 2.f; il.z *= 2.f; il.w *= 2.f;
-      const uint32_t oR = tc::kmaj_off(c, 4 * rg, G_LBO, G_SBO), oI = tc::kmaj_off(64 + c, 4 * rg, G_LBO, G_SBO);
-      *reinterpret_cast<float4*>(hi + oR) = rh;
-      *reinterpret_cast<float4*>(lo2 + oR) = rl;
-      *reinterpret_cast<float4*>(hi + oI) = ih;
-      *reinterpret_cast<float4*>(lo2 + oI) = il;
-    }
-    tc::fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after_sync();
-      const uint32_t ah = tc::smem_u32(hi), al = tc::smem_u32(lo2);
-#pragma unroll
-      for (int st2 = 0; st2 < GKC / 8; ++st2) {
-        const uint32_t off = 2 * st2 * G_LBO;
-        const uint64_t dh = tc::make_desc(ah + off, G_LBO, G_SBO), dl = tc::make_desc(al + off, G_LBO, G_SBO);
-        tc::mma_tf32(tmem, dh, dh, idesc, (q > 0 || st2 > 0) ? 1u : 0u);
-        tc::mma_tf32(tmem, dh, dl, idesc, 1u);
-      }
-      tc::mma_commit(&mbar[b]);
-    }
-    __syncwarp();
-  }
-  tc::mbar_wait(&mbar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
-  tc::fence_after_sync();
+  const int tid = threadIdx.x;
+  tc_setup(mbar, &tbase);
   float* Ds = reinterpret_cast<float*>(base);  // [128][129]
-  const int row = warp * 32 + lane;
-#pragma unroll 1
-  for (int c = 0; c < 128; c += 8) {
-    float v[8];
-    tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) Ds[row * 129 + c + i] = v[i];
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+  gram_panel(reinterpret_cast<const float2*>(slab + gd.ws_theta), gd.m, n, I, J, base, mbar, tbase, Ds);
+  if ((tid >> 5) == 0) tc::tmem_dealloc(tbase, 128);
   // thread j (< 64) = panel column j; partners: the other block (always) and its own block (round 0)
   if (tid < 64) {
     const int j = tid, cj = colof(j, I, J);
@@ -1035,20 +968,23 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   const dim3 grid(pairs_max, count);
+  static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
   int sweep = 0;
   bool done = false;
   for (; sweep < max_sweeps && !done; ++sweep) {
     for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
       tcj::k_tc_gram<<<grid, 128, tcj::kGramSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
-      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, 2);
-      tcj::k_tc_rot<<<grid, 128, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps);
+      tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
       launches += 3;
     }
     k_block_check<<<1, 256, 0, s>>>(d_desc, d_list, count, ctl, unconv, 0);
     ++launches;
-    cudaMemcpyAsync(h_pinned_flag, unconv, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(h_pinned_flag, unconv, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    done = (*h_pinned_flag == 0);
+    done = (h_pinned_flag[0] == 0);
+    static const bool dbg = getenv("EAMPS_TC_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
   }
   if (!done) *error_out = -6;
   k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);

@@ -1,0 +1,23 @@
+"""Aggregate an `ncu --metrics gpu__time_duration.sum --csv` launch list by kernel: count, total, share."""
+import collections, csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, agg = None, collections.defaultdict(lambda: [0, 0.0])
+for r in rows:
+    if "Kernel Name" in r:
+        hdr = r
+        continue
+    if hdr is None or len(r) != len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    v = float(d["Metric Value"].replace(",", ""))
+    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(d["Metric Unit"], 1.0)
+    k = d["Kernel Name"].split("(")[0][-50:]
+    agg[k][0] += 1
+    agg[k][1] += v
+tot = sum(v[1] for v in agg.values())
+print("| kernel | launches | total us | share | avg us |")
+print("|---|---|---|---|---|")
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
+    print("| %s | %d | %.1f | %.1f%% | %.1f |" % (k, n, t, 100 * t / tot, t / n))
