@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
 // FP64-anchored polish.
 __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                   int rnd, uint8_t* slab, LargeCtl* ctl, const double* norm2,
-                                                  int inner_sweeps) {
+                                                  int inner_sweeps, float tol_floor, float tol_internal) {
   const int gi = blockIdx.y;
   if (ctl[gi].conv) return;
   const GateDesc& gd = desc[list[gi]];
@@ -601,16 +601,23 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   }
   __syncthreads();
   const float skip = (float)(norm2[gi] * 3.552713678800501e-15);  // (2^-24)^2 ||theta||^2
-  const float tol = fmaxf(7.62939453125e-6f, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
-  int any = 0;
+  const float tol = fmaxf(tol_floor, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
+  const float tol_int = fmaxf(tol, tol_internal);
+  int any = 0, internal = 0;
   for (int x = tid; x < 64 * 64; x += 256) {
     const int p = x >> 6, q = x & 63;
     if (p < q) {
       const float al = Gs[p][p].x, be = Gs[q][q].x;
       const float g = sqrtf(Gs[p][q].x * Gs[p][q].x + Gs[p][q].y * Gs[p][q].y);
-      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) any = 1;
+      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) {
+        any = 1;
+        // within-block non-orthogonality above tol_int forces the full tournament (and round 0 of
+        // every sweep always runs it, so each block's internal pairs are revisited once a sweep)
+        if ((p < 32) == (q < 32) && (rnd == 0 || g > tol_int * sqrtf(al) * sqrtf(be))) internal = 1;
+      }
     }
   }
+  internal = __syncthreads_or(internal);
   if (!__syncthreads_or(any)) {
     if (tid == 0) rflag[pair] = 0;
     return;
@@ -619,52 +626,103 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
     rflag[pair] = 1;
     atomicAdd(&ctl[gi].rot, 1);
   }
-  const int grp = tid >> 3, t8 = tid & 7;
+  // When both blocks are already internally orthogonal (to tol), the off-diagonal mass of G sits
+  // in the I x J block and an inner sweep only needs the 32 x 32 cross pairs
+  // (p = i, q = 32 + (i + rr) mod 32): 32 rounds. Otherwise the full 64-column tournament (63).
+  // A round: (A) each of the 32 pairs computes its rotation J_k from its 2x2 diagonal block;
+  // (B) every 2x2 block (pair a rows, pair b cols), a <= b, becomes J_a^H X J_b and is mirrored
+  // (G Hermitian: half the work of separate column and row passes, one barrier fewer), and
+  // W <- W J (columns p_k, q_k).
+  __shared__ float4 par[32];      // c, s, er, ei
+  __shared__ int2 pq[32];
+  __shared__ uint16_t blk[496];   // the off-diagonal block pairs a < b
+  for (int x = tid; x < 496; x += 256) {
+    int aa = 0, rem = x;
+    while (rem >= 31 - aa) { rem -= 31 - aa; ++aa; }
+    blk[x] = (uint16_t)(aa | ((aa + 1 + rem) << 8));
+  }
+  const int nrr = internal ? 63 : 32;
   for (int isw = 0; isw < inner_sweeps; ++isw) {
     int rot = 0;
-    for (int rr = 0; rr < 63; ++rr) {
-      int p, q;
-      circle_pair(grp, rr, 64, p, q);
-      const float al = Gs[p][p].x, be = Gs[q][q].x;
-      const float2 gm = Gs[p][q];
-      const float g2 = gm.x * gm.x + gm.y * gm.y;
-      float c = 1.f, s = 0.f, er = 1.f, ei = 0.f;
-      if (fminf(al, be) > skip && g2 > 1e-13f * al * be) {
-        const float ig = rsqrtf(g2);
-        er = gm.x * ig;
-        ei = gm.y * ig;
-        const float zeta = 0.5f * (be - al) * ig;
-        const float az = fabsf(zeta);
-        const float t = copysignf(1.f, zeta) / (az + sqrtf(fmaf(az, az, 1.f)));
-        c = rsqrtf(fmaf(t, t, 1.f));
-        s = c * t;
-        rot = 1;
+    for (int rr = 0; rr < nrr; ++rr) {
+      if (tid < 32) {
+        int p, q;
+        if (internal) {
+          circle_pair(tid, rr, 64, p, q);
+        } else {
+          p = tid;
+          q = 32 + ((tid + rr) & 31);
+        }
+        const float al = Gs[p][p].x, be = Gs[q][q].x;
+        const float2 gm = Gs[p][q];
+        const float g2 = gm.x * gm.x + gm.y * gm.y;
+        float c = 1.f, sn = 0.f, er = 1.f, ei = 0.f;
+        if (fminf(al, be) > skip && g2 > 1e-13f * al * be) {
+          const float ig = rsqrtf(g2);
+          er = gm.x * ig;
+          ei = gm.y * ig;
+          const float zeta = 0.5f * (be - al) * ig;
+          const float az = fabsf(zeta);
+          const float t = copysignf(1.f, zeta) / (az + sqrtf(fmaf(az, az, 1.f)));
+          c = rsqrtf(fmaf(t, t, 1.f));
+          sn = c * t;
+          rot = 1;
+          // the pair's own 2x2 block J^H X J is diagonal: (alpha - t|gamma|, beta + t|gamma|)
+          const float tg = t * (g2 * ig);
+          Gs[p][p] = make_float2(al - tg, 0.f);
+          Gs[q][q] = make_float2(be + tg, 0.f);
+          Gs[p][q] = make_float2(0.f, 0.f);
+          Gs[q][p] = make_float2(0.f, 0.f);
+        }
+        par[tid] = make_float4(c, sn, er, ei);
+        pq[tid] = make_int2(p, q);
       }
-      __syncthreads();   // every group has read its 2x2 block before any column is rotated
-      if (s != 0.f) {
+      __syncthreads();
+      for (int x = tid; x < 496; x += 256) {
+        const int ia = blk[x] & 0xFF, ib = blk[x] >> 8;
+        const float4 Ja = par[ia], Jb = par[ib];
+        if (Ja.y == 0.f && Jb.y == 0.f) continue;
+        const int2 ra = pq[ia], cb = pq[ib];
+        float2 X[2][2] = {{Gs[ra.x][cb.x], Gs[ra.x][cb.y]}, {Gs[ra.y][cb.x], Gs[ra.y][cb.y]}};
+        if (Jb.y != 0.f) {   // columns: (x, y) -> (c x - s conj(e) y, s x + c conj(e) y)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const float2 xx = X[r][0], yy = X[r][1];
+            const float2 ey = make_float2(Jb.z * yy.x + Jb.w * yy.y, Jb.z * yy.y - Jb.w * yy.x);
+            X[r][0] = make_float2(Jb.x * xx.x - Jb.y * ey.x, Jb.x * xx.y - Jb.y * ey.y);
+            X[r][1] = make_float2(Jb.y * xx.x + Jb.x * ey.x, Jb.y * xx.y + Jb.x * ey.y);
+          }
+        }
+        if (Ja.y != 0.f) {   // rows: (u, v) -> (c u - s e v, s u + c e v)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const float2 uu = X[0][cc], vv = X[1][cc];
+            const float2 ev = make_float2(Ja.z * vv.x - Ja.w * vv.y, Ja.z * vv.y + Ja.w * vv.x);
+            X[0][cc] = make_float2(Ja.x * uu.x - Ja.y * ev.x, Ja.x * uu.y - Ja.y * ev.y);
+            X[1][cc] = make_float2(Ja.y * uu.x + Ja.x * ev.x, Ja.y * uu.y + Ja.x * ev.y);
+          }
+        }
+        Gs[ra.x][cb.x] = X[0][0]; Gs[ra.x][cb.y] = X[0][1];
+        Gs[ra.y][cb.x] = X[1][0]; Gs[ra.y][cb.y] = X[1][1];
+        // Hermitian mirror
+        Gs[cb.x][ra.x] = make_float2(X[0][0].x, -X[0][0].y); Gs[cb.y][ra.x] = make_float2(X[0][1].x, -X[0][1].y);
+        Gs[cb.x][ra.y] = make_float2(X[1][0].x, -X[1][0].y); Gs[cb.y][ra.y] = make_float2(X[1][1].x, -X[1][1].y);
+      }
+      {   // W <- W J for every pair: thread (pair k = tid / 8, rows (tid % 8) + 8 i)
+        const int k = tid >> 3;
+        const float4 J = par[k];
+        if (J.y != 0.f) {
+          const int2 cq = pq[k];
 #pragma unroll 4
-        for (int x = t8; x < 64; x += 8) {   // columns: G J and W J
-          float2 a = Gs[x][p], b = Gs[x][q];
-          float2 eb = make_float2(er * b.x + ei * b.y, er * b.y - ei * b.x);
-          Gs[x][p] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
-          Gs[x][q] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
-          a = Ws[x][p]; b = Ws[x][q];
-          eb = make_float2(er * b.x + ei * b.y, er * b.y - ei * b.x);
-          Ws[x][p] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
-          Ws[x][q] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
+          for (int x = tid & 7; x < 64; x += 8) {
+            const float2 xx = Ws[x][cq.x], yy = Ws[x][cq.y];
+            const float2 ey = make_float2(J.z * yy.x + J.w * yy.y, J.z * yy.y - J.w * yy.x);
+            Ws[x][cq.x] = make_float2(J.x * xx.x - J.y * ey.x, J.x * xx.y - J.y * ey.y);
+            Ws[x][cq.y] = make_float2(J.y * xx.x + J.x * ey.x, J.y * xx.y + J.x * ey.y);
+          }
         }
       }
       __syncthreads();
-      if (s != 0.f) {
-#pragma unroll 4
-        for (int x = t8; x < 64; x += 8) {   // rows: J^H G
-          float2 a = Gs[p][x], b = Gs[q][x];
-          float2 eb = make_float2(er * b.x - ei * b.y, er * b.y + ei * b.x);
-          Gs[p][x] = make_float2(c * a.x - s * eb.x, c * a.y - s * eb.y);
-          Gs[q][x] = make_float2(s * a.x + c * eb.x, s * a.y + c * eb.y);
-        }
-      }
-      __syncthreads();   // rows written before the next round reads its 2x2 blocks
     }
     if (!__syncthreads_or(rot)) break;
   }
@@ -805,16 +863,18 @@ __global__ void __launch_bounds__(256) k_tc_rot(const GateDesc* __restrict__ des
     tc::mbar_wait(&mbar[(chunk_ctr - 1) & 1], ((chunk_ctr - 1) >> 1) & 1);
     tc::fence_after_sync();
     const int r = r0 + row_l;
+    // thread (row, half) writes whole complex entries of columns 32 half .. 32 half + 31 (coalesced)
 #pragma unroll 1
-    for (int c = 0; c < PWC; c += 8) {
-      float d[8];
-      tc::tmem_ld8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + 64 * half + c, d);
+    for (int c = 32 * half; c < 32 * half + 32; c += 8) {
+      float dr[8], di[8];
+      const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+      tc::tmem_ld8(ta + c, dr);
+      tc::tmem_ld8(ta + 64 + c, di);
       if (r < rows) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const float2 v = raw[(c + u) * 128 + row_l];
-          float* pp = reinterpret_cast<float*>(M + (int64_t)colof(c + u, I, J) * rows + r) + half;
-          *pp = (half ? v.y : v.x) + d[u];
+          M[(int64_t)colof(c + u, I, J) * rows + r] = make_float2(v.x + dr[u], v.y + di[u]);
         }
       }
     }
@@ -969,15 +1029,36 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   const dim3 grid(pairs_max, count);
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
+  static const float tol_floor = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
+  static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 1e-2f;
   int sweep = 0;
   bool done = false;
   for (; sweep < max_sweeps && !done; ++sweep) {
+    static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
+    static cudaEvent_t ev[4];
+    static double acc[3] = {0, 0, 0};
+    if (prof && !ev[0])
+      for (int e = 0; e < 4; ++e) cudaEventCreate(&ev[e]);
     for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
+      if (prof) cudaEventRecord(ev[0], s);
       tcj::k_tc_gram<<<grid, 128, tcj::kGramSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
-      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps);
+      if (prof) cudaEventRecord(ev[1], s);
+      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps, tol_floor,
+                                                         tol_internal);
+      if (prof) cudaEventRecord(ev[2], s);
       tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      if (prof) {
+        cudaEventRecord(ev[3], s);
+        cudaEventSynchronize(ev[3]);
+        for (int e = 0; e < 3; ++e) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
+          acc[e] += ms;
+        }
+      }
       launches += 3;
     }
+    if (prof) fprintf(stderr, "[tc prof] cumulative ms: gram %.1f inner %.1f rot %.1f\n", acc[0], acc[1], acc[2]);
     k_block_check<<<1, 256, 0, s>>>(d_desc, d_list, count, ctl, unconv, 0);
     ++launches;
     cudaMemcpyAsync(h_pinned_flag, unconv, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
