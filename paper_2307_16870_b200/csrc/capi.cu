@@ -288,7 +288,7 @@ mps_status wave_front(mps_t h) {
   // small / medium buckets by lane-group size GT (one launch per bucket); `small` holds them
   // back to back, [bstart, bend) per bucket
   struct Bucket {
-    int regime, gt, begin, end, threads, tile_rows;
+    int regime, gt, begin, end, threads, tile_rows, rpl;
     size_t smem, smem2;
   };
   std::vector<Bucket> buckets;
@@ -306,7 +306,7 @@ mps_status wave_front(mps_t h) {
     const size_t kmn = (size_t)std::min(gd.m, gd.n);
     // E (k x k, reabsorb); the large regime's polish also keeps shift | den (2 n_pad doubles) there
     gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, gd.regime == 1 ? (size_t)16 * gd.n_pad : (size_t)0));
-    gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8)
+    gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
                 : gd.regime == 1 ? (int64_t)take(svd_tc_scratch_bytes(gd.n_pad))
                                  : 0;
     hd[x] = gd;
@@ -316,15 +316,23 @@ mps_status wave_front(mps_t h) {
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
   }
+  // buckets: (regime, lane-group size GT, rows per lane R); R > 0 keeps a pair's rows in registers
   for (int reg : {0, 2}) {
     for (int gt : {4, 8, 16, 32}) {
-      Bucket b{reg, gt, (int)small.size(), 0, 64, 64, 0, 0};
+     for (int rpl : {1, 2, 4, 8, 16, 0}) {
+      Bucket b{reg, gt, (int)small.size(), 0, 64, 64, rpl, 0, 0};
       int maxn = 2;
       for (int x = 0; x < Gw; ++x) {
         const GateDesc& gd = hd[x];
         if (gd.regime != reg) continue;
-        const int g_gt = std::min(small_group(gd.m), std::max(4, 2048 / gd.n));
+        // lane-group size: small regime as before; medium regime (theta 96-210 KB, V replayed) with
+        // at most 512 threads so the rows-per-lane registers fit (one pair per group)
+        const int g_gt = reg == 0 ? std::min(small_group(gd.m), std::max(4, 2048 / gd.n))
+                                  : std::min(small_group(gd.m), std::max(4, 1024 / gd.n));
         if (g_gt != gt) continue;
+        const int rm = rows_per_lane(gd.m, gt), rn = rows_per_lane(gd.n, gt);
+        const int g_r = (rm == 0 || rn == 0) ? 0 : std::max(rm, rn);
+        if (g_r != rpl) continue;
         small.push_back(x);
         maxn = std::max(maxn, gd.n);
         if (reg == 0) {
@@ -340,8 +348,9 @@ mps_status wave_front(mps_t h) {
       if (reg == 2) {
         for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
       }
-      b.threads = (int)std::min<size_t>(1024, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
+      b.threads = (int)std::min<size_t>(reg == 0 ? 1024 : 512, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
       buckets.push_back(b);
+     }
     }
   }
   if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
@@ -392,12 +401,12 @@ mps_status wave_front(mps_t h) {
   // a2 + a3 SVD, small regime: one CTA per theta
   for (const Bucket& b : buckets) {
     if (b.regime == 0) {
-      launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.threads,
+      launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.threads,
                        h->slab, h->dst, h->s);
       ++h->launches;
     } else {
       launch_svd_medium(d_desc, d_small + b.begin, b.end - b.begin, b.smem, b.smem2, b.tile_rows, h->cfg.max_sweeps,
-                        b.gt, b.threads, h->slab, h->dst, h->s);
+                        b.gt, b.rpl, b.threads, h->slab, h->dst, h->s);
       h->launches += 2;
     }
     CKL("svd_small/medium");
@@ -700,7 +709,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
     // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)
-    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 8
+    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                                        : (gd.regime == 1 ? svd_tc_scratch_bytes(gd.n_pad) : 0);
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;

@@ -52,7 +52,7 @@ struct GateDesc {
   int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large
   int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
   int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
-  int64_t ws_log;                   // medium regime: rotation log, log_sweeps x (n-1) x n/2 float2 (t, arg e)
+  int64_t ws_log;                   // medium: rotation log, log_sweeps x (n-1) x n/2 float4 (c, s, e); large: TC scratch
   int32_t log_sweeps, pad0;
   int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
   int32_t k, capped;                // outputs of the selector
@@ -93,17 +93,25 @@ __host__ __device__ inline T* at(uint8_t* slab, int64_t off) { return reinterpre
 // ---- kernels (launched by capi.cu) -------------------------------------------------------------
 void launch_contract(const GateDesc* d_desc, const int32_t* d_tile_prefix, int G, int total_tiles, int d,
                      uint8_t* slab, const DevState* st, const float2* d_us, cudaStream_t s);
+// rows per lane for a GT-lane group over `rows` rows: a power of two <= 16, or 0 (no register path)
+inline int rows_per_lane(int rows, int gt) {
+  const int need = (rows + gt - 1) / gt;
+  int r = 1;
+  while (r < need) r <<= 1;
+  return r <= 16 ? r : 0;
+}
 size_t svd_small_smem(int m, int n);
 bool svd_small_fits(int m, int n);
 int small_group(int m);
-void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt,
+void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
                       int threads, uint8_t* slab, DevState* st, cudaStream_t s);
 size_t svd_theta_smem(int m, int n);
 size_t svd_vrep_smem(int n, int tile_rows);
 bool svd_medium_fits(int m, int n);
 int vrep_tile_rows(int m, int n);
 void launch_svd_medium(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
-                       int tile_rows, int max_sweeps, int gt, int threads, uint8_t* slab, DevState* st, cudaStream_t s);
+                       int tile_rows, int max_sweeps, int gt, int rpl, int threads, uint8_t* slab, DevState* st,
+                       cudaStream_t s);
 // blocked (large) path: returns launches issued
 int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                     int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,

@@ -46,6 +46,79 @@ __device__ __forceinline__ void apply_rot(float2& x, float2& y, const Rot& R) {
   y = ny;
 }
 
+// The rows of a column pair held in registers between the dot products and the rotation: lane
+// lg of a GT-lane group owns rows lg, lg + GT, ..., lg + (R-1) GT (R = rows per lane, a compile-time
+// bound; the caller guarantees m <= R GT). One shared-memory read and one write per element per
+// round instead of two reads and one write.
+template <int GT, int R>
+struct PairRegs {
+  float2 x[R], y[R];
+  // row of register slot u for lane lg: lg + GT ((u + sh) mod R), sh = the group's index within its
+  // warp, so the groups of a warp hit different shared-memory banks (2 wavefronts per float2 access)
+  static __device__ __forceinline__ int row(int lg, int u, int sh) { return lg + GT * ((u + sh) & (R - 1)); }
+  __device__ __forceinline__ void load(const float2* ap, const float2* aq, int m, int lg, int sh) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = row(lg, u, sh);
+      const bool ok = i < m;
+      x[u] = ok ? ap[i] : make_float2(0.f, 0.f);
+      y[u] = ok ? aq[i] : make_float2(0.f, 0.f);
+    }
+  }
+  __device__ __forceinline__ void load_full(const float2* ap, const float2* aq, int lg, int sh) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = row(lg, u, sh);
+      x[u] = ap[i];
+      y[u] = aq[i];
+    }
+  }
+  __device__ __forceinline__ void dots(float& al, float& be, float& gr, float& gi) const {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const float2 a = x[u], b = y[u];
+      al = fmaf(a.x, a.x, fmaf(a.y, a.y, al));
+      be = fmaf(b.x, b.x, fmaf(b.y, b.y, be));
+      gr = fmaf(a.x, b.x, fmaf(a.y, b.y, gr));    // Re conj(a) b
+      gi = fmaf(a.x, b.y, fmaf(-a.y, b.x, gi));   // Im conj(a) b
+    }
+  }
+  __device__ __forceinline__ void rotate_store(float2* ap, float2* aq, int m, int lg, int sh, const Rot& Rt) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = row(lg, u, sh);
+      if (i < m) {
+        float2 a = x[u], b = y[u];
+        apply_rot(a, b, Rt);
+        ap[i] = a;
+        aq[i] = b;
+      }
+    }
+  }
+  __device__ __forceinline__ void rotate_store_full(float2* ap, float2* aq, int lg, int sh, const Rot& Rt) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int i = row(lg, u, sh);
+      float2 a = x[u], b = y[u];
+      apply_rot(a, b, Rt);
+      ap[i] = a;
+      aq[i] = b;
+    }
+  }
+};
+
+// GT-lane xor-butterfly sum of the four pair statistics (bit-identical in every lane of the group)
+template <int GT>
+__device__ __forceinline__ void group_sum4(float& al, float& be, float& gr, float& gi) {
+#pragma unroll
+  for (int o = GT / 2; o > 0; o >>= 1) {
+    al += __shfl_xor_sync(0xffffffffu, al, o);
+    be += __shfl_xor_sync(0xffffffffu, be, o);
+    gr += __shfl_xor_sync(0xffffffffu, gr, o);
+    gi += __shfl_xor_sync(0xffffffffu, gi, o);
+  }
+}
+
 __device__ __forceinline__ double warp_sum_d32(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -4,10 +4,9 @@
 // Two one-CTA-per-theta kernels instead of a cluster: the rotations are data-independent of V,
 // so V can be built afterwards from a log of the rotations.
 //   k_svd_theta : the one-sided Jacobi of svd_small.cu on theta alone (theta in shared memory);
-//                 every round's rotation per column pair goes to a log in the workspace as
-//                 (t = s/c, arg e): 8 B per pair-round, ~0.7 MB per theta for 11 sweeps at n = 128.
-//                 V only has to be a unitary product of (nearly) the same rotations: the replay
-//                 recomputing c, s, e from (t, arg e) to 1 ulp does not affect sigma or the update.
+//                 every round's rotation per column pair goes to a log in the workspace exactly as
+//                 applied, (c, s, Re e, Im e): 16 B per pair-round, ~1.5 MB per theta for 12
+//                 sweeps at n = 128 (no transcendental on either side).
 //   k_svd_vrep  : V = I R_1 R_2 ... R_T replayed from the log in shared memory (the same circle
 //                 order, identity rotations skipped), then sigma_j^2 = ||theta v_j||^2/||v_j||^2
 //                 with theta streamed from the workspace in row tiles (FP64 products), V to
@@ -22,23 +21,38 @@ namespace eamps {
 
 namespace {
 
-template <int GT>
-__global__ void __launch_bounds__(1024) k_svd_theta(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
+// The circle-method schedule of one sweep, (p | q << 8) per (round, slot), built once per CTA in
+// shared memory (n <= 256): no integer modulo on the per-round path.
+__device__ __forceinline__ void build_schedule(uint16_t* sched, int n) {
+  const int half = n / 2;
+  for (int x = threadIdx.x; x < (n - 1) * half; x += blockDim.x) {
+    const int rnd = x / half, slot = x % half;
+    int p, q;
+    circle_pair_n(slot, rnd, n, p, q);
+    sched[x] = (uint16_t)(p | (q << 8));
+  }
+}
+
+template <int GT, int R>
+__global__ void __launch_bounds__(512) k_svd_theta(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                     DevState* st, int max_sweeps) {
   extern __shared__ __align__(16) uint8_t sm[];
   GateDesc& gd = desc[list[blockIdx.x]];
   const int m = gd.m, n = gd.n;
   float2* A = reinterpret_cast<float2*>(sm);
+  uint16_t* sched = reinterpret_cast<uint16_t*>(A + (size_t)m * n);   // (n - 1) x n/2
   __shared__ float s_wn[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);
-  float2* lg = reinterpret_cast<float2*>(slab + gd.ws_log);
+  float4* lg = reinterpret_cast<float4*>(slab + gd.ws_log);
   float nrm = 0.f;
   for (int x = tid; x < m * n; x += blockDim.x) {
     float2 v = gth[x];
     A[x] = v;
     nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
   }
+  const bool use_sched = n <= 256 && R > 0;
+  if (use_sched) build_schedule(sched, n);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
   if (lane == 0) s_wn[warp] = nrm;
@@ -48,62 +62,101 @@ __global__ void __launch_bounds__(1024) k_svd_theta(GateDesc* desc, const int32_
   const float skip = norm2 * 3.5527137e-15f;
   const float tol = fmaxf(7.62939453e-6f, 4.f * sqrtf((float)m) * 5.96046448e-8f);
   const int groups = blockDim.x / GT, gid = tid / GT, lgi = tid % GT;
+  const int half = n / 2;
   const int cap = min(max_sweeps, gd.log_sweeps);
   int sweep = 0;
   bool converged = (n < 2);
-  for (; sweep < cap && !converged; ++sweep) {
-    int any = 0;
-    for (int rnd = 0; rnd < n - 1; ++rnd) {
-      bool rot = false;
-      float2* lrow = lg + ((size_t)sweep * (n - 1) + rnd) * (n / 2);
-      for (int base = 0; base < n / 2; base += groups) {
-        const int slot = base + gid;
-        const bool active = slot < n / 2;
-        int p = 0, q = 1;
-        if (active) circle_pair_n(slot, rnd, n, p, q);
-        float2* ap = A + (size_t)p * m;
-        float2* aq = A + (size_t)q * m;
-        float al = 0.f, be = 0.f, gr = 0.f, gi = 0.f;
+  if (R > 0 && groups >= half) {
+    // fast path: one column pair per lane group (groups >= n/2, checked by the host), the pair's
+    // rows in registers, schedule from shared memory, 32-bit log index
+    const bool active = gid < half;
+    const bool full = (m == R * GT);   // (R > 0 here)
+    const int sh = gid & (32 / GT - 1); // group index within the warp (bank spreading)
+    uint32_t li = (uint32_t)gid;      // log index = (sweep (n-1) + rnd) n/2 + slot
+    for (; sweep < cap && !converged; ++sweep) {
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd, li += half) {
+        bool rot = false;
         if (active) {
-          for (int i = lgi; i < m; i += GT) {
-            float2 x = ap[i], y = aq[i];
-            al = fmaf(x.x, x.x, fmaf(x.y, x.y, al));
-            be = fmaf(y.x, y.x, fmaf(y.y, y.y, be));
-            gr = fmaf(x.x, y.x, fmaf(x.y, y.y, gr));
-            gi = fmaf(x.x, y.y, fmaf(-x.y, y.x, gi));
+          int p, q;
+          if (use_sched) {
+            const uint32_t pq = sched[rnd * half + gid];
+            p = pq & 0xFF;
+            q = pq >> 8;
+          } else {
+            circle_pair_n(gid, rnd, n, p, q);
+          }
+          float2* ap = A + p * m;
+          float2* aq = A + q * m;
+          constexpr int RR = R > 0 ? R : 1;
+          PairRegs<GT, RR> pr;
+          float al = 0.f, be = 0.f, gr = 0.f, gi = 0.f;
+          if (full) pr.load_full(ap, aq, lgi, sh);
+          else pr.load(ap, aq, m, lgi, sh);
+          pr.dots(al, be, gr, gi);
+          group_sum4<GT>(al, be, gr, gi);
+          Rot Rt;
+          const bool doit = jacobi_rot(al, be, gr, gi, skip, tol, Rt);
+          if (lgi == 0) lg[li] = make_float4(Rt.c, Rt.s, Rt.er, Rt.ei);
+          if (doit) {
+            rot = true;
+            if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
+            else pr.rotate_store(ap, aq, m, lgi, sh, Rt);
           }
         }
-#pragma unroll
-        for (int o = GT / 2; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          gr += __shfl_xor_sync(0xffffffffu, gr, o);
-          gi += __shfl_xor_sync(0xffffffffu, gi, o);
-        }
-        Rot R;
-        const bool doit = active && jacobi_rot(al, be, gr, gi, skip, tol, R);
-        // log (t = s/c, phase of e): 8 B per pair-round; identity rotations are logged as t = 0
-        if (active && lgi == 0) lrow[slot] = make_float2(doit ? R.s / R.c : 0.f, atan2f(R.ei, R.er));
-        if (doit) {
-          rot = true;
-          for (int i = lgi; i < m; i += GT) {
-            float2 x = ap[i], y = aq[i];
-            apply_rot(x, y, R);
-            ap[i] = x;
-            aq[i] = y;
-          }
-        }
+        any |= __syncthreads_or(rot);
       }
-      any |= __syncthreads_or(rot);
+      converged = (any == 0);
     }
-    converged = (any == 0);
+  } else {
+    for (; sweep < cap && !converged; ++sweep) {
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd) {
+        bool rot = false;
+        float4* lrow = lg + ((size_t)sweep * (n - 1) + rnd) * half;
+        for (int base = 0; base < half; base += groups) {
+          const int slot = base + gid;
+          const bool active = slot < half;
+          int p = 0, q = 1;
+          if (active) circle_pair_n(slot, rnd, n, p, q);
+          float2* ap = A + (size_t)p * m;
+          float2* aq = A + (size_t)q * m;
+          float al = 0.f, be = 0.f, gr = 0.f, gi = 0.f;
+          if (active) {
+            for (int i = lgi; i < m; i += GT) {
+              float2 x = ap[i], y = aq[i];
+              al = fmaf(x.x, x.x, fmaf(x.y, x.y, al));
+              be = fmaf(y.x, y.x, fmaf(y.y, y.y, be));
+              gr = fmaf(x.x, y.x, fmaf(x.y, y.y, gr));
+              gi = fmaf(x.x, y.y, fmaf(-x.y, y.x, gi));
+            }
+          }
+          group_sum4<GT>(al, be, gr, gi);
+          Rot Rt;
+          const bool doit = active && jacobi_rot(al, be, gr, gi, skip, tol, Rt);
+          // log the applied rotation exactly (c, s, Re e, Im e); identity rotations have s = 0
+          if (active && lgi == 0) lrow[slot] = make_float4(Rt.c, Rt.s, Rt.er, Rt.ei);
+          if (doit) {
+            rot = true;
+            for (int i = lgi; i < m; i += GT) {
+              float2 x = ap[i], y = aq[i];
+              apply_rot(x, y, Rt);
+              ap[i] = x;
+              aq[i] = y;
+            }
+          }
+        }
+        any |= __syncthreads_or(rot);
+      }
+      converged = (any == 0);
+    }
   }
   if (!converged && tid == 0) atomicCAS(&st->led.error, 0, -6 /* MPS_E_NOCONV */);
   if (tid == 0) gd.sweeps = sweep;
 }
 
-template <int GT>
-__global__ void __launch_bounds__(1024) k_svd_vrep(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
+template <int GT, int R>
+__global__ void __launch_bounds__(512) k_svd_vrep(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                    DevState* st, int tile_rows) {
   extern __shared__ __align__(16) uint8_t sm[];
   const GateDesc& gd = desc[list[blockIdx.x]];
@@ -116,34 +169,61 @@ __global__ void __launch_bounds__(1024) k_svd_vrep(GateDesc* desc, const int32_t
   double* s2 = reinterpret_cast<double*>(T + (size_t)tile_rows * ldt);
   int32_t* six = reinterpret_cast<int32_t*>(s2 + npow2);
   double* part = reinterpret_cast<double*>(six + npow2 + (npow2 & 1));
+  uint16_t* sched = reinterpret_cast<uint16_t*>(part + blockDim.x);   // (n - 1) x n/2 when n <= 256
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int x = tid; x < n * n; x += blockDim.x) V[x] = make_float2((x / n) == (x % n) ? 1.f : 0.f, 0.f);
+  const bool use_sched = n <= 256;
+  if (use_sched) build_schedule(sched, n);
   __syncthreads();
-  const float2* lg = reinterpret_cast<const float2*>(slab + gd.ws_log);
+  const float4* lg = reinterpret_cast<const float4*>(slab + gd.ws_log);
   const int groups = blockDim.x / GT, gid = tid / GT, lgi = tid % GT;
-  for (int sw = 0; sw < S; ++sw) {
-    for (int rnd = 0; rnd < n - 1; ++rnd) {
-      const float2* lrow = lg + ((size_t)sw * (n - 1) + rnd) * (n / 2);
-      for (int slot = gid; slot < n / 2; slot += groups) {
-        const float2 r = lrow[slot];
-        if (r.x == 0.f) continue;  // identity rotation (uniform within the group)
-        int p, q;
+  // V = I R_1 R_2 ... replayed from the log; each group prefetches its next log entry one round
+  // ahead (the log is read once, from HBM/L2)
+  const int total = S * (n - 1);
+  float4 nxt = make_float4(1.f, 0.f, 1.f, 0.f);
+  if (total > 0 && gid < n / 2) nxt = lg[gid];
+  for (int t = 0; t < total; ++t) {
+    const int rnd = t % (n - 1);
+    const float4* lrow = lg + (size_t)t * (n / 2);
+    for (int slot = gid; slot < n / 2; slot += groups) {
+      float4 r;
+      if (slot == gid) {
+        r = nxt;
+        if (t + 1 < total) nxt = lrow[n / 2 + gid];   // prefetch: same slot, next round
+      } else {
+        r = lrow[slot];
+      }
+      if (r.y == 0.f) continue;  // identity rotation (uniform within the group)
+      int p, q;
+      if (use_sched) {
+        const uint32_t pq = sched[rnd * (n / 2) + slot];
+        p = pq & 0xFF;
+        q = pq >> 8;
+      } else {
         circle_pair_n(slot, rnd, n, p, q);
-        Rot R;
-        R.c = rsqrtf(1.f + r.x * r.x);
-        R.s = R.c * r.x;
-        sincosf(r.y, &R.ei, &R.er);
-        float2* vp = V + (size_t)p * n;
-        float2* vq = V + (size_t)q * n;
+      }
+      Rot Rt;
+      Rt.c = r.x;
+      Rt.s = r.y;
+      Rt.er = r.z;
+      Rt.ei = r.w;
+      float2* vp = V + (size_t)p * n;
+      float2* vq = V + (size_t)q * n;
+      if constexpr (R > 0) {
+        const int sh = gid & (32 / GT - 1);
+        PairRegs<GT, R> pv;
+        pv.load(vp, vq, n, lgi, sh);
+        pv.rotate_store(vp, vq, n, lgi, sh, Rt);
+      } else {
         for (int i = lgi; i < n; i += GT) {
           float2 x = vp[i], y = vq[i];
-          apply_rot(x, y, R);
+          apply_rot(x, y, Rt);
           vp[i] = x;
           vq[i] = y;
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
   // Rayleigh quotient with theta streamed in row tiles: num_j = sum_i |(theta V)_ij|^2 in FP64
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);  // m x n, ld m
@@ -192,12 +272,13 @@ __global__ void __launch_bounds__(1024) k_svd_vrep(GateDesc* desc, const int32_t
 
 }  // namespace
 
-size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + 64; }
+size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + (size_t)(n - 1) * (n / 2) * 2 + 64; }
 
 size_t svd_vrep_smem(int n, int tile_rows) {
   int npow2 = 1;
   while (npow2 < n) npow2 <<= 1;
-  return (size_t)n * n * 8 + (size_t)tile_rows * (n + 1) * 8 + (size_t)npow2 * 12 + 16 + 1024 * 8;
+  return (size_t)n * n * 8 + (size_t)tile_rows * (n + 1) * 8 + (size_t)npow2 * 12 + 16 + 1024 * 8 +
+         (n <= 256 ? (size_t)(n - 1) * (n / 2) * 2 : 0);
 }
 
 bool svd_medium_fits(int m, int n) { return svd_theta_smem(m, n) <= 210 * 1024 && svd_vrep_smem(n, 8) <= 210 * 1024; }
@@ -208,29 +289,42 @@ int vrep_tile_rows(int m, int n) {
   return std::min(t, m);
 }
 
-void launch_svd_medium(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
-                       int tile_rows, int max_sweeps, int gt, int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
-  if (count <= 0) return;
+template <int GT, int R>
+static void launch_medium_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
+                            int tile_rows, int max_sweeps, int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-#define EAMPS_ATTR(GTV)                                                                                  \
-  cudaFuncSetAttribute(k_svd_theta<GTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);      \
-  cudaFuncSetAttribute(k_svd_vrep<GTV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    EAMPS_ATTR(4) EAMPS_ATTR(8) EAMPS_ATTR(16) EAMPS_ATTR(32)
-#undef EAMPS_ATTR
+    cudaFuncSetAttribute(k_svd_theta<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_svd_vrep<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
+  k_svd_theta<GT, R><<<count, threads, smem_theta, s>>>(d_desc, d_list, slab, st, max_sweeps);
+  k_svd_vrep<GT, R><<<count, threads, smem_vrep, s>>>(d_desc, d_list, slab, st, tile_rows);
+}
+
+template <int GT>
+static void launch_medium_r(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
+                            int tile_rows, int max_sweeps, int rpl, int threads, uint8_t* slab, DevState* st,
+                            cudaStream_t s) {
+  switch (rpl) {
+    case 1: launch_medium_t<GT, 1>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+    case 2: launch_medium_t<GT, 2>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+    case 4: launch_medium_t<GT, 4>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+    case 8: launch_medium_t<GT, 8>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+    case 16: launch_medium_t<GT, 16>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+    default: launch_medium_t<GT, 0>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, threads, slab, st, s); break;
+  }
+}
+
+void launch_svd_medium(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
+                       int tile_rows, int max_sweeps, int gt, int rpl, int threads, uint8_t* slab, DevState* st,
+                       cudaStream_t s) {
+  if (count <= 0) return;
   switch (gt) {
-#define EAMPS_CASE(GTV)                                                                                   \
-  case GTV:                                                                                               \
-    k_svd_theta<GTV><<<count, threads, smem_theta, s>>>(d_desc, d_list, slab, st, max_sweeps);           \
-    k_svd_vrep<GTV><<<count, threads, smem_vrep, s>>>(d_desc, d_list, slab, st, tile_rows);              \
-    break;
-    EAMPS_CASE(4) EAMPS_CASE(8) EAMPS_CASE(16)
-    default:
-      k_svd_theta<32><<<count, threads, smem_theta, s>>>(d_desc, d_list, slab, st, max_sweeps);
-      k_svd_vrep<32><<<count, threads, smem_vrep, s>>>(d_desc, d_list, slab, st, tile_rows);
-#undef EAMPS_CASE
+    case 4: launch_medium_r<4>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, rpl, threads, slab, st, s); break;
+    case 8: launch_medium_r<8>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, rpl, threads, slab, st, s); break;
+    case 16: launch_medium_r<16>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, rpl, threads, slab, st, s); break;
+    default: launch_medium_r<32>(d_desc, d_list, count, smem_theta, smem_vrep, tile_rows, max_sweeps, rpl, threads, slab, st, s); break;
   }
 }
 

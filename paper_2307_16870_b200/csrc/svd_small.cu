@@ -18,11 +18,13 @@ namespace eamps {
 namespace {
 
 // One round for all pairs. Returns (to the calling thread) whether it rotated something.
-template <int GT>
+// R > 0: the pair's rows (m <= R GT) and V rows (n <= R GT) are register-resident across the dot
+// products and the rotation; R = 0: the generic two-pass loop (tall or wide thetas).
+template <int GT, int R>
 __device__ __forceinline__ bool round_pairs(float2* A, int m, int n, float2* V, int rnd, float skip, float tol) {
   const int tid = threadIdx.x;
   const int groups = blockDim.x / GT, gid = tid / GT, lg = tid % GT;
-  const unsigned mask = 0xffffffffu;
+  const int sh = gid & (32 / GT - 1);   // group index within the warp (bank spreading)
   bool rot = false;
   for (int base = 0; base < n / 2; base += groups) {
     const int slot = base + gid;
@@ -32,45 +34,58 @@ __device__ __forceinline__ bool round_pairs(float2* A, int m, int n, float2* V, 
     float2* ap = A + (size_t)p * m;
     float2* aq = A + (size_t)q * m;
     float al = 0.f, be = 0.f, gr = 0.f, gi = 0.f;
-    if (active) {
-      for (int i = lg; i < m; i += GT) {
-        float2 x = ap[i], y = aq[i];
-        al = fmaf(x.x, x.x, fmaf(x.y, x.y, al));
-        be = fmaf(y.x, y.x, fmaf(y.y, y.y, be));
-        gr = fmaf(x.x, y.x, fmaf(x.y, y.y, gr));    // Re conj(x) y
-        gi = fmaf(x.x, y.y, fmaf(-x.y, y.x, gi));   // Im conj(x) y
+    if constexpr (R > 0) {
+      PairRegs<GT, R> pr;
+      if (active) {
+        pr.load(ap, aq, m, lg, sh);
+        pr.dots(al, be, gr, gi);
       }
-    }
-#pragma unroll
-    for (int o = GT / 2; o > 0; o >>= 1) {
-      al += __shfl_xor_sync(mask, al, o);
-      be += __shfl_xor_sync(mask, be, o);
-      gr += __shfl_xor_sync(mask, gr, o);
-      gi += __shfl_xor_sync(mask, gi, o);
-    }
-    Rot R;
-    if (active && jacobi_rot(al, be, gr, gi, skip, tol, R)) {
-      rot = true;
-      for (int i = lg; i < m; i += GT) {
-        float2 x = ap[i], y = aq[i];
-        apply_rot(x, y, R);
-        ap[i] = x;
-        aq[i] = y;
+      group_sum4<GT>(al, be, gr, gi);
+      Rot Rt;
+      if (active && jacobi_rot(al, be, gr, gi, skip, tol, Rt)) {
+        rot = true;
+        pr.rotate_store(ap, aq, m, lg, sh, Rt);
+        PairRegs<GT, R> pv;
+        float2* vp = V + (size_t)p * n;
+        float2* vq = V + (size_t)q * n;
+        pv.load(vp, vq, n, lg, sh);
+        pv.rotate_store(vp, vq, n, lg, sh, Rt);
       }
-      float2* vp = V + (size_t)p * n;
-      float2* vq = V + (size_t)q * n;
-      for (int i = lg; i < n; i += GT) {
-        float2 x = vp[i], y = vq[i];
-        apply_rot(x, y, R);
-        vp[i] = x;
-        vq[i] = y;
+    } else {
+      if (active) {
+        for (int i = lg; i < m; i += GT) {
+          float2 x = ap[i], y = aq[i];
+          al = fmaf(x.x, x.x, fmaf(x.y, x.y, al));
+          be = fmaf(y.x, y.x, fmaf(y.y, y.y, be));
+          gr = fmaf(x.x, y.x, fmaf(x.y, y.y, gr));    // Re conj(x) y
+          gi = fmaf(x.x, y.y, fmaf(-x.y, y.x, gi));   // Im conj(x) y
+        }
+      }
+      group_sum4<GT>(al, be, gr, gi);
+      Rot Rt;
+      if (active && jacobi_rot(al, be, gr, gi, skip, tol, Rt)) {
+        rot = true;
+        for (int i = lg; i < m; i += GT) {
+          float2 x = ap[i], y = aq[i];
+          apply_rot(x, y, Rt);
+          ap[i] = x;
+          aq[i] = y;
+        }
+        float2* vp = V + (size_t)p * n;
+        float2* vq = V + (size_t)q * n;
+        for (int i = lg; i < n; i += GT) {
+          float2 x = vp[i], y = vq[i];
+          apply_rot(x, y, Rt);
+          vp[i] = x;
+          vq[i] = y;
+        }
       }
     }
   }
   return rot;
 }
 
-template <int GT>
+template <int GT, int R>
 __global__ void __launch_bounds__(1024) k_svd_small(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                     DevState* st, int max_sweeps) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -108,7 +123,7 @@ __global__ void __launch_bounds__(1024) k_svd_small(GateDesc* desc, const int32_
   bool converged = (n < 2);
   for (; sweep < max_sweeps && !converged; ++sweep) {
     int any = 0;
-    for (int rnd = 0; rnd < n - 1; ++rnd) any |= __syncthreads_or(round_pairs<GT>(A, m, n, V, rnd, skip, tol));
+    for (int rnd = 0; rnd < n - 1; ++rnd) any |= __syncthreads_or(round_pairs<GT, R>(A, m, n, V, rnd, skip, tol));
     converged = (any == 0);
   }
   if (!converged && tid == 0) atomicCAS(&st->led.error, 0, -6 /* MPS_E_NOCONV */);
@@ -135,22 +150,38 @@ int small_group(int m) {
   return 32;
 }
 
-void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt,
-                      int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
-  if (count <= 0) return;
+template <int GT, int R>
+static void launch_small_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int threads,
+                           uint8_t* slab, DevState* st, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_svd_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_svd_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_svd_small<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_svd_small<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_svd_small<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
+  k_svd_small<GT, R><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
+}
+
+template <int GT>
+static void launch_small_r(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int rpl,
+                           int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
+  switch (rpl) {
+    case 1: launch_small_t<GT, 1>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+    case 2: launch_small_t<GT, 2>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+    case 4: launch_small_t<GT, 4>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+    case 8: launch_small_t<GT, 8>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+    case 16: launch_small_t<GT, 16>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+    default: launch_small_t<GT, 0>(d_desc, d_list, count, smem, max_sweeps, threads, slab, st, s); break;
+  }
+}
+
+void launch_svd_small(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
+                      int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
+  if (count <= 0) return;
   switch (gt) {
-    case 4: k_svd_small<4><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps); break;
-    case 8: k_svd_small<8><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps); break;
-    case 16: k_svd_small<16><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps); break;
-    default: k_svd_small<32><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps); break;
+    case 4: launch_small_r<4>(d_desc, d_list, count, smem, max_sweeps, rpl, threads, slab, st, s); break;
+    case 8: launch_small_r<8>(d_desc, d_list, count, smem, max_sweeps, rpl, threads, slab, st, s); break;
+    case 16: launch_small_r<16>(d_desc, d_list, count, smem, max_sweeps, rpl, threads, slab, st, s); break;
+    default: launch_small_r<32>(d_desc, d_list, count, smem, max_sweeps, rpl, threads, slab, st, s); break;
   }
 }
 
