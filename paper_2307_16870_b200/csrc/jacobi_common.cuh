@@ -38,6 +38,28 @@ __device__ __forceinline__ bool jacobi_rot(float al, float be, float gr, float g
   return true;
 }
 
+// The same rotation with fast reciprocals (rsqrt / rcp): e = gamma rsqrt(|gamma|^2), the
+// criterion compared in squares; returns t |gamma| for the cached-norm update
+// alpha' = alpha - t|gamma|, beta' = beta + t|gamma| (SURVEY §8(c) algorithm item 3, checked there
+// in numpy). |e| and c^2 + s^2 are 1 to a few ulp.
+__device__ __forceinline__ bool jacobi_rot_fast(float al, float be, float gr, float gi, float skip, float tol2, Rot& R,
+                                                float& tg) {
+  R.c = 1.f; R.s = 0.f; R.er = 1.f; R.ei = 0.f;
+  tg = 0.f;
+  const float g2 = fmaf(gr, gr, gi * gi);
+  if (fminf(al, be) <= skip || !(g2 > tol2 * al * be)) return false;
+  const float ig = rsqrtf(g2);
+  R.er = gr * ig;
+  R.ei = gi * ig;
+  const float zeta = 0.5f * (be - al) * ig;
+  const float az = fabsf(zeta);
+  const float t = copysignf(__frcp_rn(az + sqrtf(fmaf(az, az, 1.f))), zeta);
+  R.c = rsqrtf(fmaf(t, t, 1.f));
+  R.s = R.c * t;
+  tg = t * (g2 * ig);
+  return true;
+}
+
 __device__ __forceinline__ void apply_rot(float2& x, float2& y, const Rot& R) {
   const float2 ey = make_float2(R.er * y.x + R.ei * y.y, R.er * y.y - R.ei * y.x);  // conj(e) y
   const float2 nx = make_float2(R.c * x.x - R.s * ey.x, R.c * x.y - R.s * ey.y);
@@ -73,6 +95,14 @@ struct PairRegs {
       y[u] = aq[i];
     }
   }
+  __device__ __forceinline__ void cross(float& gr, float& gi) const {   // gamma = a_p^H a_q only
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const float2 a = x[u], b = y[u];
+      gr = fmaf(a.x, b.x, fmaf(a.y, b.y, gr));
+      gi = fmaf(a.x, b.y, fmaf(-a.y, b.x, gi));
+    }
+  }
   __device__ __forceinline__ void dots(float& al, float& be, float& gr, float& gi) const {
 #pragma unroll
     for (int u = 0; u < R; ++u) {
@@ -106,6 +136,15 @@ struct PairRegs {
     }
   }
 };
+
+template <int GT>
+__device__ __forceinline__ void group_sum2(float& a, float& b) {
+#pragma unroll
+  for (int o = GT / 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+}
 
 // GT-lane xor-butterfly sum of the four pair statistics (bit-identical in every lane of the group)
 template <int GT>

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(512) k_svd_theta(GateDesc* desc, const int32_t
     A[x] = v;
     nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
   }
-  const bool use_sched = n <= 256 && R > 0;
+  const bool use_sched = n <= 256 && R > 0 && blockDim.x / GT >= n / 2;   // (the fast path below)
   if (use_sched) build_schedule(sched, n);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
@@ -66,42 +66,57 @@ __global__ void __launch_bounds__(512) k_svd_theta(GateDesc* desc, const int32_t
   const int cap = min(max_sweeps, gd.log_sweeps);
   int sweep = 0;
   bool converged = (n < 2);
-  if (R > 0 && groups >= half) {
+  if (use_sched) {
     // fast path: one column pair per lane group (groups >= n/2, checked by the host), the pair's
-    // rows in registers, schedule from shared memory, 32-bit log index
+    // rows in registers, schedule from shared memory, 32-bit log index, and cached column norms
+    // (recomputed exactly at every sweep start, updated analytically after each rotation), so a
+    // round only forms gamma = a_p^H a_q
     const bool active = gid < half;
     const bool full = (m == R * GT);   // (R > 0 here)
     const int sh = gid & (32 / GT - 1); // group index within the warp (bank spreading)
+    float* cn = reinterpret_cast<float*>(sched + (n - 1) * half + 2);   // n cached |a_j|^2
+    const float tol2 = tol * tol;
     uint32_t li = (uint32_t)gid;      // log index = (sweep (n-1) + rnd) n/2 + slot
     for (; sweep < cap && !converged; ++sweep) {
+      for (int j = warp; j < n; j += (int)(blockDim.x >> 5)) {   // exact norms at the sweep start
+        float a = 0.f;
+        for (int i = lane; i < m; i += 32) {
+          const float2 v = A[j * m + i];
+          a = fmaf(v.x, v.x, fmaf(v.y, v.y, a));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) cn[j] = a;
+      }
+      __syncthreads();
       int any = 0;
       for (int rnd = 0; rnd < n - 1; ++rnd, li += half) {
         bool rot = false;
         if (active) {
-          int p, q;
-          if (use_sched) {
-            const uint32_t pq = sched[rnd * half + gid];
-            p = pq & 0xFF;
-            q = pq >> 8;
-          } else {
-            circle_pair_n(gid, rnd, n, p, q);
-          }
+          const uint32_t pq = sched[rnd * half + gid];
+          const int p = pq & 0xFF, q = pq >> 8;
           float2* ap = A + p * m;
           float2* aq = A + q * m;
           constexpr int RR = R > 0 ? R : 1;
           PairRegs<GT, RR> pr;
-          float al = 0.f, be = 0.f, gr = 0.f, gi = 0.f;
           if (full) pr.load_full(ap, aq, lgi, sh);
           else pr.load(ap, aq, m, lgi, sh);
-          pr.dots(al, be, gr, gi);
-          group_sum4<GT>(al, be, gr, gi);
+          float gr = 0.f, gi = 0.f;
+          pr.cross(gr, gi);
+          group_sum2<GT>(gr, gi);
+          const float al = cn[p], be = cn[q];
           Rot Rt;
-          const bool doit = jacobi_rot(al, be, gr, gi, skip, tol, Rt);
+          float tg;
+          const bool doit = jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg);
           if (lgi == 0) lg[li] = make_float4(Rt.c, Rt.s, Rt.er, Rt.ei);
           if (doit) {
             rot = true;
             if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
             else pr.rotate_store(ap, aq, m, lgi, sh, Rt);
+            if (lgi == 0) {
+              cn[p] = al - tg;
+              cn[q] = be + tg;
+            }
           }
         }
         any |= __syncthreads_or(rot);
@@ -272,7 +287,7 @@ __global__ void __launch_bounds__(512) k_svd_vrep(GateDesc* desc, const int32_t*
 
 }  // namespace
 
-size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + (size_t)(n - 1) * (n / 2) * 2 + 64; }
+size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + (size_t)(n - 1) * (n / 2) * 2 + 8 + (size_t)n * 4 + 64; }
 
 size_t svd_vrep_smem(int n, int tile_rows) {
   int npow2 = 1;
