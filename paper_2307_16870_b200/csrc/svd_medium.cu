@@ -21,6 +21,15 @@ namespace eamps {
 
 namespace {
 
+__device__ __forceinline__ void tc_cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tc_cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // The circle-method schedule of one sweep, (p | q << 8) per (round, slot), built once per CTA in
 // shared memory (n <= 256): no integer modulo on the per-round path.
 __device__ __forceinline__ void build_schedule(uint16_t* sched, int n) {
@@ -192,54 +201,78 @@ __global__ void __launch_bounds__(512) k_svd_vrep(GateDesc* desc, const int32_t*
   __syncthreads();
   const float4* lg = reinterpret_cast<const float4*>(slab + gd.ws_log);
   const int groups = blockDim.x / GT, gid = tid / GT, lgi = tid % GT;
-  // V = I R_1 R_2 ... replayed from the log; each group prefetches its next log entry one round
-  // ahead (the log is read once, from HBM/L2)
+  const int half = n / 2;
+  // V = I R_1 R_2 ... replayed from the log. The log streams through shared memory in chunks of
+  // LR rounds (cp.async, double-buffered in the space of the Rayleigh tile T), so the per-round
+  // reads are shared-memory reads; the log is read once from HBM/L2.
+  constexpr int LR = 8;
   const int total = S * (n - 1);
-  float4 nxt = make_float4(1.f, 0.f, 1.f, 0.f);
-  if (total > 0 && gid < n / 2) nxt = lg[gid];
-  for (int t = 0; t < total; ++t) {
-    const int rnd = t % (n - 1);
-    const float4* lrow = lg + (size_t)t * (n / 2);
-    for (int slot = gid; slot < n / 2; slot += groups) {
-      float4 r;
-      if (slot == gid) {
-        r = nxt;
-        if (t + 1 < total) nxt = lrow[n / 2 + gid];   // prefetch: same slot, next round
-      } else {
-        r = lrow[slot];
-      }
-      if (r.y == 0.f) continue;  // identity rotation (uniform within the group)
-      int p, q;
-      if (use_sched) {
-        const uint32_t pq = sched[rnd * (n / 2) + slot];
-        p = pq & 0xFF;
-        q = pq >> 8;
-      } else {
-        circle_pair_n(slot, rnd, n, p, q);
-      }
-      Rot Rt;
-      Rt.c = r.x;
-      Rt.s = r.y;
-      Rt.er = r.z;
-      Rt.ei = r.w;
-      float2* vp = V + (size_t)p * n;
-      float2* vq = V + (size_t)q * n;
-      if constexpr (R > 0) {
-        const int sh = gid & (32 / GT - 1);
-        PairRegs<GT, R> pv;
-        pv.load(vp, vq, n, lgi, sh);
-        pv.rotate_store(vp, vq, n, lgi, sh, Rt);
-      } else {
-        for (int i = lgi; i < n; i += GT) {
-          float2 x = vp[i], y = vq[i];
-          apply_rot(x, y, Rt);
-          vp[i] = x;
-          vq[i] = y;
+  const int nchunks = (total + LR - 1) / LR;
+  float4* lbuf = reinterpret_cast<float4*>(T);                      // 2 x LR x n/2 float4
+  const size_t lbuf_need = (size_t)2 * LR * half * sizeof(float4);
+  const bool staged = lbuf_need <= (size_t)tile_rows * ldt * sizeof(float2);
+  auto issue = [&](int c) {
+    if (staged && c < nchunks) {
+      const int t0 = c * LR, nt = min(LR, total - t0);
+      float4* dst = lbuf + (size_t)(c & 1) * LR * half;
+      const float4* src = lg + (size_t)t0 * half;
+      for (int x = tid; x < nt * half; x += blockDim.x) tc_cp_async16(dst + x, src + x);
+    }
+    tc_cp_async_commit();
+  };
+  issue(0);
+  const bool full = R > 0 && n == R * GT;
+  const int sh = gid & (32 / GT - 1);
+  for (int c = 0; c < nchunks; ++c) {
+    issue(c + 1);
+    tc_cp_async_wait1();
+    __syncthreads();
+    const float4* lrow0 = staged ? lbuf + (size_t)(c & 1) * LR * half : lg + (size_t)c * LR * half;
+    const int t0 = c * LR, nt = min(LR, total - t0);
+    for (int tt = 0; tt < nt; ++tt) {
+      const int rnd = (t0 + tt) % (n - 1);
+      const float4* lrow = lrow0 + (size_t)tt * half;
+      for (int slot = gid; slot < half; slot += groups) {
+        const float4 r = lrow[slot];
+        if (r.y == 0.f) continue;  // identity rotation (uniform within the group)
+        int p, q;
+        if (use_sched) {
+          const uint32_t pq = sched[rnd * half + slot];
+          p = pq & 0xFF;
+          q = pq >> 8;
+        } else {
+          circle_pair_n(slot, rnd, n, p, q);
+        }
+        Rot Rt;
+        Rt.c = r.x;
+        Rt.s = r.y;
+        Rt.er = r.z;
+        Rt.ei = r.w;
+        float2* vp = V + (size_t)p * n;
+        float2* vq = V + (size_t)q * n;
+        if constexpr (R > 0) {
+          PairRegs<GT, R> pv;
+          if (full) {
+            pv.load_full(vp, vq, lgi, sh);
+            pv.rotate_store_full(vp, vq, lgi, sh, Rt);
+          } else {
+            pv.load(vp, vq, n, lgi, sh);
+            pv.rotate_store(vp, vq, n, lgi, sh, Rt);
+          }
+        } else {
+          for (int i = lgi; i < n; i += GT) {
+            float2 x = vp[i], y = vq[i];
+            apply_rot(x, y, Rt);
+            vp[i] = x;
+            vq[i] = y;
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
+  tc_cp_async_wait0();
+  __syncthreads();   // the log buffers (in T) are dead before the Rayleigh tiles overwrite them
   // Rayleigh quotient with theta streamed in row tiles: num_j = sum_i |(theta V)_ij|^2 in FP64
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);  // m x n, ld m
   for (int j = tid; j < n; j += blockDim.x) s2[j] = 0.0;
