@@ -316,6 +316,21 @@ mps_status wave_front(mps_t h) {
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
   }
+  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits
+  for (int gt : {4, 8, 16, 32}) {
+    for (int rpl : {1, 2, 4, 8, 16}) {
+      Bucket b{3, gt, (int)small.size(), 0, 512, 0, rpl, 0, 0};
+      for (int x = 0; x < Gw; ++x) {
+        const GateDesc& gd = hd[x];
+        int g_gt = 0, g_r = 0;
+        if (gd.regime != 3 || !svd_qr_fits(gd.m, gd.n, &g_gt, &g_r) || g_gt != gt || g_r != rpl) continue;
+        small.push_back(x);
+        b.smem = std::max(b.smem, svd_qr_smem(gd.m, gd.n));
+      }
+      b.end = (int)small.size();
+      if (b.end != b.begin) buckets.push_back(b);
+    }
+  }
   // buckets: (regime, lane-group size GT, rows per lane R); R > 0 keeps a pair's rows in registers
   for (int reg : {0, 2}) {
     for (int gt : {4, 8, 16, 32}) {
@@ -400,7 +415,11 @@ mps_status wave_front(mps_t h) {
   if (prof) CK(cudaEventRecord(h->ev[1], h->s));
   // a2 + a3 SVD, small regime: one CTA per theta
   for (const Bucket& b : buckets) {
-    if (b.regime == 0) {
+    if (b.regime == 3) {
+      launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, h->slab,
+                    h->dst, h->s);
+      ++h->launches;
+    } else if (b.regime == 0) {
       launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.threads,
                        h->slab, h->dst, h->s);
       ++h->launches;
@@ -705,7 +724,14 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     gd.n = d * gd.r;
     // SVD regime: 0 small (theta + V in one CTA), 2 medium (theta in one CTA, V replayed from a
     // rotation log), 1 large (blocked, HBM-resident)
-    gd.regime = svd_small_fits(gd.m, gd.n) ? 0 : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
+    // SVD regime: 3 QR-preconditioned Jacobi (m >= n, fits one CTA, no V accumulation), else
+    // 0 small (theta + V in one CTA), 2 medium (theta in one CTA, V replayed from a rotation log),
+    // 1 large (tcgen05 block Jacobi, HBM-resident)
+    int qgt = 0, qr = 0;
+    static const bool no_qr = getenv("EAMPS_NO_QR") != nullptr;   // dev A/B switch
+    gd.regime = (!no_qr && svd_qr_fits(gd.m, gd.n, &qgt, &qr)) ? 3
+                : svd_small_fits(gd.m, gd.n)                  ? 0
+                : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
     // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)

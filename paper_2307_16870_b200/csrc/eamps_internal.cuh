@@ -49,7 +49,7 @@ struct DevPool {
 // One per gate of a wave (device array, built by the host).
 struct GateDesc {
   int32_t site, l, mid, r;          // chi_l, chi_m, chi_r
-  int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large
+  int32_t m, n, n_pad, regime;      // theta is m x n (m = d l, n = d r); regime 0 small, 1 large, 2 medium, 3 QR
   int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
   int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
   int64_t ws_log;                   // medium: rotation log, log_sweeps x (n-1) x n/2 float4 (c, s, e); large: TC scratch
@@ -100,6 +100,10 @@ inline int rows_per_lane(int rows, int gt) {
   while (r < need) r <<= 1;
   return r <= 16 ? r : 0;
 }
+size_t svd_qr_smem(int m, int n);
+bool svd_qr_fits(int m, int n, int* gt_out, int* rpl_out);
+void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
+                   uint8_t* slab, DevState* st, cudaStream_t s);
 size_t svd_small_smem(int m, int n);
 bool svd_small_fits(int m, int n);
 int small_group(int m);

@@ -158,6 +158,17 @@ __device__ __forceinline__ void group_sum4(float& al, float& be, float& gr, floa
   }
 }
 
+// The circle-method schedule of one sweep, (p | q << 8) per (round, slot), in shared memory (n <= 256)
+__device__ __forceinline__ void build_circle_schedule(uint16_t* sched, int n) {
+  const int half = n / 2;
+  for (int x = threadIdx.x; x < (n - 1) * half; x += blockDim.x) {
+    const int rnd = x / half, slot = x % half;
+    int p, q;
+    circle_pair_n(slot, rnd, n, p, q);
+    sched[x] = (uint16_t)(p | (q << 8));
+  }
+}
+
 __device__ __forceinline__ double warp_sum_d32(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -101,18 +101,23 @@ __global__ void __launch_bounds__(512) k_svd_theta(GateDesc* desc, const int32_t
       int any = 0;
       for (int rnd = 0; rnd < n - 1; ++rnd, li += half) {
         bool rot = false;
+        // (a warp may hold active and idle groups: the shuffles run unconditionally)
+        constexpr int RR = R > 0 ? R : 1;
+        PairRegs<GT, RR> pr;
+        int p = 0, q = 1;
+        float gr = 0.f, gi = 0.f;
         if (active) {
           const uint32_t pq = sched[rnd * half + gid];
-          const int p = pq & 0xFF, q = pq >> 8;
+          p = pq & 0xFF;
+          q = pq >> 8;
+          if (full) pr.load_full(A + p * m, A + q * m, lgi, sh);
+          else pr.load(A + p * m, A + q * m, m, lgi, sh);
+          pr.cross(gr, gi);
+        }
+        group_sum2<GT>(gr, gi);
+        if (active) {
           float2* ap = A + p * m;
           float2* aq = A + q * m;
-          constexpr int RR = R > 0 ? R : 1;
-          PairRegs<GT, RR> pr;
-          if (full) pr.load_full(ap, aq, lgi, sh);
-          else pr.load(ap, aq, m, lgi, sh);
-          float gr = 0.f, gi = 0.f;
-          pr.cross(gr, gi);
-          group_sum2<GT>(gr, gi);
           const float al = cn[p], be = cn[q];
           Rot Rt;
           float tg;

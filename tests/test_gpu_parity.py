@@ -162,6 +162,18 @@ def test_config2_chi256_blocked_path_parity():
     assert worst < SIG_RTOL, worst
 
 
+@pytest.mark.parametrize("chi,count", [(128, 2), (512, 1)])
+def test_config2_tensor_core_path_parity(chi, count):
+    """the tcgen05 3xTF32 block Jacobi + FP64-anchored polish (large regime, chi >= 128 in config 2)
+    at the strict bar: relative 1e-5 on every sigma >= 1e-6 sigma_max (sigma_min / sigma_max =
+    (2 chi)^-1.5 = 3e-5 at chi = 512), identical kept ranks, f to 1e-6."""
+    gpu, orc, G = _micro(chi, count)
+    worst, same = compare_layer(gpu, orc, G)
+    assert same
+    assert worst < SIG_RTOL, worst
+    assert all(gpu.mps_last_sweeps(g) > 0 for g in range(G))
+
+
 def test_hastings_update_keeps_state():
     """no truncation (t = 1): the reabsorbed pair reproduces Theta' (gauge-invariant check)."""
     pk = _pk()
