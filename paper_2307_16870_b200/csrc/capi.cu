@@ -305,7 +305,7 @@ mps_status wave_front(mps_t h) {
     gd.ws_pi = (int64_t)take((size_t)gd.n_pad * 4);
     const size_t kmn = (size_t)std::min(gd.m, gd.n);
     // E (k x k, reabsorb); the large regime's polish also keeps shift | den (2 n_pad doubles) there
-    gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, gd.regime == 1 ? (size_t)16 * gd.n_pad : (size_t)0));
+    gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, (gd.regime == 1 || gd.regime == 3) ? (size_t)16 * gd.n_pad : (size_t)0));
     gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
                 : gd.regime == 1 ? (int64_t)take(svd_tc_scratch_bytes(gd.n_pad))
                                  : 0;
@@ -418,7 +418,9 @@ mps_status wave_front(mps_t h) {
     if (b.regime == 3) {
       launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, h->slab,
                     h->dst, h->s);
-      ++h->launches;
+      int maxn = 0;
+      for (int i = b.begin; i < b.end; ++i) maxn = std::max(maxn, hd[small[i]].n);
+      h->launches += 1 + launch_spectrum_polish(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->dst, h->s);
     } else if (b.regime == 0) {
       launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.threads,
                        h->slab, h->dst, h->s);
@@ -742,7 +744,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     const int kmn = std::min(gd.m, gd.n);
     p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
            align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) +
-           align_up(std::max((size_t)kmn * kmn * 8, gd.regime == 1 ? (size_t)16 * gd.n_pad : (size_t)0)) +
+           align_up(std::max((size_t)kmn * kmn * 8, (gd.regime == 1 || gd.regime == 3) ? (size_t)16 * gd.n_pad : (size_t)0)) +
            align_up(logb);
     int kmax = std::min(gd.m, gd.n);
     if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);

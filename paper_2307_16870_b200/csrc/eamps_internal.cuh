@@ -125,6 +125,8 @@ size_t svd_tc_scratch_bytes(int n_pad);
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,
                cudaStream_t s, int* error_out);
+int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, DevState* st,
+                           cudaStream_t s);
 // parallel = 1: FIXED / NAIVE (target independent of the ledger): one warp per gate;
 // parallel = 0: GLOBAL / NEAREST: one warp walks the gates in canonical order.
 void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s);

@@ -900,11 +900,11 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
                                                    uint8_t* slab) {
   const int gi = blockIdx.y, rnd = blockIdx.z;
   const GateDesc& gd = desc[list[gi]];
-  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  const int n = gd.n, np = gd.n_pad;
+  const int nb = ((n + PWC - 1) / PWC) * 2, pair = blockIdx.x;   // blocks of 32 over n rounded up to 64
   if (pair >= nb / 2 || rnd >= nb - 1) return;
   int I, J;
   circle_pair(pair, rnd, nb, I, J);
-  const int n = gd.n, np = gd.n_pad;
   if (I * TB >= n && J * TB >= n) return;
   const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
   double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
@@ -933,8 +933,14 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
           const int cl = colof(l, I, J);
           if (l == j || cl >= n) continue;
           const double gr = sym(l, j) + sym(64 + l, 64 + j), gim = sym(l, 64 + j) - sym(64 + l, j);
+          const double al_ = s2[cl];
+          // only well-separated pairs (ratio > 4): the contamination of a small sigma^2 by a large
+          // one. Between near-degenerate pairs C_lj also holds the product of their shared
+          // contaminations (a fourth-order coupling over a small gap) that the pairwise formula
+          // would turn into a spurious shift; their own mixing moves sigma^2 by at most ~tol.
+          if (fmax(aj, al_) < 4.0 * fmin(aj, al_)) continue;
           const double g2 = (gr * gr + gim * gim) / (dj * den[cl]);
-          const double dlt = aj - s2[cl];
+          const double dlt = aj - al_;
           const double h = 0.5 * fabs(dlt);
           const double sh = g2 / (h + sqrt(h * h + g2));
           acc += dlt >= 0.0 ? sh : -sh;
@@ -1000,6 +1006,29 @@ int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_l
 }
 
 size_t svd_tc_scratch_bytes(int n_pad) { return tcj::Scratch::total(n_pad / tcj::PWC); }
+
+// Rayleigh quotients + FP64-anchored polish + sort/tails for gates whose V (ld n_pad) is in the
+// workspace (the large regime and the QR-preconditioned regime). Returns launches issued.
+int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, DevState* st,
+                           cudaStream_t s) {
+  if (count <= 0) return 0;
+  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
+  static bool pattr = false;
+  if (!pattr) {
+    cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
+    pattr = true;
+  }
+  const int nb = ((max_n + tcj::PWC - 1) / tcj::PWC) * 2;
+  static const bool no_polish = getenv("EAMPS_NO_POLISH") != nullptr;   // dev A/B switch
+  if (!no_polish && nb >= 2)
+    tcj::k_tc_polish<<<dim3(nb / 2, count, nb - 1), 128, tcj::kGramSmem, s>>>(d_desc, d_list, slab);
+  int npow2 = 1;
+  while (npow2 < max_n) npow2 <<= 1;
+  const size_t smem = (size_t)npow2 * 12 + 16 + 1024 * 8;
+  cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
+  return 3;
+}
 
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_scratch, int32_t* h_pinned_flag, cudaStream_t s,
@@ -1068,19 +1097,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
   }
   if (!done) *error_out = -6;
-  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
-  static bool pattr = false;
-  if (!pattr) {
-    cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
-    pattr = true;
-  }
-  tcj::k_tc_polish<<<dim3(pairs_max, count, nb_max - 1), 128, tcj::kGramSmem, s>>>(d_desc, d_list, slab);
-  int npow2 = 1;
-  while (npow2 < max_n) npow2 <<= 1;
-  size_t smem = (size_t)npow2 * 12 + 16 + 1024 * 8;
-  cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
-  launches += 3;
+  launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
   return launches;
 }
 

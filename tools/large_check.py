@@ -26,6 +26,10 @@ if os.environ.get("ORACLE", "1") == "1":
         rel = np.abs(sg[mask] - so[mask]) / so[mask]
         kg = gpu.mps_truncation_log()[g]["chi_after"]; ko = orc.records()[g]["chi_after"]
         print("gate", g, "max rel sigma err %.3e" % rel.max(), "at j", int(rel.argmax()), "k", kg, ko, flush=True)
+        if os.environ.get("DETAIL"):
+            idx = np.argsort(-rel)[:8]
+            print("   worst j:", idx.tolist(), "rel:", ["%.1e" % rel[i] for i in idx], "sigma/s0:", ["%.1e" % (so[mask][i] / so[0]) for i in idx])
+            print("   signed (g-o)/o at worst:", ["%.1e" % ((sg[mask][i] - so[mask][i]) / so[mask][i]) for i in idx])
 if Gt:
     tensors, gates = workloads.micro_chain(chi, Gt)
     m2 = pk.MPS(2 * Gt, strategy="fixed", f_fixed=0.9999, slab_bytes=int(os.environ.get("SLAB_GB", "40")) << 30)
