@@ -430,6 +430,7 @@ constexpr size_t kGramSmem = 4 * (size_t)128 * 32 * 4 + 2 * (size_t)64 * 288 + 1
 constexpr size_t kRotStage = (size_t)128 * 16 * 4;          // one image of a 128 x 16 chunk: 8 KB
 constexpr size_t kRotSmem = (size_t)EIMG_FLOATS * 4 + 2 * (size_t)64 * 128 * 8 + 2 * 2 * kRotStage + 1024;
 constexpr size_t kInnerSmem = 2 * sizeof(float2) * 64 * 65;
+constexpr int kInnerT = 512;   // threads of the inner solve (more warps per SM hide shared-memory latency)
 
 struct Scratch {                  // per gate: slab offset of its TC scratch (GateDesc::ws_log)
   static __host__ __device__ size_t gram_bytes(int pairs) { return (size_t)pairs * 64 * 64 * 8; }
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
 // group (no broadcast round trip). W's FP32 drift from unitarity (~1e-6) is consistent between
 // theta and V (the same E rotates both) and is absorbed by the Rayleigh normalisation and the
 // FP64-anchored polish.
-__global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                   int rnd, uint8_t* slab, LargeCtl* ctl, const double* norm2,
                                                   int inner_sweeps, float tol_floor, float tol_internal) {
   const int gi = blockIdx.y;
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(dsm);
   float2(*Ws)[65] = Gs + 64;
   const int tid = threadIdx.x;
-  for (int x = tid; x < 64 * 64; x += 256) {
+  for (int x = tid; x < 64 * 64; x += kInnerT) {
     const int a = x >> 6, b = x & 63;
     Gs[a][b] = Gin[x];
     Ws[a][b] = make_float2(a == b ? 1.f : 0.f, 0.f);
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   const float tol = fmaxf(tol_floor, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
   const float tol_int = fmaxf(tol, tol_internal);
   int any = 0, internal = 0;
-  for (int x = tid; x < 64 * 64; x += 256) {
+  for (int x = tid; x < 64 * 64; x += kInnerT) {
     const int p = x >> 6, q = x & 63;
     if (p < q) {
       const float al = Gs[p][p].x, be = Gs[q][q].x;
@@ -636,7 +637,7 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   __shared__ float4 par[32];      // c, s, er, ei
   __shared__ int2 pq[32];
   __shared__ uint16_t blk[496];   // the off-diagonal block pairs a < b
-  for (int x = tid; x < 496; x += 256) {
+  for (int x = tid; x < 496; x += kInnerT) {
     int aa = 0, rem = x;
     while (rem >= 31 - aa) { rem -= 31 - aa; ++aa; }
     blk[x] = (uint16_t)(aa | ((aa + 1 + rem) << 8));
@@ -678,7 +679,7 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
         pq[tid] = make_int2(p, q);
       }
       __syncthreads();
-      for (int x = tid; x < 496; x += 256) {
+      for (int x = tid; x < 496; x += kInnerT) {
         const int ia = blk[x] & 0xFF, ib = blk[x] >> 8;
         const float4 Ja = par[ia], Jb = par[ib];
         if (Ja.y == 0.f && Jb.y == 0.f) continue;
@@ -708,13 +709,13 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
         Gs[cb.x][ra.x] = make_float2(X[0][0].x, -X[0][0].y); Gs[cb.y][ra.x] = make_float2(X[0][1].x, -X[0][1].y);
         Gs[cb.x][ra.y] = make_float2(X[1][0].x, -X[1][0].y); Gs[cb.y][ra.y] = make_float2(X[1][1].x, -X[1][1].y);
       }
-      {   // W <- W J for every pair: thread (pair k = tid / 8, rows (tid % 8) + 8 i)
-        const int k = tid >> 3;
+      {   // W <- W J for every pair: thread (pair k = tid / (T/32), rows tid % (T/32) + (T/32) i)
+        const int k = tid / (kInnerT / 32);
         const float4 J = par[k];
         if (J.y != 0.f) {
           const int2 cq = pq[k];
 #pragma unroll 4
-          for (int x = tid & 7; x < 64; x += 8) {
+          for (int x = tid % (kInnerT / 32); x < 64; x += kInnerT / 32) {
             const float2 xx = Ws[x][cq.x], yy = Ws[x][cq.y];
             const float2 ey = make_float2(J.z * yy.x + J.w * yy.y, J.z * yy.y - J.w * yy.x);
             Ws[x][cq.x] = make_float2(J.x * xx.x - J.y * ey.x, J.x * xx.y - J.y * ey.y);
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(256) k_tc_inner(const GateDesc* __restrict__ d
   }
   __syncthreads();
   // E = W - I as the rotation's B images (hi, lo), Re then Im: element (n = out col, k = in col) = E[k][n]
-  for (int x = tid; x < 64 * 64; x += 256) {
+  for (int x = tid; x < 64 * 64; x += kInnerT) {
     const int k = x >> 6, n = x & 63;
     float2 w = Ws[k][n];
     if (k == n) w.x -= 1.f;
@@ -1072,7 +1073,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
       if (prof) cudaEventRecord(ev[0], s);
       tcj::k_tc_gram<<<grid, 128, tcj::kGramSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
       if (prof) cudaEventRecord(ev[1], s);
-      tcj::k_tc_inner<<<grid, 256, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps, tol_floor,
+      tcj::k_tc_inner<<<grid, tcj::kInnerT, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps, tol_floor,
                                                          tol_internal);
       if (prof) cudaEventRecord(ev[2], s);
       tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
