@@ -996,7 +996,13 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
     e.chr = dm[2];
     e.src_elem = elems;
     elems += (int64_t)dm[0] * h->d * dm[2];
-    if (lamlen[e.site] != e.chl) { e.resetL = e.chl; lamlen[e.site] = e.chl; }
+    if (lamlen[e.site] != e.chl) {
+      e.resetL = e.chl;
+      lamlen[e.site] = e.chl;
+      // the previous entry may already reset this bond (its right bond): the device scatter runs
+      // the entries in parallel, so only the later reset may stay (sequential import semantics)
+      if (x > 0) ent[x - 1].resetR = 0;
+    }
     if (lamlen[e.site + 1] != e.chr) { e.resetR = e.chr; lamlen[e.site + 1] = e.chr; }
   }
   st = sync_state(h);

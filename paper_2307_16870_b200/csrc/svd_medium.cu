@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(512) k_svd_theta(GateDesc* desc, const int32_t
     const bool active = gid < half;
     const bool full = (m == R * GT);   // (R > 0 here)
     const int sh = gid & (32 / GT - 1); // group index within the warp (bank spreading)
-    float* cn = reinterpret_cast<float*>(sched + (n - 1) * half + 2);   // n cached |a_j|^2
+    float* cn = reinterpret_cast<float*>(                                 // n cached |a_j|^2
+        (reinterpret_cast<uintptr_t>(sched + (n - 1) * half) + 15) & ~uintptr_t(15));
     const float tol2 = tol * tol;
     uint32_t li = (uint32_t)gid;      // log index = (sweep (n-1) + rnd) n/2 + slot
     for (; sweep < cap && !converged; ++sweep) {
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(512) k_svd_vrep(GateDesc* desc, const int32_t*
 
 }  // namespace
 
-size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + (size_t)(n - 1) * (n / 2) * 2 + 8 + (size_t)n * 4 + 64; }
+size_t svd_theta_smem(int m, int n) { return (size_t)m * n * 8 + (size_t)(n - 1) * (n / 2) * 2 + 16 + (size_t)n * 4 + 64; }
 
 size_t svd_vrep_smem(int n, int tile_rows) {
   int npow2 = 1;

@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
   int32_t* six = reinterpret_cast<int32_t*>(s2 + npow2);
   double* part = reinterpret_cast<double*>(six + npow2 + (npow2 & 1));       // QR_T doubles
   uint16_t* sched = reinterpret_cast<uint16_t*>(part + QR_T);                // (n-1) x n/2
-  float* cn = reinterpret_cast<float*>(sched + (n - 1) * half + 2);          // n cached |b_j|^2
+  float* cn = reinterpret_cast<float*>(                                        // n cached |b_j|^2
+      (reinterpret_cast<uintptr_t>(sched + (n - 1) * half) + 15) & ~uintptr_t(15));
   __shared__ float2 s_rdiag[256];                                             // R_jj
   __shared__ float s_wn[32];
   __shared__ float s_xn2, s_beta;
@@ -248,7 +249,7 @@ size_t svd_qr_smem(int m, int n) {
   int npow2 = 1;
   while (npow2 < n) npow2 <<= 1;
   return (size_t)m * n * 8 + (size_t)QR_TILE * (n + 1) * 8 + (size_t)npow2 * 12 + 16 + QR_T * 8 +
-         (size_t)(n - 1) * (n / 2) * 2 + 8 + (size_t)n * 4 + 64;
+         (size_t)(n - 1) * (n / 2) * 2 + 16 + (size_t)n * 4 + 64;
 }
 
 // QR path: m >= n, n <= 256, one pair per lane group with at most QR_T threads, rows per lane

@@ -1,0 +1,135 @@
+"""GPU edge cases against the oracle (same seeded inputs, the north-star bars of test_gpu_parity):
+ragged and rectangular thetas in every SVD regime (small, QR-preconditioned, medium with m < n,
+tcgen05 large regime with column padding, m < n and m >> n), an empty layer, product gates
+(rank-1 updates), the bond cap (capped truncations, guarantee lost) and the
+non-convergence error path."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from test_gpu_parity import EST_ATOL, SIG_RTOL, compare_layer
+
+pytestmark = pytest.mark.gpu
+
+
+def _pk():
+    import paper_2307_16870_b200 as pk
+    return pk
+
+
+def _pair(chil, chim, chir, seed):
+    """random normalised B_left (chil, 2, chim), B_right (chim, 2, chir) and a Haar gate (complex64)."""
+    rng = workloads.rng_for(9, chil, chim, chir, seed)
+    L = rng.standard_normal((chil, 2, chim)) + 1j * rng.standard_normal((chil, 2, chim))
+    R = rng.standard_normal((chim, 2, chir)) + 1j * rng.standard_normal((chim, 2, chir))
+    L /= np.linalg.norm(L)
+    R /= np.linalg.norm(R) / np.sqrt(chim)
+    U = workloads.haar_u4(9, chil, chir, seed)
+    return L.astype(np.complex64), R.astype(np.complex64), U
+
+
+def _run_pair(shapes, f=0.9999, chi_cap=0):
+    pk = _pk()
+    tensors, gates = [], []
+    for x, (l, mid, r) in enumerate(shapes):
+        L, R, U = _pair(l, mid, r, x)
+        tensors += [L, R]
+        gates.append(U)
+    N = 2 * len(shapes)
+    gates = np.stack(gates)
+    big = max(max(l, r) for l, _, r in shapes)
+    gpu = pk.MPS(N, strategy="fixed", f_fixed=f, chi_cap=chi_cap, slab_bytes=max(256 << 20, 64 * (2 * big) ** 2 * 8 * len(shapes)))
+    orc = oracle.OracleMPS(N, strategy="fixed", f_fixed=f, chi_cap=chi_cap)
+    gpu.mps_import_sites(0, tensors)
+    for i, B in enumerate(tensors):
+        orc.import_site(i, B)
+    sites = np.arange(0, N, 2, dtype=np.int32)
+    gpu.mps_apply_layer(sites, gates)
+    orc.apply_layer(sites, gates)
+    return gpu, orc, len(shapes)
+
+
+@pytest.mark.parametrize("shape,regime", [
+    ((5, 9, 7), "small (ragged, m < n)"),
+    ((48, 40, 37), "QR (n = 74, partially active warps)"),
+    ((40, 64, 80), "medium (m = 80 < n = 160)"),
+    ((70, 90, 100), "large tcgen05 (n = 200 -> n_pad 256)"),
+    ((64, 100, 150), "large, m = 128 < n = 300"),
+    ((200, 120, 70), "large, m = 400 >> n = 140"),
+])
+def test_ragged_regimes_parity(shape, regime):
+    gpu, orc, G = _run_pair([shape])
+    worst, same = compare_layer(gpu, orc, G)
+    assert same, regime
+    assert worst < SIG_RTOL, (regime, worst)
+
+
+def test_mixed_wave_all_regimes():
+    """one layer whose gates fall into every regime at once (bucketing, one wave)."""
+    shapes = [(5, 9, 7), (48, 40, 37), (40, 64, 80), (70, 90, 100), (3, 4, 2), (33, 20, 31)]
+    gpu, orc, G = _run_pair(shapes)
+    worst, same = compare_layer(gpu, orc, G)
+    assert same and worst < SIG_RTOL, worst
+
+
+def test_empty_layer_is_a_no_op():
+    pk = _pk()
+    gpu = pk.MPS(6, f_min=0.99, n_planned=4, slab_bytes=64 << 20)
+    gpu.mps_apply_layer(np.zeros(0, np.int32), np.zeros((0, 4, 4), np.complex64))
+    assert list(gpu.mps_bond_dims()) == [1] * 5
+    assert gpu.mps_fidelity_estimate()["n_done"] == 0
+
+
+def test_product_gates_keep_rank_one():
+    """U = u1 (x) u2 on a product state: theta has rank 1, every update keeps chi = 1, f = 1."""
+    pk = _pk()
+    N = 8
+    rng = np.random.default_rng(5)
+    u1 = workloads.haar_from_ginibre(workloads.ginibre(rng, 2))
+    u2 = workloads.haar_from_ginibre(workloads.ginibre(rng, 2))
+    U = np.kron(u1, u2).astype(np.complex64)
+    gpu = pk.MPS(N, f_min=0.9, n_planned=8, strategy="global", slab_bytes=64 << 20)
+    orc = oracle.OracleMPS(N, f_min=0.9, n_planned=8, strategy="global")
+    for t in range(2):
+        sites = np.array(workloads.brickwork_sites(N, t), np.int32)
+        us = np.stack([U] * len(sites))
+        gpu.mps_apply_layer(sites, us)
+        orc.apply_layer(sites, us)
+    assert list(gpu.mps_bond_dims()) == [1] * (N - 1) == list(orc.bond_dims())
+    recs = gpu.mps_truncation_log()
+    assert all(r["chi_after"] == 1 and abs(r["achieved_f"] - 1.0) < 1e-6 for r in recs)
+    sg, so = gpu.mps_to_statevector(), orc.statevector()
+    assert abs(np.vdot(so, sg)) ** 2 / (np.vdot(so, so).real * np.vdot(sg, sg).real) > 1 - 1e-6
+
+
+def test_bond_cap_forces_capped_truncations():
+    """config 1 with chi_cap = 4: capped records, guarantee lost, same ranks and
+    ledger as the oracle with the same cap."""
+    pk = _pk()
+    N, depth = 12, 8
+    layers = workloads.brickwork_circuit(1, N, depth)
+    npl = workloads.n_two_qubit_gates(layers)
+    gpu = pk.MPS(N, f_min=0.99, n_planned=npl, strategy="global", chi_cap=4, slab_bytes=128 << 20)
+    orc = oracle.OracleMPS(N, f_min=0.99, n_planned=npl, strategy="global", chi_cap=4)
+    for sites, us in layers:
+        gpu.mps_apply_layer(sites, us)
+        orc.apply_layer(sites, us)
+        assert list(gpu.mps_bond_dims()) == list(orc.bond_dims())
+    assert max(gpu.mps_bond_dims()) <= 4
+    eg, eo = gpu.mps_fidelity_estimate(), orc.estimate()
+    assert not eg["guarantee_held"] and not eo["guarantee_held"]
+    assert abs(eg["est"] - eo["est"]) < EST_ATOL
+    assert any(r["capped"] for r in gpu.mps_truncation_log())
+
+
+def test_nonconvergence_is_reported_and_sticky():
+    pk = _pk()
+    tensors, gates = workloads.micro_chain(64, 1)
+    gpu = pk.MPS(2, strategy="fixed", f_fixed=0.9999, max_sweeps=1, slab_bytes=256 << 20)
+    gpu.mps_import_sites(0, tensors)
+    with pytest.raises(pk.EampsError) as e:
+        gpu.mps_apply_layer(np.zeros(1, np.int32), gates)
+    assert e.value.status == pk.MPS_E_NOCONV
+    with pytest.raises(pk.EampsError):
+        gpu.mps_fidelity_estimate()
