@@ -886,6 +886,195 @@ __global__ void __launch_bounds__(256) k_tc_rot(const GateDesc* __restrict__ des
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
+// ---- P <- P + P E, warp-specialised (the default rotation kernel). grid (pairs max, count);
+// 288 threads = 9 warps:
+//   warp 0      : one elected thread issues the MMAs (12 per 8-column chunk, 3xTF32, N = 64) into
+//                 one of two TMEM accumulators (tile t uses buffer t % 2);
+//   warps 1-4   : producers, thread = row of the 128-row tile: global -> registers -> TF32 hi/lo
+//                 images in a 4-deep shared-memory ring (full / empty mbarriers);
+//   warps 5-8   : epilogue, thread = row: TMEM -> registers, P' = P + D with P re-read from L2,
+//                 coalesced stores; then releases the accumulator buffer.
+// Loads, MMAs and stores of consecutive chunks and tiles overlap (the simple kernel serialised a
+// chunk's conversion with the previous chunk's MMAs and the tile epilogue with both).
+constexpr int WS_NS = 4;                                     // image ring depth
+constexpr int WS_RAW = 8;                                    // raw chunks in flight per producer row
+constexpr size_t kRotWsSmem = (size_t)EIMG_FLOATS * 4 + (size_t)WS_NS * 2 * kRotStage + (size_t)WS_RAW * 8 * 128 * 8 + 1024;
+__global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                   int rnd, uint8_t* slab, const LargeCtl* ctl) {
+  const int gi = blockIdx.y;
+  if (ctl[gi].conv) return;
+  const GateDesc& gd = desc[list[gi]];
+  const int nb = gd.n_pad / TB, pair = blockIdx.x;
+  if (pair >= nb / 2 || rnd >= nb - 1) return;
+  const int pairs = gd.n_pad / PWC;
+  const int32_t* rflag =
+      reinterpret_cast<const int32_t*>(slab + gd.ws_log + Scratch::gram_bytes(pairs) + Scratch::eimg_bytes(pairs));
+  if (!rflag[pair]) return;
+  int I, J;
+  circle_pair(pair, rnd, nb, I, J);
+  const float* Eg = reinterpret_cast<const float*>(slab + gd.ws_log + Scratch::gram_bytes(pairs)) + (size_t)pair * EIMG_FLOATS;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  float* Es = reinterpret_cast<float*>(base);                      // 64 KB: Re h|l, Im h|l
+  uint8_t* ring = base + (size_t)EIMG_FLOATS * 4;                  // WS_NS x (hi, lo) x 8 KB
+  float2* rawr = reinterpret_cast<float2*>(ring + (size_t)WS_NS * 2 * kRotStage);   // WS_RAW x [8 cols][128 rows]
+  __shared__ uint64_t full[WS_NS], empty[WS_NS], tfull[2], tempty[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int x = tid; x < EIMG_FLOATS / 4; x += blockDim.x) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
+  tc::cp_async_commit();
+  if (warp == 0) tc::tmem_alloc(&tbase, 256);
+  if (tid == 0) {
+    for (int i = 0; i < WS_NS; ++i) {
+      tc::mbar_init(&full[i], 128);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  tc::cp_async_wait_all();
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tbase;
+  const int m = gd.m, np = gd.n_pad;
+  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128, ntiles = tiles_th + tiles_v;
+  constexpr int CH = PWC / 8;                                     // chunks per tile
+  if (warp == 0) {
+    // ---------------- MMA issuer
+    if (tid == 0) {
+      const uint32_t id_p = tc::make_idesc_tf32(128, 64, false, false);
+      const uint32_t id_n = id_p | (1u << 14);   // negate B (-E_im)
+      const uint32_t e0 = tc::smem_u32(Es);
+      constexpr uint32_t EI = 16384;
+      int u = 0;                                 // chunk counter
+      for (int t = 0; t < ntiles; ++t) {
+        const int ab = t & 1;
+        if (t >= 2) tc::mbar_wait(&tempty[ab], ((t - 2) >> 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t dRe = tmem + 128 * ab, dIm = dRe + 64;
+        for (int q = 0; q < CH; ++q, ++u) {
+          const int sl = u % WS_NS;
+          tc::mbar_wait(&full[sl], (u / WS_NS) & 1);
+          tc::fence_after_sync();
+          const uint32_t a0 = tc::smem_u32(ring + (size_t)sl * 2 * kRotStage);
+          const uint32_t eoff = 2 * q * E_LBO;
+          const uint64_t aRh = tc::make_desc(a0, R_LBO, R_SBO), aRl = tc::make_desc(a0 + kRotStage, R_LBO, R_SBO);
+          const uint64_t aIh = tc::make_desc(a0 + 2 * R_LBO, R_LBO, R_SBO);
+          const uint64_t aIl = tc::make_desc(a0 + kRotStage + 2 * R_LBO, R_LBO, R_SBO);
+          const uint64_t bRh = tc::make_desc(e0 + eoff, E_LBO, E_SBO), bRl = tc::make_desc(e0 + EI + eoff, E_LBO, E_SBO);
+          const uint64_t bIh = tc::make_desc(e0 + 2 * EI + eoff, E_LBO, E_SBO);
+          const uint64_t bIl = tc::make_desc(e0 + 3 * EI + eoff, E_LBO, E_SBO);
+          const uint32_t acc0 = q > 0 ? 1u : 0u;
+          tc::mma_tf32(dRe, aRh, bRh, id_p, acc0);
+          tc::mma_tf32(dRe, aRh, bRl, id_p, 1u);
+          tc::mma_tf32(dRe, aRl, bRh, id_p, 1u);
+          tc::mma_tf32(dRe, aIh, bIh, id_n, 1u);
+          tc::mma_tf32(dRe, aIh, bIl, id_n, 1u);
+          tc::mma_tf32(dRe, aIl, bIh, id_n, 1u);
+          tc::mma_tf32(dIm, aRh, bIh, id_p, acc0);
+          tc::mma_tf32(dIm, aRh, bIl, id_p, 1u);
+          tc::mma_tf32(dIm, aRl, bIh, id_p, 1u);
+          tc::mma_tf32(dIm, aIh, bRh, id_p, 1u);
+          tc::mma_tf32(dIm, aIh, bRl, id_p, 1u);
+          tc::mma_tf32(dIm, aIl, bRh, id_p, 1u);
+          tc::mma_commit(&empty[sl]);            // the slot is free once these MMAs completed
+        }
+        tc::mma_commit(&tfull[ab]);              // the tile's accumulator is complete
+      }
+    }
+    __syncwarp();
+  } else if (warp <= 4) {
+    // ---------------- producers: thread = row. Each thread copies its own row of the next WS_RAW
+    // chunks with 8-byte cp.async (64 KB in flight per CTA), then converts its row into the images.
+    const int row_l = tid - 32;
+    const int total = ntiles * CH;
+    auto issue = [&](int uu) {
+      if (uu < total) {
+        const int t = uu / CH, q = uu % CH;
+        const bool isV = t >= tiles_th;
+        const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+        const int rows = isV ? np : m;
+        const int r = (isV ? t - tiles_th : t) * 128 + row_l;
+        float2* dst = rawr + (size_t)(uu % WS_RAW) * 8 * 128 + row_l;
+        if (r < rows) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) tc::cp_async8(dst + c * 128, M + (int64_t)colof(8 * q + c, I, J) * rows + r);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) dst[c * 128] = make_float2(0.f, 0.f);
+        }
+      }
+      tc::cp_async_commit();
+    };
+    for (int uu = 0; uu < WS_RAW - 1; ++uu) issue(uu);
+    for (int u = 0; u < total; ++u) {
+      issue(u + WS_RAW - 1);
+      tc::cp_async_wait<WS_RAW - 1>();                  // this thread's copies of chunk u landed
+      const float2* src = rawr + (size_t)(u % WS_RAW) * 8 * 128 + row_l;
+      float2 z[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) z[c] = src[c * 128];
+      const int sl = u % WS_NS;
+      if (u >= WS_NS) tc::mbar_wait(&empty[sl], ((u / WS_NS) - 1) & 1);
+      uint8_t* hi = ring + (size_t)sl * 2 * kRotStage;
+      uint8_t* lo = hi + kRotStage;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 rh, rl, ih, il;
+        tc::split_tf32(z[4 * h + 0].x, rh.x, rl.x); tc::split_tf32(z[4 * h + 1].x, rh.y, rl.y);
+        tc::split_tf32(z[4 * h + 2].x, rh.z, rl.z); tc::split_tf32(z[4 * h + 3].x, rh.w, rl.w);
+        tc::split_tf32(z[4 * h + 0].y, ih.x, il.x); tc::split_tf32(z[4 * h + 1].y, ih.y, il.y);
+        tc::split_tf32(z[4 * h + 2].y, ih.z, il.z); tc::split_tf32(z[4 * h + 3].y, ih.w, il.w);
+        const uint32_t oR = tc::kmaj_off(row_l, 4 * h, R_LBO, R_SBO), oI = tc::kmaj_off(row_l, 8 + 4 * h, R_LBO, R_SBO);
+        *reinterpret_cast<float4*>(hi + oR) = rh;
+        *reinterpret_cast<float4*>(lo + oR) = rl;
+        *reinterpret_cast<float4*>(hi + oI) = ih;
+        *reinterpret_cast<float4*>(lo + oI) = il;
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&full[sl]);
+    }
+    tc::cp_async_wait<0>();
+  } else {
+    // ---------------- epilogue: thread = row, TMEM lane quadrant = warp % 4
+    const int row_l = (warp & 3) * 32 + (tid & 31);
+    for (int t = 0; t < ntiles; ++t) {
+      const bool isV = t >= tiles_th;
+      float2* M = reinterpret_cast<float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+      const int rows = isV ? np : m;
+      const int r = (isV ? t - tiles_th : t) * 128 + row_l;
+      const int ab = t & 1;
+      tc::mbar_wait(&tfull[ab], (t >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * ab;
+#pragma unroll 1
+      for (int c = 0; c < PWC; c += 8) {
+        float dr[8], di[8];
+        tc::tmem_ld8(ta + c, dr);
+        tc::tmem_ld8(ta + 64 + c, di);
+        if (r < rows) {
+          float2 v[8];
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2) v[u2] = M[(int64_t)colof(c + u2, I, J) * rows + r];
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2)
+            M[(int64_t)colof(c + u2, I, J) * rows + r] = make_float2(v[u2].x + dr[u2], v[u2].y + di[u2]);
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[ab]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 // ---- FP64-anchored polish of the spectrum (after convergence). With B = theta V (FP64-accumulated,
 // stored FP32 in the theta workspace) and C = B^H B, the Rayleigh values c_j = C_jj / |v_j|^2 are
 // exact eigenvalues of C only if the off-diagonal C_lj vanish; the FP32 accumulation of V leaves
@@ -1054,11 +1243,13 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
     cudaFuncSetAttribute(tcj::k_tc_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kInnerSmem);
     cudaFuncSetAttribute(tcj::k_tc_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotSmem);
+    cudaFuncSetAttribute(tcj::k_tc_rot_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotWsSmem);
     attr = true;
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   const dim3 grid(pairs_max, count);
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
+  static const bool rot_simple = getenv("EAMPS_ROT_SIMPLE") != nullptr;   // dev A/B switch
   static const float tol_floor = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
   static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 1e-2f;
   int sweep = 0;
@@ -1076,7 +1267,8 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
       tcj::k_tc_inner<<<grid, tcj::kInnerT, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps, tol_floor,
                                                          tol_internal);
       if (prof) cudaEventRecord(ev[2], s);
-      tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      if (rot_simple) tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
+      else tcj::k_tc_rot_ws<<<grid, 288, tcj::kRotWsSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
       if (prof) {
         cudaEventRecord(ev[3], s);
         cudaEventSynchronize(ev[3]);
