@@ -235,6 +235,15 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
 // ---- one wave of a layer: the front half (a0 staging, a1 contract, a2+a3 SVD) is issued by
 // wave_front; the back half (a4 select + ledger, a5 reabsorb, readback) by wave_back. Between the
 // two the caller may replace the ledger (mps_ledger_set): the multi-rank token chain of §8(e).
+// lane-group size of the small (reg 0) and medium (reg 2) Jacobi kernels: a power of two in
+// [4, 32], from the rows (small_group(m)) and the CTA width (2048 / n resp. 1024 / n lanes per pair)
+int lane_group(int m, int n, int reg) {
+  int cap = std::max(4, (reg == 0 ? 2048 : 1024) / std::max(n, 1));
+  int p2 = 4;
+  while (p2 * 2 <= cap && p2 < 32) p2 *= 2;
+  return std::min(small_group(m), p2);
+}
+
 mps_status wave_front(mps_t h) {
   LayerJob& J = h->job;
   std::vector<LayerPlan>& plan = J.plan;
@@ -342,8 +351,7 @@ mps_status wave_front(mps_t h) {
         if (gd.regime != reg) continue;
         // lane-group size: small regime as before; medium regime (theta 96-210 KB, V replayed) with
         // at most 512 threads so the rows-per-lane registers fit (one pair per group)
-        const int g_gt = reg == 0 ? std::min(small_group(gd.m), std::max(4, 2048 / gd.n))
-                                  : std::min(small_group(gd.m), std::max(4, 1024 / gd.n));
+        const int g_gt = lane_group(gd.m, gd.n, reg);
         if (g_gt != gt) continue;
         const int rm = rows_per_lane(gd.m, gt), rn = rows_per_lane(gd.n, gt);
         const int g_r = (rm == 0 || rn == 0) ? 0 : std::max(rm, rn);
@@ -369,6 +377,11 @@ mps_status wave_front(mps_t h) {
     }
   }
   if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
+  {   // every gate of the small / medium / QR regimes must sit in exactly one bucket
+    size_t want = 0;
+    for (int x = 0; x < Gw; ++x) want += hd[x].regime != 1;
+    if (want != small.size()) return set_err(h, MPS_E_STATE, "internal: SVD bucketing lost a gate");
+  }
   // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
   const size_t tail = align_up(staged_bytes, 64);  // 3 small pinned slots after the staged block
   uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));

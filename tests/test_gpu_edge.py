@@ -52,6 +52,7 @@ def _run_pair(shapes, f=0.9999, chi_cap=0):
 
 @pytest.mark.parametrize("shape,regime", [
     ((5, 9, 7), "small (ragged, m < n)"),
+    ((49, 35, 53), "small, m = 98 < n = 106 (2048 / n not a power of two; config 5 layer 7)"),
     ((48, 40, 37), "QR (n = 74, partially active warps)"),
     ((40, 64, 80), "medium (m = 80 < n = 160)"),
     ((70, 90, 100), "large tcgen05 (n = 200 -> n_pad 256)"),
