@@ -155,7 +155,17 @@ mps_status device_error(mps_t h) {
   if (e == 0) return MPS_OK;
   h->sticky = e;
   if (e == MPS_E_NOMEM) h->poisoned = true;  // the site table may be half-updated
-  return set_err(h, e, std::string("device: ") + status_name(e));
+  std::string detail;
+  if (e == MPS_E_NOMEM) {
+    const DevPool& P = h->hstate.pool;
+    char buf[256];
+    int worst = 0;
+    for (int c = 0; c < kMaxClasses; ++c) worst = std::max(worst, (int)P.count[c]);
+    snprintf(buf, sizeof buf, " (pool bump %llu, ceiling %llu, slab %zu, fullest free stack %d of %lld)",
+             (unsigned long long)P.bump, (unsigned long long)P.ceiling, h->slab_bytes, worst, (long long)P.stack_cap);
+    detail = buf;
+  }
+  return set_err(h, e, std::string("device: ") + status_name(e) + detail);
 }
 
 // ---- device pool helpers for host-side operations (not on the hot path) -------------------
@@ -563,7 +573,12 @@ mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* 
   const size_t bonds_off = align_up(sites_off + sizeof(SiteEntry) * n_sites);
   const int64_t pend_cap = 3 * (int64_t)n_sites + 64;
   const size_t pend_off = align_up(bonds_off + sizeof(BondEntry) * (n_sites + 1));
-  const int64_t stack_cap = 3 * (int64_t)n_sites + 64;  // >= live + pending blocks of any class
+  // Free-stack capacity per size class. A class's population only grows when an allocation finds
+  // its stack empty, i.e. when population = live + pending (<= (2N+1) + 1.5N, the frees are
+  // deferred one commit), plus that commit's allocations (<= 1.5N): population <= 5N + 2. (3N + 64
+  // overflowed on config 5 at layer 10: the deferred frees of the first layer double the
+  // population of the smallest class.)
+  const int64_t stack_cap = 6 * (int64_t)n_sites + 256;
   const size_t stack_off = align_up(pend_off + 16 * pend_cap);
   const size_t pool_base = align_up(stack_off + 8 * (size_t)kMaxClasses * stack_cap);
   const size_t init_end = pool_base + kAlign * (2 * (size_t)n_sites + 1);

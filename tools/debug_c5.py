@@ -13,7 +13,7 @@ for t, (sites, us) in enumerate(layers):
     try:
         m.mps_apply_layer(sites, us)
     except Exception as e:
-        print("layer", t, "FAILED", str(e)[:150], flush=True)
+        print("layer", t, "FAILED", str(e)[:300], flush=True)
         raise SystemExit(1)
     b = m.mps_bond_dims()
     print("layer", t, "gates", len(sites), "max chi", int(b.max()), "%.2fs" % (time.time() - t0), flush=True)
