@@ -121,10 +121,66 @@ __global__ void __launch_bounds__(1024) k_svd_small(GateDesc* desc, const int32_
 
   int sweep = 0;
   bool converged = (n < 2);
-  for (; sweep < max_sweeps && !converged; ++sweep) {
-    int any = 0;
-    for (int rnd = 0; rnd < n - 1; ++rnd) any |= __syncthreads_or(round_pairs<GT, R>(A, m, n, V, rnd, skip, tol));
-    converged = (any == 0);
+  const int half = n / 2, gid = tid / GT, lg = tid % GT;
+  if (R > 0 && n <= 256 && (int)(blockDim.x / GT) >= half) {
+    // fast path (as the QR kernel): one pair per lane group, rows of theta and V in registers,
+    // schedule from shared memory, cached column norms (exact at each sweep start), gamma-only dots
+    constexpr int RR = R > 0 ? R : 1;
+    uint16_t* sched = reinterpret_cast<uint16_t*>(part + blockDim.x);
+    float* cn = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sched + (n - 1) * half) + 15) & ~uintptr_t(15));
+    build_circle_schedule(sched, n);
+    const bool active = gid < half;
+    const int sh = gid & (32 / GT - 1);
+    const float tol2 = tol * tol;
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+      for (int j = warp; j < n; j += (int)(blockDim.x >> 5)) {
+        float a = 0.f;
+        for (int i = lane; i < m; i += 32) a = fmaf(A[j * m + i].x, A[j * m + i].x, fmaf(A[j * m + i].y, A[j * m + i].y, a));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) cn[j] = a;
+      }
+      __syncthreads();
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd) {
+        bool rot = false;
+        int p = 0, q = 1;
+        float gr = 0.f, gi = 0.f;
+        PairRegs<GT, RR> pr;
+        if (active) {
+          const uint32_t pq = sched[rnd * half + gid];
+          p = pq & 0xFF;
+          q = pq >> 8;
+          pr.load(A + p * m, A + q * m, m, lg, sh);
+          pr.cross(gr, gi);
+        }
+        group_sum2<GT>(gr, gi);   // (all lanes: a warp may hold active and idle groups)
+        if (active) {
+          const float al = cn[p], be = cn[q];
+          Rot Rt;
+          float tg;
+          if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
+            rot = true;
+            pr.rotate_store(A + p * m, A + q * m, m, lg, sh, Rt);
+            PairRegs<GT, RR> pv;
+            pv.load(V + p * n, V + q * n, n, lg, sh);
+            pv.rotate_store(V + p * n, V + q * n, n, lg, sh, Rt);
+            if (lg == 0) {
+              cn[p] = al - tg;
+              cn[q] = be + tg;
+            }
+          }
+        }
+        any |= __syncthreads_or(rot);
+      }
+      converged = (any == 0);
+    }
+  } else {
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd) any |= __syncthreads_or(round_pairs<GT, R>(A, m, n, V, rnd, skip, tol));
+      converged = (any == 0);
+    }
   }
   if (!converged && tid == 0) atomicCAS(&st->led.error, 0, -6 /* MPS_E_NOCONV */);
   for (int x = tid; x < m * n; x += blockDim.x) A[x] = gth[x];  // the original theta for the Rayleigh quotient
@@ -138,7 +194,8 @@ __global__ void __launch_bounds__(1024) k_svd_small(GateDesc* desc, const int32_
 size_t svd_small_smem(int m, int n) {
   int npow2 = 1;
   while (npow2 < n) npow2 <<= 1;
-  return (size_t)m * n * 8 + (size_t)n * n * 8 + (size_t)npow2 * 12 + 16 + 1024 * 8;
+  return (size_t)m * n * 8 + (size_t)n * n * 8 + (size_t)npow2 * 12 + 16 + 1024 * 8 +
+         (n <= 256 ? (size_t)(n - 1) * (n / 2) * 2 + 16 + (size_t)n * 4 : 0);
 }
 
 bool svd_small_fits(int m, int n) { return svd_small_smem(m, n) <= 210 * 1024; }
