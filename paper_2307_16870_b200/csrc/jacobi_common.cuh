@@ -60,10 +60,27 @@ __device__ __forceinline__ bool jacobi_rot_fast(float al, float be, float gr, fl
   return true;
 }
 
+// Packed FP32x2 arithmetic (Blackwell FFMA2 / FMUL2: one instruction for both halves of a complex
+// number), used by the rotation -- the most frequent operation of every Jacobi kernel.
+__device__ __forceinline__ uint64_t f2_pack(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 f2_unpack(uint64_t d) { return *reinterpret_cast<float2*>(&d); }
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(d);
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+  return f2_unpack(d);
+}
+
+// (x, y) <- (c x - s conj(e) y, s x + c conj(e) y):
+//   conj(e) y = (er, er) * (y.re, y.im) + (ei, -ei) * (y.im, y.re)
 __device__ __forceinline__ void apply_rot(float2& x, float2& y, const Rot& R) {
-  const float2 ey = make_float2(R.er * y.x + R.ei * y.y, R.er * y.y - R.ei * y.x);  // conj(e) y
-  const float2 nx = make_float2(R.c * x.x - R.s * ey.x, R.c * x.y - R.s * ey.y);
-  const float2 ny = make_float2(R.s * x.x + R.c * ey.x, R.s * x.y + R.c * ey.y);
+  const float2 ey = f2_fma(make_float2(R.ei, -R.ei), make_float2(y.y, y.x), f2_mul(make_float2(R.er, R.er), y));
+  const float2 nx = f2_fma(make_float2(-R.s, -R.s), ey, f2_mul(make_float2(R.c, R.c), x));
+  const float2 ny = f2_fma(make_float2(R.c, R.c), ey, f2_mul(make_float2(R.s, R.s), x));
   x = nx;
   y = ny;
 }
@@ -96,12 +113,16 @@ struct PairRegs {
     }
   }
   __device__ __forceinline__ void cross(float& gr, float& gi) const {   // gamma = a_p^H a_q only
+    // (a.re, a.re) (b.re, b.im) + (a.im, -a.im) (b.im, b.re), two packed accumulators
+    float2 acc1 = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int u = 0; u < R; ++u) {
       const float2 a = x[u], b = y[u];
-      gr = fmaf(a.x, b.x, fmaf(a.y, b.y, gr));
-      gi = fmaf(a.x, b.y, fmaf(-a.y, b.x, gi));
+      acc1 = f2_fma(make_float2(a.x, a.x), b, acc1);
+      acc2 = f2_fma(make_float2(a.y, -a.y), make_float2(b.y, b.x), acc2);
     }
+    gr += acc1.x + acc2.x;
+    gi += acc1.y + acc2.y;
   }
   __device__ __forceinline__ void dots(float& al, float& be, float& gr, float& gi) const {
 #pragma unroll

@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "eamps_internal.cuh"
+#include "jacobi_common.cuh"
 #include "sort_tails.cuh"
 #include "tc_common.cuh"
 
@@ -686,22 +687,14 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
         const int2 ra = pq[ia], cb = pq[ib];
         float2 X[2][2] = {{Gs[ra.x][cb.x], Gs[ra.x][cb.y]}, {Gs[ra.y][cb.x], Gs[ra.y][cb.y]}};
         if (Jb.y != 0.f) {   // columns: (x, y) -> (c x - s conj(e) y, s x + c conj(e) y)
+          const Rot rb{Jb.x, Jb.y, Jb.z, Jb.w};
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const float2 xx = X[r][0], yy = X[r][1];
-            const float2 ey = make_float2(Jb.z * yy.x + Jb.w * yy.y, Jb.z * yy.y - Jb.w * yy.x);
-            X[r][0] = make_float2(Jb.x * xx.x - Jb.y * ey.x, Jb.x * xx.y - Jb.y * ey.y);
-            X[r][1] = make_float2(Jb.y * xx.x + Jb.x * ey.x, Jb.y * xx.y + Jb.x * ey.y);
-          }
+          for (int r = 0; r < 2; ++r) apply_rot(X[r][0], X[r][1], rb);
         }
-        if (Ja.y != 0.f) {   // rows: (u, v) -> (c u - s e v, s u + c e v)
+        if (Ja.y != 0.f) {   // rows: (u, v) -> (c u - s e v, s u + c e v), i.e. the rotation with conj(e) -> e
+          const Rot ra{Ja.x, Ja.y, Ja.z, -Ja.w};
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const float2 uu = X[0][cc], vv = X[1][cc];
-            const float2 ev = make_float2(Ja.z * vv.x - Ja.w * vv.y, Ja.z * vv.y + Ja.w * vv.x);
-            X[0][cc] = make_float2(Ja.x * uu.x - Ja.y * ev.x, Ja.x * uu.y - Ja.y * ev.y);
-            X[1][cc] = make_float2(Ja.y * uu.x + Ja.x * ev.x, Ja.y * uu.y + Ja.x * ev.y);
-          }
+          for (int cc = 0; cc < 2; ++cc) apply_rot(X[0][cc], X[1][cc], ra);
         }
         Gs[ra.x][cb.x] = X[0][0]; Gs[ra.x][cb.y] = X[0][1];
         Gs[ra.y][cb.x] = X[1][0]; Gs[ra.y][cb.y] = X[1][1];
@@ -715,11 +708,12 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
         if (J.y != 0.f) {
           const int2 cq = pq[k];
 #pragma unroll 4
+          const Rot rw{J.x, J.y, J.z, J.w};
           for (int x = tid % (kInnerT / 32); x < 64; x += kInnerT / 32) {
-            const float2 xx = Ws[x][cq.x], yy = Ws[x][cq.y];
-            const float2 ey = make_float2(J.z * yy.x + J.w * yy.y, J.z * yy.y - J.w * yy.x);
-            Ws[x][cq.x] = make_float2(J.x * xx.x - J.y * ey.x, J.x * xx.y - J.y * ey.y);
-            Ws[x][cq.y] = make_float2(J.y * xx.x + J.x * ey.x, J.y * xx.y + J.x * ey.y);
+            float2 xx = Ws[x][cq.x], yy = Ws[x][cq.y];
+            apply_rot(xx, yy, rw);
+            Ws[x][cq.x] = xx;
+            Ws[x][cq.y] = yy;
           }
         }
       }
