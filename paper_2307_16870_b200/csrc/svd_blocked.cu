@@ -293,41 +293,59 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
   double num[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) num[j] = 0.0;
+  // theta (= lambda (x) Theta', FP32) and V tiles of the next 16-column chunk are fetched into
+  // registers while the current chunk's FP64 products run (one barrier pair per chunk)
+  auto fetch = [&](int r0, int k0, float2* ra, float2* rb) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;  // 1024 = 16 k x 64 rows
+      const int i = e & (RC - 1), kk = e >> 6;
+      const int row = r0 + i, k = k0 + kk;
+      float2 v = make_float2(0.f, 0.f);
+      if (row < m && k < n) {
+        const float2 tp = thp[(int64_t)k * m + row];
+        const float la = lam[row / dd];
+        v = make_float2(la * tp.x, la * tp.y);
+      }
+      ra[it] = v;
+    }
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int e = tid + it * 256;  // 512 = 32 j x 16 k
+      const int kk = e & 15, jj = e >> 4;
+      const int k = k0 + kk, j = j0 + jj;
+      rb[it] = (k < n && j < n) ? V[(int64_t)j * np + k] : make_float2(0.f, 0.f);
+    }
+  };
+  const int nk = (n + 15) / 16;
   for (int r0 = 0; r0 < m; r0 += RC) {
     double2 w[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) w[j] = make_double2(0.0, 0.0);
-    for (int k0 = 0; k0 < n; k0 += 16) {
+    float2 ra[4], rb[2];
+    fetch(r0, 0, ra, rb);
+    for (int kc = 0; kc < nk; ++kc) {
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
-        int e = tid + it * 256;  // 1024 = 16 k x 64 rows
-        int i = e & (RC - 1), kk = e >> 6;
-        int row = r0 + i, k = k0 + kk;
-        float2 v = make_float2(0.f, 0.f);
-        if (row < m && k < n) {
-          float2 tp = thp[(int64_t)k * m + row];
-          float la = lam[row / dd];
-          v = make_float2(la * tp.x, la * tp.y);
-        }
-        As[kk][i] = v;
+        const int e = tid + it * 256;
+        As[e >> 6][e & (RC - 1)] = ra[it];
       }
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
-        int e = tid + it * 256;  // 512 = 32 j x 16 k
-        int kk = e & 15, jj = e >> 4;
-        int k = k0 + kk, j = j0 + jj;
-        Bs[kk][jj] = (k < n && j < n) ? V[(int64_t)j * np + k] : make_float2(0.f, 0.f);
+        const int e = tid + it * 256;
+        Bs[e & 15][e >> 4] = rb[it];
       }
       __syncthreads();
+      if (kc + 1 < nk) fetch(r0, (kc + 1) * 16, ra, rb);
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         float2 a = As[kk][oi];
         double ax = a.x, ay = a.y;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float2 b = Bs[kk][oj + j];
-          w[j].x = fma(ax, (double)b.x, fma(-ay, (double)b.y, w[j].x));
-          w[j].y = fma(ax, (double)b.y, fma(ay, (double)b.x, w[j].y));
+          float2 bq = Bs[kk][oj + j];
+          w[j].x = fma(ax, (double)bq.x, fma(-ay, (double)bq.y, w[j].x));
+          w[j].y = fma(ax, (double)bq.y, fma(ay, (double)bq.x, w[j].y));
         }
       }
       __syncthreads();
