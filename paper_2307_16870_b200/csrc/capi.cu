@@ -335,20 +335,24 @@ mps_status wave_front(mps_t h) {
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
   }
-  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits
+  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not
   for (int gt : {4, 8, 16, 32}) {
-    for (int rpl : {1, 2, 4, 8, 16}) {
-      Bucket b{3, gt, (int)small.size(), 0, 512, 0, rpl, 0, 0};
+   for (int rpl : {1, 2, 4, 8, 16}) {
+    for (int pk : {0, 1}) {
+      Bucket b{3, gt, (int)small.size(), 0, 512, pk, rpl, 0, 0};   // (tile_rows carries the packed flag)
       for (int x = 0; x < Gw; ++x) {
         const GateDesc& gd = hd[x];
         int g_gt = 0, g_r = 0;
         if (gd.regime != 3 || !svd_qr_fits(gd.m, gd.n, &g_gt, &g_r) || g_gt != gt || g_r != rpl) continue;
+        const int g_pk = (gd.n == g_r * g_gt && gd.m % 2 == 0 && g_r >= 2) ? 1 : 0;
+        if (g_pk != pk) continue;
         small.push_back(x);
         b.smem = std::max(b.smem, svd_qr_smem(gd.m, gd.n));
       }
       b.end = (int)small.size();
       if (b.end != b.begin) buckets.push_back(b);
     }
+   }
   }
   // buckets: (regime, lane-group size GT, rows per lane R); R > 0 keeps a pair's rows in registers
   for (int reg : {0, 2}) {
@@ -439,8 +443,8 @@ mps_status wave_front(mps_t h) {
   // a2 + a3 SVD, small regime: one CTA per theta
   for (const Bucket& b : buckets) {
     if (b.regime == 3) {
-      launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, h->slab,
-                    h->dst, h->s);
+      launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.tile_rows,
+                    h->slab, h->dst, h->s);
       int maxn = 0;
       for (int i = b.begin; i < b.end; ++i) maxn = std::max(maxn, hd[small[i]].n);
       h->launches += 1 + launch_spectrum_polish(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->dst, h->s);

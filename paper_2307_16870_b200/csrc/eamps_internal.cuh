@@ -102,8 +102,9 @@ inline int rows_per_lane(int rows, int gt) {
 }
 size_t svd_qr_smem(int m, int n);
 bool svd_qr_fits(int m, int n, int* gt_out, int* rpl_out);
+// packed = 1: n == rpl * gt and m even (16-byte row pairs); buckets must not mix packed and unpacked
 void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
-                   uint8_t* slab, DevState* st, cudaStream_t s);
+                   int packed, uint8_t* slab, DevState* st, cudaStream_t s);
 size_t svd_small_smem(int m, int n);
 bool svd_small_fits(int m, int n);
 int small_group(int m);

@@ -167,6 +167,49 @@ __device__ __forceinline__ void group_sum2(float& a, float& b) {
   }
 }
 
+// As PairRegs, but each register slot holds two consecutive rows loaded/stored as one 16-byte
+// access: lane lg owns rows 2 (lg + GT v) and 2 (lg + GT v) + 1, v < R/2 (the caller guarantees
+// rows == R GT, rows even). Half the shared-memory instructions of PairRegs; a warp's groups read
+// 128 contiguous bytes each (the minimum number of wavefronts).
+template <int GT, int R>
+struct PairRegs2 {
+  float2 x[R], y[R];
+  __device__ __forceinline__ void load_full(const float2* ap, const float2* aq, int lg) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      const int i = 2 * (lg + GT * v);
+      const float4 a = *reinterpret_cast<const float4*>(ap + i);
+      const float4 b = *reinterpret_cast<const float4*>(aq + i);
+      x[2 * v] = make_float2(a.x, a.y);
+      x[2 * v + 1] = make_float2(a.z, a.w);
+      y[2 * v] = make_float2(b.x, b.y);
+      y[2 * v + 1] = make_float2(b.z, b.w);
+    }
+  }
+  __device__ __forceinline__ void cross(float& gr, float& gi) const {
+    float2 acc1 = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const float2 a = x[u], b = y[u];
+      acc1 = f2_fma(make_float2(a.x, a.x), b, acc1);
+      acc2 = f2_fma(make_float2(a.y, -a.y), make_float2(b.y, b.x), acc2);
+    }
+    gr += acc1.x + acc2.x;
+    gi += acc1.y + acc2.y;
+  }
+  __device__ __forceinline__ void rotate_store_full(float2* ap, float2* aq, int lg, const Rot& Rt) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      const int i = 2 * (lg + GT * v);
+      float2 a0 = x[2 * v], b0 = y[2 * v], a1 = x[2 * v + 1], b1 = y[2 * v + 1];
+      apply_rot(a0, b0, Rt);
+      apply_rot(a1, b1, Rt);
+      *reinterpret_cast<float4*>(ap + i) = make_float4(a0.x, a0.y, a1.x, a1.y);
+      *reinterpret_cast<float4*>(aq + i) = make_float4(b0.x, b0.y, b1.x, b1.y);
+    }
+  }
+};
+
 // GT-lane xor-butterfly sum of the four pair statistics (bit-identical in every lane of the group)
 template <int GT>
 __device__ __forceinline__ void group_sum4(float& al, float& be, float& gr, float& gi) {

@@ -12,6 +12,8 @@
 // The preconditioner cuts the sweeps (config 2 chi = 64: 12 -> 9, numpy check of the same
 // tournament) and removes the V half of every round. PAPER.md:65 (M = U Lambda V^dagger, V^dagger
 // right-normalised) and :114 ("performing its SVD"); SURVEY §8(a) a2.
+#include <type_traits>
+
 #include "jacobi_common.cuh"
 
 namespace eamps {
@@ -21,7 +23,7 @@ namespace {
 constexpr int QR_T = 512;          // threads per CTA
 constexpr int QR_TILE = 32;        // Rayleigh row tile
 
-template <int GT, int R>
+template <int GT, int R, int PK>
 __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                  DevState* st, int max_sweeps) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -177,13 +179,18 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
       // (a warp may hold active and idle groups: the shuffles run unconditionally)
       int p = 0, q = 1;
       float gr = 0.f, gi = 0.f;
-      PairRegs<GT, R> pr;
+      // PK: the columns fill the groups exactly (n = R GT, m even): 16-byte row pairs (PairRegs2)
+      typename std::conditional<PK != 0, PairRegs2<GT, (R >= 2 ? R : 2)>, PairRegs<GT, R>>::type pr;
       if (active) {
         const uint32_t pq = sched[rnd * half + gid];
         p = pq & 0xFF;
         q = pq >> 8;
-        if (full) pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi, sh);
-        else pr.load(A + (size_t)p * m, A + (size_t)q * m, n, lgi, sh);
+        if constexpr (PK != 0) {
+          pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi);
+        } else {
+          if (full) pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi, sh);
+          else pr.load(A + (size_t)p * m, A + (size_t)q * m, n, lgi, sh);
+        }
         pr.cross(gr, gi);
       }
       group_sum2<GT>(gr, gi);
@@ -195,8 +202,12 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
         float tg;
         if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
           rot = true;
-          if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
-          else pr.rotate_store(ap, aq, n, lgi, sh, Rt);
+          if constexpr (PK != 0) {
+            pr.rotate_store_full(ap, aq, lgi, Rt);
+          } else {
+            if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
+            else pr.rotate_store(ap, aq, n, lgi, sh, Rt);
+          }
           if (lgi == 0) {
             cn[p] = al - tg;
             cn[q] = be + tg;
@@ -232,15 +243,15 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
   (void)part;
 }
 
-template <int GT, int R>
+template <int GT, int R, int PK>
 void launch_qr_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, uint8_t* slab,
                  DevState* st, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_svd_qr<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_svd_qr<GT, R, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
-  k_svd_qr<GT, R><<<count, QR_T, smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
+  k_svd_qr<GT, R, PK><<<count, QR_T, smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
 }
 
 }  // namespace
@@ -271,10 +282,13 @@ bool svd_qr_fits(int m, int n, int* gt_out, int* rpl_out) {
 }
 
 void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
-                   uint8_t* slab, DevState* st, cudaStream_t s) {
+                   int packed, uint8_t* slab, DevState* st, cudaStream_t s) {
   if (count <= 0) return;
-#define EAMPS_QR(G, RR) \
-  if (gt == G && rpl == RR) return launch_qr_t<G, RR>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
+#define EAMPS_QR(G, RR)                                                                              \
+  if (gt == G && rpl == RR) {                                                                        \
+    if (RR >= 2 && packed) return launch_qr_t<G, RR, 1>(d_desc, d_list, count, smem, max_sweeps, slab, st, s); \
+    return launch_qr_t<G, RR, 0>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);              \
+  }
   EAMPS_QR(4, 16) EAMPS_QR(4, 8) EAMPS_QR(4, 4) EAMPS_QR(4, 2) EAMPS_QR(4, 1)
   EAMPS_QR(8, 16) EAMPS_QR(8, 8) EAMPS_QR(8, 4) EAMPS_QR(8, 2) EAMPS_QR(8, 1)
   EAMPS_QR(16, 16) EAMPS_QR(16, 8) EAMPS_QR(16, 4) EAMPS_QR(16, 2) EAMPS_QR(16, 1)
