@@ -121,6 +121,12 @@ mps_status mps_layer_step(mps_t, int32_t* remaining);
 mps_status mps_ledger_get(mps_t, double* log_E, int64_t* j, int32_t* guarantee);
 mps_status mps_ledger_set(mps_t, double log_E, int64_t j, int32_t guarantee);
 
+/* Planning introspection (host only; no handle, no device work): the SVD regime the layer planner
+ * picks for an m x n theta (3 QR-preconditioned, 0 small, 2 medium, 1 tcgen05 large), the lane-group
+ * size and rows per lane of its bucket (0 for the large regime / the generic path) and the padded
+ * column count. MPS_E_INVAL for m, n < 1 or NULL outputs. */
+mps_status mps_plan_regime(int32_t m, int32_t n, int32_t* regime, int32_t* gt, int32_t* rpl, int32_t* n_pad);
+
 /* Running estimate (E12/E13): est = exp(log_est); n_done = truncations so far; guarantee_held =
  * no cap fired; is_lower_bound = 1 for the MPO (noisy) regime (E13). Any pointer may be NULL. */
 mps_status mps_fidelity_estimate(mps_t, double* est, double* log_est, int64_t* n_done,

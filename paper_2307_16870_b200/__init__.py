@@ -27,7 +27,7 @@ ABI_FUNCTIONS = [
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
-    "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set",
+    "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
 ]
 
 
@@ -93,6 +93,7 @@ def lib():
             "mps_layer_step": [_P, _P],
             "mps_ledger_get": [_P, _P, _P, _P],
             "mps_ledger_set": [_P, dbl, i64, i32],
+            "mps_plan_regime": [i32, i32, _P, _P, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -100,6 +101,15 @@ def lib():
             f.restype = C.c_char_p if name in ("mps_last_error", "mps_status_string") else C.c_int32
         _lib = L
     return _lib
+
+
+def mps_plan_regime(m: int, n: int):
+    """(regime, lane group, rows per lane, n_pad) the layer planner picks for an m x n theta (host only)."""
+    out = [C.c_int32(0) for _ in range(4)]
+    rc = lib().mps_plan_regime(int(m), int(n), *[C.byref(o) for o in out])
+    if rc != 0:
+        raise EampsError(rc, lib().mps_status_string(rc).decode())
+    return tuple(o.value for o in out)
 
 
 def _ptr(a):

@@ -860,6 +860,28 @@ mps_status mps_fidelity_estimate(mps_t h, double* est, double* log_est, int64_t*
 
 // The ledger token of the multi-rank chain (§8(e)): (log E, j, guarantee). get synchronises;
 // set is stream-ordered (it lands before the next wave's select).
+// Planning introspection (host only, no device work): the SVD regime of an m x n theta and the
+// lane-group size / rows per lane its bucket launches with -- the invariants the CPU tests check.
+mps_status mps_plan_regime(int32_t m, int32_t n, int32_t* regime, int32_t* gt, int32_t* rpl, int32_t* n_pad) {
+  if (m < 1 || n < 1 || !regime || !gt || !rpl || !n_pad) return MPS_E_INVAL;
+  int qgt = 0, qr = 0;
+  if (svd_qr_fits(m, n, &qgt, &qr)) {
+    *regime = 3; *gt = qgt; *rpl = qr; *n_pad = n;
+    return MPS_OK;
+  }
+  const int reg = svd_small_fits(m, n) ? 0 : (svd_medium_fits(m, n) ? 2 : 1);
+  *regime = reg;
+  if (reg == 1) {
+    *gt = 0; *rpl = 0; *n_pad = (int)align_up((size_t)n, 64);
+    return MPS_OK;
+  }
+  *gt = lane_group(m, n, reg);
+  const int rm = rows_per_lane(m, *gt), rn = rows_per_lane(n, *gt);
+  *rpl = (rm == 0 || rn == 0) ? 0 : std::max(rm, rn);
+  *n_pad = n;
+  return MPS_OK;
+}
+
 mps_status mps_ledger_get(mps_t h, double* log_E, int64_t* j, int32_t* guarantee) {
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);

@@ -54,7 +54,8 @@ def _run_pair(shapes, f=0.9999, chi_cap=0):
     ((5, 9, 7), "small (ragged, m < n)"),
     ((49, 35, 53), "small, m = 98 < n = 106 (2048 / n not a power of two; config 5 layer 7)"),
     ((48, 40, 37), "QR (n = 74, partially active warps)"),
-    ((40, 64, 80), "medium (m = 80 < n = 160)"),
+    ((32, 40, 72), "medium (m = 64 < n = 144)"),
+    ((40, 64, 80), "large tcgen05, m = 80 < n = 160"),
     ((70, 90, 100), "large tcgen05 (n = 200 -> n_pad 256)"),
     ((64, 100, 150), "large, m = 128 < n = 300"),
     ((200, 120, 70), "large, m = 400 >> n = 140"),
