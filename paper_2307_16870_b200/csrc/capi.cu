@@ -335,16 +335,17 @@ mps_status wave_front(mps_t h) {
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
   }
-  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not
+  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not, or
+  // the block-recursive ordering (n = 64, 128; its own lane groups, see svd_qr.cu)
   for (int gt : {4, 8, 16, 32}) {
    for (int rpl : {1, 2, 4, 8, 16}) {
-    for (int pk : {0, 1}) {
+    for (int pk : {0, 1, 2}) {
       Bucket b{3, gt, (int)small.size(), 0, 512, pk, rpl, 0, 0};   // (tile_rows carries the packed flag)
       for (int x = 0; x < Gw; ++x) {
         const GateDesc& gd = hd[x];
         int g_gt = 0, g_r = 0;
         if (gd.regime != 3 || !svd_qr_fits(gd.m, gd.n, &g_gt, &g_r) || g_gt != gt || g_r != rpl) continue;
-        const int g_pk = (gd.n == g_r * g_gt && gd.m % 2 == 0 && g_r >= 2) ? 1 : 0;
+        const int g_pk = qr_block_order(gd.m, gd.n) ? 2 : (gd.n == g_r * g_gt && gd.m % 2 == 0 && g_r >= 2) ? 1 : 0;
         if (g_pk != pk) continue;
         small.push_back(x);
         b.smem = std::max(b.smem, svd_qr_smem(gd.m, gd.n));

@@ -102,6 +102,7 @@ inline int rows_per_lane(int rows, int gt) {
 }
 size_t svd_qr_smem(int m, int n);
 bool svd_qr_fits(int m, int n, int* gt_out, int* rpl_out);
+bool qr_block_order(int m, int n);
 // packed = 1: n == rpl * gt and m even (16-byte row pairs); buckets must not mix packed and unpacked
 void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
                    int packed, uint8_t* slab, DevState* st, cudaStream_t s);

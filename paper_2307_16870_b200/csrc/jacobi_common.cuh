@@ -38,7 +38,7 @@ __device__ __forceinline__ bool jacobi_rot(float al, float be, float gr, float g
   return true;
 }
 
-// The same rotation with fast reciprocals (rsqrt / rcp): e = gamma rsqrt(|gamma|^2), the
+// The same rotation with fast reciprocals (rsqrt / rcp.approx; sqrt(q) = q rsqrt(q)): e = gamma rsqrt(|gamma|^2), the
 // criterion compared in squares; returns t |gamma| for the cached-norm update
 // alpha' = alpha - t|gamma|, beta' = beta + t|gamma| (SURVEY §8(c) algorithm item 3, checked there
 // in numpy). |e| and c^2 + s^2 are 1 to a few ulp.
@@ -53,7 +53,10 @@ __device__ __forceinline__ bool jacobi_rot_fast(float al, float be, float gr, fl
   R.ei = gi * ig;
   const float zeta = 0.5f * (be - al) * ig;
   const float az = fabsf(zeta);
-  const float t = copysignf(__frcp_rn(az + sqrtf(fmaf(az, az, 1.f))), zeta);
+  const float q = fmaf(az, az, 1.f);             // az <= sqrt(alpha / skip) / tol: no overflow
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(az + q * rsqrtf(q)));
+  t = copysignf(t, zeta);
   R.c = rsqrtf(fmaf(t, t, 1.f));
   R.s = R.c * t;
   tg = t * (g2 * ig);

@@ -12,6 +12,7 @@
 // The preconditioner cuts the sweeps (config 2 chi = 64: 12 -> 9, numpy check of the same
 // tournament) and removes the V half of every round. PAPER.md:65 (M = U Lambda V^dagger, V^dagger
 // right-normalised) and :114 ("performing its SVD"); SURVEY §8(a) a2.
+#include <cstdlib>
 #include <type_traits>
 
 #include "jacobi_common.cuh"
@@ -22,6 +23,170 @@ namespace {
 
 constexpr int QR_T = 512;          // threads per CTA
 constexpr int QR_TILE = 32;        // Rayleigh row tile
+
+// One column of B in a lane group's registers, PAIR-PLANAR: shared memory holds each column as
+// float4 (Re b_2i, Re b_2i+1, Im b_2i, Im b_2i+1) (pair_planar below), lane lg owns row pairs
+// i = lg + GT v, v < R / 2, and keeps re[v] = (Re b_2i, Re b_2i+1), im[v] = (Im b_2i, Im b_2i+1):
+// every complex operation below is a packed FP32x2 instruction on two rows with broadcast scalar
+// coefficients -- no (re, im) swaps or negations to build operand pairs (15% of the instructions
+// with the interleaved layout, ncu).
+template <int GT, int R>
+struct ColRegs {
+  float2 re[R / 2], im[R / 2];
+  __device__ __forceinline__ void load(const float2* a, int lg) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      const float4 t = *reinterpret_cast<const float4*>(a + 2 * (lg + GT * v));
+      re[v] = make_float2(t.x, t.y);
+      im[v] = make_float2(t.z, t.w);
+    }
+  }
+  __device__ __forceinline__ void store(float2* a, int lg) const {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v)
+      *reinterpret_cast<float4*>(a + 2 * (lg + GT * v)) = make_float4(re[v].x, re[v].y, im[v].x, im[v].y);
+  }
+};
+
+// in-place layout change of B's n columns (ld m) between interleaved float2 rows and pair-planar
+// float4 (Re 2i, Re 2i+1, Im 2i, Im 2i+1); the permutation is its own inverse
+__device__ __forceinline__ void pair_planar(float2* A, int m, int n) {
+  for (int x = threadIdx.x; x < n * (n / 2); x += blockDim.x) {
+    float4* q = reinterpret_cast<float4*>(A + (size_t)(x / (n / 2)) * m) + x % (n / 2);
+    const float4 t = *q;
+    *q = make_float4(t.x, t.z, t.y, t.w);
+  }
+}
+
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+
+// gamma = b_p^H b_q over the group (bit-identical in every lane), then the rotation of the pair in
+// registers and the cached-norm update alpha' = alpha - t|gamma|, beta' = beta + t|gamma|.
+// With P + iQ = s e, U + iW = c e (e = gamma / |gamma|):
+//   x' = c x - s conj(e) y:  Re x' = c Re x - P Re y - Q Im y,  Im x' = c Im x - P Im y + Q Re y
+//   y' = s x + c conj(e) y:  Re y' = s Re x + U Re y + W Im y,  Im y' = s Im x + U Im y - W Re y
+template <int GT, int R>
+__device__ __forceinline__ void pair_step(ColRegs<GT, R>& X, ColRegs<GT, R>& Y, float& al, float& be, float skip,
+                                          float tol2, int& rot) {
+  float2 a1 = make_float2(0.f, 0.f), a2 = a1, a3 = a1, a4 = a1;
+#pragma unroll
+  for (int v = 0; v < R / 2; ++v) {
+    a1 = f2_fma(X.re[v], Y.re[v], a1);     // Re conj(x) y = xr yr + xi yi
+    a2 = f2_fma(X.im[v], Y.im[v], a2);
+    a3 = f2_fma(X.re[v], Y.im[v], a3);     // Im conj(x) y = xr yi - xi yr
+    a4 = f2_fma(X.im[v], Y.re[v], a4);
+  }
+  float gr = (a1.x + a1.y) + (a2.x + a2.y), gi = (a3.x + a3.y) - (a4.x + a4.y);
+  group_sum2<GT>(gr, gi);
+  Rot Rt;
+  float tg;
+  if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
+    rot = 1;
+    const float P = Rt.s * Rt.er, Q = Rt.s * Rt.ei, U = Rt.c * Rt.er, W = Rt.c * Rt.ei;
+    const float2 c2 = f2s(Rt.c), s2 = f2s(Rt.s), mP = f2s(-P), mQ = f2s(-Q), pQ = f2s(Q), U2 = f2s(U), W2 = f2s(W),
+                 mW = f2s(-W);
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      const float2 xr = X.re[v], xi = X.im[v], yr = Y.re[v], yi = Y.im[v];
+      X.re[v] = f2_fma(mQ, yi, f2_fma(mP, yr, f2_mul(c2, xr)));
+      X.im[v] = f2_fma(pQ, yr, f2_fma(mP, yi, f2_mul(c2, xi)));
+      Y.re[v] = f2_fma(W2, yi, f2_fma(U2, yr, f2_mul(s2, xr)));
+      Y.im[v] = f2_fma(mW, yr, f2_fma(U2, yi, f2_mul(s2, xi)));
+    }
+    al -= tg;
+    be += tg;
+  }
+}
+
+// One-sided Jacobi sweeps over the n = R GT columns of B (ld m, m even) in the block-recursive
+// resident/visitor ordering. Level s (s = n, n/2, ..., 4): the columns split into sets of s
+// consecutive columns; in each set the first s/2 are residents, held two per lane group
+// (s/4 groups per set), the last s/2 visitors. Round k (k < s/2): group li of the set meets
+// visitor (2 li + k) mod (s/2) with both its residents in turn. Then every set splits in halves
+// (residents, visitors) for the next level; the last level rotates the pairs (4g, 4g+1) (still
+// in registers after level 4) and (4g+2, 4g+3). Every pair is rotated exactly once per sweep, n - 1 rounds of n/2 rotations, as in
+// the circle method (a numpy model of both orderings on config 2 thetas: 9 sweeps each). Visitor
+// parity alternates between rounds, so round k+1's visitor is idle in round k and is prefetched.
+template <int GT, int R>
+__device__ __forceinline__ void jacobi_block_recursive(float2* A, int m, int n, float* cn, float skip, float tol2,
+                                                       int max_sweeps, int& sweep, bool& converged) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int gid = tid / GT, lg = tid % GT;
+  const bool active = gid < n / 4;                  // whole warps (n/4 * GT is a multiple of 32)
+  for (; sweep < max_sweeps && !converged; ++sweep) {
+    for (int j = warp; j < n; j += nw) {
+      float a = 0.f;
+      for (int i = lane; i < n; i += 32) {
+        const float2 v = A[(size_t)j * m + i];
+        a = fmaf(v.x, v.x, fmaf(v.y, v.y, a));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) cn[j] = a;
+    }
+    __syncthreads();
+    int rot = 0;
+    for (int s = n; s >= 4; s >>= 1) {
+      const int gps = s / 4, h = s / 2;
+      const int li = gid % gps, base = (gid / gps) * s;
+      ColRegs<GT, R> X1, X2, Y, Yn;
+      float a1 = 0.f, a2 = 0.f, bY = 0.f, bn = 0.f;
+      int v = base + h + 2 * li;                      // round 0 visitor (2 li < h)
+      if (active) {
+        X1.load(A + (size_t)(base + 2 * li) * m, lg);
+        X2.load(A + (size_t)(base + 2 * li + 1) * m, lg);
+        a1 = cn[base + 2 * li];
+        a2 = cn[base + 2 * li + 1];
+        Y.load(A + (size_t)v * m, lg);
+        bY = cn[v];
+      }
+      // round k: rotate with Yc (visitor v), prefetch round k+1's visitor into Yp (ping-pong, h even)
+      auto visit = [&](ColRegs<GT, R>& Yc, ColRegs<GT, R>& Yp, int k) {
+        int vi = 2 * li + k + 1;                      // < 2h: (2 li + k + 1) mod h without a division
+        if (vi >= h) vi -= h;
+        const int vn = base + h + vi;
+        if (active) {
+          if (k + 1 < h) {
+            Yp.load(A + (size_t)vn * m, lg);
+            bn = cn[vn];
+          }
+          pair_step(X1, Yc, a1, bY, skip, tol2, rot);
+          pair_step(X2, Yc, a2, bY, skip, tol2, rot);
+          Yc.store(A + (size_t)v * m, lg);
+          if (lg == 0) cn[v] = bY;
+        }
+        __syncthreads();
+        bY = bn;
+        v = vn;
+      };
+      for (int k = 0; k < h; k += 2) {
+        visit(Y, Yn, k);
+        visit(Yn, Y, k + 1);
+      }
+      if (active) {
+        if (s == 4) pair_step(X1, X2, a1, a2, skip, tol2, rot);   // last level, first pair (4g, 4g+1)
+        X1.store(A + (size_t)(base + 2 * li) * m, lg);
+        X2.store(A + (size_t)(base + 2 * li + 1) * m, lg);
+        if (lg == 0) {
+          cn[base + 2 * li] = a1;
+          cn[base + 2 * li + 1] = a2;
+        }
+      }
+      __syncthreads();
+    }
+    if (active) {                                   // last level, second pair (4g+2, 4g+3)
+      ColRegs<GT, R> Y, Z;
+      const int c = 4 * gid + 2;
+      Y.load(A + (size_t)c * m, lg);
+      Z.load(A + (size_t)(c + 1) * m, lg);
+      float a3 = cn[c], a4 = cn[c + 1];
+      pair_step(Y, Z, a3, a4, skip, tol2, rot);
+      Y.store(A + (size_t)c * m, lg);
+      Z.store(A + (size_t)(c + 1) * m, lg);
+    }
+    converged = (__syncthreads_or(rot) == 0);
+  }
+}
 
 template <int GT, int R, int PK>
 __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
@@ -161,62 +326,74 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
   const bool full = (n == R * GT);
   int sweep = 0;
   bool converged = (n < 2);
-  for (; sweep < max_sweeps && !converged; ++sweep) {
-    for (int j = warp; j < n; j += nw) {
-      float a = 0.f;
-      for (int i = lane; i < n; i += 32) {
-        const float2 v = A[(size_t)j * m + i];
-        a = fmaf(v.x, v.x, fmaf(v.y, v.y, a));
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (lane == 0) cn[j] = a;
-    }
+  if constexpr (PK == 2) {
+    // ---- block-recursive resident/visitor ordering (n = 4 * groups, a power of two): see
+    // jacobi_block_recursive below. Two resident columns per lane group stay in registers while
+    // the visitors stream through shared memory: one column load + one store per two rotations.
+    (void)sched;
+    pair_planar(A, m, n);
     __syncthreads();
-    int any = 0;
-    for (int rnd = 0; rnd < n - 1; ++rnd) {
-      bool rot = false;
-      // (a warp may hold active and idle groups: the shuffles run unconditionally)
-      int p = 0, q = 1;
-      float gr = 0.f, gi = 0.f;
-      // PK: the columns fill the groups exactly (n = R GT, m even): 16-byte row pairs (PairRegs2)
-      typename std::conditional<PK != 0, PairRegs2<GT, (R >= 2 ? R : 2)>, PairRegs<GT, R>>::type pr;
-      if (active) {
-        const uint32_t pq = sched[rnd * half + gid];
-        p = pq & 0xFF;
-        q = pq >> 8;
-        if constexpr (PK != 0) {
-          pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi);
-        } else {
-          if (full) pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi, sh);
-          else pr.load(A + (size_t)p * m, A + (size_t)q * m, n, lgi, sh);
+    jacobi_block_recursive<GT, R>(A, m, n, cn, skip, tol2, max_sweeps, sweep, converged);
+    pair_planar(A, m, n);
+    __syncthreads();
+  } else {
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+      for (int j = warp; j < n; j += nw) {
+        float a = 0.f;
+        for (int i = lane; i < n; i += 32) {
+          const float2 v = A[(size_t)j * m + i];
+          a = fmaf(v.x, v.x, fmaf(v.y, v.y, a));
         }
-        pr.cross(gr, gi);
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) cn[j] = a;
       }
-      group_sum2<GT>(gr, gi);
-      if (active) {
-        float2* ap = A + (size_t)p * m;
-        float2* aq = A + (size_t)q * m;
-        const float al = cn[p], be = cn[q];
-        Rot Rt;
-        float tg;
-        if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
-          rot = true;
+      __syncthreads();
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd) {
+        bool rot = false;
+        // (a warp may hold active and idle groups: the shuffles run unconditionally)
+        int p = 0, q = 1;
+        float gr = 0.f, gi = 0.f;
+        // PK: the columns fill the groups exactly (n = R GT, m even): 16-byte row pairs (PairRegs2)
+        typename std::conditional<PK != 0, PairRegs2<GT, (R >= 2 ? R : 2)>, PairRegs<GT, R>>::type pr;
+        if (active) {
+          const uint32_t pq = sched[rnd * half + gid];
+          p = pq & 0xFF;
+          q = pq >> 8;
           if constexpr (PK != 0) {
-            pr.rotate_store_full(ap, aq, lgi, Rt);
+            pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi);
           } else {
-            if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
-            else pr.rotate_store(ap, aq, n, lgi, sh, Rt);
+            if (full) pr.load_full(A + (size_t)p * m, A + (size_t)q * m, lgi, sh);
+            else pr.load(A + (size_t)p * m, A + (size_t)q * m, n, lgi, sh);
           }
-          if (lgi == 0) {
-            cn[p] = al - tg;
-            cn[q] = be + tg;
+          pr.cross(gr, gi);
+        }
+        group_sum2<GT>(gr, gi);
+        if (active) {
+          float2* ap = A + (size_t)p * m;
+          float2* aq = A + (size_t)q * m;
+          const float al = cn[p], be = cn[q];
+          Rot Rt;
+          float tg;
+          if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
+            rot = true;
+            if constexpr (PK != 0) {
+              pr.rotate_store_full(ap, aq, lgi, Rt);
+            } else {
+              if (full) pr.rotate_store_full(ap, aq, lgi, sh, Rt);
+              else pr.rotate_store(ap, aq, n, lgi, sh, Rt);
+            }
+            if (lgi == 0) {
+              cn[p] = al - tg;
+              cn[q] = be + tg;
+            }
           }
         }
+        any |= __syncthreads_or(rot);
       }
-      any |= __syncthreads_or(rot);
+      converged = (any == 0);
     }
-    converged = (any == 0);
   }
   if (!converged && tid == 0) atomicCAS(&st->led.error, 0, -6 /* MPS_E_NOCONV */);
   if (tid == 0) gd.sweeps = sweep;
@@ -281,9 +458,22 @@ bool svd_qr_fits(int m, int n, int* gt_out, int* rpl_out) {
   return true;
 }
 
+// The block-recursive resident/visitor ordering (jacobi_block_recursive) applies to n = 64 and
+// 128 with m even; EAMPS_QR_CIRCLE=1 keeps the circle method for A/B comparisons.
+bool qr_block_order(int m, int n) {
+  static const bool circle = getenv("EAMPS_QR_CIRCLE") != nullptr;
+  return !circle && (n == 64 || n == 128) && m % 2 == 0;
+}
+
 void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int gt, int rpl,
                    int packed, uint8_t* slab, DevState* st, cudaStream_t s) {
   if (count <= 0) return;
+  if (packed == 2) {                                 // block-recursive ordering (qr_block_order)
+    const int n = gt * rpl;
+    if (n == 128) return launch_qr_t<16, 8, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
+    if (n == 64) return launch_qr_t<16, 4, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
+    return;
+  }
 #define EAMPS_QR(G, RR)                                                                              \
   if (gt == G && rpl == RR) {                                                                        \
     if (RR >= 2 && packed) return launch_qr_t<G, RR, 1>(d_desc, d_list, count, smem, max_sweeps, slab, st, s); \
