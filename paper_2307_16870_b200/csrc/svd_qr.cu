@@ -21,7 +21,10 @@ namespace eamps {
 
 namespace {
 
-constexpr int QR_T = 512;          // threads per CTA
+constexpr int QR_T = 512;          // threads per CTA (circle-method kernels)
+// block-recursive kernels: one lane group of GT per two residents, n / 4 = R GT / 4 groups
+template <int GT, int R, int PK>
+__host__ __device__ constexpr int qr_threads() { return PK == 2 ? R * GT * GT / 4 : QR_T; }
 constexpr int QR_TILE = 32;        // Rayleigh row tile
 
 // One column of B in a lane group's registers, PAIR-PLANAR: shared memory holds each column as
@@ -189,7 +192,7 @@ __device__ __forceinline__ void jacobi_block_recursive(float2* A, int m, int n, 
 }
 
 template <int GT, int R, int PK>
-__global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
+__global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                  DevState* st, int max_sweeps) {
   extern __shared__ __align__(16) uint8_t sm[];
   GateDesc& gd = desc[list[blockIdx.x]];
@@ -206,12 +209,13 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
       (reinterpret_cast<uintptr_t>(sched + (n - 1) * half) + 15) & ~uintptr_t(15));
   __shared__ float2 s_rdiag[256];                                             // R_jj
   __shared__ float s_wn[32];
-  __shared__ float s_xn2, s_beta;
-  __shared__ float2 s_x0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = QR_T / 32;
+  __shared__ float s_xn2[2];                                                  // by step parity
+  __shared__ float2 s_x0[2];
+  constexpr int NT = qr_threads<GT, R, PK>();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);
   float nrm = 0.f;
-  for (int x = tid; x < m * n; x += QR_T) {
+  for (int x = tid; x < m * n; x += NT) {
     const float2 v = gth[x];
     A[x] = v;
     nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
@@ -230,17 +234,21 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) {
-      s_xn2 = a;
-      s_x0 = A[0];
+      s_xn2[0] = a;
+      s_x0[0] = A[0];
     }
   }
   __syncthreads();
   constexpr int QG = 8;                          // lanes per column in the update
-  const int qg = tid / QG, ql = tid % QG, ngr = QR_T / QG;
+  const int qg = tid / QG, ql = tid % QG, ngr = NT / QG;
+  // One barrier per reflector: every thread derives the reflector from the (norm, leading entry)
+  // pair the previous step left in s_xn2 / s_x0[j & 1] and keeps v_0 in a register (v's other
+  // entries are column j's rows > j, which step j does not modify); the group of column j+1
+  // publishes the next pair into the other parity slot. Q is never formed, so v_0 is not stored.
   for (int j = 0; j < n; ++j) {
     // reflector H = I - beta v v^H with v = x - alpha e_1, alpha = -(x0/|x0|) |x|
-    const float xn2 = s_xn2;
-    const float2 x0 = s_x0;
+    const float xn2 = s_xn2[j & 1];
+    const float2 x0 = s_x0[j & 1];
     const float xn = sqrtf(xn2);
     const float ax0 = sqrtf(x0.x * x0.x + x0.y * x0.y);
     const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
@@ -249,25 +257,32 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
     const float vn2 = xn2 - ax0 * ax0 + (v0.x * v0.x + v0.y * v0.y);
     const bool skipj = !(xn2 > 0.f) || !(vn2 > 0.f);
     const float beta = skipj ? 0.f : 2.f / vn2;
-    float2* vj = A + (size_t)j * m;              // v lives in column j, rows j..m-1
-    __syncthreads();                             // everyone has read s_xn2 / s_x0 / A[j][j]
-    if (tid == 0) {
-      s_rdiag[j] = skipj ? x0 : alpha;
-      if (!skipj) vj[j] = v0;
-    }
-    __syncthreads();
+    const float2* vj = A + (size_t)j * m;        // v: v0, then column j's rows j+1..m-1
+    if (tid == 0) s_rdiag[j] = skipj ? x0 : alpha;
     // columns c > j: w = v^H a_c ; a_c -= beta w v ; the group of column j+1 also returns its new
     // tail norm and leading entry for the next reflector
     for (int c0 = j + 1; c0 < n; c0 += ngr) {
       const int c = c0 + qg;
-      float wr = 0.f, wi = 0.f;
       float2* ac = A + (size_t)c * m;
+      float wr = 0.f, wi = 0.f;
       if (c < n && !skipj) {
-        for (int i = j + ql; i < m; i += QG) {
-          const float2 v = vj[i], a = ac[i];
+        float wr1 = 0.f, wi1 = 0.f;              // two accumulator pairs (shorter FMA chains)
+        int i = j + ql;
+        for (; i + QG < m; i += 2 * QG) {
+          const float2 v = i == j ? v0 : vj[i], a = ac[i];
+          const float2 v1 = vj[i + QG], a1 = ac[i + QG];
           wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));     // Re conj(v) a
           wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));    // Im conj(v) a
+          wr1 = fmaf(v1.x, a1.x, fmaf(v1.y, a1.y, wr1));
+          wi1 = fmaf(v1.x, a1.y, fmaf(-v1.y, a1.x, wi1));
         }
+        if (i < m) {
+          const float2 v = i == j ? v0 : vj[i], a = ac[i];
+          wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));
+          wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));
+        }
+        wr += wr1;
+        wi += wi1;
       }
 #pragma unroll
       for (int o = QG / 2; o > 0; o >>= 1) {
@@ -275,36 +290,39 @@ __global__ void __launch_bounds__(QR_T) k_svd_qr(GateDesc* desc, const int32_t* 
         wi += __shfl_xor_sync(0xffffffffu, wi, o);
       }
       float t2 = 0.f;
-      if (c < n) {
+      if (c < n && !skipj) {
         const float br = beta * wr, bi = beta * wi;
         for (int i = j + ql; i < m; i += QG) {
           float2 a = ac[i];
-          if (!skipj) {
-            const float2 v = vj[i];
-            a.x -= br * v.x - bi * v.y;
-            a.y -= br * v.y + bi * v.x;
-            ac[i] = a;
-          }
-          if (c == j + 1 && i > j) t2 = fmaf(a.x, a.x, fmaf(a.y, a.y, t2));
+          const float2 v = i == j ? v0 : vj[i];
+          a.x -= br * v.x - bi * v.y;
+          a.y -= br * v.y + bi * v.x;
+          ac[i] = a;
+          if (i > j) t2 = fmaf(a.x, a.x, fmaf(a.y, a.y, t2));
         }
+      } else if (c < n) {
+        for (int i = j + 1 + ql; i < m; i += QG) t2 = fmaf(ac[i].x, ac[i].x, fmaf(ac[i].y, ac[i].y, t2));
       }
-      // (every lane takes part in the shuffle; only the group of column j+1 keeps the result)
+      // only warp 0's first iteration holds the group of column j+1 (warp-uniform branch)
+      if (c0 == j + 1 && warp == 0) {
 #pragma unroll
-      for (int o = QG / 2; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-      if (c == j + 1 && ql == 0) {
-        s_xn2 = t2;
-        s_x0 = ac[j + 1];
+        for (int o = QG / 2; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        __syncwarp();                            // row j+1 was written by another lane of the group
+        if (qg == 0 && ql == 0) {
+          s_xn2[(j + 1) & 1] = t2;
+          s_x0[(j + 1) & 1] = ac[j + 1];
+        }
       }
     }
     __syncthreads();
   }
   // ---- B = R^H in place (top n x n block, ld m); rows >= n and R's lower part (the reflectors) -> 0
-  for (int x = tid; x < n * m; x += QR_T) {
+  for (int x = tid; x < n * m; x += NT) {
     const int c = x / m, r = x % m;
     if (r > c) A[x] = make_float2(0.f, 0.f);
   }
   __syncthreads();
-  for (int x = tid; x < n * n; x += QR_T) {
+  for (int x = tid; x < n * n; x += NT) {
     const int c = x / n, r = x % n;               // R[r][c], r < c  ->  B[c][r] = conj(R[r][c])
     if (r < c) {
       const float2 v = A[(size_t)c * m + r];
@@ -428,7 +446,7 @@ void launch_qr_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem
     cudaFuncSetAttribute(k_svd_qr<GT, R, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
-  k_svd_qr<GT, R, PK><<<count, QR_T, smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
+  k_svd_qr<GT, R, PK><<<count, qr_threads<GT, R, PK>(), smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
 }
 
 }  // namespace
@@ -470,7 +488,9 @@ void launch_svd_qr(GateDesc* d_desc, const int32_t* d_list, int count, size_t sm
   if (count <= 0) return;
   if (packed == 2) {                                 // block-recursive ordering (qr_block_order)
     const int n = gt * rpl;
-    if (n == 128) return launch_qr_t<16, 8, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
+    static const bool g16 = getenv("EAMPS_QR_GT16") != nullptr;
+    if (n == 128 && g16) return launch_qr_t<16, 8, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
+    if (n == 128) return launch_qr_t<8, 16, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
     if (n == 64) return launch_qr_t<16, 4, 2>(d_desc, d_list, count, smem, max_sweeps, slab, st, s);
     return;
   }
