@@ -191,6 +191,160 @@ __device__ __forceinline__ void jacobi_block_recursive(float2* A, int m, int n, 
   }
 }
 
+// Element (r, c) of a pair-planar column-major matrix (ld m, m even): column c's row pair r/2 is
+// the float4 (Re 2p, Re 2p+1, Im 2p, Im 2p+1).
+__device__ __forceinline__ float2 pl_get(const float2* A, int m, int c, int r) {
+  const float* f = reinterpret_cast<const float*>(A + (size_t)c * m) + (r >> 1) * 4 + (r & 1);
+  return make_float2(f[0], f[2]);
+}
+__device__ __forceinline__ void pl_set(float2* A, int m, int c, int r, float2 v) {
+  float* f = reinterpret_cast<float*>(A + (size_t)c * m) + (r >> 1) * 4 + (r & 1);
+  f[0] = v.x;
+  f[2] = v.y;
+}
+
+// Householder QR of theta (m x n, m >= n, m even) in shared memory, PAIR-PLANAR: theta is loaded
+// as row pairs (Re 2p, Re 2p+1, Im 2p, Im 2p+1), so every dot product and rank-1 update below is a
+// packed FP32x2 instruction on two rows (half the instructions of the interleaved version), then
+// B = R^H is formed in place in the same layout (the Jacobi's layout). Same arithmetic as the
+// interleaved path: reflector H = I - beta v v^H, v = x - alpha e_1, alpha = -(x0/|x0|) |x|,
+// one barrier per reflector (the group of column j+1 publishes the next (|x|^2, x0) pair).
+// Returns |theta|_F^2. Needs NT threads, s_wn >= NT / 32 floats.
+template <int NT>
+__device__ float householder_planar(const float2* __restrict__ gth, float2* A, int m, int n, float2* s_rdiag,
+                                    float* s_wn, float* s_xn2, float2* s_x0) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mh = m / 2;
+  const float4* g4 = reinterpret_cast<const float4*>(gth);
+  float4* A4 = reinterpret_cast<float4*>(A);
+  float nrm = 0.f;
+  for (int x = tid; x < n * mh; x += NT) {
+    const float4 t = g4[x];                        // (Re 2p, Im 2p, Re 2p+1, Im 2p+1)
+    A4[x] = make_float4(t.x, t.z, t.y, t.w);
+    nrm = fmaf(t.x, t.x, fmaf(t.y, t.y, fmaf(t.z, t.z, fmaf(t.w, t.w, nrm))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+  if (lane == 0) s_wn[warp] = nrm;
+  __syncthreads();
+  float norm2 = 0.f;
+  for (int w = 0; w < NT / 32; ++w) norm2 += s_wn[w];
+  if (warp == 0) {
+    float a = 0.f;
+    for (int p = lane; p < mh; p += 32) {
+      const float4 t = A4[p];
+      a = fmaf(t.x, t.x, fmaf(t.y, t.y, fmaf(t.z, t.z, fmaf(t.w, t.w, a))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      s_xn2[0] = a;
+      s_x0[0] = make_float2(A4[0].x, A4[0].z);
+    }
+  }
+  __syncthreads();
+  constexpr int QG = 8;                            // lanes per column
+  const int qg = tid / QG, ql = tid % QG, ngr = NT / QG;
+  for (int j = 0; j < n; ++j) {
+    const float xn2 = s_xn2[j & 1];
+    const float2 x0 = s_x0[j & 1];
+    const float xn = sqrtf(xn2);
+    const float ax0 = sqrtf(x0.x * x0.x + x0.y * x0.y);
+    const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
+    const float2 alpha = make_float2(-ph.x * xn, -ph.y * xn);
+    const float2 v0 = make_float2(x0.x - alpha.x, x0.y - alpha.y);
+    const float vn2 = xn2 - ax0 * ax0 + (v0.x * v0.x + v0.y * v0.y);
+    const bool skipj = !(xn2 > 0.f) || !(vn2 > 0.f);
+    const float beta = skipj ? 0.f : 2.f / vn2;
+    if (tid == 0) s_rdiag[j] = skipj ? x0 : alpha;
+    const float4* vj = A4 + (size_t)j * mh;
+    const int pj = j >> 1;
+    const bool odd = j & 1;
+    // v on row pair p: column j's rows, with row j -> v0 and row j-1 (j odd) -> 0
+    auto vpair = [&](int p) {
+      float4 v = vj[p];
+      if (p == pj) {
+        if (odd) v = make_float4(0.f, v0.x, 0.f, v0.y);
+        else v = make_float4(v0.x, v.y, v0.y, v.w);
+      }
+      return v;
+    };
+    for (int c0 = j + 1; c0 < n; c0 += ngr) {
+      const int c = c0 + qg;
+      float4* ac = A4 + (size_t)c * mh;
+      float2 ar = make_float2(0.f, 0.f), ai = ar, ai2 = ar;
+      if (c < n && !skipj) {
+        for (int p = pj + ql; p < mh; p += QG) {
+          const float4 v = vpair(p), a = ac[p];
+          const float2 vr = make_float2(v.x, v.y), vi = make_float2(v.z, v.w);
+          const float2 a_r = make_float2(a.x, a.y), a_i = make_float2(a.z, a.w);
+          ar = f2_fma(vr, a_r, ar);                  // Re conj(v) a = vr ar + vi ai
+          ar = f2_fma(vi, a_i, ar);
+          ai = f2_fma(vr, a_i, ai);                  // Im conj(v) a = vr ai - vi ar
+          ai2 = f2_fma(vi, a_r, ai2);
+        }
+      }
+      float wr = ar.x + ar.y, wi = (ai.x + ai.y) - (ai2.x + ai2.y);
+#pragma unroll
+      for (int o = QG / 2; o > 0; o >>= 1) {
+        wr += __shfl_xor_sync(0xffffffffu, wr, o);
+        wi += __shfl_xor_sync(0xffffffffu, wi, o);
+      }
+      const bool nextc = (c == j + 1);
+      float t2 = 0.f;
+      auto tail2 = [&](int p, const float4& a) {     // |a|^2 over rows >= j+1 of the pair
+        if (p == pj) return odd ? 0.f : fmaf(a.y, a.y, a.w * a.w);
+        return fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, a.w * a.w)));
+      };
+      if (c < n && !skipj) {
+        const float br = beta * wr, bi = beta * wi;
+        const float2 mbr = make_float2(-br, -br), pbi = make_float2(bi, bi), mbi = make_float2(-bi, -bi);
+        for (int p = pj + ql; p < mh; p += QG) {
+          const float4 v = vpair(p), a = ac[p];
+          const float2 vr = make_float2(v.x, v.y), vi = make_float2(v.z, v.w);
+          float2 a_r = make_float2(a.x, a.y), a_i = make_float2(a.z, a.w);
+          a_r = f2_fma(pbi, vi, f2_fma(mbr, vr, a_r));   // a -= (beta w) v
+          a_i = f2_fma(mbi, vr, f2_fma(mbr, vi, a_i));
+          const float4 an = make_float4(a_r.x, a_r.y, a_i.x, a_i.y);
+          ac[p] = an;
+          if (nextc) t2 += tail2(p, an);
+        }
+      } else if (c < n && nextc) {
+        for (int p = pj + ql; p < mh; p += QG) t2 += tail2(p, ac[p]);
+      }
+      if (c0 == j + 1 && warp == 0) {                 // warp-uniform: holds the group of column j+1
+#pragma unroll
+        for (int o = QG / 2; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        __syncwarp();                                 // row j+1 was written by another lane
+        if (qg == 0 && ql == 0) {
+          s_xn2[(j + 1) & 1] = t2;
+          s_x0[(j + 1) & 1] = pl_get(A, m, j + 1, j + 1);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- B = R^H in place (top n x n block); rows >= n and R's lower part (the reflectors) -> 0
+  for (int x = tid; x < n * m; x += NT) {
+    const int c = x / m, r = x % m;
+    if (r > c) pl_set(A, m, c, r, make_float2(0.f, 0.f));
+  }
+  __syncthreads();
+  for (int x = tid; x < n * n; x += NT) {
+    const int c = x / n, r = x % n;                  // R[r][c], r < c  ->  B[c][r] = conj(R[r][c])
+    if (r < c) {
+      const float2 v = pl_get(A, m, c, r);
+      pl_set(A, m, r, c, make_float2(v.x, -v.y));
+      pl_set(A, m, c, r, make_float2(0.f, 0.f));
+    } else if (r == c) {
+      const float2 d = s_rdiag[r];
+      pl_set(A, m, r, r, make_float2(d.x, -d.y));
+    }
+  }
+  __syncthreads();
+  return norm2;
+}
+
 template <int GT, int R, int PK>
 __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
                                                  DevState* st, int max_sweeps) {
@@ -214,126 +368,131 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
   constexpr int NT = qr_threads<GT, R, PK>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const float2* __restrict__ gth = reinterpret_cast<const float2*>(slab + gd.ws_theta);
-  float nrm = 0.f;
-  for (int x = tid; x < m * n; x += NT) {
-    const float2 v = gth[x];
-    A[x] = v;
-    nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
-  }
   build_circle_schedule(sched, n);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-  if (lane == 0) s_wn[warp] = nrm;
-  __syncthreads();
   float norm2 = 0.f;
-  for (int w = 0; w < nw; ++w) norm2 += s_wn[w];
-  // ---- Householder QR: column j's norm and leading entry come from the previous step
-  if (warp == 0) {
-    float a = 0.f;
-    for (int i = lane; i < m; i += 32) a = fmaf(A[i].x, A[i].x, fmaf(A[i].y, A[i].y, a));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) {
-      s_xn2[0] = a;
-      s_x0[0] = A[0];
+  if constexpr (PK == 2) {
+    // pair-planar Householder QR and B = R^H (householder_planar): packed FP32x2 row pairs
+    norm2 = householder_planar<NT>(gth, A, m, n, s_rdiag, s_wn, s_xn2, s_x0);
+  } else {
+    float nrm = 0.f;
+    for (int x = tid; x < m * n; x += NT) {
+      const float2 v = gth[x];
+      A[x] = v;
+      nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
     }
-  }
-  __syncthreads();
-  constexpr int QG = 8;                          // lanes per column in the update
-  const int qg = tid / QG, ql = tid % QG, ngr = NT / QG;
-  // One barrier per reflector: every thread derives the reflector from the (norm, leading entry)
-  // pair the previous step left in s_xn2 / s_x0[j & 1] and keeps v_0 in a register (v's other
-  // entries are column j's rows > j, which step j does not modify); the group of column j+1
-  // publishes the next pair into the other parity slot. Q is never formed, so v_0 is not stored.
-  for (int j = 0; j < n; ++j) {
-    // reflector H = I - beta v v^H with v = x - alpha e_1, alpha = -(x0/|x0|) |x|
-    const float xn2 = s_xn2[j & 1];
-    const float2 x0 = s_x0[j & 1];
-    const float xn = sqrtf(xn2);
-    const float ax0 = sqrtf(x0.x * x0.x + x0.y * x0.y);
-    const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
-    const float2 alpha = make_float2(-ph.x * xn, -ph.y * xn);
-    const float2 v0 = make_float2(x0.x - alpha.x, x0.y - alpha.y);
-    const float vn2 = xn2 - ax0 * ax0 + (v0.x * v0.x + v0.y * v0.y);
-    const bool skipj = !(xn2 > 0.f) || !(vn2 > 0.f);
-    const float beta = skipj ? 0.f : 2.f / vn2;
-    const float2* vj = A + (size_t)j * m;        // v: v0, then column j's rows j+1..m-1
-    if (tid == 0) s_rdiag[j] = skipj ? x0 : alpha;
-    // columns c > j: w = v^H a_c ; a_c -= beta w v ; the group of column j+1 also returns its new
-    // tail norm and leading entry for the next reflector
-    for (int c0 = j + 1; c0 < n; c0 += ngr) {
-      const int c = c0 + qg;
-      float2* ac = A + (size_t)c * m;
-      float wr = 0.f, wi = 0.f;
-      if (c < n && !skipj) {
-        float wr1 = 0.f, wi1 = 0.f;              // two accumulator pairs (shorter FMA chains)
-        int i = j + ql;
-        for (; i + QG < m; i += 2 * QG) {
-          const float2 v = i == j ? v0 : vj[i], a = ac[i];
-          const float2 v1 = vj[i + QG], a1 = ac[i + QG];
-          wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));     // Re conj(v) a
-          wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));    // Im conj(v) a
-          wr1 = fmaf(v1.x, a1.x, fmaf(v1.y, a1.y, wr1));
-          wi1 = fmaf(v1.x, a1.y, fmaf(-v1.y, a1.x, wi1));
-        }
-        if (i < m) {
-          const float2 v = i == j ? v0 : vj[i], a = ac[i];
-          wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));
-          wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));
-        }
-        wr += wr1;
-        wi += wi1;
-      }
 #pragma unroll
-      for (int o = QG / 2; o > 0; o >>= 1) {
-        wr += __shfl_xor_sync(0xffffffffu, wr, o);
-        wi += __shfl_xor_sync(0xffffffffu, wi, o);
-      }
-      float t2 = 0.f;
-      if (c < n && !skipj) {
-        const float br = beta * wr, bi = beta * wi;
-        for (int i = j + ql; i < m; i += QG) {
-          float2 a = ac[i];
-          const float2 v = i == j ? v0 : vj[i];
-          a.x -= br * v.x - bi * v.y;
-          a.y -= br * v.y + bi * v.x;
-          ac[i] = a;
-          if (i > j) t2 = fmaf(a.x, a.x, fmaf(a.y, a.y, t2));
-        }
-      } else if (c < n) {
-        for (int i = j + 1 + ql; i < m; i += QG) t2 = fmaf(ac[i].x, ac[i].x, fmaf(ac[i].y, ac[i].y, t2));
-      }
-      // only warp 0's first iteration holds the group of column j+1 (warp-uniform branch)
-      if (c0 == j + 1 && warp == 0) {
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) s_wn[warp] = nrm;
+    __syncthreads();
+    for (int w = 0; w < nw; ++w) norm2 += s_wn[w];
+    // ---- Householder QR: column j's norm and leading entry come from the previous step
+    if (warp == 0) {
+      float a = 0.f;
+      for (int i = lane; i < m; i += 32) a = fmaf(A[i].x, A[i].x, fmaf(A[i].y, A[i].y, a));
 #pragma unroll
-        for (int o = QG / 2; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-        __syncwarp();                            // row j+1 was written by another lane of the group
-        if (qg == 0 && ql == 0) {
-          s_xn2[(j + 1) & 1] = t2;
-          s_x0[(j + 1) & 1] = ac[j + 1];
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) {
+        s_xn2[0] = a;
+        s_x0[0] = A[0];
+      }
+    }
+    __syncthreads();
+    constexpr int QG = 8;                          // lanes per column in the update
+    const int qg = tid / QG, ql = tid % QG, ngr = NT / QG;
+    // One barrier per reflector: every thread derives the reflector from the (norm, leading entry)
+    // pair the previous step left in s_xn2 / s_x0[j & 1] and keeps v_0 in a register (v's other
+    // entries are column j's rows > j, which step j does not modify); the group of column j+1
+    // publishes the next pair into the other parity slot. Q is never formed, so v_0 is not stored.
+    for (int j = 0; j < n; ++j) {
+      // reflector H = I - beta v v^H with v = x - alpha e_1, alpha = -(x0/|x0|) |x|
+      const float xn2 = s_xn2[j & 1];
+      const float2 x0 = s_x0[j & 1];
+      const float xn = sqrtf(xn2);
+      const float ax0 = sqrtf(x0.x * x0.x + x0.y * x0.y);
+      const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
+      const float2 alpha = make_float2(-ph.x * xn, -ph.y * xn);
+      const float2 v0 = make_float2(x0.x - alpha.x, x0.y - alpha.y);
+      const float vn2 = xn2 - ax0 * ax0 + (v0.x * v0.x + v0.y * v0.y);
+      const bool skipj = !(xn2 > 0.f) || !(vn2 > 0.f);
+      const float beta = skipj ? 0.f : 2.f / vn2;
+      const float2* vj = A + (size_t)j * m;        // v: v0, then column j's rows j+1..m-1
+      if (tid == 0) s_rdiag[j] = skipj ? x0 : alpha;
+      // columns c > j: w = v^H a_c ; a_c -= beta w v ; the group of column j+1 also returns its new
+      // tail norm and leading entry for the next reflector
+      for (int c0 = j + 1; c0 < n; c0 += ngr) {
+        const int c = c0 + qg;
+        float2* ac = A + (size_t)c * m;
+        float wr = 0.f, wi = 0.f;
+        if (c < n && !skipj) {
+          float wr1 = 0.f, wi1 = 0.f;              // two accumulator pairs (shorter FMA chains)
+          int i = j + ql;
+          for (; i + QG < m; i += 2 * QG) {
+            const float2 v = i == j ? v0 : vj[i], a = ac[i];
+            const float2 v1 = vj[i + QG], a1 = ac[i + QG];
+            wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));     // Re conj(v) a
+            wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));    // Im conj(v) a
+            wr1 = fmaf(v1.x, a1.x, fmaf(v1.y, a1.y, wr1));
+            wi1 = fmaf(v1.x, a1.y, fmaf(-v1.y, a1.x, wi1));
+          }
+          if (i < m) {
+            const float2 v = i == j ? v0 : vj[i], a = ac[i];
+            wr = fmaf(v.x, a.x, fmaf(v.y, a.y, wr));
+            wi = fmaf(v.x, a.y, fmaf(-v.y, a.x, wi));
+          }
+          wr += wr1;
+          wi += wi1;
         }
+#pragma unroll
+        for (int o = QG / 2; o > 0; o >>= 1) {
+          wr += __shfl_xor_sync(0xffffffffu, wr, o);
+          wi += __shfl_xor_sync(0xffffffffu, wi, o);
+        }
+        float t2 = 0.f;
+        if (c < n && !skipj) {
+          const float br = beta * wr, bi = beta * wi;
+          for (int i = j + ql; i < m; i += QG) {
+            float2 a = ac[i];
+            const float2 v = i == j ? v0 : vj[i];
+            a.x -= br * v.x - bi * v.y;
+            a.y -= br * v.y + bi * v.x;
+            ac[i] = a;
+            if (i > j) t2 = fmaf(a.x, a.x, fmaf(a.y, a.y, t2));
+          }
+        } else if (c < n) {
+          for (int i = j + 1 + ql; i < m; i += QG) t2 = fmaf(ac[i].x, ac[i].x, fmaf(ac[i].y, ac[i].y, t2));
+        }
+        // only warp 0's first iteration holds the group of column j+1 (warp-uniform branch)
+        if (c0 == j + 1 && warp == 0) {
+#pragma unroll
+          for (int o = QG / 2; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+          __syncwarp();                            // row j+1 was written by another lane of the group
+          if (qg == 0 && ql == 0) {
+            s_xn2[(j + 1) & 1] = t2;
+            s_x0[(j + 1) & 1] = ac[j + 1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- B = R^H in place (top n x n block, ld m); rows >= n and R's lower part (the reflectors) -> 0
+    for (int x = tid; x < n * m; x += NT) {
+      const int c = x / m, r = x % m;
+      if (r > c) A[x] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int x = tid; x < n * n; x += NT) {
+      const int c = x / n, r = x % n;               // R[r][c], r < c  ->  B[c][r] = conj(R[r][c])
+      if (r < c) {
+        const float2 v = A[(size_t)c * m + r];
+        A[(size_t)r * m + c] = make_float2(v.x, -v.y);
+        A[(size_t)c * m + r] = make_float2(0.f, 0.f);
+      } else if (r == c) {
+        const float2 d = s_rdiag[r];
+        A[(size_t)r * m + r] = make_float2(d.x, -d.y);
       }
     }
     __syncthreads();
   }
-  // ---- B = R^H in place (top n x n block, ld m); rows >= n and R's lower part (the reflectors) -> 0
-  for (int x = tid; x < n * m; x += NT) {
-    const int c = x / m, r = x % m;
-    if (r > c) A[x] = make_float2(0.f, 0.f);
-  }
-  __syncthreads();
-  for (int x = tid; x < n * n; x += NT) {
-    const int c = x / n, r = x % n;               // R[r][c], r < c  ->  B[c][r] = conj(R[r][c])
-    if (r < c) {
-      const float2 v = A[(size_t)c * m + r];
-      A[(size_t)r * m + c] = make_float2(v.x, -v.y);
-      A[(size_t)c * m + r] = make_float2(0.f, 0.f);
-    } else if (r == c) {
-      const float2 d = s_rdiag[r];
-      A[(size_t)r * m + r] = make_float2(d.x, -d.y);
-    }
-  }
-  __syncthreads();
   // ---- one-sided Jacobi on B's n columns of length n (ld m): registers, cached norms, schedule
   const float skip = norm2 * 3.5527137e-15f;
   const float tol = fmaxf(7.62939453e-6f, 4.f * sqrtf((float)n) * 5.96046448e-8f);
@@ -349,8 +508,6 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
     // jacobi_block_recursive below. Two resident columns per lane group stay in registers while
     // the visitors stream through shared memory: one column load + one store per two rotations.
     (void)sched;
-    pair_planar(A, m, n);
-    __syncthreads();
     jacobi_block_recursive<GT, R>(A, m, n, cn, skip, tol2, max_sweeps, sweep, converged);
     pair_planar(A, m, n);
     __syncthreads();
@@ -362,7 +519,7 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
           const float2 v = A[(size_t)j * m + i];
           a = fmaf(v.x, v.x, fmaf(v.y, v.y, a));
         }
-  #pragma unroll
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
         if (lane == 0) cn[j] = a;
       }
