@@ -1,5 +1,5 @@
 # usage: bash tools/ab_bench.sh "ENV1=.." "ENV2=.." ... ; one bench line per setting (value, sweeps, svd ms)
 for e in "$@"; do
-  env $e python bench.py > gpurun_out/ab.log 2>&1
+  env $e timeout 300 python bench.py > gpurun_out/ab.log 2>&1
   echo "$e: $(tail -1 gpurun_out/ab.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['sweeps_mean'],2), round(d['phase_ms_per_step']['svd_small'],2), round(d['roofline']['frac'],3))")"
 done
