@@ -285,10 +285,11 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
   const float* lam = reinterpret_cast<const float*>(slab + bonds[gd.site].off);
   const float2* thp = reinterpret_cast<const float2*>(slab + gd.ws_thetap);
   const float2* V = reinterpret_cast<const float2*>(slab + gd.ws_V);
-  __shared__ float2 As[16][RC + 1];
-  __shared__ float2 Bs[16][33];
-  __shared__ double red[4][RC];
-  const int tid = threadIdx.x;
+  // tiles are staged in FP64 (one conversion per element per chunk, not one per product)
+  __shared__ double2 As[16][RC + 1];
+  __shared__ double2 Bs[16][33];
+  __shared__ double red[8][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int oi = tid & (RC - 1), oj = (tid >> 6) * 8;   // 64 rows x (4 groups x 8 columns)
   double num[8];
 #pragma unroll
@@ -328,24 +329,23 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
         const int e = tid + it * 256;
-        As[e >> 6][e & (RC - 1)] = ra[it];
+        As[e >> 6][e & (RC - 1)] = make_double2(ra[it].x, ra[it].y);
       }
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
         const int e = tid + it * 256;
-        Bs[e & 15][e >> 4] = rb[it];
+        Bs[e & 15][e >> 4] = make_double2(rb[it].x, rb[it].y);
       }
       __syncthreads();
       if (kc + 1 < nk) fetch(r0, (kc + 1) * 16, ra, rb);
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
-        float2 a = As[kk][oi];
-        double ax = a.x, ay = a.y;
+        const double2 a = As[kk][oi];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float2 bq = Bs[kk][oj + j];
-          w[j].x = fma(ax, (double)bq.x, fma(-ay, (double)bq.y, w[j].x));
-          w[j].y = fma(ax, (double)bq.y, fma(ay, (double)bq.x, w[j].y));
+          const double2 bq = Bs[kk][oj + j];
+          w[j].x = fma(a.x, bq.x, fma(-a.y, bq.y, w[j].x));
+          w[j].y = fma(a.x, bq.y, fma(a.y, bq.x, w[j].y));
         }
       }
       __syncthreads();
@@ -362,31 +362,44 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
       }
     }
   }
-  // reduce num over the 64 row-threads of each column group (fixed order -> deterministic)
-  __shared__ double colsum[32];
-  const int grp = tid >> 6;
-  for (int jj = 0; jj < 8; ++jj) {
-    red[grp][oi] = num[jj];
-    __syncthreads();
-    if (oi == 0) {
-      double sum = 0.0;
-      for (int i = 0; i < RC; ++i) sum += red[grp][i];
-      colsum[oj + jj] = sum;
-    }
-    __syncthreads();
+  // reduce num over the 64 row-threads of each column group: warp butterflies, then the two warps
+  // of a group in a fixed order (deterministic)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) num[j] += __shfl_xor_sync(0xffffffffu, num[j], o);
   }
-  if (tid < 32) {
-    int j = j0 + tid;
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[warp][j] = num[j];
+  }
+  // den_j = |v_j|^2: warp w handles columns 4w .. 4w+3, lanes stride over k (coalesced)
+  double den[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int j = j0 + warp * 4 + c;
+    double d = 0.0;
     if (j < n) {
-      double den = 0.0;
       const float2* vj = V + (int64_t)j * np;
-      for (int k = 0; k < n; ++k) den += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
-      double v = den > 0.0 ? colsum[tid] / den : 0.0;
+      for (int k = lane; k < n; k += 32) d += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    den[c] = d;
+  }
+  __syncthreads();
+  if (lane < 4) {
+    const int jl = warp * 4 + lane, j = j0 + jl;    // column jl belongs to group jl / 8 = warps 2g, 2g+1
+    const double dj = lane == 0 ? den[0] : lane == 1 ? den[1] : lane == 2 ? den[2] : den[3];
+    if (j < n) {
+      const int g = jl >> 3, jj = jl & 7;
+      const double numj = red[2 * g][jj] + red[2 * g + 1][jj];
+      const double v = dj > 0.0 ? numj / dj : 0.0;
       reinterpret_cast<double*>(slab + gd.ws_sig2)[j] = v;
       if (write_b) {   // polish scratch at ws_E: shift[n_pad] | den[n_pad]
         double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
         shift[j] = 0.0;
-        shift[np + j] = den;
+        shift[np + j] = dj;
       }
     }
   }
