@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <array>
+#include <map>
 #include <vector>
 
 #include "eamps.h"
@@ -335,42 +337,51 @@ mps_status wave_front(mps_t h) {
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
   }
-  // QR-regime buckets: (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not, or
-  // the block-recursive ordering (n = 64, 128; its own lane groups, see svd_qr.cu)
-  for (int gt : {4, 8, 16, 32}) {
-   for (int rpl : {1, 2, 4, 8, 16}) {
-    for (int pk : {0, 1, 2}) {
-      Bucket b{3, gt, (int)small.size(), 0, 512, pk, rpl, 0, 0};   // (tile_rows carries the packed flag)
-      for (int x = 0; x < Gw; ++x) {
-        const GateDesc& gd = hd[x];
-        int g_gt = 0, g_r = 0;
-        if (gd.regime != 3 || !svd_qr_fits(gd.m, gd.n, &g_gt, &g_r) || g_gt != gt || g_r != rpl) continue;
-        const int g_pk = qr_block_order(gd.m, gd.n) ? 2 : (gd.n == g_r * g_gt && gd.m % 2 == 0 && g_r >= 2) ? 1 : 0;
-        if (g_pk != pk) continue;
-        small.push_back(x);
-        b.smem = std::max(b.smem, svd_qr_smem(gd.m, gd.n));
+  // SVD buckets, one launch each; `small` holds their gates back to back, [begin, end) per bucket.
+  //  QR regime (3): (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not, or the
+  //    block-recursive ordering (n = 64, 128; its own lane groups, see svd_qr.cu);
+  //  small (0) / medium (2): lane-group size GT, rows per lane R (R > 0 keeps a pair's rows in
+  //    registers). Each gate's key is computed once; the map keeps the launch order by key.
+  {
+    auto gidx = [](int gt) { return gt == 4 ? 0 : gt == 8 ? 1 : gt == 16 ? 2 : 3; };
+    auto ridx = [](int r) { return r == 1 ? 0 : r == 2 ? 1 : r == 4 ? 2 : r == 8 ? 3 : r == 16 ? 4 : 5; };
+    std::map<int, std::vector<int32_t>> keyed;   // key = ((class * 4 + gt) * 6 + rpl) * 3 + pk
+    std::map<int, std::array<int, 4>> kparm;     // regime, gt, rpl, pk
+    for (int x = 0; x < Gw; ++x) {
+      const GateDesc& gd = hd[x];
+      int reg = gd.regime, gt = 0, rpl = 0, pk = 0, cls = 0;
+      if (reg == 1) continue;
+      if (reg == 3) {
+        if (!svd_qr_fits(gd.m, gd.n, &gt, &rpl)) return set_err(h, MPS_E_STATE, "internal: QR regime without a QR fit");
+        pk = qr_block_order(gd.m, gd.n) ? 2 : (gd.n == rpl * gt && gd.m % 2 == 0 && rpl >= 2) ? 1 : 0;
+        cls = 0;
+      } else {
+        gt = lane_group(gd.m, gd.n, reg);
+        const int rm = rows_per_lane(gd.m, gt), rn = rows_per_lane(gd.n, gt);
+        rpl = (rm == 0 || rn == 0) ? 0 : std::max(rm, rn);
+        cls = reg == 0 ? 1 : 2;
       }
-      b.end = (int)small.size();
-      if (b.end != b.begin) buckets.push_back(b);
+      const int key = ((cls * 4 + gidx(gt)) * 6 + ridx(rpl)) * 3 + pk;
+      keyed[key].push_back(x);
+      kparm[key] = {reg, gt, rpl, pk};
     }
-   }
-  }
-  // buckets: (regime, lane-group size GT, rows per lane R); R > 0 keeps a pair's rows in registers
-  for (int reg : {0, 2}) {
-    for (int gt : {4, 8, 16, 32}) {
-     for (int rpl : {1, 2, 4, 8, 16, 0}) {
+    for (auto& kv : keyed) {
+      const std::array<int, 4>& pr = kparm[kv.first];
+      const int reg = pr[0], gt = pr[1], rpl = pr[2];
+      if (reg == 3) {
+        Bucket b{3, gt, (int)small.size(), 0, 512, pr[3], rpl, 0, 0};   // (tile_rows carries the packed flag)
+        for (int x : kv.second) {
+          small.push_back(x);
+          b.smem = std::max(b.smem, svd_qr_smem(hd[x].m, hd[x].n));
+        }
+        b.end = (int)small.size();
+        buckets.push_back(b);
+        continue;
+      }
       Bucket b{reg, gt, (int)small.size(), 0, 64, 64, rpl, 0, 0};
       int maxn = 2;
-      for (int x = 0; x < Gw; ++x) {
+      for (int x : kv.second) {
         const GateDesc& gd = hd[x];
-        if (gd.regime != reg) continue;
-        // lane-group size: small regime as before; medium regime (theta 96-210 KB, V replayed) with
-        // at most 512 threads so the rows-per-lane registers fit (one pair per group)
-        const int g_gt = lane_group(gd.m, gd.n, reg);
-        if (g_gt != gt) continue;
-        const int rm = rows_per_lane(gd.m, gt), rn = rows_per_lane(gd.n, gt);
-        const int g_r = (rm == 0 || rn == 0) ? 0 : std::max(rm, rn);
-        if (g_r != rpl) continue;
         small.push_back(x);
         maxn = std::max(maxn, gd.n);
         if (reg == 0) {
@@ -382,13 +393,11 @@ mps_status wave_front(mps_t h) {
         }
       }
       b.end = (int)small.size();
-      if (b.end == b.begin) continue;
       if (reg == 2) {
         for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
       }
       b.threads = (int)std::min<size_t>(reg == 0 ? 1024 : 512, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
       buckets.push_back(b);
-     }
     }
   }
   if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
