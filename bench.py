@@ -91,16 +91,55 @@ def max_over_ranks(value, device=None):
 
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
+    """SM clock + clock-event reasons sampled DURING the timed region: NVML polled every 2 ms from a
+    thread (short timed regions still get samples); nvidia-smi -lms 200 if NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.gpu = gpu_index
         self.p = None
+        self.nv = None
+        self.rows = []
+        self.run = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            idx = gpu_index
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ids = [x.strip() for x in vis.split(",") if x.strip()]
+                if gpu_index < len(ids) and ids[gpu_index].isdigit():
+                    idx = int(ids[gpu_index])
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = nv
+            self.bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        while self.run:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append(dict(sm=sm, mx=mx, reasons=["active" if rs & b else "" for b in self.bits]))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.run = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
                                        "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
@@ -108,31 +147,33 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
-        if self.p is None:
-            return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
         rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
+        if self.nv is not None:
+            self.run = False
+            self.t.join(timeout=5)
+            rows = self.rows
+        elif self.p is not None:
+            self.p.terminate()
             try:
-                rows.append(dict(sm=float(parts[1]), mx=float(parts[2]), pw=float(parts[3]), reasons=parts[5:9]))
-            except ValueError:
-                continue
-        os.unlink(self.f.name)
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.flush()
+            for line in open(self.f.name):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append(dict(sm=float(parts[1]), mx=float(parts[2]), reasons=parts[5:9]))
+                except ValueError:
+                    continue
+            os.unlink(self.f.name)
         if not rows:
             return None
         loaded = [r for r in rows if r["sm"] > 300] or rows
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        seen = sorted({names[i] for r in rows for i, v in enumerate(r["reasons"]) if v.lower() == "active"})
+        seen = sorted({self.NAMES[i] for r in rows for i, v in enumerate(r["reasons"]) if v.lower() == "active"})
         return {"sm_mhz": float(np.median([r["sm"] for r in loaded])), "sm_max_mhz": rows[0]["mx"],
-                "reasons": seen, "samples": len(rows)}
+                "reasons": seen, "samples": len(rows), "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------------------ reference arm
