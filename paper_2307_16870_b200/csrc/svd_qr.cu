@@ -347,7 +347,7 @@ __device__ float householder_planar(const float2* __restrict__ gth, float2* A, i
 
 template <int GT, int R, int PK>
 __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* desc, const int32_t* __restrict__ list, uint8_t* slab,
-                                                 DevState* st, int max_sweeps) {
+                                                 DevState* st, int max_sweeps, float tol_min) {
   extern __shared__ __align__(16) uint8_t sm[];
   GateDesc& gd = desc[list[blockIdx.x]];
   const int m = gd.m, n = gd.n, half = n / 2;
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
   }
   // ---- one-sided Jacobi on B's n columns of length n (ld m): registers, cached norms, schedule
   const float skip = norm2 * 3.5527137e-15f;
-  const float tol = fmaxf(7.62939453e-6f, 4.f * sqrtf((float)n) * 5.96046448e-8f);
+  const float tol = fmaxf(tol_min, 4.f * sqrtf((float)n) * 5.96046448e-8f);
   const float tol2 = tol * tol;
   const int gid = tid / GT, lgi = tid % GT;
   const int sh = gid & (32 / GT - 1);
@@ -603,7 +603,9 @@ void launch_qr_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem
     cudaFuncSetAttribute(k_svd_qr<GT, R, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
-  k_svd_qr<GT, R, PK><<<count, qr_threads<GT, R, PK>(), smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
+  // Jacobi tolerance (relative |gamma| / sqrt(alpha beta)); EAMPS_QR_TOL overrides it for A/B runs
+  static const float tol_min = getenv("EAMPS_QR_TOL") ? (float)atof(getenv("EAMPS_QR_TOL")) : 7.62939453e-6f;
+  k_svd_qr<GT, R, PK><<<count, qr_threads<GT, R, PK>(), smem, s>>>(d_desc, d_list, slab, st, max_sweeps, tol_min);
 }
 
 }  // namespace
