@@ -249,6 +249,10 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
 // two the caller may replace the ledger (mps_ledger_set): the multi-rank token chain of §8(e).
 // lane-group size of the small (reg 0) and medium (reg 2) Jacobi kernels: a power of two in
 // [4, 32], from the rows (small_group(m)) and the CTA width (2048 / n resp. 1024 / n lanes per pair)
+size_t large_scratch_bytes(const GateDesc& gd) {
+  return std::max(svd_tc_scratch_bytes(gd.n_pad), gd.jrows > 0 ? large_precond_scratch(gd.n) : (size_t)0);
+}
+
 int lane_group(int m, int n, int reg) {
   int cap = std::max(4, (reg == 0 ? 2048 : 1024) / std::max(n, 1));
   int p2 = 4;
@@ -328,7 +332,7 @@ mps_status wave_front(mps_t h) {
     // E (k x k, reabsorb); the large regime's polish also keeps shift | den (2 n_pad doubles) there
     gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, (gd.regime == 1 || gd.regime == 3) ? (size_t)16 * gd.n_pad : (size_t)0));
     gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
-                : gd.regime == 1 ? (int64_t)take(svd_tc_scratch_bytes(gd.n_pad))
+                : gd.regime == 1 ? (int64_t)take(large_scratch_bytes(gd))
                                  : 0;
     hd[x] = gd;
     cpre[x + 1] = cpre[x] + p.ctiles;
@@ -779,8 +783,11 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
     // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)
+    // large regime with m >= n: the R-preconditioner (FP64 Gram + Cholesky, Jacobi on B = L with n
+    // rows, no V accumulation); its FP64 Gram shares the tensor-core scratch (dead until the sweeps)
+    gd.jrows = (gd.regime == 1 && gd.m >= gd.n && large_precond_enabled()) ? gd.n : 0;
     const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
-                                       : (gd.regime == 1 ? svd_tc_scratch_bytes(gd.n_pad) : 0);
+                                       : (gd.regime == 1 ? large_scratch_bytes(gd) : 0);
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
     const int kmn = std::min(gd.m, gd.n);

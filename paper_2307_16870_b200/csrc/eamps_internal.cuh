@@ -53,7 +53,9 @@ struct GateDesc {
   int64_t ws_theta, ws_thetap, ws_V, ws_sig2, ws_T, ws_pi;   // slab offsets
   int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
   int64_t ws_log;                   // medium: rotation log, log_sweeps x (n-1) x n/2 float4 (c, s, e); large: TC scratch
-  int32_t log_sweeps, pad0;
+  int32_t log_sweeps;
+  int32_t jrows;                    // large regime: 0 = Jacobi on theta (m rows) with V accumulated;
+                                    // > 0 = preconditioned, Jacobi on B = L (jrows = n rows), no V
   int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
   int32_t k, capped;                // outputs of the selector
   int64_t off_newL, off_newR, off_newLam;                    // outputs of the selector
@@ -61,6 +63,8 @@ struct GateDesc {
   double f, t;                      // achieved / target truncation fidelity
   double dlogE, disc;               // log f, discarded weight T_k / P
 };
+
+__host__ __device__ inline int jacobi_rows(const GateDesc& g) { return g.jrows > 0 ? g.jrows : g.m; }
 
 struct Record {                     // == mps_record
   int64_t gate_index;
@@ -124,6 +128,11 @@ int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_l
                     cudaStream_t s, int* error_out);
 // tensor-core (tcgen05 3xTF32) blocked Jacobi: n_pad multiple of 64, per-gate scratch at ws_log
 size_t svd_tc_scratch_bytes(int n_pad);
+// large-regime R-preconditioner (precond_large.cu): FP64 Gram + Cholesky -> B = L, no V accumulation
+bool large_precond_enabled();
+size_t large_precond_scratch(int n);
+int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s);
+int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab, cudaStream_t s);
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,
                cudaStream_t s, int* error_out);

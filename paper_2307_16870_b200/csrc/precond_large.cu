@@ -1,0 +1,296 @@
+// precond_large.cu -- step a2, large regime: the R-preconditioner of the tcgen05 block Jacobi
+// (the large-theta counterpart of svd_qr.cu's Householder preconditioner).
+//
+//   G = theta^H theta               (FP64 products of the FP32 theta, FP64 sums; k_pc_gram)
+//   G = L L^H                       (blocked left-looking Cholesky in FP64; k_pc_chol)
+//   B = L (= R^H for theta = Q R)   (FP32, n x n, the block Jacobi's working matrix; k_pc_b_from_l)
+//   block Jacobi on B's columns, no V accumulation: B W = U Sigma gives R = W Sigma U^H and
+//   theta = (Q W) Sigma U^H, so theta's right singular vectors are the normalised converged
+//   columns of B (k_pc_vnorm); sigma then comes from the Rayleigh quotient with the ORIGINAL theta
+//   and the FP64-anchored polish (launch_spectrum_polish), exactly as in the QR regime.
+// Q is never formed. Accuracy: the FP64 Gram and Cholesky give R with relative backward error
+// ~ eps64 kappa(theta)^2 (config 2 chi = 1024: 1e-16 x 1.2e10 ~ 1e-6 of the smallest sigma's
+// direction, below the FP32 Jacobi's own tolerance), and the Rayleigh quotient is second order in
+// the direction error. A pivot below n eps64 max_i G_ii (theta numerically rank-deficient) zeroes its
+// column of L: that direction gets sigma = 0 (it lies in the FP32 noise of theta anyway).
+// The preconditioner removes the V half of every rotation and cuts the sweeps (the QR regime:
+// 12 -> 9 at chi = 64). PAPER.md:65 (M = U Lambda V^dagger), :114 ("performing its SVD");
+// SURVEY §8(a) a2.
+#include "eamps_internal.cuh"
+
+namespace eamps {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul_conj_acc(double2 acc, double2 a, double2 b) {   // acc + conj(a) b
+  acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+  return acc;
+}
+
+// G[i][j] = sum_r conj(theta[r][i]) theta[r][j] for the 64 x 64 tiles with ti >= tj (the lower
+// triangle the Cholesky reads). theta: ws_theta (FP32, ld m); G: ws_log (FP64 complex, ld n).
+__global__ void __launch_bounds__(256) k_pc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                 uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.y]];
+  if (gd.jrows <= 0) return;
+  const int m = gd.m, n = gd.n, T = (n + 63) / 64;
+  const int t = blockIdx.x;
+  if (t >= T * (T + 1) / 2) return;
+  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (ti * (ti + 1) / 2 > t) --ti;
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  const float2* th = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+  double2* G = reinterpret_cast<double2*>(slab + gd.ws_log);
+  __shared__ double2 Ai[16][65], Aj[16][65];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double2 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  for (int r0 = 0; r0 < m; r0 += 16) {
+    for (int x = tid; x < 16 * 64; x += 256) {
+      const int c = x >> 4, rr = x & 15, r = r0 + rr;
+      const int ci = ti * 64 + c, cj = tj * 64 + c;
+      const float2 vi = (r < m && ci < n) ? th[(int64_t)ci * m + r] : make_float2(0.f, 0.f);
+      const float2 vj = (r < m && cj < n) ? th[(int64_t)cj * m + r] : make_float2(0.f, 0.f);
+      Ai[rr][c] = make_double2(vi.x, vi.y);
+      Aj[rr][c] = make_double2(vj.x, vj.y);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      double2 xi[4], yj[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xi[a] = Ai[k][ty * 4 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) yj[b] = Aj[k][tx * 4 + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = cmul_conj_acc(acc[a][b], xi[a], yj[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ti * 64 + ty * 4 + a, j = tj * 64 + tx * 4 + b;
+      if (i < n && j < n) G[(int64_t)j * n + i] = acc[a][b];
+    }
+}
+
+// In-place blocked left-looking Cholesky G = L L^H (lower), one CTA per gate, panels of 32
+// columns: (1) every 32-row block of the panel gets G[i][panel] -= L[i][0:c0] L[panel][0:c0]^H;
+// (2) the diagonal block is factored in shared memory (pivots <= tau -> zero column) and inverted;
+// (3) the blocks below become X = G_blk L_JJ^-H = G_blk (L_JJ^-1)^H (a small GEMM, no serial solve).
+__global__ void __launch_bounds__(256) k_pc_chol(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                 uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.x]];
+  if (gd.jrows <= 0) return;
+  const int n = gd.n;
+  double2* G = reinterpret_cast<double2*>(slab + gd.ws_log);
+  struct Smem {
+    double2 Lp[32][33];   // factored diagonal block L_JJ; later the row block being solved
+    double2 Mi[32][33];   // L_JJ^-1 (lower)
+    double2 As[32][17], Bs[32][17];
+  };
+  extern __shared__ __align__(16) uint8_t pc_sm[];
+  Smem& S = *reinterpret_cast<Smem*>(pc_sm);
+  auto& Lp = S.Lp;
+  auto& Mi = S.Mi;
+  auto& As = S.As;
+  auto& Bs = S.Bs;
+  auto& Tt = S.Lp;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rr = tid >> 3, cb = (tid & 7) * 4;    // 32 x 32 tile: row rr, columns cb .. cb+3
+  // pivot threshold tau = n eps64 max_i G_ii
+  double dm = 0.0;
+  for (int i = tid; i < n; i += 256) dm = fmax(dm, G[(int64_t)i * n + i].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+  if (lane == 0) s_red[warp] = dm;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int w = 0; w < 8; ++w) gmax = fmax(gmax, s_red[w]);
+  const double tau = (double)n * 2.220446049250313e-16 * gmax;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int w = min(32, n - c0);
+    for (int i0 = c0; i0 < n; i0 += 32) {
+      double2 acc[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + rr, j = c0 + cb + b;
+        acc[b] = (i < n && j < c0 + w) ? G[(int64_t)j * n + i] : make_double2(0.0, 0.0);
+      }
+      for (int k0 = 0; k0 < c0; k0 += 16) {       // k0 + 16 <= c0 (c0 is a multiple of 32)
+        for (int x = tid; x < 32 * 16; x += 256) {
+          const int r = x & 31, kk = x >> 5;
+          const int k = k0 + kk;
+          As[r][kk] = (i0 + r < n) ? G[(int64_t)k * n + i0 + r] : make_double2(0.0, 0.0);
+          Bs[r][kk] = (c0 + r < n) ? G[(int64_t)k * n + c0 + r] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < 16; ++kk) {
+          const double2 a = As[rr][kk];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double2 q = Bs[cb + b][kk];   // acc -= a conj(q)
+            acc[b].x -= a.x * q.x + a.y * q.y;
+            acc[b].y -= a.y * q.x - a.x * q.y;
+          }
+        }
+        __syncthreads();
+      }
+      if (i0 == c0) {
+        // ---- factor the diagonal block in shared memory (right-looking, unblocked)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Lp[rr][cb + b] = acc[b];
+        __syncthreads();
+        for (int j = 0; j < w; ++j) {
+          const double d = Lp[j][j].x;
+          const bool ok = d > tau;
+          const double il = ok ? rsqrt(d) : 0.0;
+          __syncthreads();
+          if (tid >= j && tid < w) {                 // column j: scale (rows >= j)
+            const int i = tid;
+            if (i == j) Lp[j][j] = make_double2(ok ? d * il : 0.0, 0.0);
+            else Lp[i][j] = make_double2(Lp[i][j].x * il, Lp[i][j].y * il);
+          }
+          __syncthreads();
+          // trailing update: Lp[i][k] -= Lp[i][j] conj(Lp[k][j]), j < k <= i < w
+          for (int x = tid; x < 32 * 32; x += 256) {
+            const int i = x >> 5, k = x & 31;
+            if (k > j && k <= i && i < w) {
+              const double2 a = Lp[i][j], q = Lp[k][j];
+              Lp[i][k].x -= a.x * q.x + a.y * q.y;
+              Lp[i][k].y -= a.y * q.x - a.x * q.y;
+            }
+          }
+          __syncthreads();
+        }
+        // ---- inverse of the lower-triangular L_JJ, column by column (thread j < w owns column j)
+        if (tid < 32) {
+          const int j = tid;
+          for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
+          if (j < w && Lp[j][j].x > 0.0) {
+            Mi[j][j] = make_double2(1.0 / Lp[j][j].x, 0.0);
+            for (int i = j + 1; i < w; ++i) {
+              double2 s = make_double2(0.0, 0.0);
+              for (int k = j; k < i; ++k) {      // s += L[i][k] M[k][j]
+                const double2 a = Lp[i][k], q = Mi[k][j];
+                s.x += a.x * q.x - a.y * q.y;
+                s.y += a.x * q.y + a.y * q.x;
+              }
+              const double li = Lp[i][i].x;
+              Mi[i][j] = li > 0.0 ? make_double2(-s.x / li, -s.y / li) : make_double2(0.0, 0.0);
+            }
+          }
+        }
+        __syncthreads();
+        // ---- write L_JJ (lower part) back
+        for (int x = tid; x < 32 * 32; x += 256) {
+          const int i = x >> 5, j = x & 31;
+          if (i < w && j <= i) G[(int64_t)(c0 + j) * n + c0 + i] = Lp[i][j];
+        }
+      } else {
+        // ---- X = T (L_JJ^-1)^H: x_j = sum_{k <= j} t_k conj(M[j][k])
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Tt[rr][cb + b] = acc[b];
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = cb + b;
+          double2 x = make_double2(0.0, 0.0);
+          for (int k = 0; k <= j && k < w; ++k) {
+            const double2 tk = Tt[rr][k], q = Mi[j][k];
+            x.x += tk.x * q.x + tk.y * q.y;
+            x.y += tk.y * q.x - tk.x * q.y;
+          }
+          const int i = i0 + rr;
+          if (i < n && j < w) G[(int64_t)(c0 + j) * n + i] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// B = L in FP32 (n x n_pad, ld n): the lower triangle of L, zeros above it and in the pad columns
+__global__ void k_pc_b_from_l(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.y]];
+  if (gd.jrows <= 0) return;
+  const int n = gd.n, np = gd.n_pad;
+  const double2* G = reinterpret_cast<const double2*>(slab + gd.ws_log);
+  float2* B = reinterpret_cast<float2*>(slab + gd.ws_theta);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < (int64_t)n * np;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(x / n), i = (int)(x % n);
+    float2 v = make_float2(0.f, 0.f);
+    if (j < n && i >= j) {
+      const double2 g = G[(int64_t)j * n + i];
+      v = make_float2((float)g.x, (float)g.y);
+    }
+    B[x] = v;
+  }
+}
+
+// V[:, j] = b_j / |b_j| (FP64 norm) for j < n, rows n .. n_pad and columns n .. n_pad zero
+__global__ void k_pc_vnorm(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.y]];
+  if (gd.jrows <= 0) return;
+  const int n = gd.n, np = gd.n_pad;
+  const float2* B = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+  float2* V = reinterpret_cast<float2*>(slab + gd.ws_V);
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= np) return;
+  double a = 0.0;
+  if (j < n)
+    for (int i = lane; i < n; i += 32) a += (double)B[(int64_t)j * n + i].x * B[(int64_t)j * n + i].x +
+                                            (double)B[(int64_t)j * n + i].y * B[(int64_t)j * n + i].y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  const float sc = a > 0.0 ? (float)(1.0 / sqrt(a)) : 0.f;
+  for (int i = lane; i < np; i += 32) {
+    const float2 b = (j < n && i < n) ? B[(int64_t)j * n + i] : make_float2(0.f, 0.f);
+    V[(int64_t)j * np + i] = make_float2(b.x * sc, b.y * sc);
+  }
+}
+
+}  // namespace
+
+bool large_precond_enabled() {
+  static const bool off = getenv("EAMPS_NO_LARGE_PRECOND") != nullptr || getenv("EAMPS_LARGE_SIMT") != nullptr;
+  return !off;
+}
+
+size_t large_precond_scratch(int n) { return (size_t)16 * n * n; }
+
+int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s) {
+  if (count <= 0) return 0;
+  const int T = (max_n + 63) / 64;
+  k_pc_gram<<<dim3(T * (T + 1) / 2, count), 256, 0, s>>>(d_desc, d_list, slab);
+  constexpr int kCholSmem = (2 * 32 * 33 + 2 * 32 * 17) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pc_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
+    attr = true;
+  }
+  k_pc_chol<<<count, 256, kCholSmem, s>>>(d_desc, d_list, slab);
+  k_pc_b_from_l<<<dim3(64, count), 256, 0, s>>>(d_desc, d_list, slab);
+  return 3;
+}
+
+int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab, cudaStream_t s) {
+  if (count <= 0) return 0;
+  k_pc_vnorm<<<dim3((max_np + 7) / 8, count), 256, 0, s>>>(d_desc, d_list, slab);
+  return 1;
+}
+
+}  // namespace eamps

@@ -45,6 +45,7 @@ struct LargeCtl {               // per gate in the large list
 
 __global__ void k_large_init(GateDesc* desc, const int32_t* list, uint8_t* slab) {
   GateDesc& gd = desc[list[blockIdx.y]];
+  if (gd.jrows > 0) return;   // preconditioned: B (with its zero pad columns) and V written elsewhere
   const int m = gd.m, n = gd.n, np = gd.n_pad;
   float2* th = reinterpret_cast<float2*>(slab + gd.ws_theta);
   float2* V = reinterpret_cast<float2*>(slab + gd.ws_V);
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(128) k_tc_gram(const GateDesc* __restrict__ de
   __shared__ uint32_t tbase;
   tc_setup(mbar, &tbase);
   float* Ds = reinterpret_cast<float*>(base);
-  gram_panel(reinterpret_cast<const float2*>(slab + gd.ws_theta), gd.m, gd.n_pad, I, J, base, mbar, tbase, Ds);
+  gram_panel(reinterpret_cast<const float2*>(slab + gd.ws_theta), jacobi_rows(gd), gd.n_pad, I, J, base, mbar, tbase, Ds);
   if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(tbase, 128);
   float2* Gout = reinterpret_cast<float2*>(slab + gd.ws_log) + (size_t)pair * 64 * 64;
   auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
   }
   __syncthreads();
   const float skip = (float)(norm2[gi] * 3.552713678800501e-15);  // (2^-24)^2 ||theta||^2
-  const float tol = fmaxf(tol_floor, 4.f * sqrtf((float)gd.m) * 5.960464477539063e-8f);
+  const float tol = fmaxf(tol_floor, 4.f * sqrtf((float)jacobi_rows(gd)) * 5.960464477539063e-8f);
   const float tol_int = fmaxf(tol, tol_internal);
   int any = 0, internal = 0;
   for (int x = tid; x < 64 * 64; x += kInnerT) {
@@ -795,8 +796,8 @@ __global__ void __launch_bounds__(256) k_tc_rot(const GateDesc* __restrict__ des
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5, row_l = tid & 127, half = tid >> 7;
-  const int m = gd.m, np = gd.n_pad;
-  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128, ntiles = tiles_th + tiles_v;
+  const int m = jacobi_rows(gd), np = gd.n_pad;   // preconditioned: B (n rows), no V tiles
+  const int tiles_th = (m + 127) / 128, tiles_v = gd.jrows > 0 ? 0 : (np + 127) / 128, ntiles = tiles_th + tiles_v;
   for (int x = tid; x < EIMG_FLOATS / 4; x += 256) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
   auto issue_tile = [&](int tile) {
     if (tile < ntiles) {
@@ -966,8 +967,8 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tbase;
-  const int m = gd.m, np = gd.n_pad;
-  const int tiles_th = (m + 127) / 128, tiles_v = (np + 127) / 128, ntiles = tiles_th + tiles_v;
+  const int m = jacobi_rows(gd), np = gd.n_pad;   // preconditioned: B (n rows), no V tiles
+  const int tiles_th = (m + 127) / 128, tiles_v = gd.jrows > 0 ? 0 : (np + 127) / 128, ntiles = tiles_th + tiles_v;
   constexpr int CH = PWC / 8;                                     // chunks per tile
   if (warp == 0) {
     // ---------------- MMA issuer
@@ -1263,6 +1264,9 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   k_large_init<<<dim3(256, count), 256, 0, s>>>(d_desc, d_list, slab);
   k_large_norm<<<count, 256, 0, s>>>(d_desc, d_list, slab, norm2);
   launches += 2;
+  bool any_pc = false;
+  for (int g = 0; g < count; ++g) any_pc |= h_desc[h_list[g]].jrows > 0;
+  if (any_pc) launches += launch_precond_large(d_desc, d_list, count, max_n, slab, s);   // after the norm
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
@@ -1318,6 +1322,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
   }
   if (!done) *error_out = -6;
+  if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, s);
   launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
   return launches;
 }
