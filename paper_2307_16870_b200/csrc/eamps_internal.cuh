@@ -132,7 +132,8 @@ size_t svd_tc_scratch_bytes(int n_pad);
 bool large_precond_enabled();
 size_t large_precond_scratch(int n);
 int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s);
-int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab, cudaStream_t s);
+int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab,
+                         const double* norm2, cudaStream_t s);
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_counters, int32_t* h_pinned_flag,
                cudaStream_t s, int* error_out);

@@ -241,7 +241,10 @@ __global__ void k_pc_b_from_l(const GateDesc* __restrict__ desc, const int32_t* 
 }
 
 // V[:, j] = b_j / |b_j| (FP64 norm) for j < n, rows n .. n_pad and columns n .. n_pad zero
-__global__ void k_pc_vnorm(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab) {
+// A column at or below the Jacobi's rounding floor (|b_j|^2 <= (2^-24 |theta|_F)^2) was never rotated,
+// so its direction is not orthogonal to the others: it carries no singular value (v_j = 0).
+__global__ void k_pc_vnorm(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab,
+                           const double* __restrict__ norm2) {
   const GateDesc& gd = desc[list[blockIdx.y]];
   if (gd.jrows <= 0) return;
   const int n = gd.n, np = gd.n_pad;
@@ -256,7 +259,7 @@ __global__ void k_pc_vnorm(const GateDesc* __restrict__ desc, const int32_t* __r
                                             (double)B[(int64_t)j * n + i].y * B[(int64_t)j * n + i].y;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  const float sc = a > 0.0 ? (float)(1.0 / sqrt(a)) : 0.f;
+  const float sc = a > norm2[blockIdx.y] * 3.552713678800501e-15 ? (float)(1.0 / sqrt(a)) : 0.f;
   for (int i = lane; i < np; i += 32) {
     const float2 b = (j < n && i < n) ? B[(int64_t)j * n + i] : make_float2(0.f, 0.f);
     V[(int64_t)j * np + i] = make_float2(b.x * sc, b.y * sc);
@@ -287,9 +290,10 @@ int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int
   return 3;
 }
 
-int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab, cudaStream_t s) {
+int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab,
+                         const double* norm2, cudaStream_t s) {
   if (count <= 0) return 0;
-  k_pc_vnorm<<<dim3((max_np + 7) / 8, count), 256, 0, s>>>(d_desc, d_list, slab);
+  k_pc_vnorm<<<dim3((max_np + 7) / 8, count), 256, 0, s>>>(d_desc, d_list, slab, norm2);
   return 1;
 }
 

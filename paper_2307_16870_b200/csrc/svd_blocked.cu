@@ -1155,6 +1155,7 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
           // contaminations (a fourth-order coupling over a small gap) that the pairwise formula
           // would turn into a spurious shift; their own mixing moves sigma^2 by at most ~tol.
           if (fmax(aj, al_) < 4.0 * fmin(aj, al_)) continue;
+          if (!(dj > 0.0) || !(den[cl] > 0.0)) continue;   // a zero column (rank-deficient theta)
           const double g2 = (gr * gr + gim * gim) / (dj * den[cl]);
           const double dlt = aj - al_;
           const double h = 0.5 * fabs(dlt);
@@ -1322,7 +1323,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
   }
   if (!done) *error_out = -6;
-  if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, s);
+  if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);
   launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
   return launches;
 }

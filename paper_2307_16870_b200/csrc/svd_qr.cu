@@ -579,7 +579,9 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
     double a = 0.0;
     for (int i = lane; i < n; i += 32) a += (double)bj[i].x * bj[i].x + (double)bj[i].y * bj[i].y;
     a = warp_sum_d32(a);
-    const float sc = a > 0.0 ? (float)(1.0 / sqrt(a)) : 0.f;
+    // a column at or below the rounding floor was never rotated (the Jacobi skips it), so its
+    // direction is not orthogonal to the others: it carries no singular value (v_j = 0, sigma_j = 0)
+    const float sc = a > (double)skip ? (float)(1.0 / sqrt(a)) : 0.f;
     for (int i = lane; i < n; i += 32) {
       const float2 v = make_float2(bj[i].x * sc, bj[i].y * sc);
       bj[i] = v;

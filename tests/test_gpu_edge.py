@@ -1,6 +1,7 @@
 """GPU edge cases against the oracle (same seeded inputs, the north-star bars of test_gpu_parity):
 ragged and rectangular thetas in every SVD regime (small, QR-preconditioned, medium with m < n,
-tcgen05 large regime with column padding, m < n and m >> n), an empty layer, product gates
+tcgen05 large regime with column padding, m < n and m >> n, the R-preconditioned large regime with
+a rank-deficient theta), an empty layer, product gates
 (rank-1 updates), the bond cap (capped truncations, guarantee lost) and the
 non-convergence error path."""
 import numpy as np
@@ -54,11 +55,14 @@ def _run_pair(shapes, f=0.9999, chi_cap=0):
     ((5, 9, 7), "small (ragged, m < n)"),
     ((49, 35, 53), "small, m = 98 < n = 106 (2048 / n not a power of two; config 5 layer 7)"),
     ((48, 40, 37), "QR (n = 74, partially active warps)"),
+    ((48, 10, 40), "QR circle path, rank <= 40 < n = 80 (tiny columns get v = 0)"),
+    ((64, 12, 64), "QR block-recursive path, rank <= 48 < n = 128"),
     ((32, 40, 72), "medium (m = 64 < n = 144)"),
     ((40, 64, 80), "large tcgen05, m = 80 < n = 160"),
     ((70, 90, 100), "large tcgen05 (n = 200 -> n_pad 256)"),
     ((64, 100, 150), "large, m = 128 < n = 300"),
-    ((200, 120, 70), "large, m = 400 >> n = 140"),
+    ((200, 120, 70), "large, m = 400 >> n = 140 (R-preconditioned: Gram + Cholesky, B = L)"),
+    ((100, 20, 90), "large, R-preconditioned, rank <= 80 < n = 180 (zero Cholesky pivots)"),
 ])
 def test_ragged_regimes_parity(shape, regime):
     gpu, orc, G = _run_pair([shape])
@@ -69,7 +73,7 @@ def test_ragged_regimes_parity(shape, regime):
 
 def test_mixed_wave_all_regimes():
     """one layer whose gates fall into every regime at once (bucketing, one wave)."""
-    shapes = [(5, 9, 7), (48, 40, 37), (40, 64, 80), (70, 90, 100), (3, 4, 2), (33, 20, 31)]
+    shapes = [(5, 9, 7), (48, 40, 37), (40, 64, 80), (70, 90, 100), (3, 4, 2), (33, 20, 31), (100, 20, 90)]
     gpu, orc, G = _run_pair(shapes)
     worst, same = compare_layer(gpu, orc, G)
     assert same and worst < SIG_RTOL, worst
