@@ -30,7 +30,7 @@ __device__ __forceinline__ double2 cmul_conj_acc(double2 acc, double2 a, double2
 
 // G[i][j] = sum_r conj(theta[r][i]) theta[r][j] for the 64 x 64 tiles with ti >= tj (the lower
 // triangle the Cholesky reads). theta: ws_theta (FP32, ld m); G: ws_log (FP64 complex, ld n).
-__global__ void __launch_bounds__(256) k_pc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(256, 2) k_pc_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                  uint8_t* slab) {
   const GateDesc& gd = desc[list[blockIdx.y]];
   if (gd.jrows <= 0) return;
