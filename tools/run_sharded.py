@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--cap", type=int, default=4096)
     ap.add_argument("--full-depth", type=int, default=75, help="n_planned is the full circuit's gate count")
     ap.add_argument("--slab-gb", type=float, default=0.0)
+    ap.add_argument("--progress", action="store_true", help="per-layer time and bond dimension (rank 0)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -48,8 +49,18 @@ def main():
     layers = workloads.brickwork_circuit(5, N, args.depth)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for sites, us in layers:
+    nrec = 0
+    for li, (sites, us) in enumerate(layers):
+        tl = time.perf_counter()
         sh.apply_layer(sites, us)
+        if args.progress:
+            torch.cuda.synchronize()
+            recs = sh.records()
+            chi = max((r["chi_after"] for r in recs[nrec:]), default=0)
+            nrec = len(recs)
+            if sh.rank == 0:
+                print("layer %d: %d gates, %.2f s, max chi_after (this rank) %d" % (li, len(sites), time.perf_counter() - tl, chi),
+                      flush=True)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     led = sh.ledger()
