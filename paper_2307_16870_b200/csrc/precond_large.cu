@@ -64,9 +64,9 @@ __global__ void __launch_bounds__(256, 2) k_pc_gram(const GateDesc* __restrict__
     for (int k = 0; k < 16; ++k) {
       double2 xi[4], yj[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) xi[a] = Ai[k][ty * 4 + a];
+      for (int a = 0; a < 4; ++a) xi[a] = Ai[k][ty + 16 * a];   // 2 addresses per warp (broadcast)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) yj[b] = Aj[k][tx * 4 + b];
+      for (int b = 0; b < 4; ++b) yj[b] = Aj[k][tx + 16 * b];   // consecutive: no bank conflicts
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256, 2) k_pc_gram(const GateDesc* __restrict__
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int i = ti * 64 + ty * 4 + a, j = tj * 64 + tx * 4 + b;
+      const int i = ti * 64 + ty + 16 * a, j = tj * 64 + tx + 16 * b;
       if (i < n && j < n) G[(int64_t)j * n + i] = acc[a][b];
     }
 }
