@@ -627,6 +627,13 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
   extern __shared__ __align__(16) uint8_t dsm[];
   float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(dsm);
   float2(*Ws)[65] = Gs + 64;
+  // G is Hermitian: only its upper triangle is kept current; (i, j) with i > j reads / writes the
+  // conjugate at (j, i) (no mirror stores: a third of the shared-memory stores of a round)
+  auto gld = [&](int i, int j) {
+    const float2 v = Gs[min(i, j)][max(i, j)];
+    return i <= j ? v : make_float2(v.x, -v.y);
+  };
+  auto gst = [&](int i, int j, float2 v) { Gs[min(i, j)][max(i, j)] = i <= j ? v : make_float2(v.x, -v.y); };
   const int tid = threadIdx.x;
   for (int x = tid; x < 64 * 64; x += kInnerT) {
     const int a = x >> 6, b = x & 63;
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
   // in the I x J block and an inner sweep only needs the 32 x 32 cross pairs
   // (p = i, q = 32 + (i + rr) mod 32): 32 rounds. Otherwise the full 64-column tournament (63).
   // A round: (A) each of the 32 pairs computes its rotation J_k from its 2x2 diagonal block;
-  // (B) every 2x2 block (pair a rows, pair b cols), a <= b, becomes J_a^H X J_b and is mirrored
+  // (B) every 2x2 block (pair a rows, pair b cols), a < b, becomes J_a^H X J_b in the upper triangle
   // (G Hermitian: half the work of separate column and row passes, one barrier fewer), and
   // W <- W J (columns p_k, q_k).
   __shared__ float4 par[32];      // c, s, er, ei
@@ -688,7 +695,7 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
           q = 32 + ((tid + rr) & 31);
         }
         const float al = Gs[p][p].x, be = Gs[q][q].x;
-        const float2 gm = Gs[p][q];
+        const float2 gm = gld(p, q);
         const float g2 = gm.x * gm.x + gm.y * gm.y;
         float c = 1.f, sn = 0.f, er = 1.f, ei = 0.f;
         if (fminf(al, be) > skip && g2 > 1e-13f * al * be) {
@@ -705,8 +712,7 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
           const float tg = t * (g2 * ig);
           Gs[p][p] = make_float2(al - tg, 0.f);
           Gs[q][q] = make_float2(be + tg, 0.f);
-          Gs[p][q] = make_float2(0.f, 0.f);
-          Gs[q][p] = make_float2(0.f, 0.f);
+          gst(p, q, make_float2(0.f, 0.f));
         }
         par[tid] = make_float4(c, sn, er, ei);
         pq[tid] = make_int2(p, q);
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
         const float4 Ja = par[ia], Jb = par[ib];
         if (Ja.y == 0.f && Jb.y == 0.f) continue;
         const int2 ra = pq[ia], cb = pq[ib];
-        float2 X[2][2] = {{Gs[ra.x][cb.x], Gs[ra.x][cb.y]}, {Gs[ra.y][cb.x], Gs[ra.y][cb.y]}};
+        float2 X[2][2] = {{gld(ra.x, cb.x), gld(ra.x, cb.y)}, {gld(ra.y, cb.x), gld(ra.y, cb.y)}};
         if (Jb.y != 0.f) {   // columns: (x, y) -> (c x - s conj(e) y, s x + c conj(e) y)
           const Rot rb{Jb.x, Jb.y, Jb.z, Jb.w};
 #pragma unroll
@@ -728,11 +734,8 @@ __global__ void __launch_bounds__(kInnerT) k_tc_inner(const GateDesc* __restrict
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) apply_rot(X[0][cc], X[1][cc], ra);
         }
-        Gs[ra.x][cb.x] = X[0][0]; Gs[ra.x][cb.y] = X[0][1];
-        Gs[ra.y][cb.x] = X[1][0]; Gs[ra.y][cb.y] = X[1][1];
-        // Hermitian mirror
-        Gs[cb.x][ra.x] = make_float2(X[0][0].x, -X[0][0].y); Gs[cb.y][ra.x] = make_float2(X[0][1].x, -X[0][1].y);
-        Gs[cb.x][ra.y] = make_float2(X[1][0].x, -X[1][0].y); Gs[cb.y][ra.y] = make_float2(X[1][1].x, -X[1][1].y);
+        gst(ra.x, cb.x, X[0][0]); gst(ra.x, cb.y, X[0][1]);
+        gst(ra.y, cb.x, X[1][0]); gst(ra.y, cb.y, X[1][1]);
       }
       {   // W <- W J for every pair: thread (pair k = tid / (T/32), rows tid % (T/32) + (T/32) i)
         const int k = tid / (kInnerT / 32);
