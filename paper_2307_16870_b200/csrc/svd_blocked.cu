@@ -1280,7 +1280,6 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     attr = true;
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
-  const dim3 grid(pairs_max, count);
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
   static const bool rot_simple = getenv("EAMPS_ROT_SIMPLE") != nullptr;   // dev A/B switch
   static const float tol_floor = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
@@ -1288,33 +1287,62 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   // sits in exactly one round-0 panel); the other rounds rotate the 32 x 32 cross pairs only.
   // Measured: chi = 256 inner solve -35%, chi = 1024 -35% with 0.8 fewer sweeps; sigma unchanged.
   static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 3.0e38f;
+  // The gates are split over two streams: one group's SIMT inner solves run beside the other
+  // group's HBM-bound rotations and tensor-core Grams (the three launches of a round depend on
+  // each other only within a gate). EAMPS_TC_STREAMS=1: one stream (dev A/B).
+  static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
+  static const int nstreams = getenv("EAMPS_TC_STREAMS") ? atoi(getenv("EAMPS_TC_STREAMS")) : 2;
+  // (only for small round grids: measured chi = 1024 x 16 gates, 512 CTAs a round: -8.5%;
+  // chi = 256 x 1024 gates, 8192 CTAs a round: +2%)
+  const int ngroups = (!prof && nstreams >= 2 && count >= 2 && count * pairs_max < 2048) ? 2 : 1;
+  const int gsplit[3] = {0, ngroups == 2 ? count / 2 : count, count};
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_go = nullptr, ev_done = nullptr;
+  if (ngroups == 2) {
+    cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ev_go, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    cudaEventRecord(ev_go, s);              // the preconditioner / init / norms are done
+    cudaStreamWaitEvent(s2, ev_go, 0);
+  }
   int sweep = 0;
   bool done = false;
   for (; sweep < max_sweeps && !done; ++sweep) {
-    static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
     static cudaEvent_t ev[4];
     static double acc[3] = {0, 0, 0};
     if (prof && !ev[0])
       for (int e = 0; e < 4; ++e) cudaEventCreate(&ev[e]);
     for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
-      if (prof) cudaEventRecord(ev[0], s);
-      tcj::k_tc_gram<<<grid, 128, tcj::kGramSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
-      if (prof) cudaEventRecord(ev[1], s);
-      tcj::k_tc_inner<<<grid, tcj::kInnerT, tcj::kInnerSmem, s>>>(d_desc, d_list, rnd, slab, ctl, norm2, inner_sweeps, tol_floor,
-                                                         tol_internal);
-      if (prof) cudaEventRecord(ev[2], s);
-      if (rot_simple) tcj::k_tc_rot<<<grid, 256, tcj::kRotSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
-      else tcj::k_tc_rot_ws<<<grid, 288, tcj::kRotWsSmem, s>>>(d_desc, d_list, rnd, slab, ctl);
-      if (prof) {
-        cudaEventRecord(ev[3], s);
-        cudaEventSynchronize(ev[3]);
-        for (int e = 0; e < 3; ++e) {
-          float ms = 0.f;
-          cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
-          acc[e] += ms;
+      for (int gg = 0; gg < ngroups; ++gg) {
+        const int g0 = gsplit[gg], gc = gsplit[gg + 1] - g0;
+        if (gc <= 0) continue;
+        cudaStream_t ss = gg == 0 ? s : s2;
+        const dim3 gridg(pairs_max, gc);
+        const int32_t* dl = d_list + g0;
+        LargeCtl* cg = ctl + g0;
+        if (prof) cudaEventRecord(ev[0], ss);
+        tcj::k_tc_gram<<<gridg, 128, tcj::kGramSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+        if (prof) cudaEventRecord(ev[1], ss);
+        tcj::k_tc_inner<<<gridg, tcj::kInnerT, tcj::kInnerSmem, ss>>>(d_desc, dl, rnd, slab, cg, norm2 + g0, inner_sweeps,
+                                                                     tol_floor, tol_internal);
+        if (prof) cudaEventRecord(ev[2], ss);
+        if (rot_simple) tcj::k_tc_rot<<<gridg, 256, tcj::kRotSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+        else tcj::k_tc_rot_ws<<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+        if (prof) {
+          cudaEventRecord(ev[3], ss);
+          cudaEventSynchronize(ev[3]);
+          for (int e = 0; e < 3; ++e) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
+            acc[e] += ms;
+          }
         }
+        launches += 3;
       }
-      launches += 3;
+    }
+    if (ngroups == 2) {                     // the second group's round work, before the check
+      cudaEventRecord(ev_done, s2);
+      cudaStreamWaitEvent(s, ev_done, 0);
     }
     if (prof) fprintf(stderr, "[tc prof] cumulative ms: gram %.1f inner %.1f rot %.1f\n", acc[0], acc[1], acc[2]);
     k_block_check<<<1, 256, 0, s>>>(d_desc, d_list, count, ctl, unconv, 0);
@@ -1324,6 +1352,11 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     done = (h_pinned_flag[0] == 0);
     static const bool dbg = getenv("EAMPS_TC_DEBUG") != nullptr;
     if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
+  }
+  if (ngroups == 2) {
+    cudaEventDestroy(ev_go);
+    cudaEventDestroy(ev_done);
+    cudaStreamDestroy(s2);                  // (its work is complete: the last check synchronised s)
   }
   if (!done) *error_out = -6;
   if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);
