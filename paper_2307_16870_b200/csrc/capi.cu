@@ -321,7 +321,7 @@ mps_status wave_front(mps_t h) {
     LayerPlan& p = plan[g0 + x];
     GateDesc gd = p.gd;
     gd.u_index = x;
-    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)std::max(gd.m, gd.jrows) * gd.n_pad * 8;   // B = L (jrows rows) reuses it
     gd.ws_theta = (int64_t)take(mnp);
     gd.ws_thetap = (int64_t)take(mn);
     gd.ws_V = (int64_t)take((size_t)gd.n_pad * gd.n_pad * 8);
@@ -783,13 +783,14 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
     gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
     // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)
-    // large regime with m >= n: the R-preconditioner (FP64 Gram + Cholesky, Jacobi on B = L with n
-    // rows, no V accumulation); its FP64 Gram shares the tensor-core scratch (dead until the sweeps)
-    gd.jrows = (gd.regime == 1 && gd.m >= gd.n && large_precond_enabled()) ? gd.n : 0;
+    // large regime: the R-preconditioner (FP64 Gram + Cholesky, Jacobi on B = L with n rows, no V
+    // accumulation; for m < n the Gram has rank <= m and B gets zero columns); its FP64 Gram shares
+    // the tensor-core scratch (dead until the sweeps)
+    gd.jrows = (gd.regime == 1 && (gd.m >= gd.n || large_precond_wide()) && large_precond_enabled()) ? gd.n : 0;
     const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                                        : (gd.regime == 1 ? large_scratch_bytes(gd) : 0);
     gd.u_index = ord[g].second;
-    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)gd.m * gd.n_pad * 8;
+    const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)std::max(gd.m, gd.jrows) * gd.n_pad * 8;   // B = L (jrows rows) reuses it
     const int kmn = std::min(gd.m, gd.n);
     p.ws = align_up(mnp) + align_up(mn) + align_up((size_t)gd.n_pad * gd.n_pad * 8) + align_up((size_t)gd.n_pad * 8) +
            align_up((size_t)(gd.n_pad + 1) * 8) + align_up((size_t)gd.n_pad * 4) +

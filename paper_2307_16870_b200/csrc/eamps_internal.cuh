@@ -130,6 +130,7 @@ int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_l
 size_t svd_tc_scratch_bytes(int n_pad);
 // large-regime R-preconditioner (precond_large.cu): FP64 Gram + Cholesky -> B = L, no V accumulation
 bool large_precond_enabled();
+bool large_precond_wide();
 size_t large_precond_scratch(int n);
 int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s);
 int launch_precond_vnorm(GateDesc* d_desc, const int32_t* d_list, int count, int max_np, uint8_t* slab,

@@ -298,6 +298,14 @@ bool large_precond_enabled() {
   return !off;
 }
 
+// m < n (wide theta): G = theta^H theta is n x n of rank <= m; the Cholesky zeroes the dependent
+// pivots and the Jacobi runs on B = L (n x n) whose zero columns carry sigma = 0 -- still no V and
+// fewer rows per rotation than the V-accumulating path (m + n). EAMPS_NO_WIDE_PRECOND=1: off (A/B).
+bool large_precond_wide() {
+  static const bool off = getenv("EAMPS_NO_WIDE_PRECOND") != nullptr;
+  return !off;
+}
+
 size_t large_precond_scratch(int n) { return (size_t)16 * n * n + sizeof(CholScratch); }
 
 int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s) {
