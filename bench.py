@@ -350,6 +350,8 @@ def main():
         host = torch.empty(inter.numel(), dtype=torch.complex64, pin_memory=True)
         host.copy_(inter.cpu())
         reps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
         t_e2e = 0.0
         for rep in range(reps + 1):
             torch.cuda.synchronize()
@@ -361,6 +363,8 @@ def main():
             if rep > 0:
                 t_e2e += time.perf_counter() - t0
         assert len(recs) == G
+        if world > 1:   # the slowest rank defines the end-to-end step too
+            t_e2e = max_over_ranks(t_e2e, dev)
         line["e2e"] = {"value": world * G / (t_e2e / reps), "unit": UNIT,
                        "h2d_bytes_per_step": int(site_bytes + gates.nbytes),
                        "d2h_bytes_per_step": int(G * (48 + 160) + 512)}
