@@ -63,6 +63,7 @@ def _run_pair(shapes, f=0.9999, chi_cap=0):
     ((64, 100, 150), "large, m = 128 < n = 300"),
     ((200, 120, 70), "large, m = 400 >> n = 140 (R-preconditioned: Gram + Cholesky, B = L)"),
     ((100, 20, 90), "large, R-preconditioned, rank <= 80 < n = 180 (zero Cholesky pivots)"),
+    ((100, 20, 120), "large, wide (m = 200 < n = 240) preconditioned, rank <= 80"),
 ])
 def test_ragged_regimes_parity(shape, regime):
     gpu, orc, G = _run_pair([shape])
