@@ -333,6 +333,7 @@ mps_status wave_front(mps_t h) {
     gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, (gd.regime == 1 || gd.regime == 3) ? (size_t)16 * gd.n_pad : (size_t)0));
     gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
                 : gd.regime == 1 ? (int64_t)take(large_scratch_bytes(gd))
+                : (gd.regime == 3 && gd.jrows > 0) ? (int64_t)take(large_precond_scratch(gd.n))
                                  : 0;
     hd[x] = gd;
     cpre[x + 1] = cpre[x] + p.ctiles;
@@ -457,10 +458,17 @@ mps_status wave_front(mps_t h) {
   // a2 + a3 SVD, small regime: one CTA per theta
   for (const Bucket& b : buckets) {
     if (b.regime == 3) {
+      int maxn = 0;
+      bool pc = false;
+      for (int i = b.begin; i < b.end; ++i) {
+        maxn = std::max(maxn, hd[small[i]].n);
+        pc |= hd[small[i]].jrows > 0;
+      }
+      // Cholesky preconditioner (FP64 Gram + Cholesky -> B = L in the theta workspace) instead of
+      // the in-CTA FP32 Householder QR
+      if (pc) h->launches += launch_precond_large(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->s);
       launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.tile_rows,
                     h->slab, h->dst, h->s);
-      int maxn = 0;
-      for (int i = b.begin; i < b.end; ++i) maxn = std::max(maxn, hd[small[i]].n);
       h->launches += 1 + launch_spectrum_polish(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->dst, h->s);
     } else if (b.regime == 0) {
       launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.threads,
@@ -787,8 +795,14 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // accumulation; for m < n the Gram has rank <= m and B gets zero columns); its FP64 Gram shares
     // the tensor-core scratch (dead until the sweeps)
     gd.jrows = (gd.regime == 1 && (gd.m >= gd.n || large_precond_wide()) && large_precond_enabled()) ? gd.n : 0;
-    const size_t logb = gd.regime == 2 ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
-                                       : (gd.regime == 1 ? large_scratch_bytes(gd) : 0);
+    // QR regime, block-recursive kernels: B = L from the FP64 Gram + Cholesky (EAMPS_QR_HOUSEHOLDER=1:
+    // the in-CTA Householder QR instead)
+    static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
+    if (gd.regime == 3 && !qr_hh && qr_block_order(gd.m, gd.n)) gd.jrows = gd.n;
+    const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
+                        : gd.regime == 1 ? large_scratch_bytes(gd)
+                        : (gd.regime == 3 && gd.jrows > 0) ? large_precond_scratch(gd.n)
+                                         : 0;
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)std::max(gd.m, gd.jrows) * gd.n_pad * 8;   // B = L (jrows rows) reuses it
     const int kmn = std::min(gd.m, gd.n);

@@ -203,6 +203,30 @@ __device__ __forceinline__ void pl_set(float2* A, int m, int c, int r, float2 v)
   f[2] = v.y;
 }
 
+// B = L (n x n lower, ld n, FP32 interleaved) written by the Cholesky preconditioner
+// (precond_large.cu: G = theta^H theta = L L^H in FP64) -> the CTA's pair-planar A (ld m; rows >= n
+// are not read by the Jacobi). Returns |B|_F^2 = tr G = |theta|_F^2.
+template <int NT>
+__device__ float load_b_planar(const float2* __restrict__ Bg, float2* A, int m, int n, float* s_wn) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nh = n / 2;
+  const float4* b4 = reinterpret_cast<const float4*>(Bg);
+  float nrm = 0.f;
+  for (int x = tid; x < n * nh; x += NT) {
+    const int c = x / nh, p = x % nh;
+    const float4 t = b4[(size_t)c * nh + p];        // (Re 2p, Im 2p, Re 2p+1, Im 2p+1) of column c
+    reinterpret_cast<float4*>(A + (size_t)c * m)[p] = make_float4(t.x, t.z, t.y, t.w);
+    nrm = fmaf(t.x, t.x, fmaf(t.y, t.y, fmaf(t.z, t.z, fmaf(t.w, t.w, nrm))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+  if (lane == 0) s_wn[warp] = nrm;
+  __syncthreads();
+  float norm2 = 0.f;
+  for (int w = 0; w < NT / 32; ++w) norm2 += s_wn[w];
+  return norm2;
+}
+
 // Householder QR of theta (m x n, m >= n, m even) in shared memory, PAIR-PLANAR: theta is loaded
 // as row pairs (Re 2p, Re 2p+1, Im 2p, Im 2p+1), so every dot product and rank-1 update below is a
 // packed FP32x2 instruction on two rows (half the instructions of the interleaved version), then
@@ -372,7 +396,8 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
   float norm2 = 0.f;
   if constexpr (PK == 2) {
     // pair-planar Householder QR and B = R^H (householder_planar): packed FP32x2 row pairs
-    norm2 = householder_planar<NT>(gth, A, m, n, s_rdiag, s_wn, s_xn2, s_x0);
+    if (gd.jrows > 0) norm2 = load_b_planar<NT>(reinterpret_cast<const float2*>(slab + gd.ws_theta), A, m, n, s_wn);
+    else norm2 = householder_planar<NT>(gth, A, m, n, s_rdiag, s_wn, s_xn2, s_x0);
   } else {
     float nrm = 0.f;
     for (int x = tid; x < m * n; x += NT) {
