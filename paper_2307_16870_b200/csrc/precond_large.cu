@@ -246,6 +246,145 @@ __global__ void __launch_bounds__(256) k_pc_chol_panel(const GateDesc* __restric
   }
 }
 
+// Small n (<= 128, the QR regime): the whole blocked Cholesky in one CTA per gate (4096 gates give
+// the parallelism; no per-panel launches). In-place left-looking G = L L^H (lower), panels of 32
+// columns: (1) every 32-row block of the panel gets G[i][panel] -= L[i][0:c0] L[panel][0:c0]^H;
+// (2) the diagonal block is factored in shared memory (pivots <= tau -> zero column) and inverted;
+// (3) the blocks below become X = G_blk L_JJ^-H = G_blk (L_JJ^-1)^H (a small GEMM, no serial solve).
+__global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                 uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.x]];
+  if (gd.jrows <= 0) return;
+  const int n = gd.n;
+  double2* G = reinterpret_cast<double2*>(slab + gd.ws_log);
+  struct Smem {
+    double2 Lp[32][33];   // factored diagonal block L_JJ; later the row block being solved
+    double2 Mi[32][33];   // L_JJ^-1 (lower)
+    double2 As[32][17], Bs[32][17];
+  };
+  extern __shared__ __align__(16) uint8_t pc_sm[];
+  Smem& S = *reinterpret_cast<Smem*>(pc_sm);
+  auto& Lp = S.Lp;
+  auto& Mi = S.Mi;
+  auto& As = S.As;
+  auto& Bs = S.Bs;
+  auto& Tt = S.Lp;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rr = tid >> 3, cb = (tid & 7) * 4;    // 32 x 32 tile: row rr, columns cb .. cb+3
+  // pivot threshold tau = n eps64 max_i G_ii
+  double dm = 0.0;
+  for (int i = tid; i < n; i += 256) dm = fmax(dm, G[(int64_t)i * n + i].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+  if (lane == 0) s_red[warp] = dm;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int w = 0; w < 8; ++w) gmax = fmax(gmax, s_red[w]);
+  const double tau = (double)n * 2.220446049250313e-16 * gmax;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int w = min(32, n - c0);
+    for (int i0 = c0; i0 < n; i0 += 32) {
+      double2 acc[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + rr, j = c0 + cb + b;
+        acc[b] = (i < n && j < c0 + w) ? G[(int64_t)j * n + i] : make_double2(0.0, 0.0);
+      }
+      for (int k0 = 0; k0 < c0; k0 += 16) {       // k0 + 16 <= c0 (c0 is a multiple of 32)
+        for (int x = tid; x < 32 * 16; x += 256) {
+          const int r = x & 31, kk = x >> 5;
+          const int k = k0 + kk;
+          As[r][kk] = (i0 + r < n) ? G[(int64_t)k * n + i0 + r] : make_double2(0.0, 0.0);
+          Bs[r][kk] = (c0 + r < n) ? G[(int64_t)k * n + c0 + r] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < 16; ++kk) {
+          const double2 a = As[rr][kk];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double2 q = Bs[cb + b][kk];   // acc -= a conj(q)
+            acc[b].x -= a.x * q.x + a.y * q.y;
+            acc[b].y -= a.y * q.x - a.x * q.y;
+          }
+        }
+        __syncthreads();
+      }
+      if (i0 == c0) {
+        // ---- factor the diagonal block in shared memory (right-looking, unblocked)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Lp[rr][cb + b] = acc[b];
+        __syncthreads();
+        for (int j = 0; j < w; ++j) {
+          const double d = Lp[j][j].x;
+          const bool ok = d > tau;
+          const double il = ok ? rsqrt(d) : 0.0;
+          __syncthreads();
+          if (tid >= j && tid < w) {                 // column j: scale (rows >= j)
+            const int i = tid;
+            if (i == j) Lp[j][j] = make_double2(ok ? d * il : 0.0, 0.0);
+            else Lp[i][j] = make_double2(Lp[i][j].x * il, Lp[i][j].y * il);
+          }
+          __syncthreads();
+          // trailing update: Lp[i][k] -= Lp[i][j] conj(Lp[k][j]), j < k <= i < w
+          for (int x = tid; x < 32 * 32; x += 256) {
+            const int i = x >> 5, k = x & 31;
+            if (k > j && k <= i && i < w) {
+              const double2 a = Lp[i][j], q = Lp[k][j];
+              Lp[i][k].x -= a.x * q.x + a.y * q.y;
+              Lp[i][k].y -= a.y * q.x - a.x * q.y;
+            }
+          }
+          __syncthreads();
+        }
+        // ---- inverse of the lower-triangular L_JJ, column by column (thread j < w owns column j)
+        if (tid < 32) {
+          const int j = tid;
+          for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
+          if (j < w && Lp[j][j].x > 0.0) {
+            Mi[j][j] = make_double2(1.0 / Lp[j][j].x, 0.0);
+            for (int i = j + 1; i < w; ++i) {
+              double2 s = make_double2(0.0, 0.0);
+              for (int k = j; k < i; ++k) {      // s += L[i][k] M[k][j]
+                const double2 a = Lp[i][k], q = Mi[k][j];
+                s.x += a.x * q.x - a.y * q.y;
+                s.y += a.x * q.y + a.y * q.x;
+              }
+              const double li = Lp[i][i].x;
+              Mi[i][j] = li > 0.0 ? make_double2(-s.x / li, -s.y / li) : make_double2(0.0, 0.0);
+            }
+          }
+        }
+        __syncthreads();
+        // ---- write L_JJ (lower part) back
+        for (int x = tid; x < 32 * 32; x += 256) {
+          const int i = x >> 5, j = x & 31;
+          if (i < w && j <= i) G[(int64_t)(c0 + j) * n + c0 + i] = Lp[i][j];
+        }
+      } else {
+        // ---- X = T (L_JJ^-1)^H: x_j = sum_{k <= j} t_k conj(M[j][k])
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Tt[rr][cb + b] = acc[b];
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = cb + b;
+          double2 x = make_double2(0.0, 0.0);
+          for (int k = 0; k <= j && k < w; ++k) {
+            const double2 tk = Tt[rr][k], q = Mi[j][k];
+            x.x += tk.x * q.x + tk.y * q.y;
+            x.y += tk.y * q.x - tk.x * q.y;
+          }
+          const int i = i0 + rr;
+          if (i < n && j < w) G[(int64_t)(c0 + j) * n + i] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // B = L in FP32 (n x n_pad, ld n): the lower triangle of L, zeros above it and in the pad columns
 __global__ void k_pc_b_from_l(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab) {
   const GateDesc& gd = desc[list[blockIdx.y]];
@@ -312,6 +451,18 @@ int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int
   if (count <= 0) return 0;
   const int T = (max_n + 63) / 64;
   k_pc_gram<<<dim3(T * (T + 1) / 2, count), 256, 0, s>>>(d_desc, d_list, slab);
+  static const bool cta_small = getenv("EAMPS_CHOL_PANELS") == nullptr;   // dev A/B switch
+  if (max_n <= 128 && cta_small) {
+    constexpr int kCholSmem = (2 * 32 * 33 + 2 * 32 * 17) * 16;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_pc_chol_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
+      attr = true;
+    }
+    k_pc_chol_cta<<<count, 256, kCholSmem, s>>>(d_desc, d_list, slab);
+    k_pc_b_from_l<<<dim3(64, count), 256, 0, s>>>(d_desc, d_list, slab);
+    return 3;
+  }
   for (int c0 = 0; c0 < max_n; c0 += 32) {
     k_pc_chol_diag<<<count, 256, 0, s>>>(d_desc, d_list, slab, c0);
     const int rb = (max_n - c0 - 1) / 32;       // row blocks below the diagonal block
