@@ -300,7 +300,7 @@ def main():
     mps.mps_set_profiling(False)
     clocks = clk.stop()
     sweeps = np.array([mps.mps_last_sweeps(g) for g in range(G)])
-    ks = np.array([r["chi_after"] for r in mps.mps_truncation_log()[-G:]])
+    ks = np.array(mps.mps_truncation_array(last=G)["chi_after"])
     if world > 1:
         total_ms = max_over_ranks(total_ms, dev)
     ms_step = total_ms / args.steps
@@ -358,7 +358,7 @@ def main():
             t0 = time.perf_counter()
             mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(host.data_ptr()), dims)
             mps.mps_apply_layer(sites, gates)
-            recs = mps.mps_truncation_log()[-G:]
+            recs = mps.mps_truncation_array(last=G)   # the step's result, D2H (no per-record Python objects)
             torch.cuda.synchronize()
             if rep > 0:
                 t_e2e += time.perf_counter() - t0

@@ -244,14 +244,21 @@ class MPS:
         self._check(lib().mps_schmidt_values(self._h, int(bond), _ptr(out), ln.value, C.byref(ln)))
         return out
 
-    def mps_truncation_log(self):
+    def mps_truncation_array(self, last: int = 0) -> np.ndarray:
+        """The truncation records as a numpy structured array (fields of mps_record); `last` > 0
+        keeps only the most recent `last` rows."""
         ln = C.c_int64(0)
         self._check(lib().mps_truncation_log(self._h, None, 0, C.byref(ln)))
         arr = (Record * max(1, ln.value))()
         self._check(lib().mps_truncation_log(self._h, arr, ln.value, C.byref(ln)))
-        return [dict(gate_index=r.gate_index, bond=r.bond, chi_before=r.chi_before, chi_after=r.chi_after,
-                     capped=bool(r.capped), target_f=r.target_f, achieved_f=r.achieved_f,
-                     discarded_weight=r.discarded_weight) for r in arr[: ln.value]]
+        a = np.ctypeslib.as_array(arr)[: ln.value]
+        return a[-last:] if last > 0 else a
+
+    def mps_truncation_log(self, last: int = 0):
+        a = self.mps_truncation_array(last)
+        return [dict(gate_index=int(r["gate_index"]), bond=int(r["bond"]), chi_before=int(r["chi_before"]),
+                     chi_after=int(r["chi_after"]), capped=bool(r["capped"]), target_f=float(r["target_f"]),
+                     achieved_f=float(r["achieved_f"]), discarded_weight=float(r["discarded_weight"])) for r in a]
 
     def mps_last_spectrum(self, g: int) -> np.ndarray:
         ln = C.c_int32(0)
