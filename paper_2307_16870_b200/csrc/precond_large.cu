@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_diag(const GateDesc* __restrict
   double2 (*Bs)[17] = AB[1];
   double2 (*Lp)[33] = reinterpret_cast<double2(*)[33]>(&AB[0][0][0]);
   __shared__ double s_red[8];
+  __shared__ double dinv_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rr = tid >> 3, cb = (tid & 7) * 4;
   double tau;
@@ -190,8 +191,10 @@ __global__ void __launch_bounds__(256) k_pc_chol_diag(const GateDesc* __restrict
   if (tid < 32) {                               // L_JJ^-1, thread j owns column j
     const int j = tid;
     for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
+    dinv_s[j] = (j < w && Lp[j][j].x > 0.0) ? 1.0 / Lp[j][j].x : 0.0;   // one division per row, in parallel
+    __syncwarp();
     if (j < w && Lp[j][j].x > 0.0) {
-      Mi[j][j] = make_double2(1.0 / Lp[j][j].x, 0.0);
+      Mi[j][j] = make_double2(dinv_s[j], 0.0);
       for (int i = j + 1; i < w; ++i) {
         double2 sacc = make_double2(0.0, 0.0);
         for (int k = j; k < i; ++k) {           // s += L[i][k] M[k][j]
@@ -199,8 +202,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_diag(const GateDesc* __restrict
           sacc.x += a.x * q.x - a.y * q.y;
           sacc.y += a.x * q.y + a.y * q.x;
         }
-        const double li = Lp[i][i].x;
-        Mi[i][j] = li > 0.0 ? make_double2(-sacc.x / li, -sacc.y / li) : make_double2(0.0, 0.0);
+        Mi[i][j] = make_double2(-sacc.x * dinv_s[i], -sacc.y * dinv_s[i]);
       }
     }
   }
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
   auto& Bs = S.Bs;
   auto& Tt = S.Lp;
   __shared__ double s_red[8];
+  __shared__ double dinv_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rr = tid >> 3, cb = (tid & 7) * 4;    // 32 x 32 tile: row rr, columns cb .. cb+3
   // pivot threshold tau = n eps64 max_i G_ii
@@ -342,8 +345,10 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
         if (tid < 32) {
           const int j = tid;
           for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
+          dinv_s[j] = (j < w && Lp[j][j].x > 0.0) ? 1.0 / Lp[j][j].x : 0.0;   // one division per row
+          __syncwarp();
           if (j < w && Lp[j][j].x > 0.0) {
-            Mi[j][j] = make_double2(1.0 / Lp[j][j].x, 0.0);
+            Mi[j][j] = make_double2(dinv_s[j], 0.0);
             for (int i = j + 1; i < w; ++i) {
               double2 s = make_double2(0.0, 0.0);
               for (int k = j; k < i; ++k) {      // s += L[i][k] M[k][j]
@@ -351,8 +356,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
                 s.x += a.x * q.x - a.y * q.y;
                 s.y += a.x * q.y + a.y * q.x;
               }
-              const double li = Lp[i][i].x;
-              Mi[i][j] = li > 0.0 ? make_double2(-s.x / li, -s.y / li) : make_double2(0.0, 0.0);
+              Mi[i][j] = make_double2(-s.x * dinv_s[i], -s.y * dinv_s[i]);
             }
           }
         }
