@@ -30,20 +30,36 @@ import numpy as np  # noqa: E402
 METRIC = "2-qubit MPS gate updates/s (contract+SVD+truncate); TFLOP/s as % of FP32 peak"
 UNIT = "gate updates/s"
 F_TRUNC = 0.9999
-# FP32 SIMT peak derived from the guide's unit counts: 148 SMs x 128 FP32
-# lanes x 2 flop/FMA x 1.965 GHz (clocks.max.sm)
-FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r02", "peaks.json")
 
 
-def _tf32_peak():
+def _peaks():
+    """Roofline denominators: MEASURED on this pool's B200s by tools/peaks/peaks.cu (committed result
+    profiles/r02/peaks.json: FFMA / FFMA2 loops for the FP32 SIMT peak, a DFMA loop for FP64, a
+    tcgen05.mma kind::tf32 M128 N256 loop for TF32 dense), else derived (the guide's unit counts x
+    clocks.max.sm, and measured bf16 x the nominal TF32/BF16 ratio), each with its source."""
+    out = {}
     try:
-        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        return mp["bf16_tflops"] * (1.13 / 2.25), "measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) x nominal TF32/BF16 1.13/2.25" % mp["bf16_tflops"]
+        pk = json.load(open(PEAKS_FILE))
+        fp32 = max(pk["fp32_ffma_tflops"], pk["fp32_ffma2_tflops"])
+        out["fp32"] = (fp32, "measured: tools/peaks FFMA2 loop %.1f TF/s (FFMA %.1f), profiles/r02/peaks.json"
+                       % (pk["fp32_ffma2_tflops"], pk["fp32_ffma_tflops"]))
+        out["tf32"] = (pk["tf32_tcgen05_m128n256_tflops"],
+                       "measured: tools/peaks tcgen05.mma kind::tf32 M128 N256 K8 loop, profiles/r02/peaks.json")
+        out["fp64"] = (pk["fp64_dfma_tflops"], "measured: tools/peaks DFMA loop, profiles/r02/peaks.json")
     except Exception:
-        return 1590.0 * (1.13 / 2.25), "fallback bf16 1590 TF/s (B200_PROFILING.md) x nominal TF32/BF16 1.13/2.25"
+        out["fp32"] = (148 * 128 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz")
+        try:
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            out["tf32"] = (mp["bf16_tflops"] * (1.13 / 2.25), "derived: measured bf16 burst x nominal TF32/BF16 1.13/2.25")
+        except Exception:
+            out["tf32"] = (1590.0 * (1.13 / 2.25), "fallback bf16 1590 TF/s x nominal TF32/BF16 1.13/2.25")
+        out["fp64"] = (148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 lanes x 2 x 1.965 GHz")
+    return out
 
 
-TF32_PEAK_TFLOPS, TF32_PEAK_SRC = _tf32_peak()
+PEAKS = _peaks()
+FP32_SIMT_PEAK_TFLOPS = PEAKS["fp32"][0]
 
 
 def parse():
@@ -56,21 +72,47 @@ def parse():
     ap.add_argument("--count", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-chi", action="store_true")
+    ap.add_argument("--per-chi", default=os.environ.get("BENCH_PER_CHI", "16:4096:5:3,256:4096:3:2,1024:512:2:1"),
+                    help="chi:count:steps:warmup sub-records (the large-chi half of configs[1])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--config5-depth", type=int, default=int(os.environ.get("BENCH_C5_DEPTH", "17")),
+                    help="layers of the config-5 sharded slice (0 = skip)")
     return ap.parse_args()
 
 
-def svd_flops(m, n, sweeps):
-    """algorithmic flops of the scalar one-sided Jacobi: (20 m n^2 + 12 n^3) per sweep."""
+def regime_of(m, n):
+    """The SVD regime the library's planner picks (C ABI mps_plan_regime, host only)."""
+    import paper_2307_16870_b200 as pk
+    return pk.mps_plan_regime(m, n)[0]
+
+
+def jacobi_flops(m, n, sweeps, regime):
+    """Algorithmic flops of the one-sided Jacobi the kernel EXECUTES (SURVEY §8(d) scalar count,
+    20 rows n^2 per sweep for the column pairs, + 12 n^3 when V is accumulated): the QR (3) and
+    large (1) regimes run on the n x n preconditioned factor B = L (rows = n) with no V; the small
+    (0) and medium (2) regimes on theta (rows = m) with V."""
+    if regime in (1, 3):
+        return sweeps * 20.0 * n ** 3
     return sweeps * (20.0 * m * n * n + 12.0 * n ** 3)
 
 
-def update_flops(chi, sweeps, k):
-    """contract + SVD + reabsorb for one config-2 theta (m = n = 2 chi, chi_m = 2 chi, d = 2)."""
+def svd_support_flops(m, n, regime):
+    """Executed flops around the Jacobi (reported, not in the roofline): FP64 Gram theta^H theta (4 m n^2,
+    Hermitian half) + Cholesky (8 n^3 / 3) for the preconditioned regimes; Rayleigh quotient theta V
+    (8 m n^2); polish C = B^H B (4 m n^2) for regimes 1 and 3."""
+    f = 8.0 * m * n * n
+    if regime in (1, 3):
+        f += 4.0 * m * n * n + 8.0 * n ** 3 / 3 + 4.0 * m * n * n
+    return f
+
+
+def update_flops(chi, sweeps, k, regime):
+    """contract + SVD (executed) + reabsorb for one config-2 theta (m = n = 2 chi, chi_m = 2 chi, d = 2)."""
     d, l, mid, r = 2, chi, 2 * chi, chi
     m, n = d * l, d * r
     contract = 8 * d * d * l * mid * r + 8 * d ** 4 * l * r
-    return contract + svd_flops(m, n, sweeps) + 8.0 * m * n * k
+    return contract + jacobi_flops(m, n, sweeps, regime) + svd_support_flops(m, n, regime) + 8.0 * m * n * k
 
 
 # ------------------------------------------------------------------------------ multi-rank
@@ -235,6 +277,182 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+def make_inputs(chi, G, first, dev, chunk=None):
+    """Config-2 contract-inclusive inputs (workloads.micro_chain_torch recipe, seeds b = first ..
+    first + G - 1), generated in chunks (the complex128 QRs of a chi = 1024 batch do not fit at once)
+    into one interleaved complex64 device buffer L0 R0 L1 R1 ..., the site dims and the gates."""
+    import torch
+
+    import workloads
+    n = 2 * chi
+    per = chi * 2 * n + n * 2 * chi
+    if chunk is None:
+        chunk = max(1, min(G, (1 << 31) // (n * n * 16 * 4)))
+    inter = torch.empty(G * per, dtype=torch.complex64, device=dev)
+    gates = []
+    for c0 in range(0, G, chunk):
+        c = min(chunk, G - c0)
+        left, right, u = workloads.micro_chain_torch(chi, c, first=first + c0, device=dev)
+        inter[c0 * per:(c0 + c) * per] = torch.cat([left.reshape(c, -1), right.reshape(c, -1)], dim=1).reshape(-1)
+        gates.append(u)
+        del left, right
+    dims = np.array([[chi, 2, n], [n, 2, chi]] * G, np.int32)
+    return inter, dims, np.concatenate(gates)
+
+
+def run_chi(chi, G, steps, warmup, rank, world, dev, clocks=True):
+    """Time `steps` mps_apply_layer calls over one G-gate config-2 layer (after `warmup` untimed
+    ones): state restored before every step (snapshot, or re-import for big site stores) and L2
+    flushed, both untimed. Returns (record, handle, device inputs, dims, gates)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2307_16870_b200 as pk
+    n = 2 * chi
+    inter, dims, gates = make_inputs(chi, G, rank_seed_range(rank, G)[0], dev)
+    site_bytes = inter.numel() * 8
+    # one wave needs: old + new site blocks (pow2 classes), theta/Theta'/V/E, the regime scratch
+    # (large: FP64 Gram 16 n^2) and small arrays; take it from the free memory
+    ws_gate = 4 * n * n * 8 + 16 * n * n + 64 * n + 8192
+    need = int(2.2 * 2 * site_bytes + G * ws_gate) + (512 << 20)
+    free, _ = torch.cuda.mem_get_info(dev)
+    slab_bytes = int(min(max(need, 1 << 30), 0.7 * free))
+    mps = pk.MPS(2 * G, strategy="fixed", f_fixed=F_TRUNC, slab_bytes=slab_bytes, device=dev)
+    mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(inter.data_ptr()), dims)
+    use_snap = site_bytes < (8 << 30)
+    snap = mps.mps_snapshot_save() if use_snap else None
+    sites = np.arange(0, 2 * G, 2, dtype=np.int32)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def restore():
+        if use_snap:
+            mps.mps_snapshot_load(snap)
+        else:
+            mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(inter.data_ptr()), dims)
+
+    def step_timed():
+        restore()
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        mps.mps_apply_layer(sites, gates)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(warmup):
+        step_timed()
+    clk = ClockSampler(torch.cuda.current_device()) if clocks else None
+    if clk:
+        clk.start()
+    mps.mps_set_profiling(True)
+    l0 = mps.mps_launch_count()
+    total_ms = 0.0
+    for _ in range(steps):
+        total_ms += step_timed()
+    launches = mps.mps_launch_count() - l0
+    phases = mps.mps_phase_times()
+    mps.mps_set_profiling(False)
+    clk_rec = clk.stop() if clk else None
+    sweeps = np.array([mps.mps_last_sweeps(g) for g in range(G)])
+    ks = np.array(mps.mps_truncation_array(last=G)["chi_after"])
+    if world > 1:
+        total_ms = max_over_ranks(total_ms, dev)
+    ms_step = total_ms / steps
+    regime = regime_of(n, n)
+    # ---- roofline of the dominant kernel: the Jacobi SVD. Its executed algorithmic flops per
+    # launch (one launch group per wave) / its CUDA-event time (sub-phase svd_jacobi when the
+    # planner times it, else the whole SVD phase, which then also holds the support kernels)
+    alg = float(sum(jacobi_flops(n, n, sw, regime) for sw in sweeps))
+    if phases["svd_jacobi"][1]:
+        kern, (kms, kn) = "svd_jacobi", phases["svd_jacobi"]
+        per_launch_alg = alg * steps / kn
+    else:
+        kern = "svd_small" if phases["svd_small"][1] else "svd_blocked"
+        kms, kn = phases[kern]
+        per_launch_alg = alg * steps / kn
+    kms_launch = kms / max(1, kn)
+    achieved = per_launch_alg / (kms_launch / 1e3) / 1e12
+    if regime == 1:
+        (peak, peak_src), bound = PEAKS["tf32"], "tensor"
+    else:
+        (peak, peak_src), bound = PEAKS["fp32"], "alu"
+    traffic = None
+    tj = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+    if os.path.exists(tj):
+        try:
+            traffic = json.load(open(tj)).get("chi%d" % chi, {}).get(kern)
+        except Exception:
+            traffic = None
+    total_flops = float(sum(update_flops(chi, sw, k, regime) for sw, k in zip(sweeps, ks)))
+    svd_phase_ms = (phases["svd_small"][0] + phases["svd_blocked"][0]) / steps
+    rec = {
+        "value": world * G / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "steps": steps, "warmup": warmup,
+        "count": G, "chi": chi, "theta": "%dx%d" % (n, n), "svd_regime": {0: "small", 1: "large (tcgen05)", 2: "medium",
+                                                                           3: "QR-preconditioned"}[regime],
+        "tflops_executed": total_flops / (ms_step / 1e3) / 1e12 * world,
+        "sweeps_mean": float(sweeps.mean()), "k_mean": float(ks.mean()),
+        "phase_ms_per_step": {p: v[0] / max(1, steps) for p, v in phases.items()},
+        "svd_phase_ms_per_step": svd_phase_ms,
+        "roofline": {"bound": bound, "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "launch_ms": kms_launch,
+                     "flops": "executed algorithmic Jacobi flops per launch: sweeps x 20 rows n^2 (+12 n^3 with V); "
+                              "rows = n for the preconditioned V-less regimes (QR, large)"},
+        "gpu_launches": int(launches),
+        "clocks": clk_rec,
+    }
+    return rec, mps, inter, dims, gates
+
+
+def run_config5_slice(depth, rank, world, dev, comm=None, solo=False):
+    """BASELINE configs[4] (config 5: N = 300, Haar brickwork, F_min = 0.9 over the full depth-75
+    circuit's gate count, cap 4096) on its first `depth` layers, sites sharded in contiguous
+    Sigma chi^3-weighted blocks over the ranks (sharded.py: NCCL point-to-point ghost fetch /
+    write-back and the ledger token). Device time (CUDA events on each rank's stream around the
+    whole slice), max over ranks. solo=True: this rank alone, world 1 (the T_1 of the efficiency)."""
+    import torch
+
+    import paper_2307_16870_b200 as pk
+    import workloads
+    from paper_2307_16870_b200.sharded import DistComm, GpuEngine, ShardedMPS, predicted_site_cost
+    N, full_depth, cap = 300, 75, 4096
+    n_planned = workloads.n_two_qubit_gates([(workloads.brickwork_sites(N, t), None) for t in range(full_depth)])
+    layers = workloads.brickwork_circuit(5, N, depth)
+    free, _ = torch.cuda.mem_get_info(dev)
+    slab = int(0.6 * free)
+    kw = dict(f_min=0.9, n_planned=n_planned, strategy="global", chi_cap=cap)
+    p = 1 if solo else world
+    comm = None if (solo or world == 1) else DistComm()
+    sh = ShardedMPS(N, lambda n: GpuEngine(pk.MPS(n, slab_bytes=slab, device=dev, **kw)), comm=comm, device=dev,
+                    weights=predicted_site_cost(N, depth, 2, cap))
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for sites, us in layers:
+        sh.apply_layer(sites, us)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3
+    if p > 1:
+        sec = max_over_ranks(sec, dev)
+    led = sh.ledger()
+    gates = workloads.n_two_qubit_gates(layers)
+    chi_max = max((r["chi_after"] for r in sh.eng.records()), default=0)
+    out = {"workload": "config5 (configs[4]) N=300 layers 0-%d of 75, cap 4096, F_min 0.9 global" % (depth - 1),
+           "ranks": p, "blocks": sh.blocks, "seconds": sec, "value": gates / sec, "unit": UNIT,
+           "boundary_messages_rank": sh.exchanges, "chi_max_rank0": int(chi_max),
+           "log_E": led[0], "truncations": int(led[1]), "guarantee_held": bool(led[2])}
+    del sh
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,104 +465,32 @@ def main():
     import torch.distributed as dist
 
     import paper_2307_16870_b200 as pk
-    import workloads
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     chi, G = args.chi, args.count
-    n = 2 * chi
-    # ---- inputs: this rank's 4096 updates (seeds b = rank*G .. rank*G + G - 1)
-    left, right, gates = workloads.micro_chain_torch(chi, G, first=rank_seed_range(rank, G)[0], device=dev)
-    site_bytes = (left.numel() + right.numel()) * 8
-    # one wave needs: old + new site blocks (pow2 classes), theta/Theta'/V/E, the medium-regime
-    # rotation log (24 sweeps x (n-1) x n/2 x 16 B) and small arrays; take it from the free memory
-    ws_gate = 4 * n * n * 8 + 24 * (n - 1) * (n // 2) * 16 + 64 * n + 8192
-    need = int(2.2 * 2 * site_bytes + G * ws_gate) + (512 << 20)
-    free, _ = torch.cuda.mem_get_info(dev)
-    slab_bytes = int(min(max(need, 1 << 30), 0.6 * free))
-    mps = pk.MPS(2 * G, strategy="fixed", f_fixed=F_TRUNC, slab_bytes=slab_bytes, device=dev)
-    inter = torch.cat([left.reshape(G, -1), right.reshape(G, -1)], dim=1).reshape(-1)  # L0 R0 L1 R1 ...
-    dims = np.array([[chi, 2, n], [n, 2, chi]] * G, np.int32)
-    mps.mps_import_sites_raw(0, 2 * G, pk.C.c_void_p(inter.data_ptr()), dims)
-    snap = mps.mps_snapshot_save()
-    sites = np.arange(0, 2 * G, 2, dtype=np.int32)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def step_timed():
-        mps.mps_snapshot_load(snap)
-        flush.zero_()  # L2 flush (256 MB > 126 MB L2)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        mps.mps_apply_layer(sites, gates)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
-
-    for _ in range(args.warmup):
-        step_timed()
-    clk = ClockSampler(torch.cuda.current_device())
-    clk.start()
-    mps.mps_set_profiling(True)
-    l0 = mps.mps_launch_count()
-    total_ms = 0.0
-    for _ in range(args.steps):
-        total_ms += step_timed()
-    launches = mps.mps_launch_count() - l0
-    phases = mps.mps_phase_times()
-    mps.mps_set_profiling(False)
-    clocks = clk.stop()
-    sweeps = np.array([mps.mps_last_sweeps(g) for g in range(G)])
-    ks = np.array(mps.mps_truncation_array(last=G)["chi_after"])
-    if world > 1:
-        total_ms = max_over_ranks(total_ms, dev)
-    ms_step = total_ms / args.steps
-    value = world * G / (ms_step / 1e3)
-
-    # ---- roofline of the dominant kernel (the SVD phase)
-    svd_key = "svd_small" if phases["svd_small"][1] else "svd_blocked"
-    svd_ms, svd_n = phases[svd_key]
-    svd_ms_per_launch = svd_ms / max(1, svd_n)
-    alg_svd = float(sum(svd_flops(n, n, s) for s in sweeps))  # per launch (one wave = the layer)
-    achieved = alg_svd / (svd_ms_per_launch / 1e3) / 1e12
-    if svd_key == "svd_blocked":
-        # large regime: tcgen05 3xTF32 block Jacobi -> the tensor roofline. TF32 dense peak = the
-        # measured cuBLAS bf16 burst x the nominal TF32/BF16 ratio (1.13 / 2.25 PFLOP/s, guide)
-        peak, bound, peak_src = TF32_PEAK_TFLOPS, "tensor", TF32_PEAK_SRC
-    else:
-        peak, bound, peak_src = FP32_SIMT_PEAK_TFLOPS, "alu", "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"
-    traffic = None
-    tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tj):
-        try:
-            traffic = json.load(open(tj)).get("chi%d" % chi, {}).get(svd_key)
-        except Exception:
-            traffic = None
-    total_flops = float(sum(update_flops(chi, s, k) for s, k in zip(sweeps, ks)))
+    rec, mps, inter, dims, gates = run_chi(chi, G, args.steps, args.warmup, rank, world, dev)
+    site_bytes = inter.numel() * 8
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 norms/Rayleigh)",
+        "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 norms/Gram/Rayleigh)",
         "data": "synthetic (seeded BASELINE configs[1] recipe: theta = X diag(k^-1.5) Y^H, Haar X/Y/U)",
         "config": {"workload": "config2_microbench chi=%d x%d contract-inclusive (configs[1])" % (chi, G),
-                   "chi": chi, "count": G, "theta": "%dx%d" % (n, n), "f_trunc": F_TRUNC, "rule": "pure",
+                   "chi": chi, "count": G, "theta": rec["theta"], "f_trunc": F_TRUNC, "rule": "pure",
                    "parallelism": "independent updates per rank" if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MB write)"},
-        "tflops_algorithmic": total_flops / (ms_step / 1e3) / 1e12 * world,
-        "pct_fp32_simt_peak": 100.0 * total_flops / (ms_step / 1e3) / 1e12 / FP32_SIMT_PEAK_TFLOPS,
-        "sweeps_mean": float(sweeps.mean()), "k_mean": float(ks.mean()),
-        "phase_ms_per_step": {p: v[0] / max(1, args.steps) for p, v in phases.items()},
-        "roofline": {"bound": bound, "kernel": svd_key, "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "flops": "algorithmic: sweeps x (20 m n^2 + 12 n^3) per theta (scalar one-sided Jacobi count)"},
-        "gpu_launches": int(launches),
-        "clocks": clocks,
+        "tflops_executed": rec["tflops_executed"],
+        "pct_fp32_simt_peak": 100.0 * rec["tflops_executed"] / world / FP32_SIMT_PEAK_TFLOPS,
+        "svd_regime": rec["svd_regime"], "sweeps_mean": rec["sweeps_mean"], "k_mean": rec["k_mean"],
+        "phase_ms_per_step": rec["phase_ms_per_step"],
+        "roofline": rec["roofline"],
+        "gpu_launches": rec["gpu_launches"],
+        "clocks": rec["clocks"],
     }
+    sites = np.arange(0, 2 * G, 2, dtype=np.int32)
     # ---- e2e: host (pinned) inputs -> H2D -> update -> D2H of the step's records, through the ABI
     if not args.no_e2e:
         host = torch.empty(inter.numel(), dtype=torch.complex64, pin_memory=True)
@@ -368,6 +514,41 @@ def main():
         line["e2e"] = {"value": world * G / (t_e2e / reps), "unit": UNIT,
                        "h2d_bytes_per_step": int(site_bytes + gates.nbytes),
                        "d2h_bytes_per_step": int(G * (48 + 160) + 512)}
+        del host
+    del mps, inter
+    torch.cuda.empty_cache()
+    # ---- the rest of configs[1]: chi = 16 / 256 / 1024 sub-records (single GPU only), each with its
+    # own stated step count (chi = 1024 on a 512-update subset of the 4096, in waves)
+    if world == 1 and not args.no_per_chi and args.per_chi:
+        line["per_chi"] = {}
+        for spec in args.per_chi.split(","):
+            c, cnt, st, wu = (int(x) for x in spec.split(":"))
+            if c == chi:
+                continue
+            try:
+                r, m2, i2, _, _ = run_chi(c, cnt, st, wu, rank, world, dev)
+                if cnt < 4096:
+                    r["subset"] = "%d of the 4096 updates (seeds 0..%d)" % (cnt, cnt - 1)
+                line["per_chi"]["chi%d" % c] = r
+                del m2, i2
+            except Exception as e:   # a sub-record never blocks the headline line
+                line["per_chi"]["chi%d" % c] = {"error": str(e)[:300]}
+            torch.cuda.empty_cache()
+    # ---- config 5 (the sharded north-star workload) on its first layers, at every N: the N-rank
+    # sharded time; at N > 1 also rank 0 alone (T_1) for the parallel efficiency T_1 / (N T_N)
+    if args.config5_depth > 0:
+        try:
+            c5 = run_config5_slice(args.config5_depth, rank, world, dev)
+            if world > 1:
+                dist.barrier()
+                t1 = run_config5_slice(args.config5_depth, rank, world, dev, solo=True) if rank == 0 else None
+                dist.barrier()
+                if rank == 0:
+                    c5["t1_seconds"] = t1["seconds"]
+                    c5["parallel_efficiency"] = t1["seconds"] / (world * c5["seconds"])
+            line["config5_slice"] = c5
+        except Exception as e:
+            line["config5_slice"] = {"error": str(e)[:300]}
     if rank == 0 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_sample(chi, args.cpu_seconds)

@@ -50,7 +50,7 @@ enum {
   MPS_E_RANGE = -2,   /* site / bond index out of range */
   MPS_E_NOMEM = -3,   /* slab or device pool exhausted */
   MPS_E_CUDA = -4,    /* CUDA runtime error (handle poisoned) */
-  MPS_E_NCCL = -5,    /* reserved for the multi-GPU boundary exchange */
+  MPS_E_NCCL = -5,    /* reserved (never returned: the boundary exchange runs above this ABI) */
   MPS_E_NOCONV = -6,  /* Jacobi SVD did not converge within max_sweeps */
   MPS_E_NUMERIC = -7, /* non-finite singular value */
   MPS_E_STATE = -8,   /* more truncations than n_planned, or bad query state */
@@ -73,10 +73,8 @@ typedef struct {
   double f_fixed;      /* per-update target for MPS_STRAT_FIXED */
   void* stream;        /* cudaStream_t; NULL = legacy default stream */
   void* dev_slab;      /* device memory owned by the caller */
-  size_t slab_bytes;
-  int32_t rank, world; /* must be 0, 1: the site-block sharding of §8(e) runs ABOVE this ABI, one
-                        * world-1 handle per rank for its block (paper_2307_16870_b200/sharded.py) */
-  const void* nccl_unique_id;
+  size_t slab_bytes;   /* the site-block sharding of SURVEY §8(e) runs ABOVE this ABI: one handle per
+                        * rank holds that rank's block (paper_2307_16870_b200/sharded.py) */
 } mps_config;
 
 /* One row per truncation (SPEC.md:189-193 TruncationRecord). */
@@ -131,12 +129,22 @@ mps_status mps_plan_regime(int32_t m, int32_t n, int32_t* regime, int32_t* gt, i
  * no cap fired; is_lower_bound = 1 for the MPO (noisy) regime (E13). Any pointer may be NULL. */
 mps_status mps_fidelity_estimate(mps_t, double* est, double* log_est, int64_t* n_done,
                                  int32_t* guarantee_held, int32_t* is_lower_bound);
-/* <digits|psi> (MPO: the vectorised element <<digits|rho>>); digits: N values in [0, d). */
+/* <digits|psi> = the coefficient C_{sigma_1..sigma_N} of E1 evaluated from the MPS
+ * product of E2 as a left-to-right chain of chi-vectors (MPO: the vectorised
+ * element <<digits|rho>> of the density-matrix expansion); digits: N values in
+ * [0, d). re_im: 2 doubles (host). Synchronising; MPS_E_RANGE for a digit >= d. */
 mps_status mps_amplitude(mps_t, const uint8_t* digits, double* re_im);
-/* Full d^N vector (interleaved complex128), site 0 most significant; d^N <= 2^26. */
+/* The full coefficient vector C of E1, contracted from the MPS of E2
+ * (PAPER.md:38-41): d^N interleaved complex128 values in `out` (host, n_doubles >= 2 d^N), site 0
+ * the most significant digit; MPS_E_TOOBIG if d^N > 2^26 (small-N verification only). */
 mps_status mps_to_statevector(mps_t, double* out, size_t n_doubles);
+/* The bond dimensions chi_1 .. chi_{N-1} of E2 as they stand (host mirror, no
+ * device work); out: N-1 int32 (host). */
 mps_status mps_bond_dims(mps_t, int32_t* out /* N-1 */);
-/* Schmidt vector lambda of `bond` (float32, descending), *len = its length. */
+/* Schmidt vector lambda of `bond` (float32, descending; bond -1..N-1, the outer two are [1]): the
+ * kept, renormalised singular values of the last SVD at that bond ("singular values in decreasing
+ * order"; the Lambda of the canonical form, PAPER.md:65 and E10 PAPER.md:117-118).
+ * out may be NULL to query *len; MPS_E_RANGE for a bond outside -1..N-1. */
 mps_status mps_schmidt_values(mps_t, int32_t bond, float* out, int32_t cap, int32_t* len);
 mps_status mps_truncation_log(mps_t, mps_record* rows, int64_t cap, int64_t* len);
 /* Sorted singular values (float64, descending, all n of them) of gate g (ascending-site order)
@@ -164,11 +172,14 @@ mps_status mps_launch_count(mps_t, int64_t* count);
 /* Jacobi sweeps of gate g of the last layer. */
 mps_status mps_last_sweeps(mps_t, int32_t g, int32_t* sweeps);
 /* Phase timers: with profiling on, apply_layer records CUDA events on cfg.stream around each
- * phase and accumulates device milliseconds: ms[0] contract, ms[1] SVD (small regime),
- * ms[2] SVD (blocked regime), ms[3] select, ms[4] reabsorb; counts[p] = waves timed.
- * mps_set_profiling resets the accumulators. */
+ * phase and accumulates device milliseconds: ms[0] contract, ms[1] SVD (small / medium / QR
+ * regimes), ms[2] SVD (large regime), ms[3] select, ms[4] reabsorb (counts[p] = waves timed);
+ * and sub-phases of the SVD (counts[p] = launch groups timed): ms[5] preconditioner (FP64 Gram +
+ * Cholesky + B = L), ms[6] the Jacobi kernel, ms[7] spectrum (Rayleigh + polish + sort). A
+ * sub-phase is timed for the regimes whose kernels are launched from the layer planner (the QR
+ * regime and the fused large regime). mps_set_profiling resets the accumulators. */
 mps_status mps_set_profiling(mps_t, int32_t on);
-mps_status mps_phase_times(mps_t, double* ms /* [5] */, int64_t* counts /* [5], may be NULL */);
+mps_status mps_phase_times(mps_t, double* ms /* [8] */, int64_t* counts /* [8], may be NULL */);
 mps_status mps_sync(mps_t);
 const char* mps_last_error(mps_t);
 const char* mps_status_string(mps_status);

@@ -41,8 +41,7 @@ class Config(C.Structure):
     _fields_ = [("f_min", C.c_double), ("n_planned", C.c_int64), ("strategy", C.c_int32),
                 ("rule", C.c_int32), ("chi_cap", C.c_int32), ("max_sweeps", C.c_int32),
                 ("f_fixed", C.c_double), ("stream", C.c_void_p), ("dev_slab", C.c_void_p),
-                ("slab_bytes", C.c_size_t), ("rank", C.c_int32), ("world", C.c_int32),
-                ("nccl_unique_id", C.c_void_p)]
+                ("slab_bytes", C.c_size_t)]
 
 
 class Record(C.Structure):
@@ -147,7 +146,7 @@ class MPS:
         self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
         cfg = Config(float(f_min), int(n_planned), STRATEGIES[strategy], RULES[rule], int(chi_cap),
                      int(max_sweeps), float(f_fixed), C.c_void_p(self.stream.cuda_stream),
-                     C.c_void_p(self.slab.data_ptr()), int(slab_bytes), 0, 1, None)
+                     C.c_void_p(self.slab.data_ptr()), int(slab_bytes))
         h = C.c_void_p()
         self._check(L.mps_create(int(n_sites), int(d), C.byref(cfg), C.byref(h)), None)
         self._h = h
@@ -323,11 +322,12 @@ class MPS:
     def mps_set_profiling(self, on: bool = True):
         self._check(lib().mps_set_profiling(self._h, int(bool(on))))
 
-    PHASES = ("contract", "svd_small", "svd_blocked", "select", "reabsorb")
+    PHASES = ("contract", "svd_small", "svd_blocked", "select", "reabsorb", "svd_precond", "svd_jacobi",
+              "svd_spectrum")
 
     def mps_phase_times(self):
-        ms = np.zeros(5)
-        cnt = np.zeros(5, np.int64)
+        ms = np.zeros(len(self.PHASES))
+        cnt = np.zeros(len(self.PHASES), np.int64)
         self._check(lib().mps_phase_times(self._h, _ptr(ms), _ptr(cnt)))
         return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
 

@@ -42,8 +42,11 @@ struct LayerJob {                  // the layer in flight (mps_layer_begin / mps
   bool ran[5] = {false, false, false, false, false};
 };
 
+constexpr int kPhases = 8;
+
 struct mps_handle {
   int N = 0, d = 0;
+  int device = 0;                          // the device of the slab: made current at every ABI entry
   mps_config cfg{};
   cudaStream_t s = nullptr;
   uint8_t* slab = nullptr;
@@ -64,9 +67,15 @@ struct mps_handle {
   size_t pinned_bytes[2] = {0, 0};
   // phase timers (mps_set_profiling): CUDA events recorded on the launch stream around each phase
   bool profiling = false;
-  double phase_ms[5] = {0, 0, 0, 0, 0};      // contract, svd_small, svd_blocked, select, reabsorb
-  int64_t phase_n[5] = {0, 0, 0, 0, 0};
+  // [0] contract [1] svd_small (small / medium / QR regimes) [2] svd_blocked (large regime) [3] select
+  // [4] reabsorb, and sub-phases of the SVD (spans, one per bucket launch group): [5] preconditioner
+  // (FP64 Gram + Cholesky + B = L) [6] the Jacobi kernel itself [7] spectrum (Rayleigh + polish + sort)
+  double phase_ms[kPhases] = {};
+  int64_t phase_n[kPhases] = {};
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> span_ev;          // event pool for the sub-phase spans of one wave
+  int span_used = 0;
+  std::vector<std::array<int, 3>> spans;     // (phase, begin event, end event)
   // host side of a snapshot
   struct Snap {
     bool valid = false;
@@ -86,6 +95,22 @@ mps_status set_err(mps_t h, mps_status st, const std::string& msg) {
   return st;
 }
 
+// Makes the handle's device current for the duration of an ABI call (the library never assumes
+// that the caller's current device is the slab's), and restores the caller's device after.
+struct DeviceGuard {
+  int prev = -1, want = -1;
+  explicit DeviceGuard(const mps_handle* h) {
+    if (!h) return;
+    want = h->device;
+    if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+    if (prev != want) cudaSetDevice(want);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+#define DEVICE_GUARD(h) DeviceGuard _device_guard(h)
+
 mps_status cuda_check(mps_t h, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return MPS_OK;
   h->poisoned = true;
@@ -103,6 +128,20 @@ mps_status cuda_check(mps_t h, cudaError_t e, const char* what) {
     mps_status _st = cuda_check(h, cudaGetLastError(), what); \
     if (_st != MPS_OK) return _st;                          \
   } while (0)
+
+// Sub-phase timing (profiling only): record a pooled event on the launch stream; returns its index.
+int prof_mark(mps_t h) {
+  if (h->span_used == (int)h->span_ev.size()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    h->span_ev.push_back(e);
+  }
+  if (cudaEventRecord(h->span_ev[h->span_used], h->s) != cudaSuccess) return -1;
+  return h->span_used++;
+}
+void prof_span(mps_t h, int phase, int a, int b) {
+  if (a >= 0 && b >= 0) h->spans.push_back({phase, a, b});
+}
 
 // Pinned staging buffers. Growing one first drains the stream so that no in-flight async copy
 // still reads or writes the old buffer.
@@ -466,10 +505,19 @@ mps_status wave_front(mps_t h) {
       }
       // Cholesky preconditioner (FP64 Gram + Cholesky -> B = L in the theta workspace) instead of
       // the in-CTA FP32 Householder QR
+      const int e0 = prof ? prof_mark(h) : -1;
       if (pc) h->launches += launch_precond_large(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->s);
+      const int e1 = prof ? prof_mark(h) : -1;
       launch_svd_qr(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.tile_rows,
                     h->slab, h->dst, h->s);
+      const int e2 = prof ? prof_mark(h) : -1;
       h->launches += 1 + launch_spectrum_polish(d_desc, d_small + b.begin, b.end - b.begin, maxn, h->slab, h->dst, h->s);
+      if (prof) {
+        const int e3 = prof_mark(h);
+        if (pc) prof_span(h, 5, e0, e1);
+        prof_span(h, 6, e1, e2);
+        prof_span(h, 7, e2, e3);
+      }
     } else if (b.regime == 0) {
       launch_svd_small(d_desc, d_small + b.begin, b.end - b.begin, b.smem, h->cfg.max_sweeps, b.gt, b.rpl, b.threads,
                        h->slab, h->dst, h->s);
@@ -545,7 +593,15 @@ mps_status wave_back(mps_t h) {
       h->phase_ms[p] += ms;
       h->phase_n[p] += 1;
     }
+    for (const auto& sp : h->spans) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h->span_ev[sp[1]], h->span_ev[sp[2]]));
+      h->phase_ms[sp[0]] += ms;
+      h->phase_n[sp[0]] += 1;
+    }
   }
+  h->spans.clear();
+  h->span_used = 0;
   mps_status de = device_error(h);
   for (int x = 0; x < Gw; ++x) {
     const GateDesc& gd = hd[x];
@@ -580,8 +636,18 @@ mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* 
   if (cfg->strategy < 0 || cfg->strategy > 3 || cfg->rule < 0 || cfg->rule > 2) return MPS_E_INVAL;
   if (cfg->strategy == MPS_STRAT_FIXED && !(cfg->f_fixed > 0.0 && cfg->f_fixed <= 1.0)) return MPS_E_INVAL;
   if (!cfg->dev_slab || cfg->slab_bytes < (1u << 20)) return MPS_E_INVAL;
-  if (cfg->world > 1) return MPS_E_INVAL;  // this build shards above the ABI (independent handles)
+  int slab_dev = -1;
+  {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, cfg->dev_slab) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return MPS_E_INVAL;   // the slab must be device memory
+    }
+    slab_dev = a.device;
+  }
   mps_t h = new mps_handle();
+  h->device = slab_dev;
+  DEVICE_GUARD(h);
   h->N = n_sites;
   h->d = d;
   h->cfg = *cfg;
@@ -672,17 +738,20 @@ mps_status mps_create(int32_t n_sites, int32_t d, const mps_config* cfg, mps_t* 
 }
 
 mps_status mps_destroy(mps_t h) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   if (h->s) cudaStreamSynchronize(h->s);
   for (int w = 0; w < 2; ++w)
     if (h->pinned[w]) cudaFreeHost(h->pinned[w]);
   for (int e = 0; e < 6; ++e)
     if (h->ev[e]) cudaEventDestroy(h->ev[e]);
+  for (cudaEvent_t e : h->span_ev) cudaEventDestroy(e);
   delete h;
   return MPS_OK;
 }
 
 mps_status mps_sync(mps_t h) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -692,17 +761,18 @@ mps_status mps_sync(mps_t h) {
 }
 
 mps_status mps_set_profiling(mps_t h, int32_t on) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   if (on && !h->ev[0])
     for (int e = 0; e < 6; ++e) CK(cudaEventCreate(&h->ev[e]));
   h->profiling = on != 0;
-  for (int p = 0; p < 5; ++p) { h->phase_ms[p] = 0; h->phase_n[p] = 0; }
+  for (int p = 0; p < kPhases; ++p) { h->phase_ms[p] = 0; h->phase_n[p] = 0; }
   return MPS_OK;
 }
 
 mps_status mps_phase_times(mps_t h, double* ms, int64_t* counts) {
   if (!h || !ms) return MPS_E_INVAL;
-  for (int p = 0; p < 5; ++p) {
+  for (int p = 0; p < kPhases; ++p) {
     ms[p] = h->phase_ms[p];
     if (counts) counts[p] = h->phase_n[p];
   }
@@ -716,6 +786,7 @@ mps_status mps_launch_count(mps_t h, int64_t* c) {
 }
 
 mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
+  DEVICE_GUARD(h);
   if (!h || !U) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -735,6 +806,7 @@ mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
 }
 
 mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float* Us, int32_t* n_waves) {
+  DEVICE_GUARD(h);
   if (n_waves) *n_waves = 0;
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
@@ -789,7 +861,9 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
                 : svd_small_fits(gd.m, gd.n)                  ? 0
                 : (svd_medium_fits(gd.m, gd.n) ? 2 : 1);
     gd.n_pad = gd.regime != 1 ? gd.n : (int)align_up(gd.n, 64);
-    gd.log_sweeps = gd.regime == 2 ? std::min(h->cfg.max_sweeps, 24) : 0;
+    // the rotation log holds every sweep the Jacobi may run (cfg.max_sweeps, default 60), so the medium
+    // regime has the same sweep limit as the others (MPS_E_NOCONV only past max_sweeps)
+    gd.log_sweeps = gd.regime == 2 ? h->cfg.max_sweeps : 0;
     // medium regime: the rotation log; large regime: the tensor-core Jacobi scratch (G, E images)
     // large regime: the R-preconditioner (FP64 Gram + Cholesky, Jacobi on B = L with n rows, no V
     // accumulation; for m < n the Gram has rank <= m and B gets zero columns); its FP64 Gram shares
@@ -798,7 +872,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // QR regime, block-recursive kernels: B = L from the FP64 Gram + Cholesky (EAMPS_QR_HOUSEHOLDER=1:
     // the in-CTA Householder QR instead)
     static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
-    if (gd.regime == 3 && !qr_hh && qr_block_order(gd.m, gd.n)) gd.jrows = gd.n;
+    if (gd.regime == 3 && !qr_hh) gd.jrows = gd.n;
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                         : gd.regime == 1 ? large_scratch_bytes(gd)
                         : (gd.regime == 3 && gd.jrows > 0) ? large_precond_scratch(gd.n)
@@ -841,6 +915,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
 }
 
 mps_status mps_layer_step(mps_t h, int32_t* remaining) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   if (remaining) *remaining = 0;
   LayerJob& J = h->job;
@@ -875,6 +950,7 @@ mps_status mps_apply_gate2(mps_t h, int32_t site, const float* U) { return mps_a
 
 mps_status mps_fidelity_estimate(mps_t h, double* est, double* log_est, int64_t* n_done, int32_t* guarantee_held,
                                  int32_t* is_lower_bound) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -915,6 +991,7 @@ mps_status mps_plan_regime(int32_t m, int32_t n, int32_t* regime, int32_t* gt, i
 }
 
 mps_status mps_ledger_get(mps_t h, double* log_E, int64_t* j, int32_t* guarantee) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -929,6 +1006,7 @@ mps_status mps_ledger_get(mps_t h, double* log_E, int64_t* j, int32_t* guarantee
 }
 
 mps_status mps_ledger_set(mps_t h, double log_E, int64_t j, int32_t guarantee) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -957,6 +1035,7 @@ mps_status mps_bond_dims(mps_t h, int32_t* out) {
 }
 
 mps_status mps_schmidt_values(mps_t h, int32_t bond, float* out, int32_t cap, int32_t* len) {
+  DEVICE_GUARD(h);
   if (!h || !len) return MPS_E_INVAL;
   if (bond < -1 || bond > h->N - 1) return set_err(h, MPS_E_RANGE, "bond out of range");
   mps_status st = check_sticky(h);
@@ -1003,6 +1082,7 @@ mps_status mps_last_sweeps(mps_t h, int32_t g, int32_t* sweeps) {
 }
 
 mps_status mps_export_site(mps_t h, int32_t site, float* B, int32_t* dims3) {
+  DEVICE_GUARD(h);
   if (!h || !dims3) return MPS_E_INVAL;
   if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
   mps_status st = check_sticky(h);
@@ -1021,6 +1101,7 @@ mps_status mps_export_site(mps_t h, int32_t site, float* B, int32_t* dims3) {
 }
 
 mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t* dims3) {
+  DEVICE_GUARD(h);
   if (!h || !B || !dims3) return MPS_E_INVAL;
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (site < 0 || site >= h->N) return set_err(h, MPS_E_RANGE, "site out of range");
@@ -1064,6 +1145,7 @@ mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t*
 }
 
 mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* B, const int32_t* dims) {
+  DEVICE_GUARD(h);
   if (!h || !B || !dims || count < 1) return MPS_E_INVAL;
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (first < 0 || first + count > h->N) return set_err(h, MPS_E_RANGE, "sites out of range");
@@ -1142,6 +1224,7 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
 }
 
 mps_status mps_set_lambda(mps_t h, int32_t bond, const float* lam, int32_t len) {
+  DEVICE_GUARD(h);
   if (!h || !lam || len < 1) return MPS_E_INVAL;
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (bond < -1 || bond > h->N - 1) return set_err(h, MPS_E_RANGE, "bond out of range");
@@ -1159,6 +1242,7 @@ mps_status mps_set_lambda(mps_t h, int32_t bond, const float* lam, int32_t len) 
 }
 
 mps_status mps_amplitude(mps_t h, const uint8_t* digits, double* re_im) {
+  DEVICE_GUARD(h);
   if (!h || !digits || !re_im) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -1192,6 +1276,7 @@ mps_status mps_amplitude(mps_t h, const uint8_t* digits, double* re_im) {
 }
 
 mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
+  DEVICE_GUARD(h);
   if (!h || !out) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -1235,6 +1320,7 @@ mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
 }
 
 mps_status mps_snapshot_save(mps_t h, void* buf, size_t buf_bytes, size_t* bytes_needed) {
+  DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);
   if (st != MPS_OK) return st;
@@ -1256,6 +1342,7 @@ mps_status mps_snapshot_save(mps_t h, void* buf, size_t buf_bytes, size_t* bytes
 }
 
 mps_status mps_snapshot_load(mps_t h, const void* buf, size_t buf_bytes) {
+  DEVICE_GUARD(h);
   if (!h || !buf) return MPS_E_INVAL;
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
   if (!h->snap.valid) return set_err(h, MPS_E_STATE, "no snapshot saved by this handle");

@@ -10,7 +10,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace eamps {
+
+// cudaFuncSetAttribute (e.g. the >48 KB dynamic shared-memory opt-in) applies to the CURRENT
+// device only: a per-call-site bit mask of the devices already configured. Returns true exactly
+// once per device (thread-safe).
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 constexpr int kMaxClasses = 48;     // pool size classes 2^0 .. 2^47 bytes (blocks >= 256 B)
 constexpr int kMinClass = 8;

@@ -458,10 +458,9 @@ int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int
   static const bool cta_small = getenv("EAMPS_CHOL_PANELS") == nullptr;   // dev A/B switch
   if (max_n <= 128 && cta_small) {
     constexpr int kCholSmem = (2 * 32 * 33 + 2 * 32 * 17) * 16;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
       cudaFuncSetAttribute(k_pc_chol_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
-      attr = true;
     }
     k_pc_chol_cta<<<count, 256, kCholSmem, s>>>(d_desc, d_list, slab);
     k_pc_b_from_l<<<dim3(64, count), 256, 0, s>>>(d_desc, d_list, slab);

@@ -225,11 +225,15 @@ __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G
       int32_t tot;
       int32_t pre = cta_exclusive_scan<int32_t>(cnt, S.iws, &tot);
       for (int x = b; x < e; ++x) S.ord[x] = (S.gk[x] > 0 && !err0) ? pre++ : -1;
+      // the chunk's ledger update, committed only if its allocations succeed (a failed chunk's gates
+      // are dropped with k = 0 and must not count)
+      double logE_c = logE;
+      int guarantee_c = guarantee;
       if (tid == 0) {
         for (int x = 0; x < gn; ++x)
           if (S.ord[x] >= 0) {  // sequential in canonical order: the same summation as the sequential selector
-            logE += S.gdl[x];
-            if (S.gc[x]) guarantee = 0;
+            logE_c += S.gdl[x];
+            if (S.gc[x]) guarantee_c = 0;
           }
       }
       __syncthreads();
@@ -244,6 +248,10 @@ __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G
       __syncthreads();
       const bool ok = pool_batch_alloc(B, 3 * gn, slab, P, &S.bump, P.ceiling, S.present);
       if (!ok && tid == 0) S.err = -3;
+      if (ok) {
+        logE = logE_c;
+        guarantee = guarantee_c;
+      }
       __syncthreads();
       for (int x = tid; x < gn; x += kCommitThreads) {
         GateDesc& gd = desc[g0 + x];
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(kCommitThreads) k_commit(GateDesc* desc, int G
         R.gate_index = j0 + S.ord[x]; R.bond = i; R.chi_before = gd.mid; R.chi_after = k; R.capped = gd.capped;
         R.target_f = gd.t; R.achieved_f = gd.f; R.discarded_weight = gd.disc;
       }
-      j0 += tot;
+      if (ok) j0 += tot;
       __syncthreads();
     }
   }
@@ -395,10 +403,9 @@ __global__ void k_import_scatter(uint8_t* slab, const ImportEntry* ent, const fl
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s) {
   if (count <= 0) return;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_import_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CommitSmem));
-    attr = true;
   }
   k_import_batch<<<1, kCommitThreads, sizeof(CommitSmem), s>>>(slab, st, d_ent, count);
   k_import_scatter<<<count, 256, 0, s>>>(slab, d_ent, src, d);
@@ -410,10 +417,9 @@ void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record*
     k_select_parallel<<<(G + 7) / 8, 256, 0, s>>>(d_desc, G, slab, st);
   else
     k_select_sequential<<<1, 32, 0, s>>>(d_desc, G, slab, st);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CommitSmem));
-    attr = true;
   }
   k_commit<<<1, kCommitThreads, sizeof(CommitSmem), s>>>(d_desc, G, slab, st, d_rec);
 }

@@ -15,6 +15,7 @@
 // Then sigma_j^2 = ||theta v_j||^2/||v_j||^2 (Rayleigh, FP64 accumulation) and sort + tails.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "eamps_internal.cuh"
 #include "jacobi_common.cuh"
@@ -1195,10 +1196,9 @@ int run_svd_blocked(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_l
   k_large_norm<<<count, 256, 0, s>>>(d_desc, d_list, slab, norm2);
   launches += 2;
   const int nb_max = max_np / BLK;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_block_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundSmem);
-    attr = true;
   }
   int sweep = 0;
   bool done = false;
@@ -1233,10 +1233,9 @@ int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, i
                            cudaStream_t s) {
   if (count <= 0) return 0;
   k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
-  static bool pattr = false;
-  if (!pattr) {
+  static std::atomic<unsigned long long> pattr{0};
+  if (first_on_device(pattr)) {
     cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
-    pattr = true;
   }
   const int nb = ((max_n + tcj::PWC - 1) / tcj::PWC) * 2;
   static const bool no_polish = getenv("EAMPS_NO_POLISH") != nullptr;   // dev A/B switch
@@ -1248,6 +1247,33 @@ int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, i
   cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
   return 3;
+}
+
+// The side stream of the two-group round schedule and its two events: created once per device
+// (cudaStream/cudaEvent are device-bound) and kept for the life of the process, instead of a
+// create/destroy per wave. Returns false (one group is used) if creation fails.
+static bool side_stream(cudaStream_t* s2, cudaEvent_t* go, cudaEvent_t* done) {
+  struct Side { cudaStream_t s = nullptr; cudaEvent_t go = nullptr, done = nullptr; bool bad = false; };
+  static Side side[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  Side& x = side[dev];
+  if (!x.s && !x.bad) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.go, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x.bad = true;
+      x.s = nullptr;
+    }
+  }
+  if (x.bad) return false;
+  *s2 = x.s;
+  *go = x.go;
+  *done = x.done;
+  return true;
 }
 
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
@@ -1271,13 +1297,12 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   bool any_pc = false;
   for (int g = 0; g < count; ++g) any_pc |= h_desc[h_list[g]].jrows > 0;
   if (any_pc) launches += launch_precond_large(d_desc, d_list, count, max_n, slab, s);   // after the norm
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
     cudaFuncSetAttribute(tcj::k_tc_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kInnerSmem);
     cudaFuncSetAttribute(tcj::k_tc_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotSmem);
     cudaFuncSetAttribute(tcj::k_tc_rot_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotWsSmem);
-    attr = true;
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
@@ -1294,16 +1319,15 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   static const int nstreams = getenv("EAMPS_TC_STREAMS") ? atoi(getenv("EAMPS_TC_STREAMS")) : 2;
   // (only for small round grids: measured chi = 1024 x 16 gates, 512 CTAs a round: -8.5%;
   // chi = 256 x 1024 gates, 8192 CTAs a round: +2%)
-  const int ngroups = (!prof && nstreams >= 2 && count >= 2 && count * pairs_max < 2048) ? 2 : 1;
-  const int gsplit[3] = {0, ngroups == 2 ? count / 2 : count, count};
+  const int ngroups_want = (!prof && nstreams >= 2 && count >= 2 && count * pairs_max < 2048) ? 2 : 1;
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_go = nullptr, ev_done = nullptr;
+  int ngroups = ngroups_want;
+  if (ngroups == 2 && !side_stream(&s2, &ev_go, &ev_done)) ngroups = 1;   // no side stream: one group
+  const int gsplit[3] = {0, ngroups == 2 ? count / 2 : count, count};
   if (ngroups == 2) {
-    cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&ev_go, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
-    cudaEventRecord(ev_go, s);              // the preconditioner / init / norms are done
-    cudaStreamWaitEvent(s2, ev_go, 0);
+    if (cudaEventRecord(ev_go, s) != cudaSuccess) return launches;   // (surfaces as MPS_E_CUDA via CKL)
+    cudaStreamWaitEvent(s2, ev_go, 0);      // the preconditioner / init / norms are done
   }
   int sweep = 0;
   bool done = false;
@@ -1352,11 +1376,6 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     done = (h_pinned_flag[0] == 0);
     static const bool dbg = getenv("EAMPS_TC_DEBUG") != nullptr;
     if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
-  }
-  if (ngroups == 2) {
-    cudaEventDestroy(ev_go);
-    cudaEventDestroy(ev_done);
-    cudaStreamDestroy(s2);                  // (its work is complete: the last check synchronised s)
   }
   if (!done) *error_out = -6;
   if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);

@@ -346,11 +346,10 @@ int vrep_tile_rows(int m, int n) {
 template <int GT, int R>
 static void launch_medium_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem_theta, size_t smem_vrep,
                             int tile_rows, int max_sweeps, int threads, uint8_t* slab, DevState* st, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaFuncSetAttribute(k_svd_theta<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_svd_vrep<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr_set = true;
   }
   k_svd_theta<GT, R><<<count, threads, smem_theta, s>>>(d_desc, d_list, slab, st, max_sweeps);
   k_svd_vrep<GT, R><<<count, threads, smem_vrep, s>>>(d_desc, d_list, slab, st, tile_rows);

@@ -398,6 +398,25 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
     // pair-planar Householder QR and B = R^H (householder_planar): packed FP32x2 row pairs
     if (gd.jrows > 0) norm2 = load_b_planar<NT>(reinterpret_cast<const float2*>(slab + gd.ws_theta), A, m, n, s_wn);
     else norm2 = householder_planar<NT>(gth, A, m, n, s_rdiag, s_wn, s_xn2, s_x0);
+  } else if (gd.jrows > 0) {
+    // B = L (= R^H) from the FP64 Gram + Cholesky preconditioner (precond_large.cu; n x n, ld n, in
+    // the theta workspace) into the top n rows of A (ld m). An FP32 Householder R would carry a
+    // normwise backward error ~eps32 sigma_max, i.e. no relative accuracy for sigma_j << sigma_max
+    // (measured: 0.19 relative on a config-4 MPO theta with sigma_min ~1e-6 sigma_max); the FP64
+    // Cholesky's error is ~eps64 kappa^2 instead.
+    const float2* __restrict__ Bg = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+    float nrm = 0.f;
+    for (int x = tid; x < m * n; x += NT) {
+      const int c = x / m, r = x % m;
+      const float2 v = r < n ? Bg[(size_t)c * n + r] : make_float2(0.f, 0.f);
+      A[x] = v;
+      nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, nrm));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) s_wn[warp] = nrm;
+    __syncthreads();
+    for (int w = 0; w < nw; ++w) norm2 += s_wn[w];
   } else {
     float nrm = 0.f;
     for (int x = tid; x < m * n; x += NT) {
@@ -625,10 +644,9 @@ __global__ void __launch_bounds__(qr_threads<GT, R, PK>()) k_svd_qr(GateDesc* de
 template <int GT, int R, int PK>
 void launch_qr_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, uint8_t* slab,
                  DevState* st, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaFuncSetAttribute(k_svd_qr<GT, R, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr_set = true;
   }
   // Jacobi tolerance (relative |gamma| / sqrt(alpha beta)); EAMPS_QR_TOL overrides it for A/B runs
   static const float tol_min = getenv("EAMPS_QR_TOL") ? (float)atof(getenv("EAMPS_QR_TOL")) : 7.62939453e-6f;

@@ -210,10 +210,9 @@ int small_group(int m) {
 template <int GT, int R>
 static void launch_small_t(GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, int max_sweeps, int threads,
                            uint8_t* slab, DevState* st, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaFuncSetAttribute(k_svd_small<GT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr_set = true;
   }
   k_svd_small<GT, R><<<count, threads, smem, s>>>(d_desc, d_list, slab, st, max_sweeps);
 }

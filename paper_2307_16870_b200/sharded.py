@@ -51,6 +51,27 @@ def partition(n_sites: int, world: int, weights=None):
     return [(cuts[g], cuts[g + 1]) for g in range(world)]
 
 
+def predicted_site_cost(n_sites: int, depth: int, d: int = 2, chi_cap: int = 0):
+    """Per-site cost model for partition(): the predicted sum over the run of chi^3 at the site's
+    right bond (the SVD of a theta with chi_l ~ chi_r ~ chi costs ~chi^3). chi of bond
+    b after t brickwork layers is bounded by the rank bound min(d^(t+1), d^(b+1), d^(N-1-b)) (the
+    bulk grows by d per layer from the product state, the chain ends are limited by the Hilbert
+    space of the shorter side, SURVEY §8(d) "rank bound"), capped at chi_cap. The ~12 edge sites
+    of a 300-site chain stay far below the bulk, so uniform blocks underload the edge ranks."""
+    cost = np.zeros(n_sites)
+    for b in range(n_sites):
+        edge = min(b + 1, n_sites - 1 - b)
+        tot = 0.0
+        for t in range(depth):
+            e = float(min(t + 1, edge))
+            chi = d ** min(e, 60.0)
+            if chi_cap > 0:
+                chi = min(chi, float(chi_cap))
+            tot += chi ** 3
+        cost[b] = max(tot, 1.0)
+    return cost
+
+
 class GpuEngine:
     """Adapter of the C-ABI binding (MPS) to the engine interface of ShardedMPS (device tensors)."""
 
@@ -179,16 +200,17 @@ class ShardedMPS:
     """
 
     def __init__(self, n_sites: int, engine_factory, comm=None, blocks=None, device=None,
-                 cdtype=torch.complex64, rdtype=torch.float32):
+                 cdtype=torch.complex64, rdtype=torch.float32, weights=None):
         """comm: DistComm() (default when torch.distributed is initialised), ThreadComm, or None
-        for a single block (world 1)."""
+        for a single block (world 1). blocks: explicit [lo, hi) per rank, else partition() by
+        `weights` (e.g. predicted_site_cost; default uniform)."""
         if comm is None and dist.is_available() and dist.is_initialized():
             comm = DistComm()
         self.comm = comm
         self.rank = comm.rank if comm is not None else 0
         self.world = comm.world if comm is not None else 1
         self.N = n_sites
-        self.blocks = partition(n_sites, self.world) if blocks is None else list(blocks)
+        self.blocks = partition(n_sites, self.world, weights) if blocks is None else list(blocks)
         self.lo, self.hi = self.blocks[self.rank]
         self.ghost = 1 if self.rank < self.world - 1 else 0
         self.eng = engine_factory(self.hi - self.lo + self.ghost)

@@ -65,3 +65,90 @@ def test_gpu_sharded_matches_single_handle(world):
     assert ov >= 1 - 1e-9, ov
     for b in range(N - 1):
         np.testing.assert_allclose(lams[b + 1].cpu().numpy(), ref.mps_schmidt_values(b), rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_sharded_boundary_gates_vs_oracle(world):
+    """a6 against the ORACLE (not the GPU itself): every boundary gate (hi_g - 1, hi_g) of the
+    sharded run -- the gate whose right site is the ghost copy fetched from rank g+1 -- is re-run on
+    a 2-site complex128 oracle holding exactly the inputs the rank's handle saw (B_{hi-1}, the
+    ghost B_hi, lambda_{hi-2}) at the target the GPU issued; spectra at the strict north-star bar,
+    kept rank (near-ties excused) and f. Then the boundary write-back is checked: rank g+1's first
+    site and lambda equal what rank g computed."""
+    import oracle
+    import paper_2307_16870_b200 as pk
+    from paper_2307_16870_b200.sharded import GpuEngine, ShardedMPS, ThreadComm
+    from test_gpu_parity import SIG_RTOL, near_tie, spectra_close
+    N, layers, kw = _circuit()
+    hub = ThreadComm.Hub(world)
+    checks, errs = {}, []
+
+    class CheckingEngine(GpuEngine):
+        def __init__(self, mps, n_local, boundary_local):
+            super().__init__(mps)
+            self.bl = boundary_local     # local site of the boundary gate (None on the last rank)
+            self.pending = None
+            self.done = []
+
+        def layer_begin(self, sites, Us):
+            self.pending = None
+            if self.bl is not None and len(sites) and int(sites[-1]) == self.bl:
+                i = self.bl
+                lam = self.m.mps_schmidt_values(i - 1) if i > 0 else None
+                self.pending = (len(sites) - 1, self.m.mps_export_site(i), self.m.mps_export_site(i + 1), lam,
+                                np.asarray(Us[-1]))
+            return super().layer_begin(sites, Us)
+
+        def layer_step(self):
+            rem = super().layer_step()
+            if rem == 0 and self.pending is not None:
+                g, BL, BR, lam, U = self.pending
+                rec = self.m.mps_truncation_log()[-(g + 1)]
+                self.done.append((BL, BR, lam, U, rec, self.m.mps_last_spectrum(g)))
+                self.pending = None
+            return rem
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            from paper_2307_16870_b200.sharded import partition
+            lo, hi = partition(N, world)[r]
+            bl = (hi - lo - 1) if r < world - 1 else None
+            eng = {}
+
+            def factory(n):
+                eng["e"] = CheckingEngine(pk.MPS(n, slab_bytes=64 << 20, **kw), n, bl)
+                return eng["e"]
+
+            sh = ShardedMPS(N, factory, comm=ThreadComm(hub, r), device="cuda:0")
+            sh.run(layers)
+            checks[r] = eng["e"].done
+        except Exception as e:
+            errs.append(e)
+            raise
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    n_checked = 0
+    for r in range(world - 1):
+        assert len(checks[r]) >= 1
+        for BL, BR, lam, U, rec, sg in checks[r]:
+            o = oracle.OracleMPS(2, strategy="fixed", f_fixed=rec["target_f"])
+            o.import_site(0, BL)
+            o.import_site(1, BR)
+            if lam is not None:
+                o.set_lambda(-1, lam.astype(np.float64))
+            o.apply_layer(np.zeros(1, np.int32), U[None])
+            so = o.last_spectrum(0)
+            assert spectra_close(sg, so) < SIG_RTOL, (r, spectra_close(sg, so))
+            ro = o.records()[0]
+            if ro["chi_after"] != rec["chi_after"]:
+                assert near_tie(so, rec["target_f"], ro["chi_after"])
+            else:
+                assert abs(ro["achieved_f"] - rec["achieved_f"]) < 1e-6
+            n_checked += 1
+    assert n_checked >= (world - 1) * 3

@@ -193,3 +193,29 @@ def test_ledger_strategy_ordering():
             logE += np.log(t + (1 - t) * 0.5 * surplus[j])
         res[strat] = np.exp(logE)
     assert fmin * (1 - 1e-10) <= res["global"] <= res["naive"]
+
+
+def _two_pair_chain(w1, w2):
+    """4-site chain of two independent pairs whose thetas have Schmidt weights w1 and w2 (lambda = 1)."""
+    tensors = []
+    for w in (w1, w2):
+        BL = np.zeros((1, 2, 2), np.complex128)
+        BL[0, 0, 0], BL[0, 1, 1] = np.sqrt(w[0]), np.sqrt(w[1])
+        BR = np.eye(2, dtype=np.complex128).reshape(2, 2, 1)
+        tensors += [BL, BR]
+    return tensors
+
+
+def test_ledger_record_example():
+    """record [0.99, 0.98] -> estimate 0.9702 (E12: the running
+    product of truncation fidelities). Two updates whose rank-1 cuts keep exactly 0.99 and 0.98 of
+    the weight, at a fixed per-update target below both."""
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))["ledger"]["record_0.99_0.98"]
+    o = oracle.OracleMPS(4, strategy="fixed", f_fixed=0.975)
+    for i, B in enumerate(_two_pair_chain((0.99, 0.01), (0.98, 0.02))):
+        o.import_site(i, B)
+    o.apply_layer(np.array([0, 2], np.int32), np.stack([np.eye(4, dtype=np.complex64)] * 2))
+    fs = [r["achieved_f"] for r in o.records()]
+    assert [r["chi_after"] for r in o.records()] == [1, 1]
+    assert abs(fs[0] - 0.99) < 1e-14 and abs(fs[1] - 0.98) < 1e-14
+    assert abs(o.estimate()["est"] - g["value"]) < 1e-14
