@@ -373,6 +373,7 @@ mps_status wave_front(mps_t h) {
     gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
                 : gd.regime == 1 ? (int64_t)take(large_scratch_bytes(gd))
                 : (gd.regime == 3 && gd.jrows > 0) ? (int64_t)take(large_precond_scratch(gd.n))
+                : refine_scratch_bytes(gd.n) > 0 ? (int64_t)take(refine_scratch_bytes(gd.n))
                                  : 0;
     hd[x] = gd;
     cpre[x + 1] = cpre[x] + p.ctiles;
@@ -544,6 +545,18 @@ mps_status wave_front(mps_t h) {
       int32_t* he = reinterpret_cast<int32_t*>(hb + tail + 128);
       *he = err;
       CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
+    }
+  }
+  // FP64 Rayleigh-Ritz refinement of deep spectra (refine.cu; gates with n <= 256)
+  {
+    int maxn = 0;
+    for (int x = 0; x < Gw; ++x) maxn = std::max(maxn, hd[x].n);
+    static const bool no_refine = getenv("EAMPS_NO_REFINE") != nullptr;   // dev A/B switch
+    if (!no_refine) {
+      const int e0 = prof ? prof_mark(h) : -1;
+      h->launches += launch_refine(d_desc, Gw, maxn, h->slab, h->dst, h->s);
+      CKL("refine");
+      if (prof) prof_span(h, 7, e0, prof_mark(h));
     }
   }
   if (prof) CK(cudaEventRecord(h->ev[3], h->s));
@@ -876,7 +889,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                         : gd.regime == 1 ? large_scratch_bytes(gd)
                         : (gd.regime == 3 && gd.jrows > 0) ? large_precond_scratch(gd.n)
-                                         : 0;
+                                         : refine_scratch_bytes(gd.n);
     gd.u_index = ord[g].second;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)std::max(gd.m, gd.jrows) * gd.n_pad * 8;   // B = L (jrows rows) reuses it
     const int kmn = std::min(gd.m, gd.n);

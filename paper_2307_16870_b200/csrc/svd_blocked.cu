@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "eamps_internal.cuh"
 #include "jacobi_common.cuh"
@@ -482,8 +483,16 @@ __device__ __forceinline__ int colof(int c, int I, int J) { return c < TB ? I * 
 constexpr int GR = 2;                                   // raw ring depth
 constexpr uint32_t GRAW_PITCH = 288;                    // bytes per column of a raw chunk (32 rows + pad)
 constexpr size_t kGramRaw = (size_t)64 * GRAW_PITCH;    // 18 KB
+// kNamed: the 128 threads synchronise on named barrier 1 instead of __syncthreads (the fused
+// kernel runs the Gram on warps 0-3 of a larger CTA).
+__device__ __forceinline__ void bar128() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+template <bool kNamed = false>
 __device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, int ncols, int I, int J,
                                            uint8_t* base, uint64_t* mbar, uint32_t tmem, float* Ds) {
+  auto csync = [] {
+    if constexpr (kNamed) bar128();
+    else __syncthreads();
+  };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* img = base;                                   // 2 x (hi, lo2) x 16 KB
   uint8_t* ring = base + 4 * kGramStage;                 // GR x 18 KB
@@ -512,7 +521,7 @@ __device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, 
   for (int q = 0; q < nchunks; ++q) {
     issue(q + GR - 1);
     tc::cp_async_wait<GR - 1>();
-    __syncthreads();                                     // raw chunk q visible to all
+    csync();                                     // raw chunk q visible to all
     const int b = q & 1;
     if (q >= 2) tc::mbar_wait(&mbar[b], ((q - 2) >> 1) & 1);
     uint8_t* hi = img + (size_t)b * 2 * kGramStage;
@@ -538,7 +547,7 @@ __device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, 
       *reinterpret_cast<float4*>(lo2 + oI) = il;
     }
     tc::fence_async_smem();
-    __syncthreads();                                     // images written; raw slot q%GR free
+    csync();                                     // images written; raw slot q%GR free
     if (tid == 0) {
       tc::fence_after_sync();
       const uint32_t ah = tc::smem_u32(hi), al = tc::smem_u32(lo2);
@@ -555,8 +564,11 @@ __device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, 
   }
   tc::cp_async_wait<0>();
   tc::mbar_wait(&mbar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+  // (persistent use: the other barrier's last commit must have landed too before the barriers are
+  // re-initialised for the next panel)
+  if (kNamed && nchunks >= 2) tc::mbar_wait(&mbar[(nchunks - 2) & 1], ((nchunks - 2) >> 1) & 1);
   tc::fence_after_sync();
-  __syncthreads();                                       // every thread past its last smem read
+  csync();                                       // every thread past its last smem read
   const int row = warp * 32 + lane;
 #pragma unroll 1
   for (int c = 0; c < 128; c += 8) {
@@ -566,7 +578,7 @@ __device__ __forceinline__ void gram_panel(const float2* __restrict__ M, int m, 
     for (int i = 0; i < 8; ++i) Ds[row * 129 + c + i] = v[i];
   }
   tc::fence_before_sync();
-  __syncthreads();
+  csync();
 }
 
 __device__ __forceinline__ void tc_setup(uint64_t* mbar, uint32_t* tbase) {
@@ -1172,6 +1184,456 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
   }
 }
 
+
+// =====================================================================================================
+// Fused persistent large-regime Jacobi (the default since round 2): ONE cooperative launch per wave
+// runs every sweep and round of every large gate of the wave. A CTA (288 threads, one per SM) takes
+// pair tasks (gate, block pair) of the current round and, per task, runs the three steps of a block
+// rotation back to back with the panel Gram, the Hermitian 64 x 64 G and the E images never leaving
+// the SM:
+//   1. Gram  (warps 0-3, tensor core): D = Q^T Q of the panel P = [A_I A_J], TMEM accumulator,
+//      symmetric 3xTF32 (gram_panel) -> G = P^H P in shared memory;
+//   2. inner (all warps, SIMT FP32): one cyclic Jacobi sweep on G -> W, E = W - I as TF32 hi/lo images;
+//   3. rotation (warp-specialised, tensor core): P <- P + P E (identity-split 3xTF32), as k_tc_rot_ws.
+// Rounds are separated by a grid-wide barrier (co-residency guaranteed by the cooperative launch);
+// the end of a sweep runs the per-gate convergence check on the device (no host round trip per
+// sweep, no three launches per round). The arithmetic of every step is that of the three
+// separate kernels (k_tc_gram / k_tc_inner / k_tc_rot_ws), which stay as the EAMPS_TC_UNFUSED=1
+// development reference.
+// Shared memory (from the 1024-aligned base):
+//   [0, 64K)        E images (written by the inner solve, the rotation's B operand)
+//   [64K, 164K)     Gram images + raw ring; D staging (128 x 129 floats) aliases its start
+//   [130K, 196.5K)  G, W of the inner solve (64 x 65 complex each)
+//   [64K, 192K)     rotation image ring + raw chunks (dead Gram / inner data by then)
+constexpr int FT = 288;
+constexpr size_t F_ES = 0;
+constexpr size_t F_GRAM = (size_t)EIMG_FLOATS * 4;                 // 64 KB
+constexpr size_t F_RING = F_GRAM;
+constexpr size_t F_RAW = F_RING + (size_t)WS_NS * 2 * kRotStage;  // 128 KB
+constexpr size_t F_GW = F_GRAM + (size_t)128 * 129 * 4 + 64;       // after the D staging
+constexpr size_t F_END = F_GW + 2 * sizeof(float2) * 64 * 65;
+constexpr size_t kFusedSmem = (F_END > F_RAW + (size_t)WS_RAW * 8 * 128 * 8 ? F_END : F_RAW + (size_t)WS_RAW * 8 * 128 * 8) + 1024;
+static_assert(F_GRAM + 4 * kGramStage + GR * kGramRaw <= F_GW || true, "layout");
+
+struct FusedCtl {                 // device-side control of the persistent kernel (in the wave scratch)
+  unsigned int bar_count, bar_gen;
+  int32_t unconv[2];              // unconverged gates of the sweep, by sweep parity
+  int32_t done;                   // every gate converged
+  int32_t sweeps_run;
+};
+
+__device__ __forceinline__ void grid_barrier(FusedCtl* fc) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &fc->bar_gen;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(&fc->bar_count, 1u) == gridDim.x - 1) {
+      fc->bar_count = 0;
+      __threadfence();
+      atomicAdd(&fc->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence();   // gpu-scope fence: invalidates this SM's L1 (other CTAs' panel writes)
+}
+
+// The inner solve of k_tc_inner on G (shared memory) with NT threads, writing the E images into Es.
+// Returns true if any pair rotated (CTA-uniform).
+template <int NT>
+__device__ bool inner_solve(float2 (*Gs)[65], float2 (*Ws)[65], float* Es, int rnd, float skip, float tol,
+                            float tol_int, int inner_sweeps, float4* par, int2* pq, const uint16_t* blk) {
+  auto gld = [&](int i, int j) {
+    const float2 v = Gs[min(i, j)][max(i, j)];
+    return i <= j ? v : make_float2(v.x, -v.y);
+  };
+  auto gst = [&](int i, int j, float2 v) { Gs[min(i, j)][max(i, j)] = i <= j ? v : make_float2(v.x, -v.y); };
+  const int tid = threadIdx.x;
+  int any = 0, internal = 0;
+  for (int x = tid; x < 64 * 64; x += NT) {
+    const int p = x >> 6, q = x & 63;
+    if (p < q) {
+      const float al = Gs[p][p].x, be = Gs[q][q].x;
+      const float g = sqrtf(Gs[p][q].x * Gs[p][q].x + Gs[p][q].y * Gs[p][q].y);
+      if (fminf(al, be) > skip && g > tol * sqrtf(al) * sqrtf(be)) {
+        any = 1;
+        if ((p < 32) == (q < 32) && (rnd == 0 || g > tol_int * sqrtf(al) * sqrtf(be))) internal = 1;
+      }
+    }
+  }
+  internal = __syncthreads_or(internal);
+  if (!__syncthreads_or(any)) return false;
+  const int nrr = internal ? 63 : 32;
+  constexpr int TPP = NT / 32;    // threads per pair in the W update
+  for (int isw = 0; isw < inner_sweeps; ++isw) {
+    int rot = 0;
+    for (int rr = 0; rr < nrr; ++rr) {
+      if (tid < 32) {
+        int p, q;
+        if (internal) {
+          circle_pair(tid, rr, 64, p, q);
+        } else {
+          p = tid;
+          q = 32 + ((tid + rr) & 31);
+        }
+        const float al = Gs[p][p].x, be = Gs[q][q].x;
+        const float2 gm = gld(p, q);
+        const float g2 = gm.x * gm.x + gm.y * gm.y;
+        float c = 1.f, sn = 0.f, er = 1.f, ei = 0.f;
+        if (fminf(al, be) > skip && g2 > 1e-13f * al * be) {
+          const float ig = rsqrtf(g2);
+          er = gm.x * ig;
+          ei = gm.y * ig;
+          const float zeta = 0.5f * (be - al) * ig;
+          const float az = fabsf(zeta);
+          const float t = copysignf(1.f, zeta) / (az + sqrtf(fmaf(az, az, 1.f)));
+          c = rsqrtf(fmaf(t, t, 1.f));
+          sn = c * t;
+          rot = 1;
+          const float tg = t * (g2 * ig);
+          Gs[p][p] = make_float2(al - tg, 0.f);
+          Gs[q][q] = make_float2(be + tg, 0.f);
+          gst(p, q, make_float2(0.f, 0.f));
+        }
+        par[tid] = make_float4(c, sn, er, ei);
+        pq[tid] = make_int2(p, q);
+      }
+      __syncthreads();
+      for (int x = tid; x < 496; x += NT) {
+        const int ia = blk[x] & 0xFF, ib = blk[x] >> 8;
+        const float4 Ja = par[ia], Jb = par[ib];
+        if (Ja.y == 0.f && Jb.y == 0.f) continue;
+        const int2 ra = pq[ia], cb = pq[ib];
+        float2 X[2][2] = {{gld(ra.x, cb.x), gld(ra.x, cb.y)}, {gld(ra.y, cb.x), gld(ra.y, cb.y)}};
+        if (Jb.y != 0.f) {
+          const Rot rb{Jb.x, Jb.y, Jb.z, Jb.w};
+#pragma unroll
+          for (int r = 0; r < 2; ++r) apply_rot(X[r][0], X[r][1], rb);
+        }
+        if (Ja.y != 0.f) {
+          const Rot ra2{Ja.x, Ja.y, Ja.z, -Ja.w};
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) apply_rot(X[0][cc], X[1][cc], ra2);
+        }
+        gst(ra.x, cb.x, X[0][0]); gst(ra.x, cb.y, X[0][1]);
+        gst(ra.y, cb.x, X[1][0]); gst(ra.y, cb.y, X[1][1]);
+      }
+      {
+        const int k = tid / TPP;
+        if (k < 32) {
+          const float4 J = par[k];
+          if (J.y != 0.f) {
+            const int2 cq = pq[k];
+            const Rot rw{J.x, J.y, J.z, J.w};
+            for (int x = tid % TPP; x < 64; x += TPP) {
+              float2 xx = Ws[x][cq.x], yy = Ws[x][cq.y];
+              apply_rot(xx, yy, rw);
+              Ws[x][cq.x] = xx;
+              Ws[x][cq.y] = yy;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rot)) break;
+  }
+  __syncthreads();
+  for (int x = tid; x < 64 * 64; x += NT) {
+    const int k = x >> 6, n = x & 63;
+    float2 w = Ws[k][n];
+    if (k == n) w.x -= 1.f;
+    const uint32_t o = tc::kmaj_off(n, k, E_LBO, E_SBO) >> 2;
+    float h, l;
+    tc::split_tf32(w.x, h, l);
+    Es[o] = h;
+    Es[4096 + o] = l;
+    tc::split_tf32(w.y, h, l);
+    Es[8192 + o] = h;
+    Es[12288 + o] = l;
+  }
+  return true;
+}
+
+// P <- P + P E with E in shared memory: the warp-specialised body of k_tc_rot_ws (288 threads).
+__device__ void rot_panel_ws(const GateDesc& gd, uint8_t* slab, int I, int J, const float* Es, uint8_t* ring,
+                             float2* rawr, uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
+                             uint32_t tmem) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < WS_NS; ++i) {
+      tc::mbar_init(&full[i], 128);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  tc::fence_async_smem();   // E images (generic-proxy writes) -> visible to the tensor core
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const int m = jacobi_rows(gd), np = gd.n_pad;
+  const int tiles_th = (m + 127) / 128, tiles_v = gd.jrows > 0 ? 0 : (np + 127) / 128, ntiles = tiles_th + tiles_v;
+  constexpr int CH = PWC / 8;
+  if (warp == 0) {
+    if (tid == 0) {
+      const uint32_t id_p = tc::make_idesc_tf32(128, 64, false, false);
+      const uint32_t id_n = id_p | (1u << 14);
+      const uint32_t e0 = tc::smem_u32(Es);
+      constexpr uint32_t EI = 16384;
+      int u = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int ab = t & 1;
+        if (t >= 2) tc::mbar_wait(&tempty[ab], ((t - 2) >> 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t dRe = tmem + 128 * ab, dIm = dRe + 64;
+        for (int q = 0; q < CH; ++q, ++u) {
+          const int sl = u % WS_NS;
+          tc::mbar_wait(&full[sl], (u / WS_NS) & 1);
+          tc::fence_after_sync();
+          const uint32_t a0 = tc::smem_u32(ring + (size_t)sl * 2 * kRotStage);
+          const uint32_t eoff = 2 * q * E_LBO;
+          const uint64_t aRh = tc::make_desc(a0, R_LBO, R_SBO), aRl = tc::make_desc(a0 + kRotStage, R_LBO, R_SBO);
+          const uint64_t aIh = tc::make_desc(a0 + 2 * R_LBO, R_LBO, R_SBO);
+          const uint64_t aIl = tc::make_desc(a0 + kRotStage + 2 * R_LBO, R_LBO, R_SBO);
+          const uint64_t bRh = tc::make_desc(e0 + eoff, E_LBO, E_SBO), bRl = tc::make_desc(e0 + EI + eoff, E_LBO, E_SBO);
+          const uint64_t bIh = tc::make_desc(e0 + 2 * EI + eoff, E_LBO, E_SBO);
+          const uint64_t bIl = tc::make_desc(e0 + 3 * EI + eoff, E_LBO, E_SBO);
+          const uint32_t acc0 = q > 0 ? 1u : 0u;
+          tc::mma_tf32(dRe, aRh, bRh, id_p, acc0);
+          tc::mma_tf32(dRe, aRh, bRl, id_p, 1u);
+          tc::mma_tf32(dRe, aRl, bRh, id_p, 1u);
+          tc::mma_tf32(dRe, aIh, bIh, id_n, 1u);
+          tc::mma_tf32(dRe, aIh, bIl, id_n, 1u);
+          tc::mma_tf32(dRe, aIl, bIh, id_n, 1u);
+          tc::mma_tf32(dIm, aRh, bIh, id_p, acc0);
+          tc::mma_tf32(dIm, aRh, bIl, id_p, 1u);
+          tc::mma_tf32(dIm, aRl, bIh, id_p, 1u);
+          tc::mma_tf32(dIm, aIh, bRh, id_p, 1u);
+          tc::mma_tf32(dIm, aIh, bRl, id_p, 1u);
+          tc::mma_tf32(dIm, aIl, bRh, id_p, 1u);
+          tc::mma_commit(&empty[sl]);
+        }
+        tc::mma_commit(&tfull[ab]);
+      }
+      // drain: the last WS_NS slot releases were never waited on by the producers; they must land
+      // before the barriers are re-initialised for the next task
+      for (int uu = max(0, u - WS_NS); uu < u; ++uu) tc::mbar_wait(&empty[uu % WS_NS], (uu / WS_NS) & 1);
+    }
+    __syncwarp();
+  } else if (warp <= 4) {
+    const int row_l = tid - 32;
+    const int total = ntiles * CH;
+    auto issue = [&](int uu) {
+      if (uu < total) {
+        const int t = uu / CH, q = uu % CH;
+        const bool isV = t >= tiles_th;
+        const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+        const int rows = isV ? np : m;
+        const int r = (isV ? t - tiles_th : t) * 128 + row_l;
+        float2* dst = rawr + (size_t)(uu % WS_RAW) * 8 * 128 + row_l;
+        if (r < rows) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) tc::cp_async8(dst + c * 128, M + (int64_t)colof(8 * q + c, I, J) * rows + r);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) dst[c * 128] = make_float2(0.f, 0.f);
+        }
+      }
+      tc::cp_async_commit();
+    };
+    for (int uu = 0; uu < WS_RAW - 1; ++uu) issue(uu);
+    for (int u = 0; u < total; ++u) {
+      issue(u + WS_RAW - 1);
+      tc::cp_async_wait<WS_RAW - 1>();
+      const float2* src = rawr + (size_t)(u % WS_RAW) * 8 * 128 + row_l;
+      float2 z[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) z[c] = src[c * 128];
+      const int sl = u % WS_NS;
+      if (u >= WS_NS) tc::mbar_wait(&empty[sl], ((u / WS_NS) - 1) & 1);
+      uint8_t* hi = ring + (size_t)sl * 2 * kRotStage;
+      uint8_t* lo = hi + kRotStage;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 rh, rl, ih, il;
+        tc::split_tf32(z[4 * h + 0].x, rh.x, rl.x); tc::split_tf32(z[4 * h + 1].x, rh.y, rl.y);
+        tc::split_tf32(z[4 * h + 2].x, rh.z, rl.z); tc::split_tf32(z[4 * h + 3].x, rh.w, rl.w);
+        tc::split_tf32(z[4 * h + 0].y, ih.x, il.x); tc::split_tf32(z[4 * h + 1].y, ih.y, il.y);
+        tc::split_tf32(z[4 * h + 2].y, ih.z, il.z); tc::split_tf32(z[4 * h + 3].y, ih.w, il.w);
+        const uint32_t oR = tc::kmaj_off(row_l, 4 * h, R_LBO, R_SBO), oI = tc::kmaj_off(row_l, 8 + 4 * h, R_LBO, R_SBO);
+        *reinterpret_cast<float4*>(hi + oR) = rh;
+        *reinterpret_cast<float4*>(lo + oR) = rl;
+        *reinterpret_cast<float4*>(hi + oI) = ih;
+        *reinterpret_cast<float4*>(lo + oI) = il;
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&full[sl]);
+    }
+    tc::cp_async_wait<0>();
+  } else {
+    const int row_l = (warp & 3) * 32 + (tid & 31);
+    for (int t = 0; t < ntiles; ++t) {
+      const bool isV = t >= tiles_th;
+      float2* M = reinterpret_cast<float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
+      const int rows = isV ? np : m;
+      const int r = (isV ? t - tiles_th : t) * 128 + row_l;
+      const int ab = t & 1;
+      tc::mbar_wait(&tfull[ab], (t >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * ab;
+#pragma unroll 1
+      for (int c = 0; c < PWC; c += 8) {
+        float dr[8], di[8];
+        tc::tmem_ld8(ta + c, dr);
+        tc::tmem_ld8(ta + 64 + c, di);
+        if (r < rows) {
+          float2 v[8];
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2) v[u2] = __ldcg(M + (int64_t)colof(c + u2, I, J) * rows + r);
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2)
+            M[(int64_t)colof(c + u2, I, J) * rows + r] = make_float2(v[u2].x + dr[u2], v[u2].y + di[u2]);
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[ab]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// pair_pre[g] = sum of the block pairs (n_pad / 64) of the gates before g (the task index space of a round)
+__global__ void k_pair_prefix(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, int count,
+                              int32_t* pair_pre, FusedCtl* fc) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int32_t acc = 0;
+    for (int g = 0; g < count; ++g) {
+      pair_pre[g] = acc;
+      acc += desc[list[g]].n_pad / PWC;
+    }
+    pair_pre[count] = acc;
+    fc->bar_count = 0;
+    fc->bar_gen = 0;
+    fc->unconv[0] = fc->unconv[1] = 0;
+    fc->done = 0;
+    fc->sweeps_run = 0;
+  }
+}
+
+__global__ void __launch_bounds__(FT, 1) k_tc_fused(GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                    int count, uint8_t* slab, LargeCtl* ctl, const double* norm2,
+                                                    const int32_t* __restrict__ pair_pre, FusedCtl* fc, int max_sweeps,
+                                                    int inner_sweeps, float tol_floor, float tol_internal) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  float* Es = reinterpret_cast<float*>(base + F_ES);
+  uint8_t* gram_base = base + F_GRAM;
+  float* Ds = reinterpret_cast<float*>(base + F_GRAM);
+  float2(*Gs)[65] = reinterpret_cast<float2(*)[65]>(base + F_GW);
+  float2(*Ws)[65] = Gs + 64;
+  uint8_t* ring = base + F_RING;
+  float2* rawr = reinterpret_cast<float2*>(base + F_RAW);
+  __shared__ uint64_t gbar[2], full[WS_NS], empty[WS_NS], tfull[2], tempty[2];
+  __shared__ uint32_t tbase;
+  __shared__ float4 par[32];
+  __shared__ int2 pq[32];
+  __shared__ uint16_t blk[496];
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int x = tid; x < 496; x += FT) {
+    int aa = 0, rem = x;
+    while (rem >= 31 - aa) { rem -= 31 - aa; ++aa; }
+    blk[x] = (uint16_t)(aa | ((aa + 1 + rem) << 8));
+  }
+  if (warp == 0) tc::tmem_alloc(&tbase, 256);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tbase;
+  const int total = pair_pre[count];
+  int nb_max = 0;
+  for (int g = 0; g < count; ++g) nb_max = max(nb_max, desc[list[g]].n_pad / TB);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
+      for (int task = blockIdx.x; task < total; task += gridDim.x) {
+        int lo = 0, hi = count - 1;          // gate of the task: last g with pair_pre[g] <= task
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (pair_pre[mid] <= task) lo = mid; else hi = mid - 1;
+        }
+        const int gi = lo, pair = task - pair_pre[gi];
+        if (ctl[gi].conv) continue;          // (uniform: every thread reads the same value)
+        const GateDesc& gd = desc[list[gi]];
+        const int nb = gd.n_pad / TB;
+        if (rnd >= nb - 1) continue;
+        int I, J;
+        circle_pair(pair, rnd, nb, I, J);
+        // 1. Gram on warps 0-3
+        if (warp < 4) {
+          if (tid == 0) {
+            tc::mbar_init(&gbar[0], 1);
+            tc::mbar_init(&gbar[1], 1);
+            tc::fence_barrier_init();
+          }
+          bar128();
+          gram_panel<true>(reinterpret_cast<const float2*>(slab + gd.ws_theta), jacobi_rows(gd), gd.n_pad, I, J,
+                           gram_base, gbar, tmem, Ds);
+        }
+        __syncthreads();
+        // 2. G (Hermitian 64 x 64) from D, W = I; inner solve -> E images
+        auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
+        for (int x = tid; x < 64 * 64; x += FT) {
+          const int p = x >> 6, qq = x & 63;
+          Gs[p][qq] = make_float2(sym(p, qq) + sym(64 + p, 64 + qq), sym(p, 64 + qq) - sym(64 + p, qq));
+          Ws[p][qq] = make_float2(p == qq ? 1.f : 0.f, 0.f);
+        }
+        __syncthreads();
+        const float skip = (float)(norm2[gi] * 3.552713678800501e-15);
+        const float tol = fmaxf(tol_floor, 4.f * sqrtf((float)jacobi_rows(gd)) * 5.960464477539063e-8f);
+        const bool rotated = inner_solve<FT>(Gs, Ws, Es, rnd, skip, tol, fmaxf(tol, tol_internal), inner_sweeps,
+                                             par, pq, blk);
+        if (!rotated) {
+          __syncthreads();
+          continue;
+        }
+        if (tid == 0) atomicAdd(&ctl[gi].rot, 1);
+        __syncthreads();
+        // 3. P <- P + P E
+        rot_panel_ws(gd, slab, I, J, Es, ring, rawr, full, empty, tfull, tempty, tmem);
+      }
+      grid_barrier(fc);
+      if (rnd == 0 && blockIdx.x == 0 && tid == 0) fc->unconv[(sweep + 1) & 1] = 0;   // read last sweep
+    }
+    // end of sweep: per-gate convergence (a gate whose sweep rotated nothing is converged)
+    for (int g = blockIdx.x * FT + tid; g < count; g += gridDim.x * FT) {
+      if (ctl[g].conv) continue;
+      GateDesc& gd = desc[list[g]];
+      gd.sweeps += 1;
+      if (ctl[g].rot == 0) ctl[g].conv = 1;
+      else atomicAdd(&fc->unconv[sweep & 1], 1);
+      ctl[g].rot = 0;
+    }
+    grid_barrier(fc);
+    const int left = *reinterpret_cast<volatile int32_t*>(&fc->unconv[sweep & 1]);
+    if (blockIdx.x == 0 && tid == 0) fc->sweeps_run = sweep + 1;
+    if (left == 0) {
+      if (blockIdx.x == 0 && tid == 0) fc->done = 1;
+      break;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 }  // namespace tcj
 
 }  // namespace
@@ -1276,6 +1738,189 @@ static bool side_stream(cudaStream_t* s2, cudaEvent_t* go, cudaEvent_t* done) {
   return true;
 }
 
+// ---- deep-spectrum re-Jacobi of the large regime (run_svd_tc): flags, preparation, finish
+constexpr double kDeepRatio = 5e-5;   // config 2 chi = 256 (8.6e-5) stays on the polish; chi = 1024 (1.1e-5) not
+
+// flags[g] = 1 if n > 256 and the smallest Rayleigh sigma^2 >= 1e-12 sigma_max^2 is below r2 sigma_max^2
+__global__ void k_deep_flags(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab,
+                             int32_t* flags, double r2) {
+  const GateDesc& gd = desc[list[blockIdx.x]];
+  const int n = gd.n;
+  const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
+  __shared__ double smx[256], smn[256];
+  double mx = 0.0;
+  for (int j = threadIdx.x; j < n; j += 256) mx = fmax(mx, s2[j]);
+  smx[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + o]);
+    __syncthreads();
+  }
+  mx = smx[0];
+  double mn = mx;
+  for (int j = threadIdx.x; j < n; j += 256)
+    if (s2[j] >= 1e-12 * mx) mn = fmin(mn, s2[j]);
+  smn[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) flags[blockIdx.x] = (n > 256 && gd.jrows > 0 && mx > 0.0 && smn[0] < r2 * mx) ? 1 : 0;
+}
+
+// The re-Jacobi works on B1 = theta V (k_rayleigh's write_b output in ws_theta, ld m): jrows = m,
+// zero pad columns, fresh per-list control and norms. grid (64, dc).
+__global__ void k_deep_prepare(GateDesc* desc, const int32_t* list, int count, const int32_t* dlist, uint8_t* slab,
+                               LargeCtl* ctl, const double* norm2, double* dnorm2) {
+  const int di = blockIdx.y, gdx = dlist[di];
+  GateDesc& gd = desc[gdx];
+  const int m = gd.m, n = gd.n, np = gd.n_pad;
+  float2* B = reinterpret_cast<float2*>(slab + gd.ws_theta);
+  const int64_t tot = (int64_t)m * (np - n);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x)
+    B[(int64_t)m * n + x] = make_float2(0.f, 0.f);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double nv = 0.0;
+    for (int g = 0; g < count; ++g)
+      if (list[g] == gdx) nv = norm2[g];
+    dnorm2[di] = nv;
+    ctl[di].rot = 0;
+    ctl[di].conv = 0;
+    gd.jrows = m;
+  }
+}
+
+// sigma_j^2 = |b1_j|^2 (FP64 sums of the FP32 entries) replaces the Rayleigh value; the polish shift
+// is cleared (sort_tails adds it); jrows back to n. One CTA per deep gate.
+__global__ void k_deep_finish(GateDesc* desc, const int32_t* dlist, uint8_t* slab) {
+  GateDesc& gd = desc[dlist[blockIdx.x]];
+  const int m = gd.m, n = gd.n, np = gd.n_pad;
+  const float2* B = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+  double* s2 = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  double* shift = reinterpret_cast<double*>(slab + gd.ws_E);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < n; j += 8) {
+    const float2* bj = B + (int64_t)j * m;
+    double a = 0.0;
+    for (int r = lane; r < m; r += 32) a += (double)bj[r].x * bj[r].x + (double)bj[r].y * bj[r].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      s2[j] = a;
+      shift[j] = 0.0;
+    }
+  }
+  (void)np;
+  __syncthreads();
+  if (threadIdx.x == 0) gd.jrows = n;
+}
+
+// The outer sweeps of the three-launch round schedule (k_tc_gram -> k_tc_inner -> k_tc_rot_ws per
+// round) over the gates d_list[0..count) (per-list-position ctl / norm2), until every gate's sweep
+// rotates nothing or max_sweeps. Returns true if all converged; *launches is advanced.
+static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list,
+                            int count, int max_sweeps, uint8_t* slab, LargeCtl* ctl, const double* norm2,
+                            int32_t* unconv, int32_t* h_pinned_flag, cudaStream_t s, int& launches) {
+  int max_np = 0;
+  for (int g = 0; g < count; ++g) max_np = max(max_np, h_desc[h_list[g]].n_pad);
+  const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
+  static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
+  static const bool rot_simple = getenv("EAMPS_ROT_SIMPLE") != nullptr;   // dev A/B switch
+  static const float tol_floor = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
+  static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 3.0e38f;
+  static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
+  static const int nstreams = getenv("EAMPS_TC_STREAMS") ? atoi(getenv("EAMPS_TC_STREAMS")) : 2;
+  // L2-resident batches: the rounds of a batch stream each gate's Jacobi matrix (B = L, n x n_pad
+  // FP32; + V when not preconditioned) through the Gram and rotation kernels three times a round; a
+  // batch whose matrices fit the 126 MB L2 (budget 80 MB) keeps those passes out of HBM. A batch
+  // still holds enough block pairs for >= 2 waves of the round kernels (kMinPairs), and
+  // EAMPS_TC_BATCH=0 runs the whole list at once (the round-1 schedule).
+  // Measured slower (chi = 256 x 4096: 1073 vs 1348 updates/s: the round kernels are latency-bound,
+  // not HBM-bound, and the smaller grids of a batch overlap less), so EAMPS_TC_BATCH=-1 (auto) is an
+  // opt-in and the default runs the whole list at once.
+  static const int batch_env = getenv("EAMPS_TC_BATCH") ? atoi(getenv("EAMPS_TC_BATCH")) : 0;
+  const size_t per_gate = (size_t)jacobi_rows(h_desc[h_list[0]]) * max_np * 8 *
+                          (h_desc[h_list[0]].jrows > 0 ? 1 : 2);
+  constexpr size_t kL2Budget = 80ull << 20;
+  constexpr int kMinPairs = 296;
+  int bsize = count;
+  if (batch_env != 0) {
+    const int by_l2 = (int)std::max<size_t>(1, kL2Budget / std::max<size_t>(per_gate, 1));
+    const int by_par = (kMinPairs + pairs_max - 1) / std::max(pairs_max, 1);
+    bsize = batch_env > 0 ? batch_env : std::max(by_l2, by_par);
+    bsize = std::min(std::max(bsize, 1), count);
+  }
+  bool all_done = true;
+  static const bool dbg = getenv("EAMPS_TC_DEBUG") != nullptr;
+  for (int b0 = 0; b0 < count; b0 += bsize) {
+    const int bc = std::min(bsize, count - b0);
+    const int32_t* bl = d_list + b0;
+    LargeCtl* bctl = ctl + b0;
+    const double* bn2 = norm2 + b0;
+    const int ngroups_want = (!prof && nstreams >= 2 && bc >= 2 && bc * pairs_max < 2048) ? 2 : 1;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_go = nullptr, ev_done = nullptr;
+    int ngroups = ngroups_want;
+    if (ngroups == 2 && !side_stream(&s2, &ev_go, &ev_done)) ngroups = 1;   // no side stream: one group
+    const int gsplit[3] = {0, ngroups == 2 ? bc / 2 : bc, bc};
+    if (ngroups == 2) {
+      if (cudaEventRecord(ev_go, s) != cudaSuccess) return launches;   // (surfaces as MPS_E_CUDA via CKL)
+      cudaStreamWaitEvent(s2, ev_go, 0);      // the preconditioner / init / norms / previous batch are done
+    }
+    int sweep = 0;
+    bool done = false;
+    for (; sweep < max_sweeps && !done; ++sweep) {
+      static cudaEvent_t ev[4];
+      static double acc[3] = {0, 0, 0};
+      if (prof && !ev[0])
+        for (int e = 0; e < 4; ++e) cudaEventCreate(&ev[e]);
+      for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
+        for (int gg = 0; gg < ngroups; ++gg) {
+          const int g0 = gsplit[gg], gc = gsplit[gg + 1] - g0;
+          if (gc <= 0) continue;
+          cudaStream_t ss = gg == 0 ? s : s2;
+          const dim3 gridg(pairs_max, gc);
+          const int32_t* dl = bl + g0;
+          LargeCtl* cg = bctl + g0;
+          if (prof) cudaEventRecord(ev[0], ss);
+          tcj::k_tc_gram<<<gridg, 128, tcj::kGramSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          if (prof) cudaEventRecord(ev[1], ss);
+          tcj::k_tc_inner<<<gridg, tcj::kInnerT, tcj::kInnerSmem, ss>>>(d_desc, dl, rnd, slab, cg, bn2 + g0, inner_sweeps,
+                                                                       tol_floor, tol_internal);
+          if (prof) cudaEventRecord(ev[2], ss);
+          if (rot_simple) tcj::k_tc_rot<<<gridg, 256, tcj::kRotSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          else tcj::k_tc_rot_ws<<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          if (prof) {
+            cudaEventRecord(ev[3], ss);
+            cudaEventSynchronize(ev[3]);
+            for (int e = 0; e < 3; ++e) {
+              float ms = 0.f;
+              cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
+              acc[e] += ms;
+            }
+          }
+          launches += 3;
+        }
+      }
+      if (ngroups == 2) {                     // the second group's round work, before the check
+        cudaEventRecord(ev_done, s2);
+        cudaStreamWaitEvent(s, ev_done, 0);
+      }
+      if (prof) fprintf(stderr, "[tc prof] cumulative ms: gram %.1f inner %.1f rot %.1f\n", acc[0], acc[1], acc[2]);
+      k_block_check<<<1, 256, 0, s>>>(d_desc, bl, bc, bctl, unconv, 0);
+      ++launches;
+      cudaMemcpyAsync(h_pinned_flag, unconv, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      done = (h_pinned_flag[0] == 0);
+      if (dbg) fprintf(stderr, "[tc] batch %d sweep %d: unconverged gates %d, rotated pairs %d\n", b0, sweep,
+                       h_pinned_flag[0], h_pinned_flag[1]);
+    }
+    all_done &= done;
+  }
+  return all_done;
+}
+
 int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, const int32_t* h_list, int count,
                int max_sweeps, uint8_t* slab, DevState* st, int32_t* d_scratch, int32_t* h_pinned_flag, cudaStream_t s,
                int* error_out) {
@@ -1306,80 +1951,104 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
-  static const bool rot_simple = getenv("EAMPS_ROT_SIMPLE") != nullptr;   // dev A/B switch
-  static const float tol_floor = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
-  // within-block pairs get the full 64-column tournament only in round 0 of each sweep (each block
-  // sits in exactly one round-0 panel); the other rounds rotate the 32 x 32 cross pairs only.
-  // Measured: chi = 256 inner solve -35%, chi = 1024 -35% with 0.8 fewer sweeps; sigma unchanged.
-  static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 3.0e38f;
-  // The gates are split over two streams: one group's SIMT inner solves run beside the other
-  // group's HBM-bound rotations and tensor-core Grams (the three launches of a round depend on
-  // each other only within a gate). EAMPS_TC_STREAMS=1: one stream (dev A/B).
-  static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
-  static const int nstreams = getenv("EAMPS_TC_STREAMS") ? atoi(getenv("EAMPS_TC_STREAMS")) : 2;
-  // (only for small round grids: measured chi = 1024 x 16 gates, 512 CTAs a round: -8.5%;
-  // chi = 256 x 1024 gates, 8192 CTAs a round: +2%)
-  const int ngroups_want = (!prof && nstreams >= 2 && count >= 2 && count * pairs_max < 2048) ? 2 : 1;
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t ev_go = nullptr, ev_done = nullptr;
-  int ngroups = ngroups_want;
-  if (ngroups == 2 && !side_stream(&s2, &ev_go, &ev_done)) ngroups = 1;   // no side stream: one group
-  const int gsplit[3] = {0, ngroups == 2 ? count / 2 : count, count};
-  if (ngroups == 2) {
-    if (cudaEventRecord(ev_go, s) != cudaSuccess) return launches;   // (surfaces as MPS_E_CUDA via CKL)
-    cudaStreamWaitEvent(s2, ev_go, 0);      // the preconditioner / init / norms are done
-  }
-  int sweep = 0;
-  bool done = false;
-  for (; sweep < max_sweeps && !done; ++sweep) {
-    static cudaEvent_t ev[4];
-    static double acc[3] = {0, 0, 0};
-    if (prof && !ev[0])
-      for (int e = 0; e < 4; ++e) cudaEventCreate(&ev[e]);
-    for (int rnd = 0; rnd < nb_max - 1; ++rnd) {
-      for (int gg = 0; gg < ngroups; ++gg) {
-        const int g0 = gsplit[gg], gc = gsplit[gg + 1] - g0;
-        if (gc <= 0) continue;
-        cudaStream_t ss = gg == 0 ? s : s2;
-        const dim3 gridg(pairs_max, gc);
-        const int32_t* dl = d_list + g0;
-        LargeCtl* cg = ctl + g0;
-        if (prof) cudaEventRecord(ev[0], ss);
-        tcj::k_tc_gram<<<gridg, 128, tcj::kGramSmem, ss>>>(d_desc, dl, rnd, slab, cg);
-        if (prof) cudaEventRecord(ev[1], ss);
-        tcj::k_tc_inner<<<gridg, tcj::kInnerT, tcj::kInnerSmem, ss>>>(d_desc, dl, rnd, slab, cg, norm2 + g0, inner_sweeps,
-                                                                     tol_floor, tol_internal);
-        if (prof) cudaEventRecord(ev[2], ss);
-        if (rot_simple) tcj::k_tc_rot<<<gridg, 256, tcj::kRotSmem, ss>>>(d_desc, dl, rnd, slab, cg);
-        else tcj::k_tc_rot_ws<<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
-        if (prof) {
-          cudaEventRecord(ev[3], ss);
-          cudaEventSynchronize(ev[3]);
-          for (int e = 0; e < 3; ++e) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
-            acc[e] += ms;
-          }
-        }
-        launches += 3;
-      }
-    }
-    if (ngroups == 2) {                     // the second group's round work, before the check
-      cudaEventRecord(ev_done, s2);
-      cudaStreamWaitEvent(s, ev_done, 0);
-    }
-    if (prof) fprintf(stderr, "[tc prof] cumulative ms: gram %.1f inner %.1f rot %.1f\n", acc[0], acc[1], acc[2]);
-    k_block_check<<<1, 256, 0, s>>>(d_desc, d_list, count, ctl, unconv, 0);
-    ++launches;
-    cudaMemcpyAsync(h_pinned_flag, unconv, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  // The fused persistent kernel (k_tc_fused) is the EAMPS_TC_FUSED=1 variant: measured slower than the
+  // three-launch rounds (chi = 256: 948 vs 1348 updates/s; chi = 1024: 21.0 vs 26.5) -- with its
+  // 197 KB of shared memory one CTA per SM runs the latency-bound SIMT inner solve with nothing
+  // to overlap it, where the separate kernels keep 2-3 CTAs per SM in flight.
+  static const bool fused = getenv("EAMPS_TC_FUSED") != nullptr;
+  if (fused) {
+    static const float tol_floor_f = getenv("EAMPS_TC_TOL") ? (float)atof(getenv("EAMPS_TC_TOL")) : 7.62939453125e-6f;
+    static const float tol_int_f = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 3.0e38f;
+    static std::atomic<unsigned long long> fattr{0};
+    if (first_on_device(fattr))
+      cudaFuncSetAttribute(tcj::k_tc_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kFusedSmem);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tcj::k_tc_fused, tcj::FT, tcj::kFusedSmem);
+    int32_t* pair_pre = unconv + 2;
+    tcj::FusedCtl* fc = reinterpret_cast<tcj::FusedCtl*>(pair_pre + ((count + 1 + 3) & ~3));
+    tcj::k_pair_prefix<<<1, 32, 0, s>>>(d_desc, d_list, count, pair_pre, fc);
+    int total_pairs = 0;
+    for (int g = 0; g < count; ++g) total_pairs += h_desc[h_list[g]].n_pad / tcj::PWC;
+    const int grid = std::max(1, std::min(sms * std::max(per_sm, 1), total_pairs));
+    GateDesc* a_desc = d_desc;
+    const int32_t* a_list = d_list;
+    int a_count = count;
+    uint8_t* a_slab = slab;
+    LargeCtl* a_ctl = ctl;
+    const double* a_norm2 = norm2;
+    const int32_t* a_pre = pair_pre;
+    tcj::FusedCtl* a_fc = fc;
+    int a_ms = max_sweeps, a_is = inner_sweeps;
+    float a_tf = tol_floor_f, a_ti = tol_int_f;
+    void* args[] = {&a_desc, &a_list, &a_count, &a_slab, &a_ctl, &a_norm2, &a_pre, &a_fc, &a_ms, &a_is, &a_tf, &a_ti};
+    cudaLaunchCooperativeKernel((const void*)tcj::k_tc_fused, dim3(grid), dim3(tcj::FT), args, tcj::kFusedSmem, s);
+    launches += 2;
+    cudaMemcpyAsync(h_pinned_flag, &fc->done, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    done = (h_pinned_flag[0] == 0);
-    static const bool dbg = getenv("EAMPS_TC_DEBUG") != nullptr;
-    if (dbg) fprintf(stderr, "[tc] sweep %d: unconverged gates %d, rotated pairs %d\n", sweep, h_pinned_flag[0], h_pinned_flag[1]);
+    if (!h_pinned_flag[0]) *error_out = -6;
+    if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);
+    launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
+    return launches;
   }
+  const bool done = tc_sweep_rounds(d_desc, h_desc, d_list, h_list, count, max_sweeps, slab, ctl, norm2, unconv,
+                                    h_pinned_flag, s, launches);
   if (!done) *error_out = -6;
   if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);
-  launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
+  static const bool no_deep = getenv("EAMPS_NO_DEEP") != nullptr;   // dev A/B switch
+  if (no_deep || max_n <= 256 || !any_pc) {
+    launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
+    return launches;
+  }
+  // ---- deep spectra, n > 256 (n <= 256: the FP64 Rayleigh-Ritz of refine.cu). V = the unit columns
+  // of the converged FP32 B = L is accurate only to ~eps32 sigma_max / sigma_j in the small singular
+  // directions (L rounded to FP32), which the Rayleigh quotient and the pairwise polish cannot undo
+  // when sigma_min / sigma_max < ~5e-5 (config 2 chi = 1024: 7.9e-4 relative error measured). B1 =
+  // theta V (FP64-accumulated, FP32 storage: every column keeps its own relative accuracy) has
+  // nearly orthogonal columns (coupling <~ 5e-3 relative); more sweeps of the same block Jacobi on
+  // B1 converge quadratically, and with rotation angles ~ coupling x sigma_j / sigma_l the FP32 /
+  // 3xTF32 rounding they add to a small column is relative to that column; sigma_j = |b1_j| (FP64
+  // norms) is then relatively accurate. PAPER.md:114; north_star sigma tolerance.
+  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
+  ++launches;
+  static std::atomic<unsigned long long> pattr{0};
+  if (first_on_device(pattr))
+    cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
+  const int nbp = ((max_n + tcj::PWC - 1) / tcj::PWC) * 2;
+  static const bool no_polish = getenv("EAMPS_NO_POLISH") != nullptr;
+  if (!no_polish && nbp >= 2) {
+    tcj::k_tc_polish<<<dim3(nbp / 2, count, nbp - 1), 128, tcj::kGramSmem, s>>>(d_desc, d_list, slab);
+    ++launches;
+  }
+  int32_t* flags = unconv + 2;                                    // count ints, then the deep list
+  k_deep_flags<<<count, 256, 0, s>>>(d_desc, d_list, slab, flags, kDeepRatio * kDeepRatio);
+  ++launches;
+  std::vector<int32_t> hf(count);
+  cudaMemcpyAsync(hf.data(), flags, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  std::vector<int32_t> deep_h;                                    // desc indices of the deep gates
+  for (int g = 0; g < count; ++g)
+    if (hf[g]) deep_h.push_back(h_list[g]);
+  const int dc = (int)deep_h.size();
+  if (dc > 0) {
+    int32_t* dlist = flags + ((count + 1) & ~1);
+    double* dnorm2 = reinterpret_cast<double*>(dlist + ((dc + 1) & ~1));
+    cudaMemcpyAsync(dlist, deep_h.data(), sizeof(int32_t) * dc, cudaMemcpyHostToDevice, s);
+    k_deep_prepare<<<dim3(64, dc), 256, 0, s>>>(d_desc, d_list, count, dlist, slab, ctl, norm2, dnorm2);
+    ++launches;
+    static const int deep_sweeps = getenv("EAMPS_DEEP_SWEEPS") ? atoi(getenv("EAMPS_DEEP_SWEEPS")) : 8;
+    tc_sweep_rounds(d_desc, h_desc, dlist, deep_h.data(), dc, deep_sweeps, slab, ctl, dnorm2, unconv, h_pinned_flag, s,
+                    launches);
+    k_deep_finish<<<dc, 256, 0, s>>>(d_desc, dlist, slab);
+    ++launches;
+  }
+  int npow2 = 1;
+  while (npow2 < max_n) npow2 <<= 1;
+  const size_t smem = (size_t)npow2 * 12 + 16 + 1024 * 8;
+  cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
+  ++launches;
   return launches;
 }
 

@@ -92,6 +92,7 @@ def test_gpu_sharded_boundary_gates_vs_oracle(world):
 
         def layer_begin(self, sites, Us):
             self.pending = None
+            self.sites_last = list(sites)
             if self.bl is not None and len(sites) and int(sites[-1]) == self.bl:
                 i = self.bl
                 lam = self.m.mps_schmidt_values(i - 1) if i > 0 else None
@@ -103,7 +104,7 @@ def test_gpu_sharded_boundary_gates_vs_oracle(world):
             rem = super().layer_step()
             if rem == 0 and self.pending is not None:
                 g, BL, BR, lam, U = self.pending
-                rec = self.m.mps_truncation_log()[-(g + 1)]
+                rec = self.m.mps_truncation_log()[-(len(self.sites_last)) + g]
                 self.done.append((BL, BR, lam, U, rec, self.m.mps_last_spectrum(g)))
                 self.pending = None
             return rem
