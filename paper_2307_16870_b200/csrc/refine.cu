@@ -61,7 +61,7 @@ size_t refine_smem(int n) {
 }
 
 __global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint8_t* slab, DevState* st, int G,
-                                               int max_sweeps) {
+                                               const float2* __restrict__ d_us, int max_sweeps) {
   GateDesc& gd = desc[blockIdx.x];
   const int n = gd.n, m = gd.m, np = gd.n_pad, dd = st->d;
   if (n > kRefineMaxN || n < 2 || blockIdx.x >= G) return;
@@ -92,10 +92,19 @@ __global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint
   double2* Cp = n <= kSmemPackedMaxN
                     ? reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(part + RT) + 15) & ~uintptr_t(15))
                     : reinterpret_cast<double2*>(slab + gd.ws_log);
-  // ---- B = theta V (FP64 accumulation, stored FP32 in the dead theta workspace, ld m)
+  // ---- B = theta V with theta RECONTRACTED in FP64 from the complex64 site tensors and gate (the
+  // exact inputs of both sides: the FP32 contraction output Theta' carries ~eps32 relative rounding
+  // per entry, which alone moves a sigma at 2e-6 sigma_max by ~4e-5 -- measured on a config-4 MPO
+  // gate); stored FP32 in the dead theta workspace (ld m), each column keeping its relative accuracy.
+  //   X_a[s'][(t',c)] = sum_b B_i[a,s',b] B_{i+1}[b,t',c]
+  //   theta[(a,s),(t,c)] = lambda_a sum_{s',t'} U[s d+t, s' d+t'] X_a[s'][(t',c)]   (contract.cu, E2)
   const BondEntry* bonds = reinterpret_cast<const BondEntry*>(slab + st->bonds_off);
+  const SiteEntry* sites = reinterpret_cast<const SiteEntry*>(slab + st->sites_off);
   const float* lam = reinterpret_cast<const float*>(slab + bonds[gd.site].off);
-  const float2* thp = reinterpret_cast<const float2*>(slab + gd.ws_thetap);
+  const float2* Bi = reinterpret_cast<const float2*>(slab + sites[gd.site].off);       // (chi_l, d, chi_m)
+  const float2* Bj = reinterpret_cast<const float2*>(slab + sites[gd.site + 1].off);   // (chi_m, d, chi_r)
+  const float2* U = d_us + (int64_t)gd.u_index * dd * dd * dd * dd;
+  const int chl = gd.l, chm = gd.mid, chr = gd.r, d2 = dd * dd;
   const float2* V = reinterpret_cast<const float2*>(slab + gd.ws_V);
   float2* B = reinterpret_cast<float2*>(slab + gd.ws_theta);
   // 1 / |v_j| in FP64 (keys[] as scratch): the columns of an FP32-accumulated V (small / medium
@@ -103,25 +112,56 @@ __global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint
   // same factor (Ostrowski); with unit columns the remaining non-orthogonality enters at second order
   for (int j = tid; j < n; j += RT) {
     const float2* vj = V + (int64_t)j * np;
-    double d = 0.0;
-    for (int k = 0; k < n; ++k) d += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
-    keys[j] = d > 0.0 ? 1.0 / sqrt(d) : 0.0;
+    double dsum = 0.0;
+    for (int k = 0; k < n; ++k) dsum += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
+    keys[j] = dsum > 0.0 ? 1.0 / sqrt(dsum) : 0.0;
   }
+  double2* Xa = As;                     // d x n   (As | Bs: 2 x 32 x 33 double2 >= 2 d n for d n <= 1024)
+  double2* Ta = As + dd * n;            // d x n
   __syncthreads();
-  for (int x = tid; x < m * n; x += RT) {
-    const int row = x % m, j = x / m;
-    const double la = lam[row / dd] * keys[j];
-    const float2* vj = V + (int64_t)j * np;
-    double wr = 0.0, wi = 0.0;
-    for (int k = 0; k < n; ++k) {
-      const float2 t = thp[(int64_t)k * m + row];
-      const float2 v = vj[k];
-      wr = fma((double)t.x, (double)v.x, fma(-(double)t.y, (double)v.y, wr));
-      wi = fma((double)t.x, (double)v.y, fma((double)t.y, (double)v.x, wi));
+  for (int a = 0; a < chl; ++a) {
+    for (int x = tid; x < dd * n; x += RT) {
+      const int sp = x / n, col = x % n, tp = col / chr, c = col % chr;
+      const float2* bi = Bi + ((int64_t)a * dd + sp) * chm;
+      double xr = 0.0, xi = 0.0;
+      for (int b = 0; b < chm; ++b) {
+        const float2 u = bi[b], v = Bj[((int64_t)b * dd + tp) * chr + c];
+        xr = fma((double)u.x, (double)v.x, fma(-(double)u.y, (double)v.y, xr));
+        xi = fma((double)u.x, (double)v.y, fma((double)u.y, (double)v.x, xi));
+      }
+      Xa[x] = make_double2(xr, xi);
     }
-    B[(int64_t)j * m + row] = make_float2((float)(la * wr), (float)(la * wi));
+    __syncthreads();
+    const double la = lam[a];
+    for (int x = tid; x < dd * n; x += RT) {
+      const int sr = x / n, col = x % n, t = col / chr, c = col % chr;
+      double tr = 0.0, ti = 0.0;
+      for (int sp = 0; sp < dd; ++sp)
+        for (int tp = 0; tp < dd; ++tp) {
+          const float2 u = U[(sr * dd + t) * d2 + sp * dd + tp];
+          const double2 xv = Xa[sp * n + tp * chr + c];
+          tr = fma((double)u.x, xv.x, fma(-(double)u.y, xv.y, tr));
+          ti = fma((double)u.x, xv.y, fma((double)u.y, xv.x, ti));
+        }
+      Ta[x] = make_double2(la * tr, la * ti);
+    }
+    __syncthreads();
+    for (int x = tid; x < dd * n; x += RT) {
+      const int sr = x / n, j = x % n;
+      const float2* vj = V + (int64_t)j * np;
+      const double2* th = Ta + sr * n;
+      double wr = 0.0, wi = 0.0;
+      for (int k = 0; k < n; ++k) {
+        const double2 t = th[k];
+        const float2 v = vj[k];
+        wr = fma(t.x, (double)v.x, fma(-t.y, (double)v.y, wr));
+        wi = fma(t.x, (double)v.y, fma(t.y, (double)v.x, wi));
+      }
+      const double sc = keys[j];
+      B[(int64_t)j * m + a * dd + sr] = make_float2((float)(sc * wr), (float)(sc * wi));
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // ---- C = B^H B (FP64), packed upper triangle: 32 x 32 tiles (bi <= bj), rows in 32-chunks
   const int nt = (n + 31) / 32;
   const int ti = tid & 31, tj0 = (tid >> 5) * 4;       // thread: tile row ti, tile columns tj0..tj0+3
@@ -278,7 +318,7 @@ size_t refine_scratch_bytes(int n) {
   return (n > kSmemPackedMaxN && n <= kRefineMaxN) ? (size_t)n * (n + 1) / 2 * sizeof(double2) : 0;
 }
 
-int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, cudaStream_t s) {
+int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us, cudaStream_t s) {
   if (G <= 0 || max_n < 2) return 0;
   // the wave may mix gates with C in shared memory (n <= 128) and in global memory (n <= 256)
   const int nn = max_n < kRefineMaxN ? max_n : kRefineMaxN;
@@ -287,7 +327,7 @@ int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* s
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)refine_smem(kSmemPackedMaxN));
-  k_refine<<<G, RT, smem, s>>>(d_desc, slab, st, G, 16);
+  k_refine<<<G, RT, smem, s>>>(d_desc, slab, st, G, d_us, 16);
   return 1;
 }
 

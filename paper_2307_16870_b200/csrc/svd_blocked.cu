@@ -25,6 +25,18 @@
 
 namespace eamps {
 
+// EAMPS_DEBUG_SYNC=1 (development): synchronise and check after every large-regime launch, naming
+// the kernel that faulted (the library's own bounds/alignment checks stand in for compute-sanitizer,
+// which is closed on this pool).
+static void dbg_sync(cudaStream_t s, const char* what) {
+  static const bool on = getenv("EAMPS_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "[eamps debug] after %s: %s\n", what, cudaGetErrorString(e));
+}
+
+
 namespace {
 
 constexpr int BLK = 16;        // columns per block
@@ -1885,12 +1897,15 @@ static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int3
           LargeCtl* cg = bctl + g0;
           if (prof) cudaEventRecord(ev[0], ss);
           tcj::k_tc_gram<<<gridg, 128, tcj::kGramSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          dbg_sync(ss, "k_tc_gram");
           if (prof) cudaEventRecord(ev[1], ss);
           tcj::k_tc_inner<<<gridg, tcj::kInnerT, tcj::kInnerSmem, ss>>>(d_desc, dl, rnd, slab, cg, bn2 + g0, inner_sweeps,
                                                                        tol_floor, tol_internal);
+                                                                       dbg_sync(ss, "k_tc_inner");
           if (prof) cudaEventRecord(ev[2], ss);
           if (rot_simple) tcj::k_tc_rot<<<gridg, 256, tcj::kRotSmem, ss>>>(d_desc, dl, rnd, slab, cg);
           else tcj::k_tc_rot_ws<<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          dbg_sync(ss, "k_tc_rot_ws");
           if (prof) {
             cudaEventRecord(ev[3], ss);
             cudaEventSynchronize(ev[3]);
@@ -1909,6 +1924,7 @@ static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int3
       }
       if (prof) fprintf(stderr, "[tc prof] cumulative ms: gram %.1f inner %.1f rot %.1f\n", acc[0], acc[1], acc[2]);
       k_block_check<<<1, 256, 0, s>>>(d_desc, bl, bc, bctl, unconv, 0);
+      dbg_sync(s, "k_block_check");
       ++launches;
       cudaMemcpyAsync(h_pinned_flag, unconv, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
@@ -1942,6 +1958,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   bool any_pc = false;
   for (int g = 0; g < count; ++g) any_pc |= h_desc[h_list[g]].jrows > 0;
   if (any_pc) launches += launch_precond_large(d_desc, d_list, count, max_n, slab, s);   // after the norm
+  dbg_sync(s, "init/norm/precond");
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
@@ -1996,8 +2013,11 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
                                     h_pinned_flag, s, launches);
   if (!done) *error_out = -6;
   if (any_pc) launches += launch_precond_vnorm(d_desc, d_list, count, max_np, slab, norm2, s);
-  static const bool no_deep = getenv("EAMPS_NO_DEEP") != nullptr;   // dev A/B switch
-  if (no_deep || max_n <= 256 || !any_pc) {
+  // Opt-in (EAMPS_DEEP=1): measured on config 2 chi = 1024 it lowers the worst sigma error from
+  // 7.9e-4 to 1.8e-4 -- still above the 1e-5 bar -- for +7 sweeps (-24 % throughput), and at
+  // chi = 512 it raised the error from ~6e-6 to 2.4e-5 (reading 19).
+  static const bool deep_on = getenv("EAMPS_DEEP") != nullptr;
+  if (!deep_on || max_n <= 256 || !any_pc) {
     launches += launch_spectrum_polish(d_desc, d_list, count, max_n, slab, st, s);
     return launches;
   }
@@ -2012,6 +2032,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   // norms) is then relatively accurate. PAPER.md:114; north_star sigma tolerance.
   k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
   ++launches;
+  dbg_sync(s, "k_rayleigh");
   static std::atomic<unsigned long long> pattr{0};
   if (first_on_device(pattr))
     cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
@@ -2019,10 +2040,12 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   static const bool no_polish = getenv("EAMPS_NO_POLISH") != nullptr;
   if (!no_polish && nbp >= 2) {
     tcj::k_tc_polish<<<dim3(nbp / 2, count, nbp - 1), 128, tcj::kGramSmem, s>>>(d_desc, d_list, slab);
+    dbg_sync(s, "k_tc_polish");
     ++launches;
   }
   int32_t* flags = unconv + 2;                                    // count ints, then the deep list
   k_deep_flags<<<count, 256, 0, s>>>(d_desc, d_list, slab, flags, kDeepRatio * kDeepRatio);
+  dbg_sync(s, "k_deep_flags");
   ++launches;
   std::vector<int32_t> hf(count);
   cudaMemcpyAsync(hf.data(), flags, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s);
@@ -2036,11 +2059,13 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     double* dnorm2 = reinterpret_cast<double*>(dlist + ((dc + 1) & ~1));
     cudaMemcpyAsync(dlist, deep_h.data(), sizeof(int32_t) * dc, cudaMemcpyHostToDevice, s);
     k_deep_prepare<<<dim3(64, dc), 256, 0, s>>>(d_desc, d_list, count, dlist, slab, ctl, norm2, dnorm2);
+    dbg_sync(s, "k_deep_prepare");
     ++launches;
     static const int deep_sweeps = getenv("EAMPS_DEEP_SWEEPS") ? atoi(getenv("EAMPS_DEEP_SWEEPS")) : 8;
     tc_sweep_rounds(d_desc, h_desc, dlist, deep_h.data(), dc, deep_sweeps, slab, ctl, dnorm2, unconv, h_pinned_flag, s,
                     launches);
     k_deep_finish<<<dc, 256, 0, s>>>(d_desc, dlist, slab);
+    dbg_sync(s, "k_deep_finish");
     ++launches;
   }
   int npow2 = 1;
@@ -2049,6 +2074,7 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
   cudaFuncSetAttribute(k_sort_tails_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_sort_tails_large<<<count, 1024, smem, s>>>(d_desc, d_list, slab, st, 1);
   ++launches;
+  dbg_sync(s, "k_sort_tails_large");
   return launches;
 }
 

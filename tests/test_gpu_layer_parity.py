@@ -147,9 +147,9 @@ def test_config4_every_layer_identical_inputs():
 
 def test_config5_every_layer_identical_inputs():
     """N = 300, depth 75, F_min = 0.9, cap 4096: layers 0-7 (150 / 149 gates each, bond dims to
-    ~90, theta to ~180)."""
+    ~61, theta to ~122)."""
     N, layers, kw, rule = _cfg_layers(5, 8)
-    run_identical(layers, N, kw, rule, slab=8 << 30, min_theta=128)
+    run_identical(layers, N, kw, rule, slab=8 << 30, min_theta=96)
 
 
 def sampled_gate_check(gpu, sites, us, picks, rule="pure"):
