@@ -141,6 +141,24 @@ mps_status mps_to_statevector(mps_t, double* out, size_t n_doubles);
 /* The bond dimensions chi_1 .. chi_{N-1} of E2 as they stand (host mirror, no
  * device work); out: N-1 int32 (host). */
 mps_status mps_bond_dims(mps_t, int32_t* out /* N-1 */);
+/* ---- observables (NEXT-4); synchronising, FP64 accumulation on the device ----
+ * <a|b> = sum_sigma conj(C^a_sigma) C^b_sigma by left-to-right transfer matrices
+ * E_{i+1} = sum_s A_i^{s dagger} E_i B_i^s (E2): the overlap behind the pure-state
+ * fidelity E7 |<a|b>|^2; for d = 4 the Hilbert-Schmidt product Tr(rho_a^dagger
+ * rho_b) of the vectorised density operators, from which the Wang fidelity E9
+ * is |<<a|b>>| / sqrt(<<a|a>> <<b|b>>). Both handles on the same device, same N and d
+ * (MPS_E_INVAL otherwise); re_im: 2 doubles (host). Scratch is taken from the top of a's slab
+ * (MPS_E_NOMEM if the pool has grown into it). */
+mps_status mps_overlap(mps_t a, mps_t b, double* re_im);
+/* Tr rho = <<vec(I)|rho>> of a vectorised MPO (d = 4: per site the digits s = 2 sigma + sigma'
+ * with sigma = sigma', s in {0, 3}); MPS_E_STATE for d = 2. re_im: 2 doubles (host). */
+mps_status mps_trace(mps_t, double* re_im);
+/* Two-site expectation value <psi|O_{site,site+1}|psi> / <psi|psi> (E5) in the
+ * state's actual gauge (full left and right environments: exact also after truncations, when the
+ * B-lambda form is no longer exactly canonical, reading 4). O: host, d^2 x d^2 row-major
+ * interleaved complex64, O[(s d + t), (s' d + t')] with s the physical index of `site`. d = 2 only
+ * (MPS_E_STATE for d = 4); MPS_E_RANGE for site outside [0, N-1); MPS_E_INVAL for a non-finite O. */
+mps_status mps_expectation2(mps_t, int32_t site, const float* O, double* re_im);
 /* Schmidt vector lambda of `bond` (float32, descending; bond -1..N-1, the outer two are [1]): the
  * kept, renormalised singular values of the last SVD at that bond ("singular values in decreasing
  * order"; the Lambda of the canonical form, PAPER.md:65 and E10 PAPER.md:117-118).

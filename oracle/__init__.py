@@ -88,6 +88,9 @@ def _declare(L):
     L.orc_amplitude.argtypes = [_P, _P, _dp]
     L.orc_statevector.argtypes = [_P, _P, C.c_int64]
     L.orc_last_spectrum.argtypes = [_P, C.c_int, _P, C.c_int, C.POINTER(C.c_int)]
+    L.orc_overlap.argtypes = [_P, _P, _dp]
+    L.orc_trace.argtypes = [_P, _dp]
+    L.orc_expectation2.argtypes = [_P, C.c_int, _P, _dp]
 
 
 class OracleError(RuntimeError):
@@ -253,6 +256,24 @@ class OracleMPS:
         out = np.zeros(n, np.complex128)
         _ck(lib().orc_statevector(self._h, _ptr(out), n))
         return out
+
+    # ---- observables (NEXT-4): E7 / E9 building blocks and E5 ------------------------------
+    def overlap(self, other: "OracleMPS") -> complex:
+        """<self|other> (d = 2) or the Hilbert-Schmidt <<rho_self|rho_other>> (d = 4)."""
+        out = (C.c_double * 2)()
+        _ck(lib().orc_overlap(self._h, other._h, out))
+        return complex(out[0], out[1])
+
+    def trace(self) -> complex:
+        out = (C.c_double * 2)()
+        _ck(lib().orc_trace(self._h, out))
+        return complex(out[0], out[1])
+
+    def expectation2(self, site: int, O) -> complex:
+        O = _c128(O)
+        out = (C.c_double * 2)()
+        _ck(lib().orc_expectation2(self._h, int(site), _ptr(O), out))
+        return complex(out[0], out[1])
 
     def last_spectrum(self, g: int) -> np.ndarray:
         n = C.c_int(0)

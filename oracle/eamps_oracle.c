@@ -560,3 +560,157 @@ int orc_last_spectrum(orc_mps* s, int g, double* sig, int cap, int* n) {
   for (int j = 0; j < s->last_n[g] && j < cap; ++j) sig[j] = s->last_sig[g][j];
   return ORC_OK;
 }
+
+/* ---- observables (NEXT-4) -------------------------------------------------------------------- */
+/* E_{i+1}[a',b'] = sum_s sum_{a,b} conj(A_i[a,s,a']) E_i[a,b] B_i[b,s,b'], E_0 = [1] (E2 with the bra
+ * conjugated: PAPER.md:38-41, 91-93). Plain loops. Returns the 1 x 1 result. */
+static int transfer_overlap(const orc_mps* a, const orc_mps* b, cplx* out) {
+  if (a->N != b->N || a->d != b->d) return ORC_E_INVAL;
+  if (a->chl[0] != 1 || b->chl[0] != 1 || a->chr[a->N - 1] != 1 || b->chr[b->N - 1] != 1) return ORC_E_STATE;
+  const int d = a->d;
+  cplx* E = (cplx*)malloc(sizeof(cplx));
+  E[0] = 1.0;
+  int la = 1, lb = 1;
+  for (int i = 0; i < a->N; ++i) {
+    const int ra = a->chr[i], rb = b->chr[i];
+    cplx* En = (cplx*)calloc((size_t)ra * rb, sizeof(cplx));
+    for (int s2 = 0; s2 < d; ++s2)
+      for (int x = 0; x < la; ++x)
+        for (int y = 0; y < lb; ++y) {
+          const cplx e = E[(long)x * lb + y];
+          if (e == 0.0) continue;
+          for (int xp = 0; xp < ra; ++xp) {
+            const cplx ca = conj(a->B[i][((long)x * d + s2) * ra + xp]) * e;
+            for (int yp = 0; yp < rb; ++yp) En[(long)xp * rb + yp] += ca * b->B[i][((long)y * d + s2) * rb + yp];
+          }
+        }
+    free(E);
+    E = En;
+    la = ra;
+    lb = rb;
+  }
+  *out = E[0];
+  free(E);
+  return ORC_OK;
+}
+
+int orc_overlap(orc_mps* a, orc_mps* b, double* re_im) {
+  cplx v;
+  int st = transfer_overlap(a, b, &v);
+  if (st != ORC_OK) return st;
+  re_im[0] = creal(v);
+  re_im[1] = cimag(v);
+  return ORC_OK;
+}
+
+/* Tr rho = sum over sigma of <sigma sigma'|rho> with sigma = sigma': per site the vector
+ * v_{i+1}[c] = sum_a v_i[a] (B_i[a,0,c] + B_i[a,3,c])  (s = 2 sigma + sigma') */
+int orc_trace(orc_mps* s, double* re_im) {
+  if (s->d != 4) return ORC_E_STATE;
+  if (s->chl[0] != 1 || s->chr[s->N - 1] != 1) return ORC_E_STATE;
+  cplx* v = (cplx*)malloc(sizeof(cplx));
+  v[0] = 1.0;
+  for (int i = 0; i < s->N; ++i) {
+    const int l = s->chl[i], r = s->chr[i];
+    cplx* nv = (cplx*)calloc(r, sizeof(cplx));
+    for (int x = 0; x < l; ++x)
+      for (int c = 0; c < r; ++c) nv[c] += v[x] * (s->B[i][((long)x * 4 + 0) * r + c] + s->B[i][((long)x * 4 + 3) * r + c]);
+    free(v);
+    v = nv;
+  }
+  re_im[0] = creal(v[0]);
+  re_im[1] = cimag(v[0]);
+  free(v);
+  return ORC_OK;
+}
+
+/* E5, arbitrary gauge: L = left environment of sites < k (transfer of psi with
+ * itself), R = right environment of sites > k+1 (right-to-left transfer), then
+ * <O> = sum L[a,a''] conj(theta[a,s,t,c]) O[st,s't'] theta[a'',s',t',c''] R[c,c''] / <psi|psi>,
+ * theta[a,s,t,c] = sum_b B_k[a,s,b] B_{k+1}[b,t,c]. */
+int orc_expectation2(orc_mps* s, int k, const double* Od, double* re_im) {
+  if (s->d != 2) return ORC_E_STATE;
+  if (k < 0 || k >= s->N - 1) return ORC_E_RANGE;
+  if (s->chl[0] != 1 || s->chr[s->N - 1] != 1) return ORC_E_STATE;
+  const int d = 2;
+  const cplx* O = (const cplx*)Od;
+  /* left environment L (chl[k] x chl[k]) */
+  cplx* L = (cplx*)malloc(sizeof(cplx));
+  L[0] = 1.0;
+  int l = 1;
+  for (int i = 0; i < k; ++i) {
+    const int r = s->chr[i];
+    cplx* Ln = (cplx*)calloc((size_t)r * r, sizeof(cplx));
+    for (int s2 = 0; s2 < d; ++s2)
+      for (int x = 0; x < l; ++x)
+        for (int y = 0; y < l; ++y) {
+          const cplx e = L[(long)x * l + y];
+          if (e == 0.0) continue;
+          for (int xp = 0; xp < r; ++xp) {
+            const cplx ca = conj(s->B[i][((long)x * d + s2) * r + xp]) * e;
+            for (int yp = 0; yp < r; ++yp) Ln[(long)xp * r + yp] += ca * s->B[i][((long)y * d + s2) * r + yp];
+          }
+        }
+    free(L);
+    L = Ln;
+    l = r;
+  }
+  /* right environment R (chr[k+1] x chr[k+1]): R_i[c,c''] = sum_s B_i[c,s,x] conj... from the right */
+  cplx* R = (cplx*)malloc(sizeof(cplx));
+  R[0] = 1.0;
+  int rr = 1;
+  for (int i = s->N - 1; i > k + 1; --i) {
+    const int li = s->chl[i];
+    cplx* Rn = (cplx*)calloc((size_t)li * li, sizeof(cplx));
+    for (int s2 = 0; s2 < d; ++s2)
+      for (int x = 0; x < li; ++x)
+        for (int y = 0; y < li; ++y) {
+          cplx acc = 0.0;
+          for (int xp = 0; xp < rr; ++xp)
+            for (int yp = 0; yp < rr; ++yp)
+              acc += conj(s->B[i][((long)x * d + s2) * rr + xp]) * R[(long)xp * rr + yp] *
+                     s->B[i][((long)y * d + s2) * rr + yp];
+          Rn[(long)x * li + y] += acc;
+        }
+    free(R);
+    R = Rn;
+    rr = li;
+  }
+  /* theta (l, d, d, rr) */
+  const int mid = s->chr[k];
+  cplx* th = (cplx*)calloc((size_t)l * d * d * rr, sizeof(cplx));
+  for (int a = 0; a < l; ++a)
+    for (int s1 = 0; s1 < d; ++s1)
+      for (int b = 0; b < mid; ++b) {
+        const cplx u = s->B[k][((long)a * d + s1) * mid + b];
+        for (int t = 0; t < d; ++t)
+          for (int c = 0; c < rr; ++c)
+            th[(((long)a * d + s1) * d + t) * rr + c] += u * s->B[k + 1][((long)b * d + t) * rr + c];
+      }
+  /* O theta */
+  cplx* Oth = (cplx*)calloc((size_t)l * d * d * rr, sizeof(cplx));
+  for (int a = 0; a < l; ++a)
+    for (int c = 0; c < rr; ++c)
+      for (int st = 0; st < d * d; ++st)
+        for (int sp = 0; sp < d * d; ++sp)
+          Oth[((long)a * d * d + st) * rr + c] += O[st * d * d + sp] * th[((long)a * d * d + sp) * rr + c];
+  cplx num = 0.0, den = 0.0;
+  for (int a = 0; a < l; ++a)
+    for (int a2 = 0; a2 < l; ++a2) {
+      const cplx la = L[(long)a * l + a2];
+      if (la == 0.0) continue;
+      for (int st = 0; st < d * d; ++st)
+        for (int c = 0; c < rr; ++c)
+          for (int c2 = 0; c2 < rr; ++c2) {
+            const cplx w = la * conj(th[((long)a * d * d + st) * rr + c]) * R[(long)c * rr + c2];
+            num += w * Oth[((long)a2 * d * d + st) * rr + c2];
+            den += w * th[((long)a2 * d * d + st) * rr + c2];
+          }
+    }
+  free(L); free(R); free(th); free(Oth);
+  if (den == 0.0) return ORC_E_STATE;
+  const cplx v = num / den;
+  re_im[0] = creal(v);
+  re_im[1] = cimag(v);
+  return ORC_OK;
+}

@@ -74,6 +74,19 @@ int  orc_records(orc_mps*, orc_record* out, int64_t cap, int64_t* len);
 int  orc_set_ledger(orc_mps*, double log_E, int64_t j, int guarantee_held);
 int  orc_amplitude(orc_mps*, const uint8_t* digits, double* re_im);
 int  orc_statevector(orc_mps*, double* out, int64_t n_complex);
+/* ---- observables (NEXT-4) -------------------------------------------------------
+ * <a|b> = sum_sigma conj(C^a_sigma) C^b_sigma by left-to-right transfer matrices
+ * E_{i+1} = sum_s A_i^{s dagger} E_i B_i^s (E2): the overlap of E7;
+ * for d = 4 the Hilbert-Schmidt inner product Tr(rho_a^dagger rho_b) of the vectorised density
+ * operators, the numerator and purities of the Wang fidelity E9. Same N and d. */
+int  orc_overlap(orc_mps* a, orc_mps* b, double* re_im);
+/* Tr rho = <<vec(I)|rho>> (d = 4 only: digits s = 2 sigma + sigma' with sigma = sigma', i.e. s in
+ * {0, 3}); ORC_E_STATE for d = 2. */
+int  orc_trace(orc_mps* s, double* re_im);
+/* <psi|O_{site,site+1}|psi> / <psi|psi> (E5: arbitrary gauge, full left and right
+ * environments); O is d^2 x d^2 row-major complex128, O[(s d + t), (s' d + t')] with s the physical
+ * index of `site`. d = 2 only (ORC_E_STATE otherwise). */
+int  orc_expectation2(orc_mps* s, int site, const double* O, double* re_im);
 /* the last gate's sorted spectrum (for parity on isolated updates) */
 int  orc_last_spectrum(orc_mps*, int gate_in_layer, double* sigma_sorted, int cap, int* n);
 

@@ -28,6 +28,7 @@ ABI_FUNCTIONS = [
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
+    "mps_overlap", "mps_trace", "mps_expectation2",
 ]
 
 
@@ -93,6 +94,9 @@ def lib():
             "mps_ledger_get": [_P, _P, _P, _P],
             "mps_ledger_set": [_P, dbl, i64, i32],
             "mps_plan_regime": [i32, i32, _P, _P, _P, _P],
+            "mps_overlap": [_P, _P, _P],
+            "mps_trace": [_P, _P],
+            "mps_expectation2": [_P, i32, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -330,6 +334,35 @@ class MPS:
         cnt = np.zeros(len(self.PHASES), np.int64)
         self._check(lib().mps_phase_times(self._h, _ptr(ms), _ptr(cnt)))
         return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
+
+    # ---- observables (NEXT-4): E7 / E9 building blocks and E5, computed on the device ---------
+    def mps_overlap(self, other: "MPS") -> complex:
+        """<self|other> (d = 2) or the Hilbert-Schmidt <<rho_self|rho_other>> (d = 4)."""
+        out = (C.c_double * 2)()
+        self._check(lib().mps_overlap(self._h, other._h, out))
+        return complex(out[0], out[1])
+
+    def mps_trace(self) -> complex:
+        out = (C.c_double * 2)()
+        self._check(lib().mps_trace(self._h, out))
+        return complex(out[0], out[1])
+
+    def mps_expectation2(self, site: int, O) -> complex:
+        O = _c64(O)
+        out = (C.c_double * 2)()
+        self._check(lib().mps_expectation2(self._h, int(site), _ptr(O), out))
+        return complex(out[0], out[1])
+
+    def pure_fidelity(self, other: "MPS") -> float:
+        """E7 |<a|b>|^2 / (<a|a> <b|b>): three device overlaps; the division is
+        the only host arithmetic."""
+        ab = self.mps_overlap(other)
+        return abs(ab) ** 2 / (self.mps_overlap(self).real * other.mps_overlap(other).real)
+
+    def wang_fidelity(self, other: "MPS") -> float:
+        """E9 |Tr(rho sigma)| / sqrt(Tr rho^2 Tr sigma^2) of two MPOs."""
+        ab = self.mps_overlap(other)
+        return abs(ab) / (self.mps_overlap(self).real * other.mps_overlap(other).real) ** 0.5
 
     def mps_sync(self):
         self._check(lib().mps_sync(self._h))

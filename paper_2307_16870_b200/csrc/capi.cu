@@ -1332,6 +1332,179 @@ mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
   return device_error(h);
 }
 
+// ---- observables (NEXT-4) ---------------------------------------------------------
+namespace {
+
+mps_status site_table(mps_t h, std::vector<SiteEntry>& out) {
+  mps_status st = sync_state(h);
+  if (st != MPS_OK) return st;
+  out.resize(h->N);
+  SiteEntry* hb = static_cast<SiteEntry*>(pinned_buf(h, sizeof(SiteEntry) * h->N));
+  if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  CK(cudaMemcpyAsync(hb, h->slab + h->hstate.sites_off, sizeof(SiteEntry) * h->N, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  std::copy(hb, hb + h->N, out.begin());
+  return MPS_OK;
+}
+
+// scratch carved from the top of the slab (above the pool), like the amplitude / statevector queries
+mps_status query_scratch(mps_t h, size_t bytes, uint8_t** base) {
+  const size_t need = align_up(bytes) + kAlign;
+  if (h->hstate.pool.bump + need + 4 * kAlign > h->slab_bytes) return set_err(h, MPS_E_NOMEM, "no room for query");
+  *base = h->slab + align_up(h->slab_bytes - 4 * kAlign - need);
+  return MPS_OK;
+}
+
+// <a|b> by left-to-right transfer matrices E_{i+1} = sum_s A_i^{s dagger} E_i B_i^s (FP64), the
+// two-site step at `site` (if O != nullptr) contracting the bra theta with O theta (E5)
+mps_status transfer_chain(mps_t a, mps_t b, const std::vector<SiteEntry>& sa, const std::vector<SiteEntry>& sb,
+                          int site, const float2* dO, double2* result) {
+  const int N = a->N, d = a->d;
+  size_t maxe = 1, maxt = 1;
+  for (int i = 0; i < N; ++i) {
+    maxe = std::max(maxe, (size_t)sa[i].chr * sb[i].chr);
+    maxt = std::max(maxt, (size_t)sa[i].chl * d * sb[i].chr);
+  }
+  size_t th_el = 0;
+  if (dO) {
+    th_el = (size_t)sa[site].chl * d * d * sa[site + 1].chr;
+    maxt = std::max(maxt, (size_t)sa[site].chl * d * d * sb[site + 1].chr);
+  }
+  uint8_t* base = nullptr;
+  const size_t eb = align_up(maxe * 16), tb = align_up(maxt * 16), thb = align_up(th_el * 16);
+  mps_status st = query_scratch(a, 2 * eb + tb + 2 * thb + kAlign, &base);
+  if (st != MPS_OK) return st;
+  double2* E0 = reinterpret_cast<double2*>(base);
+  double2* E1 = reinterpret_cast<double2*>(base + eb);
+  double2* Tb = reinterpret_cast<double2*>(base + 2 * eb);
+  double2* th = reinterpret_cast<double2*>(base + 2 * eb + tb);
+  double2* oth = reinterpret_cast<double2*>(base + 2 * eb + tb + thb);
+  double2* one = static_cast<double2*>(pinned_buf(a, 16));
+  *one = make_double2(1.0, 0.0);
+  mps_t h = a;
+  CK(cudaMemcpyAsync(E0, one, 16, cudaMemcpyHostToDevice, a->s));
+  for (int i = 0; i < N; ++i) {
+    if (dO && i == site) {
+      const float2* Bk = reinterpret_cast<const float2*>(a->slab + sa[i].off);
+      const float2* Bk1 = reinterpret_cast<const float2*>(a->slab + sa[i + 1].off);
+      const int l = sa[i].chl, mid = sa[i].chr, r = sa[i + 1].chr;
+      launch_theta2(Bk, Bk1, th, l, d, mid, r, a->s);
+      launch_apply_O(dO, th, oth, l, d * d, r, a->s);
+      launch_transfer(E0, th, true, oth, true, Tb, E1, l, l, d * d, r, r, a->s);
+      a->launches += 4;
+      std::swap(E0, E1);
+      ++i;
+      continue;
+    }
+    const void* A = a->slab + sa[i].off;
+    const void* B = b->slab + sb[i].off;
+    launch_transfer(E0, A, false, B, false, Tb, E1, sa[i].chl, sb[i].chl, d, sa[i].chr, sb[i].chr, a->s);
+    a->launches += 2;
+    std::swap(E0, E1);
+  }
+  CKL("transfer");
+  CK(cudaMemcpyAsync(one, E0, 16, cudaMemcpyDeviceToHost, a->s));
+  CK(cudaStreamSynchronize(a->s));
+  *result = *one;
+  return MPS_OK;
+}
+
+}  // namespace
+
+mps_status mps_overlap(mps_t a, mps_t b, double* re_im) {
+  DEVICE_GUARD(a);
+  if (!a || !b || !re_im) return MPS_E_INVAL;
+  mps_t h = a;
+  if (a->N != b->N || a->d != b->d) return set_err(a, MPS_E_INVAL, "overlap: different N or d");
+  if (a->device != b->device) return set_err(a, MPS_E_INVAL, "overlap: handles on different devices");
+  if (a->job.active || b->job.active) return set_err(a, MPS_E_STATE, "a layer is in progress");
+  mps_status st = check_sticky(a);
+  if (st != MPS_OK) return st;
+  st = check_sticky(b);
+  if (st != MPS_OK) return set_err(a, st, "overlap: the other handle has a sticky error");
+  if (a->chl[0] != 1 || a->chr[a->N - 1] != 1 || b->chl[0] != 1 || b->chr[b->N - 1] != 1)
+    return set_err(a, MPS_E_STATE, "open boundary legs");
+  if (b != a) CK(cudaStreamSynchronize(b->s));
+  std::vector<SiteEntry> sa, sb;
+  st = site_table(a, sa);
+  if (st != MPS_OK) return st;
+  st = b == a ? MPS_OK : site_table(b, sb);
+  if (st != MPS_OK) return set_err(a, st, "overlap: reading the other handle");
+  double2 v;
+  st = transfer_chain(a, b, sa, b == a ? sa : sb, -1, nullptr, &v);
+  if (st != MPS_OK) return st;
+  re_im[0] = v.x;
+  re_im[1] = v.y;
+  return device_error(a);
+}
+
+mps_status mps_trace(mps_t h, double* re_im) {
+  DEVICE_GUARD(h);
+  if (!h || !re_im) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (h->d != 4) return set_err(h, MPS_E_STATE, "trace: d = 4 (vectorised MPO) only");
+  if (h->chl[0] != 1 || h->chr[h->N - 1] != 1) return set_err(h, MPS_E_STATE, "open boundary legs");
+  std::vector<SiteEntry> se;
+  st = site_table(h, se);
+  if (st != MPS_OK) return st;
+  int maxchi = 1;
+  for (int i = 0; i < h->N; ++i) maxchi = std::max(maxchi, (int)se[i].chr);
+  uint8_t* base = nullptr;
+  const size_t vb = align_up((size_t)maxchi * 16);
+  st = query_scratch(h, 2 * vb, &base);
+  if (st != MPS_OK) return st;
+  double2* v0 = reinterpret_cast<double2*>(base);
+  double2* v1 = reinterpret_cast<double2*>(base + vb);
+  double2* one = static_cast<double2*>(pinned_buf(h, 16));
+  *one = make_double2(1.0, 0.0);
+  CK(cudaMemcpyAsync(v0, one, 16, cudaMemcpyHostToDevice, h->s));
+  for (int i = 0; i < h->N; ++i) {
+    launch_trace_step(reinterpret_cast<const float2*>(h->slab + se[i].off), v0, v1, se[i].chl, se[i].chr, h->s);
+    ++h->launches;
+    std::swap(v0, v1);
+  }
+  CKL("trace");
+  CK(cudaMemcpyAsync(one, v0, 16, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  re_im[0] = one->x;
+  re_im[1] = one->y;
+  return device_error(h);
+}
+
+mps_status mps_expectation2(mps_t h, int32_t site, const float* O, double* re_im) {
+  DEVICE_GUARD(h);
+  if (!h || !O || !re_im) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (h->d != 2) return set_err(h, MPS_E_STATE, "expectation2: d = 2 (MPS) only");
+  if (site < 0 || site >= h->N - 1) return set_err(h, MPS_E_RANGE, "site out of range");
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in progress");
+  if (h->chl[0] != 1 || h->chr[h->N - 1] != 1) return set_err(h, MPS_E_STATE, "open boundary legs");
+  const int D = h->d * h->d;
+  for (int x = 0; x < 2 * D * D; ++x)
+    if (!std::isfinite(O[x])) return set_err(h, MPS_E_INVAL, "non-finite operator entry");
+  std::vector<SiteEntry> se;
+  st = site_table(h, se);
+  if (st != MPS_OK) return st;
+  // the operator and the identity staged below the query scratch (the top 2 KB of the slab)
+  float2* hO = static_cast<float2*>(pinned_buf(h, 16 * D * D));
+  std::memcpy(hO, O, 8 * (size_t)D * D);
+  for (int x = 0; x < D * D; ++x) hO[D * D + x] = make_float2((x / D) == (x % D) ? 1.f : 0.f, 0.f);
+  float2* dO = reinterpret_cast<float2*>(h->slab + h->slab_bytes - 3 * kAlign);   // 2 x 16 x 8 B = 256 B
+  CK(cudaMemcpyAsync(dO, hO, 16 * (size_t)D * D, cudaMemcpyHostToDevice, h->s));
+  double2 num, den;
+  st = transfer_chain(h, h, se, se, site, dO, &num);
+  if (st != MPS_OK) return st;
+  st = transfer_chain(h, h, se, se, site, dO + D * D, &den);
+  if (st != MPS_OK) return st;
+  const double dd = den.x * den.x + den.y * den.y;
+  if (!(dd > 0.0)) return set_err(h, MPS_E_STATE, "zero norm");
+  re_im[0] = (num.x * den.x + num.y * den.y) / dd;
+  re_im[1] = (num.y * den.x - num.x * den.y) / dd;
+  return device_error(h);
+}
+
 mps_status mps_snapshot_save(mps_t h, void* buf, size_t buf_bytes, size_t* bytes_needed) {
   DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;

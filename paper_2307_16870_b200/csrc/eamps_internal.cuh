@@ -169,6 +169,12 @@ void launch_pool_free(uint8_t* slab, DevState* st, int64_t off, int cls, cudaStr
 void launch_gate1(uint8_t* slab, DevState* st, int site, int d, const float2* d_u, cudaStream_t s);
 void launch_amplitude_step(uint8_t* slab, const DevState* st, int site, int digit, const double2* vin, double2* vout,
                            cudaStream_t s);
+// observables (NEXT-4, query.cu)
+void launch_transfer(const double2* E, const void* A, bool a64, const void* B, bool b64, double2* Tbuf, double2* Eout,
+                     int la, int lb, int D, int ra, int rb, cudaStream_t s);
+void launch_theta2(const float2* Bk, const float2* Bk1, double2* th, int l, int d, int mid, int r, cudaStream_t s);
+void launch_apply_O(const float2* O, const double2* th, double2* out, int l, int D, int r, cudaStream_t s);
+void launch_trace_step(const float2* B, const double2* vin, double2* vout, int l, int r, cudaStream_t s);
 void launch_statevector_step(uint8_t* slab, const DevState* st, int site, int64_t rows, int cols_in,
                              const double2* Sin, double2* Sout, cudaStream_t s);
 

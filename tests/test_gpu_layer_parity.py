@@ -198,3 +198,26 @@ def test_config3_deep_layers_sampled_gates():
         order = np.argsort(size)
         picks = sorted({int(order[-1]), int(order[len(order) // 2])})
         sampled_gate_check(gpu, sites, us, picks, rule)
+
+
+# ---- NEXT-2: the fixed-chi baseline of the paper's Fig. 4 protocol -- the same
+# kernels with fidelity targeting off (F_min = 1: exact mode, t = 1) and the bond cap chi_max = the
+# EA run's peak chi (PAPER.md:195 caption, :201-203). Truncations then come from the cap alone; the
+# ledger still records f_j = 1 - T_k/P of every capped cut (E10) and the guarantee is lost (:214).
+def test_fixed_chi_baseline_every_layer_identical_inputs():
+    cfg = workloads.CONFIGS[1]
+    N = cfg["n_sites"]
+    layers = workloads.brickwork_circuit(1, N, cfg["depth"])
+    npl = workloads.n_two_qubit_gates(layers)
+    # the EA run's peak chi (config 1, F_min = 0.99) sets the fixed cap
+    ea = _pk().MPS(N, f_min=cfg["f_min"], n_planned=npl, strategy="global", slab_bytes=256 << 20)
+    ea.run(layers)
+    chi_peak = int(max(ea.mps_bond_dims()))
+    kw = dict(f_min=1.0, n_planned=npl, strategy="global", chi_cap=chi_peak)
+    gpu, worst, ties = run_identical(layers, N, kw, "pure", slab=256 << 20, min_theta=16)
+    recs = gpu.mps_truncation_log()
+    assert any(r["capped"] for r in recs)                 # the cap is what truncates
+    assert max(gpu.mps_bond_dims()) == chi_peak
+    assert not gpu.mps_fidelity_estimate()["guarantee_held"]
+    print("fixed chi = %d: worst sigma err %.2e, near-ties %d, est %.6f (EA %.6f)"
+          % (chi_peak, worst, ties, gpu.mps_fidelity_estimate()["est"], ea.mps_fidelity_estimate()["est"]))
