@@ -95,6 +95,13 @@ mps_status mps_destroy(mps_t);
 
 /* Single-site gate (d x d, row-major c64, host pointer), no truncation. */
 mps_status mps_apply_gate1(mps_t, int32_t site, const float* U);
+/* A layer of single-site gates on distinct sites (the one-qubit layers of the paper's random
+ * circuits, "alternates randomly chosen layers of one- and two-qubit gates"; for d = 4
+ * the 4 x 4 superoperator, e.g. (D (x) D)-free U (x) U* followed by a one-qubit channel): sites[g]
+ * (host, int32, distinct, in [0, N)), Us (host, n_gates * d^2 c64 row-major). One launch for the
+ * layer; no truncation (single-site gates do not change bond dimensions). Synchronous.
+ * MPS_E_RANGE / MPS_E_INVAL (repeated site, non-finite entry). */
+mps_status mps_apply_layer1(mps_t, int32_t n_gates, const int32_t* sites, const float* Us);
 /* One two-site gate on (site, site+1): contract -> SVD -> fidelity-driven truncation ->
  * reabsorb. U host pointer, d^2 x d^2 c64 row-major. */
 mps_status mps_apply_gate2(mps_t, int32_t site, const float* U);

@@ -209,9 +209,17 @@ class OracleMPS:
         Us = _c128(Us)
         _ck(lib().orc_apply_layer(self._h, sites.size, _ptr(sites), _ptr(Us)))
 
+    def apply_layer1(self, sites, Us):
+        """A layer of single-site gates (test plumbing: one orc_apply_gate1 per site)."""
+        for i, u in zip(np.asarray(sites).ravel(), np.asarray(Us)):
+            self.apply_gate1(int(i), u)
+
     def run(self, layers):
         for sites, us in layers:
-            self.apply_layer(sites, us)
+            if np.asarray(us).shape[-1] == self.d and len(sites):
+                self.apply_layer1(sites, us)
+            else:
+                self.apply_layer(sites, us)
 
     def bond_dims(self) -> np.ndarray:
         out = np.zeros(self.n_sites - 1, np.int32)

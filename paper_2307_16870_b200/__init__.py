@@ -28,7 +28,7 @@ ABI_FUNCTIONS = [
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
-    "mps_overlap", "mps_trace", "mps_expectation2",
+    "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1",
 ]
 
 
@@ -97,6 +97,7 @@ def lib():
             "mps_overlap": [_P, _P, _P],
             "mps_trace": [_P, _P],
             "mps_expectation2": [_P, i32, _P, _P],
+            "mps_apply_layer1": [_P, i32, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -188,6 +189,12 @@ class MPS:
         Us = _c64(Us)
         self._check(lib().mps_apply_layer(self._h, int(sites.size), _ptr(sites), _ptr(Us)))
 
+    def mps_apply_layer1(self, sites, Us):
+        """A layer of single-site gates (distinct sites)."""
+        sites = np.ascontiguousarray(sites, np.int32)
+        Us = _c64(Us)
+        self._check(lib().mps_apply_layer1(self._h, int(sites.size), _ptr(sites), _ptr(Us)))
+
     def mps_layer_begin(self, sites, Us) -> int:
         """a0-a3 of the layer's first wave, issued without waiting (returns the waves issued)."""
         sites = np.ascontiguousarray(sites, np.int32)
@@ -211,8 +218,13 @@ class MPS:
         self._check(lib().mps_ledger_set(self._h, float(log_E), int(j), int(guarantee)))
 
     def run(self, layers):
+        """Apply layers in order: a layer whose gates are d x d is a single-site layer
+        (mps_apply_layer1), d^2 x d^2 a two-site layer (mps_apply_layer)."""
         for sites, us in layers:
-            self.mps_apply_layer(sites, us)
+            if np.asarray(us).shape[-1] == self.d and len(sites):
+                self.mps_apply_layer1(sites, us)
+            else:
+                self.mps_apply_layer(sites, us)
 
     # -- queries -------------------------------------------------------------------------------
     def mps_fidelity_estimate(self):

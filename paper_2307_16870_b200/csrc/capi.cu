@@ -818,6 +818,42 @@ mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
   return MPS_OK;
 }
 
+mps_status mps_apply_layer1(mps_t h, int32_t G, const int32_t* sites, const float* Us) {
+  DEVICE_GUARD(h);
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (G < 0 || (G > 0 && (!sites || !Us))) return set_err(h, MPS_E_INVAL, "bad arguments");
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is still in progress (mps_layer_step)");
+  if (G == 0) return MPS_OK;
+  const int dd = h->d * h->d;
+  std::vector<char> seen(h->N, 0);
+  for (int g = 0; g < G; ++g) {
+    if (sites[g] < 0 || sites[g] >= h->N) return set_err(h, MPS_E_RANGE, "gate site out of range");
+    if (seen[sites[g]]) return set_err(h, MPS_E_INVAL, "two single-site gates on one site in a layer");
+    seen[sites[g]] = 1;
+  }
+  for (int64_t x = 0; x < (int64_t)G * dd * 2; ++x)
+    if (!std::isfinite(Us[x])) return set_err(h, MPS_E_INVAL, "non-finite gate entry");
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const size_t sb = align_up((size_t)G * 4), ub = (size_t)G * dd * 8;
+  const size_t need = align_up(sb + ub) + kAlign;
+  if (h->hstate.pool.bump + need + 4 * kAlign > h->slab_bytes) return set_err(h, MPS_E_NOMEM, "no room for the layer");
+  const size_t base = align_up(h->slab_bytes - 4 * kAlign - need);
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, sb + ub, 1));
+  if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  std::memcpy(hb, sites, 4 * (size_t)G);
+  std::memcpy(hb + sb, Us, ub);
+  CK(cudaMemcpyAsync(h->slab + base, hb, sb + ub, cudaMemcpyHostToDevice, h->s));
+  launch_gate1_layer(h->slab, h->dst, G, reinterpret_cast<const int32_t*>(h->slab + base),
+                     reinterpret_cast<const float2*>(h->slab + base + sb), h->d, h->s);
+  ++h->launches;
+  CKL("gate1_layer");
+  CK(cudaStreamSynchronize(h->s));   // the pinned staging buffer is reused by the next call
+  return MPS_OK;
+}
+
 mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float* Us, int32_t* n_waves) {
   DEVICE_GUARD(h);
   if (n_waves) *n_waves = 0;

@@ -167,6 +167,8 @@ void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, c
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s);
 void launch_pool_free(uint8_t* slab, DevState* st, int64_t off, int cls, cudaStream_t s);
 void launch_gate1(uint8_t* slab, DevState* st, int site, int d, const float2* d_u, cudaStream_t s);
+void launch_gate1_layer(uint8_t* slab, DevState* st, int count, const int32_t* d_sites, const float2* d_us, int d,
+                        cudaStream_t s);
 void launch_amplitude_step(uint8_t* slab, const DevState* st, int site, int digit, const double2* vin, double2* vout,
                            cudaStream_t s);
 // observables (NEXT-4, query.cu)

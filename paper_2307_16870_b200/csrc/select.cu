@@ -423,6 +423,43 @@ void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record*
   }
   k_commit<<<1, kCommitThreads, sizeof(CommitSmem), s>>>(d_desc, G, slab, st, d_rec);
 }
+// a layer of single-site gates (disjoint sites; NEXT-3's one-qubit layers): gate g acts on
+// sites[g] with U = Us + g D^2. grid (blocks, count).
+template <int D>
+__global__ void k_gate1_layer(uint8_t* slab, const DevState* st, const int32_t* __restrict__ sites,
+                              const float2* __restrict__ Us) {
+  const int g = blockIdx.y;
+  const SiteEntry e = reinterpret_cast<const SiteEntry*>(slab + st->sites_off)[sites[g]];
+  const float2* U = Us + (int64_t)g * D * D;
+  float2* B = reinterpret_cast<float2*>(slab + e.off);
+  const int64_t tot = (int64_t)e.chl * e.chr;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = x / e.chr, c = x % e.chr;
+    float2 in[D];
+#pragma unroll
+    for (int s = 0; s < D; ++s) in[s] = B[(a * D + s) * e.chr + c];
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+      float2 o = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const float2 u = U[s * D + t];
+        o.x += u.x * in[t].x - u.y * in[t].y;
+        o.y += u.x * in[t].y + u.y * in[t].x;
+      }
+      B[(a * D + s) * e.chr + c] = o;
+    }
+  }
+}
+
+void launch_gate1_layer(uint8_t* slab, DevState* st, int count, const int32_t* d_sites, const float2* d_us, int d,
+                        cudaStream_t s) {
+  if (count <= 0) return;
+  const dim3 grid(16, count);
+  if (d == 2) k_gate1_layer<2><<<grid, 256, 0, s>>>(slab, st, d_sites, d_us);
+  else k_gate1_layer<4><<<grid, 256, 0, s>>>(slab, st, d_sites, d_us);
+}
+
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s) {
   k_pool_alloc<<<1, 1, 0, s>>>(slab, st, bytes, d_out);
 }

@@ -221,3 +221,47 @@ def test_fixed_chi_baseline_every_layer_identical_inputs():
     assert not gpu.mps_fidelity_estimate()["guarantee_held"]
     print("fixed chi = %d: worst sigma err %.2e, near-ties %d, est %.6f (EA %.6f)"
           % (chi_peak, worst, ties, gpu.mps_fidelity_estimate()["est"], ea.mps_fidelity_estimate()["est"]))
+
+
+# ---- NEXT-3: paper-faithful noisy workloads on the GPU -- one-qubit layers
+# (mps_apply_layer1), the two-qubit depolarising channel fused into the superoperator, and the
+# alternating one-/two-qubit circuits of PAPER.md:201 with eps_1 = eps_2 noise,
+# every layer on identical inputs against the oracle.
+def run_identical_mixed(layers, N, kw, rule, slab=1 << 30):
+    pk = _pk()
+    gpu = pk.MPS(N, slab_bytes=slab, **kw)
+    d = kw.get("d", 2)
+    n2 = 0
+    for sites, us in layers:
+        orc = mirror(gpu, N, kw)
+        if np.asarray(us).shape[-1] == d:        # a one-qubit layer: compare the site tensors
+            gpu.mps_apply_layer1(sites, us)
+            orc.apply_layer1(sites, us)
+            for i in sites:
+                g, o = gpu.mps_export_site(int(i)), orc.export_site(int(i))
+                assert np.abs(g - o).max() <= 1e-6 * max(1e-30, np.abs(o).max()), int(i)
+        else:
+            gpu.mps_apply_layer(sites, us)
+            orc.apply_layer(sites, us)
+            compare_identical(gpu, orc, len(sites), rule)
+            eg, eo = gpu.mps_fidelity_estimate(), orc.estimate()
+            assert abs(eg["est"] - eo["est"]) < EST_ATOL
+            n2 += len(sites)
+        orc.close()
+    return gpu, n2
+
+
+def test_alternating_mps_every_layer_identical_inputs():
+    N, depth = 12, 6
+    layers = workloads.alternating_circuit(6, N, depth, "mps")
+    kw = dict(f_min=0.99, n_planned=workloads.n_two_qubit_gates_any(layers, 2), strategy="global")
+    gpu, n2 = run_identical_mixed(layers, N, kw, "pure", slab=256 << 20)
+    assert gpu.mps_fidelity_estimate()["n_done"] == n2
+
+
+def test_alternating_noisy_mpo_every_layer_identical_inputs():
+    N, depth = 8, 5
+    layers = workloads.alternating_circuit(7, N, depth, "mpo", eps1=0.05, eps2=0.05)
+    kw = dict(d=4, f_min=0.95, n_planned=workloads.n_two_qubit_gates_any(layers, 4), strategy="global", rule="wang")
+    gpu, n2 = run_identical_mixed(layers, N, kw, "wang", slab=512 << 20)
+    assert gpu.mps_fidelity_estimate()["is_lower_bound"]

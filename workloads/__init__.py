@@ -141,6 +141,70 @@ def mpo_circuit(config: int, n_sites: int, depth: int, p: float):
 
 
 # ---------------------------------------------------------------------------------------------
+# NEXT-3: paper-faithful noisy workloads. PAPER.md:201: the random circuits
+# "alternate randomly chosen layers of one- and two-qubit gates" (Cheng's definition is not in the
+# container: Haar one-qubit layers on every site alternating with Haar two-qubit brickwork layers
+# stand in); one- and two-qubit depolarising noise eps_1 = eps_2 after the gates.
+# ---------------------------------------------------------------------------------------------
+def haar_u2(*key: int) -> np.ndarray:
+    """One Haar-random U(2), rounded to complex64 (Ginibre + QR + phase fix)."""
+    return haar_from_ginibre(ginibre(rng_for(*key), 2)).astype(np.complex64)
+
+
+def depolarizing_2q(p: float) -> np.ndarray:
+    """Two-qubit depolarising superoperator on the 2-site vectorised index (4 s1 + s2,
+    s = 2 sigma + sigma'): (1 - p) rho + (p / 15) sum_{(P, Q) != (I, I)} (P (x) Q) rho (P (x) Q)^dagger
+    (the two-qubit analogue of SPEC.md:340's convention). At p = 15/16 it is the full twirl
+    rho -> Tr(rho) I / 4."""
+    paulis = [np.eye(2, dtype=np.complex128)] + list(PAULI.values())
+    D = (1.0 - p) * np.eye(16, dtype=np.complex128)
+    for a in range(4):
+        for b in range(4):
+            if a == 0 and b == 0:
+                continue
+            D += (p / 15.0) * unitary_superop(np.kron(paulis[a], paulis[b]))
+    return D
+
+
+def superop_1q(u: np.ndarray, p: float) -> np.ndarray:
+    """D_1(p) (U (x) U*) on one site's vectorised index s = 2 sigma + sigma', rounded to complex64."""
+    u = np.asarray(u, np.complex128)
+    return (depolarizing_1q(p) @ np.kron(u, np.conj(u))).astype(np.complex64)
+
+
+def superop_2q(u: np.ndarray, p: float) -> np.ndarray:
+    """D_2(p) (U (x) U*) on the 2-site vectorised index, rounded to complex64."""
+    return (depolarizing_2q(p) @ unitary_superop(u)).astype(np.complex64)
+
+
+def alternating_circuit(config: int, n_sites: int, depth: int, kind: str = "mps", eps1: float = 0.0,
+                        eps2: float = 0.0):
+    """Layers alternating a one-qubit layer (Haar U(2) on every site; seed [.., config, t, i, 1])
+    and a two-qubit brickwork layer (Haar U(4) on (i, i+1), i = t mod 2; seed [.., config, t, i]),
+    `depth` of each. kind = "mps": unitaries (d x d and d^2 x d^2); kind = "mpo": superoperators
+    with one-qubit depolarising eps1 after each one-qubit gate and two-qubit depolarising eps2
+    after each two-qubit gate. The layer's gate shape tells the two kinds apart."""
+    layers = []
+    for t in range(depth):
+        s1 = list(range(n_sites))
+        u1 = [haar_u2(config, t, i, 1) for i in s1]
+        if kind == "mpo":
+            u1 = [superop_1q(u, eps1) for u in u1]
+        layers.append((np.asarray(s1, np.int32), np.stack(u1)))
+        s2 = brickwork_sites(n_sites, t)
+        u2 = [haar_u4(config, t, i) for i in s2]
+        if kind == "mpo":
+            u2 = [superop_2q(u, eps2) for u in u2]
+        layers.append((np.asarray(s2, np.int32), np.stack(u2)))
+    return layers
+
+
+def n_two_qubit_gates_any(layers, d: int) -> int:
+    """Two-site gates of a mixed circuit (the ledger's n): layers of d^2 x d^2 gates."""
+    return int(sum(len(s) for s, u in layers if len(s) and np.asarray(u).shape[-1] == d * d))
+
+
+# ---------------------------------------------------------------------------------------------
 # Config-2 microbench (BASELINE.json configs[1]; SURVEY.md §8(d) row c2)
 # ---------------------------------------------------------------------------------------------
 def powerlaw_sigma(n: int) -> np.ndarray:
