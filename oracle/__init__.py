@@ -91,6 +91,7 @@ def _declare(L):
     L.orc_overlap.argtypes = [_P, _P, _dp]
     L.orc_trace.argtypes = [_P, _dp]
     L.orc_expectation2.argtypes = [_P, C.c_int, _P, _dp]
+    L.orc_canonicalize.argtypes = [_P]
 
 
 class OracleError(RuntimeError):
@@ -282,6 +283,10 @@ class OracleMPS:
         out = (C.c_double * 2)()
         _ck(lib().orc_expectation2(self._h, int(site), _ptr(O), out))
         return complex(out[0], out[1])
+
+    def canonicalize(self):
+        """NEXT-1: exact canonical form (right-orthonormal B, exact Schmidt lambda), no ledger entry."""
+        _ck(lib().orc_canonicalize(self._h))
 
     def last_spectrum(self, g: int) -> np.ndarray:
         n = C.c_int(0)

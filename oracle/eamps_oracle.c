@@ -714,3 +714,36 @@ int orc_expectation2(orc_mps* s, int k, const double* Od, double* re_im) {
   re_im[1] = cimag(v);
   return ORC_OK;
 }
+
+/* ---- NEXT-1: exact canonicalisation ------------------------------------------------
+ * "We apply QR to each tensor ... and similarly apply a RQ ... The state is now in canonical form"
+ * (PAPER.md:76); "the canonical form ... is enforced throughout". In the B-lambda form
+ * (reading 4) this is two sweeps of exact two-site updates with the identity gate, no
+ * truncation (t = 1: keep every sigma > 1e-14 sigma_0) and no ledger entry:
+ *   right to left (bonds N-2 .. 0): B_{i+1} <- V^H  -> every B_1 .. B_{N-1} right-orthonormal;
+ *   left to right (bonds 0 .. N-2): theta = lambda_{i-1} B_i B_{i+1} is then the exact Schmidt
+ *     decomposition at bond i (left basis orthonormal by induction, right environment right-canonical),
+ *     so lambda_i <- its singular values (renormalised) are the exact Schmidt values.
+ * The represented vector is unchanged up to the global scale. */
+int orc_canonicalize(orc_mps* s) {
+  const int d = s->d, dd = d * d, N = s->N;
+  const orc_config keep = s->cfg;
+  const double logE = s->logE;
+  const int64_t j = s->j, nrec = s->nrec;
+  const int gh = s->guarantee_held;
+  s->cfg.strategy = ORC_STRAT_FIXED;
+  s->cfg.f_fixed = 1.0;
+  s->cfg.chi_cap = 0;
+  double* ident = (double*)calloc((size_t)2 * dd * dd, sizeof(double));
+  for (int x = 0; x < dd; ++x) ident[2 * (x * dd + x)] = 1.0;
+  int st = ORC_OK;
+  for (int i = N - 2; i >= 0 && st == ORC_OK; --i) st = orc_apply_gate2(s, i, ident);
+  for (int i = 0; i <= N - 2 && st == ORC_OK; ++i) st = orc_apply_gate2(s, i, ident);
+  free(ident);
+  s->cfg = keep;
+  s->logE = logE;
+  s->j = j;
+  s->nrec = nrec;
+  s->guarantee_held = gh;
+  return st;
+}

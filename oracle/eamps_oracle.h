@@ -87,6 +87,10 @@ int  orc_trace(orc_mps* s, double* re_im);
  * environments); O is d^2 x d^2 row-major complex128, O[(s d + t), (s' d + t')] with s the physical
  * index of `site`. d = 2 only (ORC_E_STATE otherwise). */
 int  orc_expectation2(orc_mps* s, int site, const double* O, double* re_im);
+/* NEXT-1: exact canonicalisation: two sweeps of exact identity-gate two-site updates
+ * (right to left, then left to right) with no truncation and no ledger entry; afterwards every B_i
+ * (i >= 1) is right-orthonormal and every lambda_b holds the exact Schmidt values of bond b. */
+int  orc_canonicalize(orc_mps* s);
 /* the last gate's sorted spectrum (for parity on isolated updates) */
 int  orc_last_spectrum(orc_mps*, int gate_in_layer, double* sigma_sorted, int cap, int* n);
 
