@@ -148,6 +148,15 @@ mps_status mps_to_statevector(mps_t, double* out, size_t n_doubles);
 /* The bond dimensions chi_1 .. chi_{N-1} of E2 as they stand (host mirror, no
  * device work); out: N-1 int32 (host). */
 mps_status mps_bond_dims(mps_t, int32_t* out /* N-1 */);
+/* Exact canonicalisation (NEXT-1; PAPER.md:76 QR / RQ sweeps, :84 "enforced
+ * throughout"): after truncations or non-unitary MPO maps the B-lambda form is canonical only
+ * approximately (reading 4); two sequential sweeps of exact identity-gate two-site updates
+ * (right to left, then left to right; the same kernels as mps_apply_layer) make every B_i, i >= 1,
+ * right-orthonormal and every lambda the exact Schmidt values of its bond. No truncation beyond the
+ * exact-mode floor (sigma > 1e-6 sigma_0), no ledger entry (log E, j, guarantee, records restored).
+ * 2 (N - 1) sequential single-gate waves: an occasional operation ("every L layers"), not per layer.
+ * Synchronous; device errors as for mps_apply_layer. */
+mps_status mps_canonicalize(mps_t);
 /* ---- observables (NEXT-4); synchronising, FP64 accumulation on the device ----
  * <a|b> = sum_sigma conj(C^a_sigma) C^b_sigma by left-to-right transfer matrices
  * E_{i+1} = sum_s A_i^{s dagger} E_i B_i^s (E2): the overlap behind the pure-state

@@ -28,7 +28,7 @@ ABI_FUNCTIONS = [
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
-    "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1",
+    "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1", "mps_canonicalize",
 ]
 
 
@@ -98,6 +98,7 @@ def lib():
             "mps_trace": [_P, _P],
             "mps_expectation2": [_P, i32, _P, _P],
             "mps_apply_layer1": [_P, i32, _P, _P],
+            "mps_canonicalize": [_P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -194,6 +195,10 @@ class MPS:
         sites = np.ascontiguousarray(sites, np.int32)
         Us = _c64(Us)
         self._check(lib().mps_apply_layer1(self._h, int(sites.size), _ptr(sites), _ptr(Us)))
+
+    def mps_canonicalize(self):
+        """NEXT-1: exact canonical form (right-orthonormal B, exact Schmidt lambda), no ledger entry."""
+        self._check(lib().mps_canonicalize(self._h))
 
     def mps_layer_begin(self, sites, Us) -> int:
         """a0-a3 of the layer's first wave, issued without waiting (returns the waves issued)."""

@@ -1368,6 +1368,63 @@ mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
   return device_error(h);
 }
 
+// ---- NEXT-1: exact canonicalisation -----------------------------------------------
+// Two sweeps of exact two-site updates with the identity gate through the regular layer path (the
+// same kernels): right to left (bonds N-2 .. 0: every B_1 .. B_{N-1} becomes right-orthonormal,
+// B_{i+1} = V^H), then left to right (bonds 0 .. N-2: theta = lambda_{i-1} B_i B_{i+1} is then the
+// exact Schmidt decomposition at bond i, lambda_i <- its renormalised singular values). PAPER.md:76
+// (QR / RQ sweeps "the state is now in canonical form"), :84 ("enforced throughout"). The device
+// ledger runs in per-update exact mode (FIXED, t = 1, no cap) during the sweeps and is restored after
+// (log E, j, guarantee and the records are untouched); the GPU's exact mode keeps sigma > 1e-6 sigma_0
+// (reading 8), i.e. drops at most n 1e-12 of the weight per bond.
+mps_status mps_canonicalize(mps_t h) {
+  DEVICE_GUARD(h);
+  if (!h) return MPS_E_INVAL;
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is still in progress (mps_layer_step)");
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  const DevLedger saved = h->hstate.led;
+  const mps_config cfg_saved = h->cfg;
+  const size_t nrec = h->records.size();
+  DevLedger tmp = saved;
+  tmp.strategy = MPS_STRAT_FIXED;
+  tmp.log_ffixed = 0.0;
+  tmp.chi_cap = 0;
+  DevLedger* hb = static_cast<DevLedger*>(pinned_buf(h, sizeof(DevLedger)));
+  *hb = tmp;
+  CK(cudaMemcpyAsync(&h->dst->led, hb, sizeof(DevLedger), cudaMemcpyHostToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->cfg.strategy = MPS_STRAT_FIXED;
+  h->cfg.f_fixed = 1.0;
+  h->cfg.chi_cap = 0;
+  const int dd = h->d * h->d;
+  std::vector<float> ident((size_t)2 * dd * dd, 0.f);
+  for (int x = 0; x < dd; ++x) ident[2 * (x * dd + x)] = 1.f;
+  for (int i = h->N - 2; i >= 0 && st == MPS_OK; --i) st = mps_apply_layer(h, 1, &i, ident.data());
+  for (int i = 0; i <= h->N - 2 && st == MPS_OK; ++i) st = mps_apply_layer(h, 1, &i, ident.data());
+  // restore the caller's ledger and configuration (the sweeps' f_j = 1 - T_k/P ~ 1 are not counted)
+  h->cfg = cfg_saved;
+  h->records.resize(nrec);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  DevLedger back = h->hstate.led;
+  back.logE = saved.logE;
+  back.j = saved.j;
+  back.guarantee = saved.guarantee;
+  back.strategy = saved.strategy;
+  back.log_ffixed = saved.log_ffixed;
+  back.chi_cap = saved.chi_cap;
+  hb = static_cast<DevLedger*>(pinned_buf(h, sizeof(DevLedger)));
+  *hb = back;
+  CK(cudaMemcpyAsync(&h->dst->led, hb, sizeof(DevLedger), cudaMemcpyHostToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->hstate.led = back;
+  return device_error(h);
+}
+
 // ---- observables (NEXT-4) ---------------------------------------------------------
 namespace {
 
