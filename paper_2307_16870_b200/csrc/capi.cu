@@ -554,7 +554,7 @@ mps_status wave_front(mps_t h) {
     static const bool no_refine = getenv("EAMPS_NO_REFINE") != nullptr;   // dev A/B switch
     if (!no_refine) {
       const int e0 = prof ? prof_mark(h) : -1;
-      h->launches += launch_refine(d_desc, Gw, maxn, h->slab, h->dst, d_us, h->s);
+      h->launches += launch_refine(d_desc, Gw, maxn, h->slab, h->dst, d_us, reinterpret_cast<int32_t*>(h->slab + o_scr), h->s);
       CKL("refine");
       if (prof) prof_span(h, 7, e0, prof_mark(h));
     }

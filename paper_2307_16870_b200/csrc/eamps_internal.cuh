@@ -156,7 +156,8 @@ int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, i
 // gates with n > 256 or a shallow spectrum exit at once. refine_scratch_bytes: the global C
 // scratch a gate with n in (128, 256] needs at ws_log (0 otherwise).
 size_t refine_scratch_bytes(int n);
-int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us, cudaStream_t s);
+int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us,
+                  int32_t* d_list /* G + 1 ints */, cudaStream_t s);
 // parallel = 1: FIXED / NAIVE (target independent of the ledger): one warp per gate;
 // parallel = 0: GLOBAL / NEAREST: one warp walks the gates in canonical order.
 void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s);

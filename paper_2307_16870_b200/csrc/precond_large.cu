@@ -389,6 +389,179 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
   }
 }
 
+// ---- n <= 128 (the QR regime; config 2 chi = 64): Gram + Cholesky + B = L fused in ONE CTA per gate,
+// G (FP64, packed lower triangle, 132 KB at n = 128) never leaves shared memory. Same arithmetic as
+// k_pc_gram + k_pc_chol_cta + k_pc_b_from_l (FP64 products of the FP32 theta, right-looking blocked
+// Cholesky with 32-column panels, pivots <= tau = n eps64 max_i G_ii -> zero column), different
+// summation order. The three kernels take 2.54 + 4.57 + 0.47 ms per 4096-gate step (chi = 64, r02
+// launch list); this variant 9.3 ms (opt-in, see launch_precond_large).
+constexpr int kPcFusedMaxN = 128;
+__host__ __device__ inline int pc_up(int i, int j) { return i * (i + 1) / 2 + j; }   // j <= i
+size_t pc_fused_smem(int n) {
+  return (((size_t)n * (n + 1) / 2 * 16 + 15) & ~(size_t)15) + (size_t)32 * (n + 1) * 8 + 64;
+}
+
+__global__ void __launch_bounds__(256, 1) k_pc_fused(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                                                    uint8_t* slab) {
+  const GateDesc& gd = desc[list[blockIdx.x]];
+  if (gd.jrows <= 0) return;
+  const int m = gd.m, n = gd.n, np = gd.n_pad;
+  extern __shared__ __align__(16) uint8_t pf_sm[];
+  double2* G = reinterpret_cast<double2*>(pf_sm);
+  float2* Th = reinterpret_cast<float2*>(pf_sm + (((size_t)n * (n + 1) / 2 * 16 + 15) & ~(size_t)15));
+  const int pitch = n + 1;
+  __shared__ uint8_t bI[512], bJ[512];
+  __shared__ int s_nblk;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float2* __restrict__ th = reinterpret_cast<const float2*>(slab + gd.ws_theta);
+  // ---- 1. G = theta^H theta, lower triangle, 4 x 8 register blocks (I: rows 4I.., J: columns 8J..)
+  if (tid == 0) {
+    int c = 0;
+    const int NI = (n + 3) / 4, NJ = (n + 7) / 8;
+    for (int I = 0; I < NI; ++I)
+      for (int J = 0; J < NJ && 8 * J <= 4 * I + 3; ++J) {
+        bI[c] = (uint8_t)I;
+        bJ[c] = (uint8_t)J;
+        ++c;
+      }
+    s_nblk = c;
+  }
+  __syncthreads();
+  const int nblk = s_nblk;
+  for (int b0 = 0; b0 < nblk; b0 += 256) {
+    const int b = b0 + tid;
+    const bool act = b < nblk;
+    const int i0 = act ? 4 * bI[b] : 0, j0 = act ? 8 * bJ[b] : 0;
+    double2 acc[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[a][c] = make_double2(0.0, 0.0);
+    for (int r0 = 0; r0 < m; r0 += 32) {
+      __syncthreads();
+      for (int x = tid; x < 32 * n; x += 256) {
+        const int rr = x & 31, c = x >> 5, r = r0 + rr;
+        Th[rr * pitch + c] = r < m ? th[(int64_t)c * m + r] : make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll 2
+        for (int rr = 0; rr < 32; ++rr) {
+          double2 xi[4], yj[8];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const float2 v = (i0 + a < n) ? Th[rr * pitch + i0 + a] : make_float2(0.f, 0.f);
+            xi[a] = make_double2(v.x, v.y);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float2 v = (j0 + c < n) ? Th[rr * pitch + j0 + c] : make_float2(0.f, 0.f);
+            yj[c] = make_double2(v.x, v.y);
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[a][c] = cmul_conj_acc(acc[a][c], xi[a], yj[c]);
+        }
+      }
+    }
+    if (act) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = i0 + a, j = j0 + c;
+          if (i < n && j <= i) G[pc_up(i, j)] = acc[a][c];
+        }
+    }
+  }
+  __syncthreads();
+  // ---- 2. G = L L^H in place (right-looking, 32-column panels)
+  double dm = 0.0;
+  for (int i = tid; i < n; i += 256) dm = fmax(dm, G[pc_up(i, i)].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+  if (lane == 0) s_red[warp] = dm;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int w = 0; w < 8; ++w) gmax = fmax(gmax, s_red[w]);
+  const double tau = (double)n * 2.220446049250313e-16 * gmax;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int w = min(32, n - c0);
+    // (a) the diagonal block, one warp, lane = row
+    if (warp == 0) {
+      for (int j = 0; j < w; ++j) {
+        const double d = G[pc_up(c0 + j, c0 + j)].x;
+        const bool ok = d > tau;
+        const double il = ok ? rsqrt(d) : 0.0;
+        __syncwarp();
+        if (lane >= j && lane < w) {
+          const int q = pc_up(c0 + lane, c0 + j);
+          if (lane == j) G[q] = make_double2(ok ? d * il : 0.0, 0.0);
+          else G[q] = make_double2(G[q].x * il, G[q].y * il);
+        }
+        __syncwarp();
+        if (lane > j && lane < w) {           // row `lane`: G[i][k] -= G[i][j] conj(G[k][j]), j < k <= i
+          const double2 a = G[pc_up(c0 + lane, c0 + j)];
+          for (int k = j + 1; k <= lane; ++k) {
+            const double2 q = G[pc_up(c0 + k, c0 + j)];
+            double2& t = G[pc_up(c0 + lane, c0 + k)];
+            t.x -= a.x * q.x + a.y * q.y;
+            t.y -= a.y * q.x - a.x * q.y;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // (b) the rows below: x L_JJ^H = g_i by forward substitution, one thread per row
+    for (int i = c0 + w + tid; i < n; i += 256) {
+      for (int j = 0; j < w; ++j) {
+        double2 x = G[pc_up(i, c0 + j)];
+        for (int k = 0; k < j; ++k) {          // x -= L[i][k] conj(L[j][k])
+          const double2 a = G[pc_up(i, c0 + k)], q = G[pc_up(c0 + j, c0 + k)];
+          x.x -= a.x * q.x + a.y * q.y;
+          x.y -= a.y * q.x - a.x * q.y;
+        }
+        const double l = G[pc_up(c0 + j, c0 + j)].x;
+        const double il = l > 0.0 ? 1.0 / l : 0.0;
+        G[pc_up(i, c0 + j)] = make_double2(x.x * il, x.y * il);
+      }
+    }
+    __syncthreads();
+    // (c) the trailing lower triangle: G[i][s] -= sum_k L[i][k] conj(L[s][k]), c0 + w <= s <= i
+    const int r = n - c0 - w;
+    const int ntr = r * (r + 1) / 2;
+    for (int x = tid; x < ntr; x += 256) {
+      int ii = (int)((sqrt(8.0 * x + 1.0) - 1.0) * 0.5);
+      while (ii * (ii + 1) / 2 > x) --ii;
+      while ((ii + 1) * (ii + 2) / 2 <= x) ++ii;
+      const int ss = x - ii * (ii + 1) / 2;
+      const int i = c0 + w + ii, sc = c0 + w + ss;
+      double2 t = G[pc_up(i, sc)];
+      for (int k = 0; k < w; ++k) {
+        const double2 a = G[pc_up(i, c0 + k)], q = G[pc_up(sc, c0 + k)];
+        t.x -= a.x * q.x + a.y * q.y;
+        t.y -= a.y * q.x - a.x * q.y;
+      }
+      G[pc_up(i, sc)] = t;
+    }
+    __syncthreads();
+  }
+  // ---- 3. B = L in FP32 (n x n_pad, ld n), zero above the diagonal and in the pad columns
+  float2* B = reinterpret_cast<float2*>(slab + gd.ws_theta);
+  for (int x = tid; x < n * np; x += 256) {
+    const int j = x / n, i = x % n;
+    float2 v = make_float2(0.f, 0.f);
+    if (j < n && i >= j) {
+      const double2 g = G[pc_up(i, j)];
+      v = make_float2((float)g.x, (float)g.y);
+    }
+    B[x] = v;
+  }
+}
+
 // B = L in FP32 (n x n_pad, ld n): the lower triangle of L, zeros above it and in the pad columns
 __global__ void k_pc_b_from_l(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list, uint8_t* slab) {
   const GateDesc& gd = desc[list[blockIdx.y]];
@@ -453,6 +626,18 @@ size_t large_precond_scratch(int n) { return (size_t)16 * n * n + sizeof(CholScr
 
 int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, cudaStream_t s) {
   if (count <= 0) return 0;
+  // EAMPS_PC_FUSED=1: the one-CTA fused variant. Measured slower on the default bench (precond
+  // sub-phase 9.3 ms vs 7.5 ms for the three kernels: with 165 KB of shared memory one CTA per SM
+  // runs the gate's Gram passes and 32-step panel factorisations with nothing to hide their latency),
+  // so the separate kernels stay the default.
+  static const bool fused = getenv("EAMPS_PC_FUSED") != nullptr;
+  if (fused && max_n <= kPcFusedMaxN) {
+    static std::atomic<unsigned long long> fattr{0};
+    if (first_on_device(fattr))
+      cudaFuncSetAttribute(k_pc_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_fused_smem(kPcFusedMaxN));
+    k_pc_fused<<<count, 256, pc_fused_smem(max_n), s>>>(d_desc, d_list, slab);
+    return 1;
+  }
   const int T = (max_n + 63) / 64;
   k_pc_gram<<<dim3(T * (T + 1) / 2, count), 256, 0, s>>>(d_desc, d_list, slab);
   static const bool cta_small = getenv("EAMPS_CHOL_PANELS") == nullptr;   // dev A/B switch

@@ -60,28 +60,12 @@ size_t refine_smem(int n) {
   return s + 64;
 }
 
-__global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint8_t* slab, DevState* st, int G,
-                                               const float2* __restrict__ d_us, int max_sweeps) {
-  GateDesc& gd = desc[blockIdx.x];
+// One gate's refinement (one CTA; the body of k_refine).
+__device__ void refine_gate(GateDesc& gd, uint8_t* slab, DevState* st, const float2* __restrict__ d_us,
+                            int max_sweeps) {
   const int n = gd.n, m = gd.m, np = gd.n_pad, dd = st->d;
-  if (n > kRefineMaxN || n < 2 || blockIdx.x >= G) return;
   double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
-  __shared__ int s_go;
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    const double smax = gS[0];
-    double deep = smax;
-    for (int j = 1; j < n; ++j) {
-      if (gS[j] < 1e-12 * smax) break;
-      deep = gS[j];
-    }
-    // the regimes that accumulate V in FP32 (small 0, medium 2) lose relative accuracy earlier than
-    // the preconditioned ones (QR 3, large 1: V = unit columns of the converged B = L)
-    const double r = (gd.regime == 0 || gd.regime == 2) ? kRefineRatioAcc : kRefineRatio;
-    s_go = (smax > 0.0 && deep < r * r * smax) ? 1 : 0;
-  }
-  __syncthreads();
-  if (!s_go) return;
   extern __shared__ __align__(16) uint8_t sm[];
   double2* As = reinterpret_cast<double2*>(sm);                 // [32][33]
   double2* Bs = As + 32 * 33;                                    // [32][33]
@@ -312,13 +296,46 @@ __global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint
   cta_tails(keys, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
 }
 
+
+// The trigger, one warp per gate of the wave: the gates whose smallest sigma >= 1e-12 sigma_max is
+// below the regime's ratio go to a compact list (count at list[0], gates from list[1]).
+__global__ void k_refine_pick(const GateDesc* __restrict__ desc, const uint8_t* slab, int G, int32_t* list) {
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (g >= G) return;
+  const GateDesc& gd = desc[g];
+  const int n = gd.n;
+  if (n > kRefineMaxN || n < 2) return;
+  const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);   // sorted descending
+  const double smax = gS[0];
+  // the deepest sigma^2 >= 1e-12 sigma_max^2: the last j with gS[j] >= 1e-12 smax (sorted)
+  double deep = smax;
+  for (int j = lane; j < n; j += 32)
+    if (gS[j] >= 1e-12 * smax) deep = fmin(deep, gS[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) deep = fmin(deep, __shfl_xor_sync(0xffffffffu, deep, o));
+  // the regimes that accumulate V in FP32 (small 0, medium 2) lose relative accuracy earlier than
+  // the preconditioned ones (QR 3, large 1: V = unit columns of the converged B = L)
+  const double r = (gd.regime == 0 || gd.regime == 2) ? kRefineRatioAcc : kRefineRatio;
+  if (lane == 0 && smax > 0.0 && deep < r * r * smax) list[1 + atomicAdd(&list[0], 1)] = g;
+}
+
+__global__ void __launch_bounds__(RT) k_refine(GateDesc* __restrict__ desc, uint8_t* slab, DevState* st,
+                                               const int32_t* __restrict__ list, const float2* __restrict__ d_us,
+                                               int max_sweeps) {
+  const int cnt = list[0];
+  for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+    refine_gate(desc[list[1 + li]], slab, st, d_us, max_sweeps);
+    __syncthreads();
+  }
+}
 }  // namespace
 
 size_t refine_scratch_bytes(int n) {
   return (n > kSmemPackedMaxN && n <= kRefineMaxN) ? (size_t)n * (n + 1) / 2 * sizeof(double2) : 0;
 }
 
-int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us, cudaStream_t s) {
+int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us,
+                  int32_t* d_list, cudaStream_t s) {
   if (G <= 0 || max_n < 2) return 0;
   // the wave may mix gates with C in shared memory (n <= 128) and in global memory (n <= 256)
   const int nn = max_n < kRefineMaxN ? max_n : kRefineMaxN;
@@ -327,8 +344,14 @@ int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* s
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)refine_smem(kSmemPackedMaxN));
-  k_refine<<<G, RT, smem, s>>>(d_desc, slab, st, G, d_us, 16);
-  return 1;
+  cudaMemsetAsync(d_list, 0, sizeof(int32_t), s);
+  k_refine_pick<<<(G + 7) / 8, 256, 0, s>>>(d_desc, slab, G, d_list);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = G < sms ? G : sms;   // grid-stride over the compact list (most waves: none)
+  k_refine<<<grid, RT, smem, s>>>(d_desc, slab, st, d_list, d_us, 16);
+  return 2;
 }
 
 }  // namespace eamps
