@@ -935,8 +935,8 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
            align_up(logb);
     int kmax = std::min(gd.m, gd.n);
     if (h->cfg.chi_cap > 0) kmax = std::min(kmax, h->cfg.chi_cap);
-    p.reserve = ((size_t)1 << size_class((uint64_t)gd.l * d * kmax * 8)) +
-                ((size_t)1 << size_class((uint64_t)kmax * d * gd.r * 8)) + ((size_t)1 << size_class((uint64_t)kmax * 4)) +
+    p.reserve = ((size_t)class_bytes(size_class((uint64_t)gd.l * d * kmax * 8))) +
+                ((size_t)class_bytes(size_class((uint64_t)kmax * d * gd.r * 8))) + ((size_t)class_bytes(size_class((uint64_t)kmax * 4))) +
                 3 * kAlign;
     p.ctiles = ((gd.l + TA - 1) / TA) * ((gd.r + TA - 1) / TA);
     const int km = std::min(gd.m, gd.n);
@@ -1231,9 +1231,9 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
   // worst case the new blocks take fresh pool memory: keep the staging area above that
   size_t reserve = 0;
   for (const ImportEntry& e : ent)
-    reserve += ((size_t)1 << size_class((uint64_t)e.chl * h->d * e.chr * 8)) + 2 * kAlign +
-               (e.resetL ? ((size_t)1 << size_class((uint64_t)e.resetL * 4)) : 0) +
-               (e.resetR ? ((size_t)1 << size_class((uint64_t)e.resetR * 4)) : 0);
+    reserve += ((size_t)class_bytes(size_class((uint64_t)e.chl * h->d * e.chr * 8))) + 2 * kAlign +
+               (e.resetL ? ((size_t)class_bytes(size_class((uint64_t)e.resetL * 4))) : 0) +
+               (e.resetR ? ((size_t)class_bytes(size_class((uint64_t)e.resetR * 4))) : 0);
   if (h->hstate.pool.bump + reserve + ent_bytes + data_bytes + kAlign > top) {
     // host data is staged through the top of the slab: import it in two halves (each half's
     // blocks land in the pool before the next half is staged)

@@ -24,8 +24,12 @@ inline bool first_on_device(std::atomic<unsigned long long>& mask) {
   return (mask.fetch_or(bit) & bit) == 0;
 }
 
-constexpr int kMaxClasses = 48;     // pool size classes 2^0 .. 2^47 bytes (blocks >= 256 B)
-constexpr int kMinClass = 8;
+// Pool size classes (round 2): class c holds blocks of class_bytes(c) = 2^(c/2) (c even) or
+// 1.5 x 2^((c-1)/2) (c odd, from 768 B up), so a block wastes at most a third of itself instead of
+// half (power-of-two classes put a chi = 4096 site tensor of 268 MB into a 512 MB block: config 5 ran
+// out of slab at layer 20, r01). All classes are multiples of 256 B. 96 classes cover 2^47 B.
+constexpr int kMaxClasses = 96;
+constexpr int kMinClass = 16;       // 256 B
 
 struct SiteEntry {                  // B_i
   int64_t off;                      // byte offset in the slab (0 = none)
@@ -97,10 +101,15 @@ struct DevState {                   // lives at slab offset 0
   int64_t sites_off, bonds_off;     // SiteEntry[N], BondEntry[N+1]
 };
 
+__host__ __device__ inline uint64_t class_bytes(int c) {
+  return (c & 1) ? (3ull << ((c - 3) >> 1)) : (1ull << (c >> 1));
+}
 __host__ __device__ inline int size_class(uint64_t bytes) {
-  int c = kMinClass;
-  while ((1ull << c) < bytes) ++c;
-  return c;
+  if (bytes <= 256) return kMinClass;
+  int k = 9;                                  // smallest k with 2^k >= bytes
+  while ((1ull << k) < bytes) ++k;
+  if (k - 1 >= 9 && bytes <= (3ull << (k - 2))) return 2 * k - 1;   // 1.5 x 2^(k-1)
+  return 2 * k;
 }
 
 template <typename T>

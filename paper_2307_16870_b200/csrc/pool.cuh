@@ -1,6 +1,6 @@
 // pool.cuh -- the device-side pool allocator of the site store, batched over one CTA.
 //
-// Blocks are powers of two (>= 256 B) carved from the slab: per-class free stacks plus a bump
+// Blocks are size classes of 2^k and 1.5 x 2^k bytes (>= 256 B, class_bytes) carved from the slab: per-class free stacks plus a bump
 // pointer. A batch of requests (in canonical order) is resolved in parallel and
 // deterministically: the rank of a request among the batch's requests of its class comes from a
 // CTA-wide exclusive scan; the first cnt[c] requests of class c pop the stack, the rest take bump
@@ -13,8 +13,10 @@ namespace eamps {
 
 __host__ __device__ inline int size_class_fast(uint64_t bytes) {
 #ifdef __CUDA_ARCH__
-  if (bytes <= (1ull << kMinClass)) return kMinClass;
-  return 64 - __clzll(bytes - 1);
+  if (bytes <= 256) return kMinClass;
+  const int k = 64 - __clzll(bytes - 1);      // smallest k with 2^k >= bytes (k >= 9)
+  if (k - 1 >= 9 && bytes <= (3ull << (k - 2))) return 2 * k - 1;
+  return 2 * k;
 #else
   return size_class(bytes);
 #endif
@@ -131,7 +133,7 @@ __device__ inline bool pool_batch_alloc(PoolBatch& B, int n, uint8_t* slab, cons
   // pops for the first cnt[c] requests of each class, bump sizes for the rest
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int c = B.cls[i];
-    B.tmp[i] = (c >= 0 && B.rank[i] >= B.cnt[c]) ? (1ull << c) : 0ull;
+    B.tmp[i] = (c >= 0 && B.rank[i] >= B.cnt[c]) ? class_bytes(c) : 0ull;
   }
   __syncthreads();
   const uint64_t total = cta_scan_array<uint64_t>(B.tmp, B.tmp, n, B.uws);  // exclusive offsets in tmp

@@ -37,7 +37,7 @@ __device__ uint64_t pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int*
   int64_t* stk = reinterpret_cast<int64_t*>(slab + P.stack_off);
   if (P.count[c] > 0) return (uint64_t)stk[(int64_t)c * P.stack_cap + (--P.count[c])];
   uint64_t o = (P.bump + 255ull) & ~255ull;
-  uint64_t sz = 1ull << c;
+  uint64_t sz = class_bytes(c);
   if (o + sz > P.ceiling) {
     if (st->led.error == 0) st->led.error = -3;  // MPS_E_NOMEM
     return 0;
