@@ -952,7 +952,13 @@ __global__ void __launch_bounds__(256) k_tc_rot(const GateDesc* __restrict__ des
 // chunk's conversion with the previous chunk's MMAs and the tile epilogue with both).
 constexpr int WS_NS = 4;                                     // image ring depth
 constexpr int WS_RAW = 8;                                    // raw chunks in flight per producer row
-constexpr size_t kRotWsSmem = (size_t)EIMG_FLOATS * 4 + (size_t)WS_NS * 2 * kRotStage + (size_t)WS_RAW * 8 * 128 * 8 + 1024;
+constexpr size_t rot_ws_smem(int ns, int nr) { return (size_t)EIMG_FLOATS * 4 + (size_t)ns * 2 * kRotStage + (size_t)nr * 8 * 128 * 8 + 1024; }
+constexpr size_t kRotWsSmem = rot_ws_smem(WS_NS, WS_RAW);
+// the lean variant (EAMPS_ROT_LEAN=1): 2-deep image ring, 4 raw chunks in flight -- 129 KB, so that a
+// rotation CTA and an inner-solve CTA (66 KB) of the other stream's gate group fit one SM together
+constexpr int WS_NS_LEAN = 2, WS_RAW_LEAN = 4;
+constexpr size_t kRotWsSmemLean = rot_ws_smem(WS_NS_LEAN, WS_RAW_LEAN);
+template <int NS, int NR>
 __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                    int rnd, uint8_t* slab, const LargeCtl* ctl) {
   const int gi = blockIdx.y;
@@ -970,16 +976,16 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
   float* Es = reinterpret_cast<float*>(base);                      // 64 KB: Re h|l, Im h|l
-  uint8_t* ring = base + (size_t)EIMG_FLOATS * 4;                  // WS_NS x (hi, lo) x 8 KB
-  float2* rawr = reinterpret_cast<float2*>(ring + (size_t)WS_NS * 2 * kRotStage);   // WS_RAW x [8 cols][128 rows]
-  __shared__ uint64_t full[WS_NS], empty[WS_NS], tfull[2], tempty[2];
+  uint8_t* ring = base + (size_t)EIMG_FLOATS * 4;                  // NS x (hi, lo) x 8 KB
+  float2* rawr = reinterpret_cast<float2*>(ring + (size_t)NS * 2 * kRotStage);   // NR x [8 cols][128 rows]
+  __shared__ uint64_t full[NS], empty[NS], tfull[2], tempty[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
   for (int x = tid; x < EIMG_FLOATS / 4; x += blockDim.x) tc::cp_async16(Es + 4 * x, Eg + 4 * x);
   tc::cp_async_commit();
   if (warp == 0) tc::tmem_alloc(&tbase, 256);
   if (tid == 0) {
-    for (int i = 0; i < WS_NS; ++i) {
+    for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&full[i], 128);
       tc::mbar_init(&empty[i], 1);
     }
@@ -1012,8 +1018,8 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
         tc::fence_after_sync();
         const uint32_t dRe = tmem + 128 * ab, dIm = dRe + 64;
         for (int q = 0; q < CH; ++q, ++u) {
-          const int sl = u % WS_NS;
-          tc::mbar_wait(&full[sl], (u / WS_NS) & 1);
+          const int sl = u % NS;
+          tc::mbar_wait(&full[sl], (u / NS) & 1);
           tc::fence_after_sync();
           const uint32_t a0 = tc::smem_u32(ring + (size_t)sl * 2 * kRotStage);
           const uint32_t eoff = 2 * q * E_LBO;
@@ -1043,7 +1049,7 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
     }
     __syncwarp();
   } else if (warp <= 4) {
-    // ---------------- producers: thread = row. Each thread copies its own row of the next WS_RAW
+    // ---------------- producers: thread = row. Each thread copies its own row of the next NR
     // chunks with 8-byte cp.async (64 KB in flight per CTA), then converts its row into the images.
     const int row_l = tid - 32;
     const int total = ntiles * CH;
@@ -1054,7 +1060,7 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
         const float2* M = reinterpret_cast<const float2*>(slab + (isV ? gd.ws_V : gd.ws_theta));
         const int rows = isV ? np : m;
         const int r = (isV ? t - tiles_th : t) * 128 + row_l;
-        float2* dst = rawr + (size_t)(uu % WS_RAW) * 8 * 128 + row_l;
+        float2* dst = rawr + (size_t)(uu % NR) * 8 * 128 + row_l;
         if (r < rows) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) tc::cp_async8(dst + c * 128, M + (int64_t)colof(8 * q + c, I, J) * rows + r);
@@ -1065,16 +1071,16 @@ __global__ void __launch_bounds__(288) k_tc_rot_ws(const GateDesc* __restrict__ 
       }
       tc::cp_async_commit();
     };
-    for (int uu = 0; uu < WS_RAW - 1; ++uu) issue(uu);
+    for (int uu = 0; uu < NR - 1; ++uu) issue(uu);
     for (int u = 0; u < total; ++u) {
-      issue(u + WS_RAW - 1);
-      tc::cp_async_wait<WS_RAW - 1>();                  // this thread's copies of chunk u landed
-      const float2* src = rawr + (size_t)(u % WS_RAW) * 8 * 128 + row_l;
+      issue(u + NR - 1);
+      tc::cp_async_wait<NR - 1>();                  // this thread's copies of chunk u landed
+      const float2* src = rawr + (size_t)(u % NR) * 8 * 128 + row_l;
       float2 z[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) z[c] = src[c * 128];
-      const int sl = u % WS_NS;
-      if (u >= WS_NS) tc::mbar_wait(&empty[sl], ((u / WS_NS) - 1) & 1);
+      const int sl = u % NS;
+      if (u >= NS) tc::mbar_wait(&empty[sl], ((u / NS) - 1) & 1);
       uint8_t* hi = ring + (size_t)sl * 2 * kRotStage;
       uint8_t* lo = hi + kRotStage;
 #pragma unroll
@@ -1843,6 +1849,7 @@ static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int3
   static const float tol_internal = getenv("EAMPS_TC_TOL_INT") ? (float)atof(getenv("EAMPS_TC_TOL_INT")) : 3.0e38f;
   static const bool prof = getenv("EAMPS_TC_PROF") != nullptr;   // dev: per-kernel device time
   static const int nstreams = getenv("EAMPS_TC_STREAMS") ? atoi(getenv("EAMPS_TC_STREAMS")) : 2;
+  static const bool rot_lean = getenv("EAMPS_ROT_LEAN") != nullptr;   // dev A/B switch
   // L2-resident batches: the rounds of a batch stream each gate's Jacobi matrix (B = L, n x n_pad
   // FP32; + V when not preconditioned) through the Gram and rotation kernels three times a round; a
   // batch whose matrices fit the 126 MB L2 (budget 80 MB) keeps those passes out of HBM. A batch
@@ -1870,7 +1877,8 @@ static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int3
     const int32_t* bl = d_list + b0;
     LargeCtl* bctl = ctl + b0;
     const double* bn2 = norm2 + b0;
-    const int ngroups_want = (!prof && nstreams >= 2 && bc >= 2 && bc * pairs_max < 2048) ? 2 : 1;
+    static const bool groups_all = getenv("EAMPS_TC_GROUPS_ALL") != nullptr;   // dev A/B: 2 groups at any size
+    const int ngroups_want = (!prof && nstreams >= 2 && bc >= 2 && (groups_all || bc * pairs_max < 2048)) ? 2 : 1;
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev_go = nullptr, ev_done = nullptr;
     int ngroups = ngroups_want;
@@ -1904,7 +1912,9 @@ static bool tc_sweep_rounds(GateDesc* d_desc, const GateDesc* h_desc, const int3
                                                                        dbg_sync(ss, "k_tc_inner");
           if (prof) cudaEventRecord(ev[2], ss);
           if (rot_simple) tcj::k_tc_rot<<<gridg, 256, tcj::kRotSmem, ss>>>(d_desc, dl, rnd, slab, cg);
-          else tcj::k_tc_rot_ws<<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
+          else if (rot_lean)
+            tcj::k_tc_rot_ws<tcj::WS_NS_LEAN, tcj::WS_RAW_LEAN><<<gridg, 288, tcj::kRotWsSmemLean, ss>>>(d_desc, dl, rnd, slab, cg);
+          else tcj::k_tc_rot_ws<tcj::WS_NS, tcj::WS_RAW><<<gridg, 288, tcj::kRotWsSmem, ss>>>(d_desc, dl, rnd, slab, cg);
           dbg_sync(ss, "k_tc_rot_ws");
           if (prof) {
             cudaEventRecord(ev[3], ss);
@@ -1964,7 +1974,10 @@ int run_svd_tc(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* d_list, 
     cudaFuncSetAttribute(tcj::k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
     cudaFuncSetAttribute(tcj::k_tc_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kInnerSmem);
     cudaFuncSetAttribute(tcj::k_tc_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotSmem);
-    cudaFuncSetAttribute(tcj::k_tc_rot_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kRotWsSmem);
+    cudaFuncSetAttribute(tcj::k_tc_rot_ws<tcj::WS_NS, tcj::WS_RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tcj::kRotWsSmem);
+    cudaFuncSetAttribute(tcj::k_tc_rot_ws<tcj::WS_NS_LEAN, tcj::WS_RAW_LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tcj::kRotWsSmemLean);
   }
   const int nb_max = max_np / tcj::TB, pairs_max = nb_max / 2;
   static const int inner_sweeps = getenv("EAMPS_INNER_SWEEPS") ? atoi(getenv("EAMPS_INNER_SWEEPS")) : 1;
