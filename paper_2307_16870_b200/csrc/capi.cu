@@ -64,6 +64,7 @@ struct mps_handle {
   std::string err;
   int64_t launches = 0;
   void* pinned[2] = {nullptr, nullptr};   // [0] general / readback, [1] layer upload staging
+  uint8_t* pinned_dev[2] = {nullptr, nullptr};   // their device (UVA-mapped) addresses
   size_t pinned_bytes[2] = {0, 0};
   // phase timers (mps_set_profiling): CUDA events recorded on the launch stream around each phase
   bool profiling = false;
@@ -150,14 +151,53 @@ void* pinned_buf(mps_t h, size_t bytes, int which = 0) {
     if (h->s) cudaStreamSynchronize(h->s); else cudaDeviceSynchronize();
     if (h->pinned[which]) cudaFreeHost(h->pinned[which]);
     size_t nb = std::max(bytes, h->pinned_bytes[which] * 2);
-    if (cudaHostAlloc(&h->pinned[which], nb, cudaHostAllocDefault) != cudaSuccess) {
+    // mapped: the small uploads below read it from the SMs (h2d_small)
+    void* dp = nullptr;
+    if (cudaHostAlloc(&h->pinned[which], nb, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostGetDevicePointer(&dp, h->pinned[which], 0) != cudaSuccess) {
+      if (h->pinned[which]) cudaFreeHost(h->pinned[which]);
       h->pinned[which] = nullptr;
       h->pinned_bytes[which] = 0;
       return nullptr;
     }
+    h->pinned_dev[which] = static_cast<uint8_t*>(dp);
     h->pinned_bytes[which] = nb;
   }
   return h->pinned[which];
+}
+
+// Small host->device uploads (layer descriptors, gate matrices, import entries, scalars) are read
+// by a copy kernel from the mapped pinned buffer instead of going through a DMA copy: a DMA H2D
+// on this stream queues behind whatever bulk H2D the caller has in flight on another stream (the
+// e2e pipeline copies the next chunk's site tensors while this chunk updates), which stalled the
+// whole layer for the length of that bulk copy (measured: tools/dev/e2e_overlap.py). `src` must
+// lie in one of the handle's pinned buffers.
+__global__ void k_h2d_mapped(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t bytes) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n16 = bytes >> 4;
+    for (size_t x = i; x < n16; x += stride) reinterpret_cast<uint4*>(dst)[x] = reinterpret_cast<const uint4*>(src)[x];
+    done = n16 << 4;
+  }
+  for (size_t x = done + i; x < bytes; x += stride) dst[x] = src[x];
+}
+
+cudaError_t h2d_small(mps_t h, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  const uint8_t* hs = static_cast<const uint8_t*>(src);
+  const uint8_t* ds = nullptr;
+  for (int w = 0; w < 2; ++w) {
+    const uint8_t* b = static_cast<const uint8_t*>(h->pinned[w]);
+    if (b && hs >= b && hs + bytes <= b + h->pinned_bytes[w]) ds = h->pinned_dev[w] + (hs - b);
+  }
+  if (!ds) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->s);
+  const size_t n16 = (bytes + 15) / 16;
+  const int blocks = (int)std::min<size_t>(296, std::max<size_t>(1, (n16 + 255) / 256));
+  k_h2d_mapped<<<blocks, 256, 0, h->s>>>(static_cast<uint8_t*>(dst), ds, bytes);
+  ++h->launches;
+  return cudaGetLastError();
 }
 
 mps_status sync_state(mps_t h) {
@@ -467,11 +507,11 @@ mps_status wave_front(mps_t h) {
   for (int x = 0; x < Gw; ++x)
     std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, J.us.data() + (size_t)J.ord[g0 + x].second * d4 * 2,
                 (size_t)d4 * 8);
-  CK(cudaMemcpyAsync(h->slab + base, hb, staged_bytes, cudaMemcpyHostToDevice, h->s));
+  CK(h2d_small(h, h->slab + base, hb, staged_bytes));
   // the pool may not grow into the workspace
   uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + tail);
   *hceil = base;
-  CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
+  CK(h2d_small(h, &h->dst->pool.ceiling, hceil, 8));
 
   GateDesc* d_desc = reinterpret_cast<GateDesc*>(h->slab + o_desc);
   J.o_desc = o_desc;
@@ -544,7 +584,7 @@ mps_status wave_front(mps_t h) {
       // record on device so that it is sticky like the small-path error
       int32_t* he = reinterpret_cast<int32_t*>(hb + tail + 128);
       *he = err;
-      CK(cudaMemcpyAsync(&h->dst->led.error, he, 4, cudaMemcpyHostToDevice, h->s));
+      CK(h2d_small(h, &h->dst->led.error, he, 4));
     }
   }
   // FP64 Rayleigh-Ritz refinement of deep spectra (refine.cu; gates with n <= 256)
@@ -810,7 +850,7 @@ mps_status mps_apply_gate1(mps_t h, int32_t site, const float* U) {
   float* hb = static_cast<float*>(pinned_buf(h, 8 * dd));
   std::memcpy(hb, U, 8 * dd);
   float2* du = reinterpret_cast<float2*>(h->slab + h->slab_bytes - 2 * kAlign);  // 2 KB scratch below the top
-  CK(cudaMemcpyAsync(du, hb, 8 * dd, cudaMemcpyHostToDevice, h->s));
+  CK(h2d_small(h, du, hb, 8 * dd));
   launch_gate1(h->slab, h->dst, site, h->d, du, h->s);
   ++h->launches;
   CKL("gate1");
@@ -845,7 +885,7 @@ mps_status mps_apply_layer1(mps_t h, int32_t G, const int32_t* sites, const floa
   if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
   std::memcpy(hb, sites, 4 * (size_t)G);
   std::memcpy(hb + sb, Us, ub);
-  CK(cudaMemcpyAsync(h->slab + base, hb, sb + ub, cudaMemcpyHostToDevice, h->s));
+  CK(h2d_small(h, h->slab + base, hb, sb + ub));
   launch_gate1_layer(h->slab, h->dst, G, reinterpret_cast<const int32_t*>(h->slab + base),
                      reinterpret_cast<const float2*>(h->slab + base + sb), h->d, h->s);
   ++h->launches;
@@ -1250,8 +1290,8 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
   std::memcpy(hb, ent.data(), sizeof(ImportEntry) * count);
   uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + ent_bytes);
   *hceil = base;
-  CK(cudaMemcpyAsync(&h->dst->pool.ceiling, hceil, 8, cudaMemcpyHostToDevice, h->s));
-  CK(cudaMemcpyAsync(h->slab + base, hb, sizeof(ImportEntry) * count, cudaMemcpyHostToDevice, h->s));
+  CK(h2d_small(h, &h->dst->pool.ceiling, hceil, 8));
+  CK(h2d_small(h, h->slab + base, hb, sizeof(ImportEntry) * count));
   const float2* src = reinterpret_cast<const float2*>(B);
   if (!dev) {
     CK(cudaMemcpyAsync(h->slab + base + ent_bytes, B, (size_t)elems * 8, cudaMemcpyHostToDevice, h->s));
