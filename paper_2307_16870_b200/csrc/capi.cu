@@ -14,6 +14,7 @@
 #include <cstring>
 #include <string>
 #include <array>
+#include <chrono>
 #include <map>
 #include <vector>
 
@@ -43,6 +44,18 @@ struct LayerJob {                  // the layer in flight (mps_layer_begin / mps
 };
 
 constexpr int kPhases = 8;
+
+// EAMPS_HOST_PROF=1: host-side time of the layer path (planning before the first launch, the
+// launch calls, the post-sync bookkeeping), printed by mps_destroy -- the GPU idles through the
+// first and the last. Development instrumentation; off by default.
+struct HostProf {
+  bool on = getenv("EAMPS_HOST_PROF") != nullptr;
+  double plan = 0, launch = 0, wait = 0, post = 0, wplan = 0, mark = 0;
+  int64_t layers = 0;
+  static double now() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+};
 
 struct mps_handle {
   int N = 0, d = 0;
@@ -74,6 +87,7 @@ struct mps_handle {
   double phase_ms[kPhases] = {};
   int64_t phase_n[kPhases] = {};
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  HostProf hp;
   std::vector<cudaEvent_t> span_ev;          // event pool for the sub-phase spans of one wave
   int span_used = 0;
   std::vector<std::array<int, 3>> spans;     // (phase, begin event, end event)
@@ -339,7 +353,21 @@ int lane_group(int m, int n, int reg) {
   return std::min(small_group(m), p2);
 }
 
+mps_status wave_front_impl(mps_t h);
 mps_status wave_front(mps_t h) {
+  const double t0 = h->hp.on ? HostProf::now() : 0.0;
+  mps_status st = wave_front_impl(h);
+  if (h->hp.on) {
+    const double t1 = HostProf::now();
+    if (h->hp.layers > 3) {            // the first layers allocate the pinned buffers
+      h->hp.wplan += h->hp.mark - t0;
+      h->hp.launch += t1 - h->hp.mark;
+    }
+  }
+  return st;
+}
+
+mps_status wave_front_impl(mps_t h) {
   LayerJob& J = h->job;
   std::vector<LayerPlan>& plan = J.plan;
   const int G = J.G, d = h->d, d4 = J.d4;
@@ -396,8 +424,35 @@ mps_status wave_front(mps_t h) {
     size_t smem, smem2;
   };
   std::vector<Bucket> buckets;
+  size_t span = 0;                     // workspace bytes of the previous gate
   for (int x = 0; x < Gw; ++x) {
     LayerPlan& p = plan[g0 + x];
+    if (x > 0) {   // same shape as the previous gate: the same workspace layout one span further
+      const GateDesc& q = hd[x - 1];
+      if (q.l == p.gd.l && q.mid == p.gd.mid && q.r == p.gd.r) {
+        GateDesc gd = q;
+        gd.site = p.gd.site;
+        gd.u_index = x;
+        const int64_t sp = (int64_t)span;
+        gd.ws_theta += sp;
+        gd.ws_thetap += sp;
+        gd.ws_V += sp;
+        gd.ws_sig2 += sp;
+        gd.ws_T += sp;
+        gd.ws_pi += sp;
+        gd.ws_E += sp;
+        if (gd.ws_log) gd.ws_log += sp;
+        cur += span;
+        hd[x] = gd;
+        cpre[x + 1] = cpre[x] + p.ctiles;
+        rpre[x + 1] = rpre[x] + p.rtiles;
+        gpre[x + 1] = gpre[x] + p.gtiles;
+        apre[x + 1] = apre[x] + p.atiles;
+        if (gd.regime == 1) large.push_back(x);
+        continue;
+      }
+    }
+    const size_t cur0 = cur;
     GateDesc gd = p.gd;
     gd.u_index = x;
     const size_t mn = (size_t)gd.m * gd.n * 8, mnp = (size_t)std::max(gd.m, gd.jrows) * gd.n_pad * 8;   // B = L (jrows rows) reuses it
@@ -415,6 +470,7 @@ mps_status wave_front(mps_t h) {
                 : (gd.regime == 3 && gd.jrows > 0) ? (int64_t)take(large_precond_scratch(gd.n))
                 : refine_scratch_bytes(gd.n) > 0 ? (int64_t)take(refine_scratch_bytes(gd.n))
                                  : 0;
+    span = cur - cur0;
     hd[x] = gd;
     cpre[x + 1] = cpre[x] + p.ctiles;
     rpre[x + 1] = rpre[x] + p.rtiles;
@@ -430,12 +486,19 @@ mps_status wave_front(mps_t h) {
   {
     auto gidx = [](int gt) { return gt == 4 ? 0 : gt == 8 ? 1 : gt == 16 ? 2 : 3; };
     auto ridx = [](int r) { return r == 1 ? 0 : r == 2 ? 1 : r == 4 ? 2 : r == 8 ? 3 : r == 16 ? 4 : 5; };
-    std::map<int, std::vector<int32_t>> keyed;   // key = ((class * 4 + gt) * 6 + rpl) * 3 + pk
-    std::map<int, std::array<int, 4>> kparm;     // regime, gt, rpl, pk
+    // key = ((class * 4 + gt) * 6 + rpl) * 3 + pk; a handful of keys per layer: a small vector
+    // (launch order = ascending key), and the key of a gate with the previous gate's shape is reused
+    std::vector<std::pair<int, std::vector<int32_t>>> keyed;
+    std::vector<std::pair<int, std::array<int, 4>>> kparm;     // regime, gt, rpl, pk
+    int last_m = -1, last_n = -1, last_reg = -1, last_slot = -1;
     for (int x = 0; x < Gw; ++x) {
       const GateDesc& gd = hd[x];
       int reg = gd.regime, gt = 0, rpl = 0, pk = 0, cls = 0;
       if (reg == 1) continue;
+      if (gd.m == last_m && gd.n == last_n && reg == last_reg) {
+        keyed[last_slot].second.push_back(x);
+        continue;
+      }
       if (reg == 3) {
         if (!svd_qr_fits(gd.m, gd.n, &gt, &rpl)) return set_err(h, MPS_E_STATE, "internal: QR regime without a QR fit");
         pk = qr_block_order(gd.m, gd.n) ? 2 : (gd.n == rpl * gt && gd.m % 2 == 0 && rpl >= 2) ? 1 : 0;
@@ -447,27 +510,47 @@ mps_status wave_front(mps_t h) {
         cls = reg == 0 ? 1 : 2;
       }
       const int key = ((cls * 4 + gidx(gt)) * 6 + ridx(rpl)) * 3 + pk;
-      keyed[key].push_back(x);
-      kparm[key] = {reg, gt, rpl, pk};
+      int slot = 0;
+      while (slot < (int)keyed.size() && keyed[slot].first != key) ++slot;
+      if (slot == (int)keyed.size()) {
+        keyed.push_back({key, {}});
+        kparm.push_back({key, {reg, gt, rpl, pk}});
+      }
+      keyed[slot].second.push_back(x);
+      last_m = gd.m;
+      last_n = gd.n;
+      last_reg = reg;
+      last_slot = slot;
     }
-    for (auto& kv : keyed) {
-      const std::array<int, 4>& pr = kparm[kv.first];
+    std::vector<int> korder(keyed.size());
+    for (size_t i = 0; i < korder.size(); ++i) korder[i] = (int)i;
+    std::sort(korder.begin(), korder.end(), [&](int a, int b) { return keyed[a].first < keyed[b].first; });
+    for (int ki : korder) {
+      auto& kv = keyed[ki];
+      const std::array<int, 4>& pr = kparm[ki].second;
       const int reg = pr[0], gt = pr[1], rpl = pr[2];
       if (reg == 3) {
         Bucket b{3, gt, (int)small.size(), 0, 512, pr[3], rpl, 0, 0};   // (tile_rows carries the packed flag)
+        int pm = -1, pn = -1;
         for (int x : kv.second) {
           small.push_back(x);
-          b.smem = std::max(b.smem, svd_qr_smem(hd[x].m, hd[x].n));
+          if (hd[x].m == pm && hd[x].n == pn) continue;
+          pm = hd[x].m;
+          pn = hd[x].n;
+          b.smem = std::max(b.smem, svd_qr_smem(pm, pn));
         }
         b.end = (int)small.size();
         buckets.push_back(b);
         continue;
       }
       Bucket b{reg, gt, (int)small.size(), 0, 64, 64, rpl, 0, 0};
-      int maxn = 2;
+      int maxn = 2, pm = -1, pn = -1;
       for (int x : kv.second) {
         const GateDesc& gd = hd[x];
         small.push_back(x);
+        if (gd.m == pm && gd.n == pn) continue;
+        pm = gd.m;
+        pn = gd.n;
         maxn = std::max(maxn, gd.n);
         if (reg == 0) {
           b.smem = std::max(b.smem, svd_small_smem(gd.m, gd.n));
@@ -479,7 +562,12 @@ mps_status wave_front(mps_t h) {
       }
       b.end = (int)small.size();
       if (reg == 2) {
-        for (int i = b.begin; i < b.end; ++i) b.smem2 = std::max(b.smem2, svd_vrep_smem(hd[small[i]].n, b.tile_rows));
+        int qn = -1;
+        for (int i = b.begin; i < b.end; ++i) {
+          if (hd[small[i]].n == qn) continue;
+          qn = hd[small[i]].n;
+          b.smem2 = std::max(b.smem2, svd_vrep_smem(qn, b.tile_rows));
+        }
       }
       b.threads = (int)std::min<size_t>(reg == 0 ? 1024 : 512, std::max<size_t>(64, align_up((size_t)(maxn / 2) * gt, 32)));
       buckets.push_back(b);
@@ -496,7 +584,6 @@ mps_status wave_front(mps_t h) {
   uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));
   if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
   J.tail = tail;
-  std::memset(hb, 0, staged_bytes);
   std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
   std::memcpy(hb + (o_cpre - base), cpre.data(), 4 * (Gw + 1));
   std::memcpy(hb + (o_rpre - base), rpre.data(), 4 * (Gw + 1));
@@ -507,6 +594,7 @@ mps_status wave_front(mps_t h) {
   for (int x = 0; x < Gw; ++x)
     std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, J.us.data() + (size_t)J.ord[g0 + x].second * d4 * 2,
                 (size_t)d4 * 8);
+  if (h->hp.on) h->hp.mark = HostProf::now();
   CK(h2d_small(h, h->slab + base, hb, staged_bytes));
   // the pool may not grow into the workspace
   uint64_t* hceil = reinterpret_cast<uint64_t*>(hb + tail);
@@ -634,7 +722,10 @@ mps_status wave_back(mps_t h) {
   CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw, d_rec, sizeof(Record) * Gw, cudaMemcpyDeviceToHost, h->s));
   CK(cudaMemcpyAsync(rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, h->dst, sizeof(DevState),
                      cudaMemcpyDeviceToHost, h->s));
+  const double hw0 = h->hp.on ? HostProf::now() : 0.0;
   CK(cudaStreamSynchronize(h->s));
+  const double hw1 = h->hp.on ? HostProf::now() : 0.0;
+  if (h->hp.on && h->hp.layers > 3) h->hp.wait += hw1 - hw0;
   std::memcpy(hd.data(), rb, sizeof(GateDesc) * Gw);
   const Record* rr = reinterpret_cast<const Record*>(rb + sizeof(GateDesc) * Gw);
   std::memcpy(&h->hstate, rb + sizeof(GateDesc) * Gw + sizeof(Record) * Gw, sizeof(DevState));
@@ -668,6 +759,7 @@ mps_status wave_back(mps_t h) {
   }
   h->last_wave_begin = (int)h->last_desc.size();
   h->last_desc.insert(h->last_desc.end(), hd.begin(), hd.end());
+  if (h->hp.on && h->hp.layers > 3) h->hp.post += HostProf::now() - hw1;
   if (de != MPS_OK) return de;
   J.g0 = J.g1;
   return MPS_OK;
@@ -794,6 +886,10 @@ mps_status mps_destroy(mps_t h) {
   DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   if (h->s) cudaStreamSynchronize(h->s);
+  if (h->hp.on && h->hp.layers > 3)
+    fprintf(stderr, "[eamps host] %lld layers, ms per layer: plan %.3f wave-plan %.3f launch %.3f wait %.3f post %.3f\n",
+            (long long)h->hp.layers - 3, h->hp.plan / (h->hp.layers - 3), h->hp.wplan / (h->hp.layers - 3),
+            h->hp.launch / (h->hp.layers - 3), h->hp.wait / (h->hp.layers - 3), h->hp.post / (h->hp.layers - 3));
   for (int w = 0; w < 2; ++w)
     if (h->pinned[w]) cudaFreeHost(h->pinned[w]);
   for (int e = 0; e < 6; ++e)
@@ -903,6 +999,8 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
   if (G < 0 || (G > 0 && (!sites || !Us))) return set_err(h, MPS_E_INVAL, "bad arguments");
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is still in progress (mps_layer_step)");
   if (G == 0) return MPS_OK;
+  const double hp0 = h->hp.on ? HostProf::now() : 0.0;
+  if (h->hp.on) ++h->hp.layers;
   const int d = h->d, d4 = d * d * d * d;
   // ---- a0: validate (in range, disjoint pairs), canonical order = ascending site
   std::vector<std::pair<int, int>> ord(G);
@@ -910,11 +1008,16 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     if (sites[g] < 0 || sites[g] >= h->N - 1) return set_err(h, MPS_E_RANGE, "gate site out of range");
     ord[g] = {sites[g], g};
   }
-  std::sort(ord.begin(), ord.end());
+  if (!std::is_sorted(ord.begin(), ord.end())) std::sort(ord.begin(), ord.end());
   for (int g = 1; g < G; ++g)
     if (ord[g].first < ord[g - 1].first + 2) return set_err(h, MPS_E_INVAL, "overlapping gates in a layer");
-  for (int64_t x = 0; x < (int64_t)G * d4 * 2; ++x)
-    if (!std::isfinite(Us[x])) return set_err(h, MPS_E_INVAL, "non-finite gate entry");
+  {   // non-finite entries: exponent bits all ones (branch-free OR over the layer, vectorisable)
+    const uint32_t* ub = reinterpret_cast<const uint32_t*>(Us);
+    uint32_t bad = 0;
+    const int64_t ne = (int64_t)G * d4 * 2;
+    for (int64_t x = 0; x < ne; ++x) bad |= (uint32_t)((ub[x] & 0x7f800000u) == 0x7f800000u);
+    if (bad) return set_err(h, MPS_E_INVAL, "non-finite gate entry");
+  }
   if (h->cfg.strategy != MPS_STRAT_FIXED && h->hstate.led.j + G > h->cfg.n_planned)
     return set_err(h, MPS_E_STATE, "more truncations than n_planned");
   for (int g = 0; g < G; ++g) {
@@ -931,8 +1034,17 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
   for (int g = 0; g < G; ++g) {
     LayerPlan& p = plan[g];
     GateDesc& gd = p.gd;
+    const int i = ord[g].first;
+    if (g > 0) {   // the plan depends on the gate's shape only: reuse the previous gate's when equal
+      const GateDesc& q = plan[g - 1].gd;
+      if (q.l == h->chl[i] && q.mid == h->chr[i] && q.r == h->chr[i + 1]) {
+        p = plan[g - 1];
+        gd.site = i;
+        gd.u_index = ord[g].second;
+        continue;
+      }
+    }
     std::memset(&gd, 0, sizeof(gd));
-    int i = ord[g].first;
     gd.site = i;
     gd.l = h->chl[i];
     gd.mid = h->chr[i];
@@ -994,6 +1106,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
   J.active = true;
   h->last_desc.clear();
   h->last_wave_begin = 0;
+  if (h->hp.on && h->hp.layers > 3) h->hp.plan += HostProf::now() - hp0;
   mps_status fs = wave_front(h);
   if (fs != MPS_OK) {
     J.active = false;
