@@ -170,6 +170,75 @@ __device__ __forceinline__ void group_sum2(float& a, float& b) {
   }
 }
 
+// One column of B in a lane group's registers, PAIR-PLANAR: shared memory holds each column as
+// float4 (Re b_2i, Re b_2i+1, Im b_2i, Im b_2i+1) (pair_planar below), lane lg owns row pairs
+// i = lg + GT v, v < R / 2, and keeps re[v] = (Re b_2i, Re b_2i+1), im[v] = (Im b_2i, Im b_2i+1):
+// every complex operation below is a packed FP32x2 instruction on two rows with broadcast scalar
+// coefficients -- no (re, im) swaps or negations to build operand pairs (15% of the instructions
+// with the interleaved layout, ncu).
+template <int GT, int R>
+struct ColRegs {
+  float2 re[R / 2], im[R / 2];
+  __device__ __forceinline__ void load(const float2* a, int lg) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      const float4 t = *reinterpret_cast<const float4*>(a + 2 * (lg + GT * v));
+      re[v] = make_float2(t.x, t.y);
+      im[v] = make_float2(t.z, t.w);
+    }
+  }
+  __device__ __forceinline__ void store(float2* a, int lg) const {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v)
+      *reinterpret_cast<float4*>(a + 2 * (lg + GT * v)) = make_float4(re[v].x, re[v].y, im[v].x, im[v].y);
+  }
+};
+
+// in-place layout change of B's n columns (ld m) between interleaved float2 rows and pair-planar
+// float4 (Re 2i, Re 2i+1, Im 2i, Im 2i+1); the permutation is its own inverse
+__device__ __forceinline__ void pair_planar(float2* A, int m, int n) {
+  for (int x = threadIdx.x; x < n * (n / 2); x += blockDim.x) {
+    float4* q = reinterpret_cast<float4*>(A + (size_t)(x / (n / 2)) * m) + x % (n / 2);
+    const float4 t = *q;
+    *q = make_float4(t.x, t.z, t.y, t.w);
+  }
+}
+
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+
+// gamma = x^H y of two pair-planar columns over the lane's rows (not yet reduced over the group)
+template <int GT, int R>
+__device__ __forceinline__ void cross_planar(const ColRegs<GT, R>& X, const ColRegs<GT, R>& Y, float& gr, float& gi) {
+  float2 a1 = make_float2(0.f, 0.f), a2 = a1, a3 = a1, a4 = a1;
+#pragma unroll
+  for (int v = 0; v < R / 2; ++v) {
+    a1 = f2_fma(X.re[v], Y.re[v], a1);     // Re conj(x) y = xr yr + xi yi
+    a2 = f2_fma(X.im[v], Y.im[v], a2);
+    a3 = f2_fma(X.re[v], Y.im[v], a3);     // Im conj(x) y = xr yi - xi yr
+    a4 = f2_fma(X.im[v], Y.re[v], a4);
+  }
+  gr = (a1.x + a1.y) + (a2.x + a2.y);
+  gi = (a3.x + a3.y) - (a4.x + a4.y);
+}
+
+// The rotation of a pair-planar column pair. With P + iQ = s e, U + iW = c e (e = gamma / |gamma|):
+//   x' = c x - s conj(e) y:  Re x' = c Re x - P Re y - Q Im y,  Im x' = c Im x - P Im y + Q Re y
+//   y' = s x + c conj(e) y:  Re y' = s Re x + U Re y + W Im y,  Im y' = s Im x + U Im y - W Re y
+template <int GT, int R>
+__device__ __forceinline__ void rot_planar(ColRegs<GT, R>& X, ColRegs<GT, R>& Y, const Rot& Rt) {
+  const float P = Rt.s * Rt.er, Q = Rt.s * Rt.ei, U = Rt.c * Rt.er, W = Rt.c * Rt.ei;
+  const float2 c2 = f2s(Rt.c), s2 = f2s(Rt.s), mP = f2s(-P), mQ = f2s(-Q), pQ = f2s(Q), U2 = f2s(U), W2 = f2s(W),
+               mW = f2s(-W);
+#pragma unroll
+  for (int v = 0; v < R / 2; ++v) {
+    const float2 xr = X.re[v], xi = X.im[v], yr = Y.re[v], yi = Y.im[v];
+    X.re[v] = f2_fma(mQ, yi, f2_fma(mP, yr, f2_mul(c2, xr)));
+    X.im[v] = f2_fma(pQ, yr, f2_fma(mP, yi, f2_mul(c2, xi)));
+    Y.re[v] = f2_fma(W2, yi, f2_fma(U2, yr, f2_mul(s2, xr)));
+    Y.im[v] = f2_fma(mW, yr, f2_fma(U2, yi, f2_mul(s2, xi)));
+  }
+}
+
 // As PairRegs, but each register slot holds two consecutive rows loaded/stored as one 16-byte
 // access: lane lg owns rows 2 (lg + GT v) and 2 (lg + GT v) + 1, v < R/2 (the caller guarantees
 // rows == R GT, rows even). Half the shared-memory instructions of PairRegs; a warp's groups read

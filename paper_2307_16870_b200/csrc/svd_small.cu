@@ -122,7 +122,76 @@ __global__ void __launch_bounds__(1024) k_svd_small(GateDesc* desc, const int32_
   int sweep = 0;
   bool converged = (n < 2);
   const int half = n / 2, gid = tid / GT, lg = tid % GT;
-  if (R > 0 && n <= 256 && (int)(blockDim.x / GT) >= half) {
+  bool planar = false;
+  if constexpr (R >= 2) planar = (m == R * GT && n == R * GT && (int)(blockDim.x / GT) >= half);
+  if (planar) {
+    // square theta whose rows fill the lane groups exactly (config 2 chi = 16: 32 x 32, 8-lane
+    // groups, 4 rows per lane): theta and V PAIR-PLANAR (as the QR kernel, jacobi_common.cuh
+    // ColRegs), so the gamma dot and both rotations are packed FFMA2 on two rows with broadcast
+    // coefficients -- no operand-building MOVs of the interleaved layout, which made this kernel
+    // issue-bound (IPC 3.0). Same circle schedule, criterion and cached norms as the path below.
+    constexpr int RR = R >= 2 ? R : 2;
+    uint16_t* sched = reinterpret_cast<uint16_t*>(part + blockDim.x);
+    float* cn = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sched + (n - 1) * half) + 15) & ~uintptr_t(15));
+    build_circle_schedule(sched, n);
+    __syncthreads();
+    pair_planar(A, m, n);
+    pair_planar(V, n, n);
+    __syncthreads();
+    const bool active = gid < half;
+    const float tol2 = tol * tol;
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+      for (int j = warp; j < n; j += (int)(blockDim.x >> 5)) {
+        float a = 0.f;
+        for (int i = lane; i < m; i += 32) a = fmaf(A[j * m + i].x, A[j * m + i].x, fmaf(A[j * m + i].y, A[j * m + i].y, a));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) cn[j] = a;
+      }
+      __syncthreads();
+      int any = 0;
+      for (int rnd = 0; rnd < n - 1; ++rnd) {
+        bool rot = false;
+        int p = 0, q = 1;
+        float gr = 0.f, gi = 0.f;
+        ColRegs<GT, RR> X, Y;
+        if (active) {
+          const uint32_t pq = sched[rnd * half + gid];
+          p = pq & 0xFF;
+          q = pq >> 8;
+          X.load(A + p * m, lg);
+          Y.load(A + q * m, lg);
+          cross_planar(X, Y, gr, gi);
+        }
+        group_sum2<GT>(gr, gi);   // (all lanes: a warp may hold active and idle groups)
+        if (active) {
+          const float al = cn[p], be = cn[q];
+          Rot Rt;
+          float tg;
+          if (jacobi_rot_fast(al, be, gr, gi, skip, tol2, Rt, tg)) {
+            rot = true;
+            rot_planar(X, Y, Rt);
+            X.store(A + p * m, lg);
+            Y.store(A + q * m, lg);
+            ColRegs<GT, RR> P, Q;
+            P.load(V + p * n, lg);
+            Q.load(V + q * n, lg);
+            rot_planar(P, Q, Rt);
+            P.store(V + p * n, lg);
+            Q.store(V + q * n, lg);
+            if (lg == 0) {
+              cn[p] = al - tg;
+              cn[q] = be + tg;
+            }
+          }
+        }
+        any |= __syncthreads_or(rot);
+      }
+      converged = (any == 0);
+    }
+    pair_planar(V, n, n);   // back to interleaved rows for the epilogue (A is reloaded below)
+    __syncthreads();
+  } else if (R > 0 && n <= 256 && (int)(blockDim.x / GT) >= half) {
     // fast path (as the QR kernel): one pair per lane group, rows of theta and V in registers,
     // schedule from shared memory, cached column norms (exact at each sweep start), gamma-only dots
     constexpr int RR = R > 0 ? R : 1;
