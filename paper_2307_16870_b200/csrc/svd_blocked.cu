@@ -290,12 +290,24 @@ __global__ void k_block_check(GateDesc* desc, const int32_t* list, int count, La
 
 // sigma_j^2 = ||theta v_j||^2 / ||v_j||^2 with theta = lambda (x) Theta' (the FP32 theta the
 // Jacobi started from), FP64 accumulation. One CTA per (32-column block, gate).
+// QR-regime gates preconditioned by the FP64 Gram + Cholesky (G = theta^H theta = L L^H, L still in
+// the precond scratch at ws_log, column-major, lower) take ||theta v||^2 = v^H G v = ||L^H v||^2
+// instead: L^H is n x n upper triangular, so the row chunk r0 only needs k >= r0 -- half the FP64
+// products of theta V (m x n). Accuracy: the FP64 Gram and Cholesky carry ~eps64 ||theta||^2 of
+// absolute error in sigma_j^2, i.e. eps64 kappa^2 relative; the gates this does not resolve
+// (sigma_min < 2e-4 sigma_max, kappa^2 > 2.5e7) are re-solved by the FP64 refinement (refine.cu)
+// from a recontracted theta anyway. B = L^H V has the Gram of theta V (V^H G V), which is all the
+// polish reads from it (rows n .. m-1 are written as zeros).
 __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ desc, const int32_t* list, uint8_t* slab,
-                                                  const DevState* st, int write_b = 0) {
+                                                  const DevState* st, int write_b = 0, int use_l = 0) {
   const GateDesc gd = desc[list[blockIdx.y]];
   const int j0 = blockIdx.x * 32;
   if (j0 >= gd.n) return;
   const int m = gd.m, n = gd.n, np = gd.n_pad, dd = st->d;
+  static_assert(RC % 16 == 0, "row chunks start on a k chunk");
+  const bool from_l = use_l && gd.regime == 3 && gd.jrows > 0;
+  const int rows = from_l ? n : m;
+  const double2* __restrict__ Lg = reinterpret_cast<const double2*>(slab + gd.ws_log);
   const BondEntry* bonds = reinterpret_cast<const BondEntry*>(slab + st->bonds_off);
   const float* lam = reinterpret_cast<const float*>(slab + bonds[gd.site].off);
   const float2* thp = reinterpret_cast<const float2*>(slab + gd.ws_thetap);
@@ -311,17 +323,22 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
   for (int j = 0; j < 8; ++j) num[j] = 0.0;
   // theta (= lambda (x) Theta', FP32) and V tiles of the next 16-column chunk are fetched into
   // registers while the current chunk's FP64 products run (one barrier pair per chunk)
-  auto fetch = [&](int r0, int k0, float2* ra, float2* rb) {
+  auto fetch = [&](int r0, int k0, double2* ra, float2* rb) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int e = tid + it * 256;  // 1024 = 16 k x 64 rows
       const int i = e & (RC - 1), kk = e >> 6;
       const int row = r0 + i, k = k0 + kk;
-      float2 v = make_float2(0.f, 0.f);
-      if (row < m && k < n) {
+      double2 v = make_double2(0.0, 0.0);
+      if (from_l) {
+        if (row < n && k < n && k >= row) {            // (L^H)[row][k] = conj(L[k][row])
+          const double2 l = Lg[(int64_t)row * n + k];
+          v = make_double2(l.x, -l.y);
+        }
+      } else if (row < m && k < n) {
         const float2 tp = thp[(int64_t)k * m + row];
         const float la = lam[row / dd];
-        v = make_float2(la * tp.x, la * tp.y);
+        v = make_double2(la * tp.x, la * tp.y);
       }
       ra[it] = v;
     }
@@ -334,17 +351,19 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
     }
   };
   const int nk = (n + 15) / 16;
-  for (int r0 = 0; r0 < m; r0 += RC) {
+  for (int r0 = 0; r0 < rows; r0 += RC) {
     double2 w[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) w[j] = make_double2(0.0, 0.0);
-    float2 ra[4], rb[2];
-    fetch(r0, 0, ra, rb);
-    for (int kc = 0; kc < nk; ++kc) {
+    double2 ra[4];
+    float2 rb[2];
+    const int kc0 = from_l ? r0 / 16 : 0;               // L^H: rows r0.. need k >= r0 only
+    fetch(r0, kc0 * 16, ra, rb);
+    for (int kc = kc0; kc < nk; ++kc) {
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
         const int e = tid + it * 256;
-        As[e >> 6][e & (RC - 1)] = make_double2(ra[it].x, ra[it].y);
+        As[e >> 6][e & (RC - 1)] = ra[it];
       }
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -370,11 +389,18 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
     if (write_b) {   // B = theta V for the FP64-anchored polish (the Jacobi's working theta is dead now)
       float2* Bw = reinterpret_cast<float2*>(slab + gd.ws_theta);
       const int row = r0 + oi;
-      if (row < m) {
+      if (row < rows) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if (j0 + oj + j < n) Bw[(int64_t)(j0 + oj + j) * m + row] = make_float2((float)w[j].x, (float)w[j].y);
       }
+    }
+  }
+  if (write_b && rows < m) {   // L^H V has n rows: the polish reads m, the rest are zero
+    float2* Bw = reinterpret_cast<float2*>(slab + gd.ws_theta);
+    for (int x = tid; x < 32 * (m - rows); x += 256) {
+      const int j = j0 + x / (m - rows), row = rows + x % (m - rows);
+      if (j < n) Bw[(int64_t)j * m + row] = make_float2(0.f, 0.f);
     }
   }
   // reduce num over the 64 row-threads of each column group: warp butterflies, then the two warps
@@ -1712,7 +1738,9 @@ size_t svd_tc_scratch_bytes(int n_pad) { return tcj::Scratch::total(n_pad / tcj:
 int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, int max_n, uint8_t* slab, DevState* st,
                            cudaStream_t s) {
   if (count <= 0) return 0;
-  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1);
+  // EAMPS_RAYLEIGH_THETA=1: the QR-regime Rayleigh quotients from theta V instead of L^H V (A/B)
+  static const int use_l = getenv("EAMPS_RAYLEIGH_THETA") ? 0 : 1;
+  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1, use_l);
   static std::atomic<unsigned long long> pattr{0};
   if (first_on_device(pattr)) {
     cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
