@@ -100,6 +100,82 @@ __device__ __forceinline__ CholScratch* chol_scratch(uint8_t* slab, const GateDe
   return reinterpret_cast<CholScratch*>(slab + gd.ws_log + (size_t)16 * gd.n * gd.n);
 }
 
+// Cholesky of the 32 x 32 diagonal block (w x w used) in shared memory by a 256-thread CTA, in the
+// square-root-free (L D L^H) form of the right-looking recurrence: step j subtracts
+// A[i][j] conj(A[k][j]) / d_j from every A[i][k], j < k <= i < w, reading the unscaled column j,
+// which no thread writes in that step -- one barrier per step instead of three (scale the column,
+// barrier, update, barrier). Then L[i][j] = A[i][j] / sqrt(d_j), L[j][j] = sqrt(d_j). A pivot
+// d_j <= tau zeroes column j (no update from it), as before. s_rs: 32 doubles of shared memory.
+__device__ __forceinline__ void chol32(double2 (*Lp)[33], int w, double tau, double* s_rs) {
+  const int tid = threadIdx.x;
+  for (int j = 0; j < w; ++j) {
+    const double d = Lp[j][j].x;
+    const double id = d > tau ? 1.0 / d : 0.0;
+    for (int x = tid; x < 32 * 32; x += 256) {
+      const int i = x >> 5, k = x & 31;
+      if (k > j && k <= i && i < w) {
+        const double2 a = Lp[i][j], q = Lp[k][j];   // A[i][k] -= A[i][j] conj(A[k][j]) / d_j
+        Lp[i][k].x -= (a.x * q.x + a.y * q.y) * id;
+        Lp[i][k].y -= (a.y * q.x - a.x * q.y) * id;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < 32) {
+    const double d = tid < w ? Lp[tid][tid].x : 0.0;
+    s_rs[tid] = d > tau ? rsqrt(d) : 0.0;
+  }
+  __syncthreads();
+  for (int x = tid; x < 32 * 32; x += 256) {
+    const int i = x >> 5, j = x & 31;
+    if (i < w && j <= i) {
+      const double r = s_rs[j];
+      const double2 a = Lp[i][j];
+      Lp[i][j] = i == j ? make_double2(a.x * r, 0.0) : make_double2(a.x * r, a.y * r);
+    }
+  }
+  __syncthreads();
+}
+
+// M = L_JJ^-1 (lower triangular, w x w of the 32 x 32 block, zeros elsewhere) by all 8 warps of a
+// 256-thread CTA: column-oriented forward substitution of L M_j = e_j with one lane per row. Warp wp
+// takes the columns j = wp, wp + 8, wp + 16, wp + 24 in lockstep; at step k lane k finalises
+// M[k][j] = b_k / L[k][k] and broadcasts it, and every lane i > k subtracts L[i][k] M[k][j] --
+// the same products in the same order (k ascending) as the row-by-row recurrence
+// M[i][j] = -(sum_{j <= k < i} L[i][k] M[k][j]) / L[i][i], but 32 lanes x 8 warps in parallel
+// instead of one thread per column (that serial loop was the CTA's critical path: ~22% of the
+// kernel's warps waited on the barrier after it, ncu r02). A zero pivot (L[k][k] = 0) zeroes row k
+// of M, and a zero L[j][j] the whole column j, as before.
+__device__ __forceinline__ void tri_inv32(const double2 (*Lp)[33], double2 (*Mi)[33], int w) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const double dl = (lane < w) ? Lp[lane][lane].x : 0.0;
+  const double di = dl > 0.0 ? 1.0 / dl : 0.0;
+  double2 b[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) b[c] = make_double2(lane == wp + 8 * c ? 1.0 : 0.0, 0.0);
+  for (int k = 0; k < w; ++k) {
+    const double2 lik = (lane > k && lane < w) ? Lp[lane][k] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (k < wp + 8 * c) continue;                 // warp-uniform
+      double2 m = make_double2(b[c].x * di, b[c].y * di);
+      m.x = __shfl_sync(0xffffffffu, m.x, k);
+      m.y = __shfl_sync(0xffffffffu, m.y, k);
+      if (lane == k) {
+        b[c] = m;
+      } else if (lane > k) {                        // b_i -= L[i][k] M[k][j]
+        b[c].x -= lik.x * m.x - lik.y * m.y;
+        b[c].y -= lik.x * m.y + lik.y * m.x;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int j = wp + 8 * c;
+    Mi[lane][j] = (j < w && lane >= j && lane < w) ? b[c] : make_double2(0.0, 0.0);
+  }
+}
+
 // acc (row rr, columns cb .. cb+3 of the 32 x 32 block at rows i0, columns c0) = G_blk - L_blk L_J^H
 __device__ __forceinline__ void chol_block_update(const double2* G, int n, int i0, int c0, int w, double2 (&acc)[4],
                                                   double2 (*As)[17], double2 (*Bs)[17]) {
@@ -144,7 +220,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_diag(const GateDesc* __restrict
   double2 (*Bs)[17] = AB[1];
   double2 (*Lp)[33] = reinterpret_cast<double2(*)[33]>(&AB[0][0][0]);
   __shared__ double s_red[8];
-  __shared__ double dinv_s[32];
+  __shared__ double s_rs[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rr = tid >> 3, cb = (tid & 7) * 4;
   double tau;
@@ -167,45 +243,8 @@ __global__ void __launch_bounds__(256) k_pc_chol_diag(const GateDesc* __restrict
 #pragma unroll
   for (int b = 0; b < 4; ++b) Lp[rr][cb + b] = acc[b];
   __syncthreads();
-  for (int j = 0; j < w; ++j) {                 // right-looking, unblocked
-    const double d = Lp[j][j].x;
-    const bool ok = d > tau;
-    const double il = ok ? rsqrt(d) : 0.0;
-    __syncthreads();
-    if (tid >= j && tid < w) {                  // column j: scale (rows >= j)
-      const int i = tid;
-      if (i == j) Lp[j][j] = make_double2(ok ? d * il : 0.0, 0.0);
-      else Lp[i][j] = make_double2(Lp[i][j].x * il, Lp[i][j].y * il);
-    }
-    __syncthreads();
-    for (int x = tid; x < 32 * 32; x += 256) {  // Lp[i][k] -= Lp[i][j] conj(Lp[k][j]), j < k <= i < w
-      const int i = x >> 5, k = x & 31;
-      if (k > j && k <= i && i < w) {
-        const double2 a = Lp[i][j], q = Lp[k][j];
-        Lp[i][k].x -= a.x * q.x + a.y * q.y;
-        Lp[i][k].y -= a.y * q.x - a.x * q.y;
-      }
-    }
-    __syncthreads();
-  }
-  if (tid < 32) {                               // L_JJ^-1, thread j owns column j
-    const int j = tid;
-    for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
-    dinv_s[j] = (j < w && Lp[j][j].x > 0.0) ? 1.0 / Lp[j][j].x : 0.0;   // one division per row, in parallel
-    __syncwarp();
-    if (j < w && Lp[j][j].x > 0.0) {
-      Mi[j][j] = make_double2(dinv_s[j], 0.0);
-      for (int i = j + 1; i < w; ++i) {
-        double2 sacc = make_double2(0.0, 0.0);
-        for (int k = j; k < i; ++k) {           // s += L[i][k] M[k][j]
-          const double2 a = Lp[i][k], q = Mi[k][j];
-          sacc.x += a.x * q.x - a.y * q.y;
-          sacc.y += a.x * q.y + a.y * q.x;
-        }
-        Mi[i][j] = make_double2(-sacc.x * dinv_s[i], -sacc.y * dinv_s[i]);
-      }
-    }
-  }
+  chol32(Lp, w, tau, s_rs);
+  tri_inv32(Lp, Mi, w);                         // L_JJ^-1
   __syncthreads();
   for (int x = tid; x < 32 * 32; x += 256) {
     const int i = x >> 5, j = x & 31;
@@ -272,7 +311,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
   auto& Bs = S.Bs;
   auto& Tt = S.Lp;
   __shared__ double s_red[8];
-  __shared__ double dinv_s[32];
+  __shared__ double s_rs[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rr = tid >> 3, cb = (tid & 7) * 4;    // 32 x 32 tile: row rr, columns cb .. cb+3
   // pivot threshold tau = n eps64 max_i G_ii
@@ -319,47 +358,9 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
 #pragma unroll
         for (int b = 0; b < 4; ++b) Lp[rr][cb + b] = acc[b];
         __syncthreads();
-        for (int j = 0; j < w; ++j) {
-          const double d = Lp[j][j].x;
-          const bool ok = d > tau;
-          const double il = ok ? rsqrt(d) : 0.0;
-          __syncthreads();
-          if (tid >= j && tid < w) {                 // column j: scale (rows >= j)
-            const int i = tid;
-            if (i == j) Lp[j][j] = make_double2(ok ? d * il : 0.0, 0.0);
-            else Lp[i][j] = make_double2(Lp[i][j].x * il, Lp[i][j].y * il);
-          }
-          __syncthreads();
-          // trailing update: Lp[i][k] -= Lp[i][j] conj(Lp[k][j]), j < k <= i < w
-          for (int x = tid; x < 32 * 32; x += 256) {
-            const int i = x >> 5, k = x & 31;
-            if (k > j && k <= i && i < w) {
-              const double2 a = Lp[i][j], q = Lp[k][j];
-              Lp[i][k].x -= a.x * q.x + a.y * q.y;
-              Lp[i][k].y -= a.y * q.x - a.x * q.y;
-            }
-          }
-          __syncthreads();
-        }
+        chol32(Lp, w, tau, s_rs);
         // ---- inverse of the lower-triangular L_JJ, column by column (thread j < w owns column j)
-        if (tid < 32) {
-          const int j = tid;
-          for (int i = 0; i < 32; ++i) Mi[i][j] = make_double2(0.0, 0.0);
-          dinv_s[j] = (j < w && Lp[j][j].x > 0.0) ? 1.0 / Lp[j][j].x : 0.0;   // one division per row
-          __syncwarp();
-          if (j < w && Lp[j][j].x > 0.0) {
-            Mi[j][j] = make_double2(dinv_s[j], 0.0);
-            for (int i = j + 1; i < w; ++i) {
-              double2 s = make_double2(0.0, 0.0);
-              for (int k = j; k < i; ++k) {      // s += L[i][k] M[k][j]
-                const double2 a = Lp[i][k], q = Mi[k][j];
-                s.x += a.x * q.x - a.y * q.y;
-                s.y += a.x * q.y + a.y * q.x;
-              }
-              Mi[i][j] = make_double2(-s.x * dinv_s[i], -s.y * dinv_s[i]);
-            }
-          }
-        }
+        tri_inv32(Lp, Mi, w);
         __syncthreads();
         // ---- write L_JJ (lower part) back
         for (int x = tid; x < 32 * 32; x += 256) {
