@@ -40,6 +40,8 @@ struct LayerJob {                  // the layer in flight (mps_layer_begin / mps
   std::vector<GateDesc> hd;          // the current wave
   std::vector<int32_t> rpre, gpre, apre;
   size_t o_desc = 0, o_rec = 0, o_gpre = 0, o_apre = 0, o_rpre = 0, tail = 0;
+  std::vector<int32_t> rsm;          // wave-local gates of the fused small reabsorb
+  size_t o_rsm = 0, rsm_smem = 0;
   bool ran[5] = {false, false, false, false, false};
 };
 
@@ -378,7 +380,7 @@ mps_status wave_front_impl(mps_t h) {
   int g1 = g0;
   while (g1 < G) {
     const int cnt = g1 - g0 + 1;
-    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 2 * align_up(4 * cnt) +
+    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 3 * align_up(4 * cnt) +
                 align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
     size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
     if (bump + r2 + fx + w2 + kAlign > top) break;
@@ -406,11 +408,14 @@ mps_status wave_front_impl(mps_t h) {
   const size_t o_apre = take(4 * (Gw + 1));
   const size_t o_small = take(4 * Gw);
   const size_t o_large = take(4 * Gw);
+  const size_t o_rsm = take(4 * Gw);
   const size_t o_us = take((size_t)Gw * d4 * 8);
   const size_t o_rec = take(sizeof(Record) * Gw);
   const size_t o_scr = take(32 * (size_t)Gw + 64);
   const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
   std::vector<int32_t> cpre(Gw + 1, 0), small, large;
+  J.rsm.clear();
+  J.rsm_smem = 0;
   J.rpre.assign(Gw + 1, 0);
   J.gpre.assign(Gw + 1, 0);
   J.apre.assign(Gw + 1, 0);
@@ -449,6 +454,7 @@ mps_status wave_front_impl(mps_t h) {
         gpre[x + 1] = gpre[x] + p.gtiles;
         apre[x + 1] = apre[x] + p.atiles;
         if (gd.regime == 1) large.push_back(x);
+        if (!J.rsm.empty() && J.rsm.back() == x - 1) J.rsm.push_back(x);   // same shape as gate x - 1
         continue;
       }
     }
@@ -477,6 +483,10 @@ mps_status wave_front_impl(mps_t h) {
     gpre[x + 1] = gpre[x] + p.gtiles;
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) large.push_back(x);
+    if (reabsorb_small_fits(gd.m, gd.n)) {
+      J.rsm.push_back(x);
+      J.rsm_smem = std::max(J.rsm_smem, reabsorb_small_smem(gd.m, gd.n));
+    }
   }
   // SVD buckets, one launch each; `small` holds their gates back to back, [begin, end) per bucket.
   //  QR regime (3): (GT, R) as chosen by svd_qr_fits, and packed (n = R GT, m even) or not, or the
@@ -591,6 +601,8 @@ mps_status wave_front_impl(mps_t h) {
   std::memcpy(hb + (o_apre - base), apre.data(), 4 * (Gw + 1));
   if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
   if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
+  if (!J.rsm.empty()) std::memcpy(hb + (o_rsm - base), J.rsm.data(), 4 * J.rsm.size());
+  J.o_rsm = o_rsm;
   for (int x = 0; x < Gw; ++x)
     std::memcpy(hb + (o_us - base) + (size_t)x * d4 * 8, J.us.data() + (size_t)J.ord[g0 + x].second * d4 * 2,
                 (size_t)d4 * 8);
@@ -711,8 +723,10 @@ mps_status wave_back(mps_t h) {
   CKL("select");
   if (prof) CK(cudaEventRecord(h->ev[4], h->s));
   // a5 reabsorb
-  launch_reabsorb(d_desc, d_gpre, J.gpre[Gw], d_apre, J.apre[Gw], d_rpre, J.rpre[Gw], Gw, h->slab, h->s);
-  h->launches += 3;
+  h->launches += launch_reabsorb(d_desc, d_gpre, J.gpre[Gw], d_apre, J.apre[Gw], d_rpre, J.rpre[Gw], Gw, h->slab, h->s);
+  launch_reabsorb_small(d_desc, reinterpret_cast<const int32_t*>(h->slab + J.o_rsm), (int)J.rsm.size(), J.rsm_smem,
+                        h->slab, h->s);
+  if (!J.rsm.empty()) ++h->launches;
   CKL("reabsorb");
   if (prof) CK(cudaEventRecord(h->ev[5], h->s));
   // read back: descriptors (k, sweeps), records, device state
@@ -1095,6 +1109,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     p.rtiles = ((gd.m + 63) / 64) * ((km + 63) / 64) + (km + 63) / 64;
     p.gtiles = ((km + 31) / 32) * ((km + 31) / 32);
     p.atiles = ((gd.n + 63) / 64) * ((km + 63) / 64);
+    if (reabsorb_small_fits(gd.m, gd.n)) p.rtiles = p.gtiles = p.atiles = 0;   // k_reabsorb_small
   }
 
   J.G = G;

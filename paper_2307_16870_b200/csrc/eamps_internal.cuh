@@ -170,8 +170,13 @@ int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* s
 // parallel = 1: FIXED / NAIVE (target independent of the ledger): one warp per gate;
 // parallel = 0: GLOBAL / NEAREST: one warp walks the gates in canonical order.
 void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s);
-void launch_reabsorb(const GateDesc* d_desc, const int32_t* d_pre_gram, int tiles_gram, const int32_t* d_pre_apply,
-                     int tiles_apply, const int32_t* d_pre_reab, int tiles_reab, int G, uint8_t* slab, cudaStream_t s);
+int launch_reabsorb(const GateDesc* d_desc, const int32_t* d_pre_gram, int tiles_gram, const int32_t* d_pre_apply,
+                    int tiles_apply, const int32_t* d_pre_reab, int tiles_reab, int G, uint8_t* slab, cudaStream_t s);
+// small gates (m, n <= 64): the reabsorb fused in one CTA per gate (list = wave-local indices)
+bool reabsorb_small_fits(int m, int n);
+size_t reabsorb_small_smem(int m, int n);
+void launch_reabsorb_small(const GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, uint8_t* slab,
+                           cudaStream_t s);
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s);
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s);

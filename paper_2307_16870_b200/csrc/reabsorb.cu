@@ -258,14 +258,125 @@ __global__ void __launch_bounds__(256) k_reabsorb(const GateDesc* __restrict__ d
   (void)inv_nu;
 }
 
+
+// ---- small gates (m, n <= 64; config 2 chi <= 32, the small bonds of every circuit): the three
+// steps above fused in ONE CTA per gate with everything in shared memory -- V_k gathered once,
+// E = (I - V_k^H V_k)/2, V_k' = V_k + V_k E, B_i' = Theta' V_k' / nu, B_{i+1}' = V_k'^H, lambda_i.
+// Same arithmetic in the same order as k_vk_gram / k_vk_apply / k_reabsorb (one 64-row FP32 chunk
+// of the Gram for n <= 64 then FP64, FP32 accumulation of V_k E in ascending a, FP32 16-column
+// chunk products with FP64 sums for B_i'), so the results are those of the tiled path; what goes
+// is three launches of mostly idle 64 x 64 tiles and the global round trips of E and V_k'.
+// Columns of V_k / V_k' are stored with stride n + 1 (odd: no shared-memory bank pile-up).
+__global__ void __launch_bounds__(256) k_reabsorb_small(const GateDesc* __restrict__ desc,
+                                                        const int32_t* __restrict__ list, uint8_t* slab) {
+  const GateDesc gd = desc[list[blockIdx.x]];
+  const int k = gd.k;
+  if (k <= 0) return;
+  const int m = gd.m, n = gd.n, np = gd.n_pad, ld = n + 1;
+  extern __shared__ __align__(16) float2 rs_sm[];
+  float2* Vs = rs_sm;                      // V[:, pi_c], column c at Vs[c * ld + row]
+  float2* Vk = Vs + (size_t)k * ld;        // V_k'
+  float2* Es = Vk + (size_t)k * ld;        // E[a][b] at Es[a * k + b]
+  float2* Ts = Es + (size_t)k * k;         // Theta' (m x n, column-major, ld m)
+  const float2* __restrict__ V = reinterpret_cast<const float2*>(slab + gd.ws_V);
+  const int32_t* __restrict__ pi = reinterpret_cast<const int32_t*>(slab + gd.ws_pi);
+  const float2* __restrict__ thp = reinterpret_cast<const float2*>(slab + gd.ws_thetap);
+  const int tid = threadIdx.x;
+  for (int x = tid; x < n * k; x += 256) {
+    const int c = x / n, row = x % n;
+    Vs[c * ld + row] = V[(int64_t)pi[c] * np + row];
+  }
+  for (int x = tid; x < m * n; x += 256) Ts[x] = thp[x];
+  __syncthreads();
+  // E[a][b] = (delta_ab - sum_i conj(V[i, pi_a]) V[i, pi_b]) / 2
+  for (int x = tid; x < k * k; x += 256) {
+    const int a = x / k, b = x % k;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int i = 0; i < n; ++i) {
+      const float2 u = Vs[a * ld + i], y = Vs[b * ld + i];
+      acc.x = fmaf(u.x, y.x, fmaf(u.y, y.y, acc.x));
+      acc.y = fmaf(u.x, y.y, fmaf(-u.y, y.x, acc.y));
+    }
+    const double dre = (double)acc.x, dim = (double)acc.y;
+    const double re = ((a == b) ? 1.0 : 0.0) - dre, im = -dim;
+    Es[x] = make_float2((float)(0.5 * re), (float)(0.5 * im));
+  }
+  __syncthreads();
+  // V_k'[:, b] = V[:, pi_b] + sum_a V[:, pi_a] E[a][b]
+  for (int x = tid; x < n * k; x += 256) {
+    const int b = x / n, row = x % n;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int a = 0; a < k; ++a) {
+      const float2 av = Vs[a * ld + row], bv = Es[a * k + b];
+      acc.x = fmaf(av.x, bv.x, fmaf(-av.y, bv.y, acc.x));
+      acc.y = fmaf(av.x, bv.y, fmaf(av.y, bv.x, acc.y));
+    }
+    const float2 v = Vs[b * ld + row];
+    Vk[b * ld + row] = make_float2(v.x + acc.x, v.y + acc.y);
+  }
+  __syncthreads();
+  // B_i'[row][j] = (Theta' V_k')[row][j] / nu: FP32 products in 16-column chunks, FP64 sums
+  float2* __restrict__ Bl = reinterpret_cast<float2*>(slab + gd.off_newL);
+  const double inv = 1.0 / gd.nu;
+  for (int x = tid; x < m * k; x += 256) {
+    const int row = x / k, j = x % k;
+    double2 dacc = make_double2(0.0, 0.0);
+    for (int c0 = 0; c0 < n; c0 += 16) {
+      float2 acc = make_float2(0.f, 0.f);
+      const int c1 = min(n, c0 + 16);
+      for (int c = c0; c < c1; ++c) {
+        const float2 av = Ts[(size_t)c * m + row], bv = Vk[j * ld + c];
+        acc.x = fmaf(av.x, bv.x, fmaf(-av.y, bv.y, acc.x));
+        acc.y = fmaf(av.x, bv.y, fmaf(av.y, bv.x, acc.y));
+      }
+      dacc.x += acc.x;
+      dacc.y += acc.y;
+    }
+    Bl[x] = make_float2((float)(dacc.x * inv), (float)(dacc.y * inv));
+  }
+  // B_{i+1}'[j][col] = conj(V_k'[col][j]) and lambda_i[j] = sigma_pi_j / nu
+  float2* __restrict__ Br = reinterpret_cast<float2*>(slab + gd.off_newR);
+  for (int x = tid; x < k * n; x += 256) {
+    const int j = x / n, col = x % n;
+    const float2 v = Vk[j * ld + col];
+    Br[x] = make_float2(v.x, -v.y);
+  }
+  if (tid < k) {
+    const double* s2 = reinterpret_cast<const double*>(slab + gd.ws_sig2);
+    reinterpret_cast<float*>(slab + gd.off_newLam)[tid] = (float)(sqrt(s2[tid]) / gd.nu);
+  }
+}
+
 }  // namespace
 
-void launch_reabsorb(const GateDesc* d_desc, const int32_t* d_pre_gram, int tiles_gram, const int32_t* d_pre_apply,
-                     int tiles_apply, const int32_t* d_pre_reab, int tiles_reab, int G, uint8_t* slab, cudaStream_t s) {
-  if (G <= 0) return;
-  if (tiles_gram > 0) k_vk_gram<<<tiles_gram, 256, 0, s>>>(d_desc, d_pre_gram, G, slab);
-  if (tiles_apply > 0) k_vk_apply<<<tiles_apply, 256, 0, s>>>(d_desc, d_pre_apply, G, slab);
-  if (tiles_reab > 0) k_reabsorb<<<tiles_reab, 256, 0, s>>>(d_desc, d_pre_reab, G, slab);
+bool reabsorb_small_fits(int m, int n) {
+  static const bool off = getenv("EAMPS_NO_REABSORB_SMALL") != nullptr;   // dev A/B switch
+  return !off && m <= 64 && n <= 64;
+}
+
+size_t reabsorb_small_smem(int m, int n) {
+  const size_t k = (size_t)std::min(m, n);
+  return 8 * (2 * k * (size_t)(n + 1) + k * k + (size_t)m * n);
+}
+
+void launch_reabsorb_small(const GateDesc* d_desc, const int32_t* d_list, int count, size_t smem, uint8_t* slab,
+                           cudaStream_t s) {
+  if (count <= 0) return;
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(k_reabsorb_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)reabsorb_small_smem(64, 64));
+  k_reabsorb_small<<<count, 256, smem, s>>>(d_desc, d_list, slab);
+}
+
+int launch_reabsorb(const GateDesc* d_desc, const int32_t* d_pre_gram, int tiles_gram, const int32_t* d_pre_apply,
+                    int tiles_apply, const int32_t* d_pre_reab, int tiles_reab, int G, uint8_t* slab, cudaStream_t s) {
+  if (G <= 0) return 0;
+  int launches = 0;
+  if (tiles_gram > 0) { k_vk_gram<<<tiles_gram, 256, 0, s>>>(d_desc, d_pre_gram, G, slab); ++launches; }
+  if (tiles_apply > 0) { k_vk_apply<<<tiles_apply, 256, 0, s>>>(d_desc, d_pre_apply, G, slab); ++launches; }
+  if (tiles_reab > 0) { k_reabsorb<<<tiles_reab, 256, 0, s>>>(d_desc, d_pre_reab, G, slab); ++launches; }
+  return launches;
 }
 
 }  // namespace eamps
