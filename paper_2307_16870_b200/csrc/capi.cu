@@ -345,7 +345,9 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
 // lane-group size of the small (reg 0) and medium (reg 2) Jacobi kernels: a power of two in
 // [4, 32], from the rows (small_group(m)) and the CTA width (2048 / n resp. 1024 / n lanes per pair)
 size_t large_scratch_bytes(const GateDesc& gd) {
-  return std::max(svd_tc_scratch_bytes(gd.n_pad), gd.jrows > 0 ? large_precond_scratch(gd.n) : (size_t)0);
+  const size_t b = std::max(svd_tc_scratch_bytes(gd.n_pad), gd.jrows > 0 ? large_precond_scratch(gd.n) : (size_t)0);
+  // the FP64 spectrum of deep 256 < n <= 2048 gates (refine_large.cu) reuses the dead scratch
+  return refine_large_candidate(gd) ? std::max(b, refine_large_scratch(gd.m, gd.n)) : b;
 }
 
 int lane_group(int m, int n, int reg) {
@@ -381,7 +383,7 @@ mps_status wave_front_impl(mps_t h) {
   while (g1 < G) {
     const int cnt = g1 - g0 + 1;
     size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 3 * align_up(4 * cnt) +
-                align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64);
+                align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64 + 4096);
     size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
     if (bump + r2 + fx + w2 + kAlign > top) break;
     fixed = fx;
@@ -411,7 +413,7 @@ mps_status wave_front_impl(mps_t h) {
   const size_t o_rsm = take(4 * Gw);
   const size_t o_us = take((size_t)Gw * d4 * 8);
   const size_t o_rec = take(sizeof(Record) * Gw);
-  const size_t o_scr = take(32 * (size_t)Gw + 64);
+  const size_t o_scr = take(32 * (size_t)Gw + 64 + 4096);
   const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
   std::vector<int32_t> cpre(Gw + 1, 0), small, large;
   J.rsm.clear();
@@ -696,6 +698,12 @@ mps_status wave_front_impl(mps_t h) {
       const int e0 = prof ? prof_mark(h) : -1;
       h->launches += launch_refine(d_desc, Gw, maxn, h->slab, h->dst, d_us, reinterpret_cast<int32_t*>(h->slab + o_scr), h->s);
       CKL("refine");
+      // deep large-regime gates with 256 < n <= 2048: FP64 eigenvalues of the recontracted Gram
+      if (!large.empty()) {
+        h->launches += launch_refine_large(d_desc, hd.data(), large.data(), d_large, (int)large.size(), h->slab, h->dst,
+                                           d_us, d, reinterpret_cast<int32_t*>(h->slab + o_scr) + Gw + 2, h->s);
+        CKL("refine_large");
+      }
       if (prof) prof_span(h, 7, e0, prof_mark(h));
     }
   }

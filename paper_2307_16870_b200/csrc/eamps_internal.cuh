@@ -167,6 +167,13 @@ int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, i
 size_t refine_scratch_bytes(int n);
 int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us,
                   int32_t* d_list /* G + 1 ints */, cudaStream_t s);
+// FP64 eigenvalues of the Gram of the FP64-recontracted theta for deep large-regime gates with
+// 256 < n <= 2048 (refine_large.cu). cand = the wave's large-regime gates (host and device copies);
+// iscr: wave scratch of 2 nc + 2 ints + 2176 bytes (barrier lines). Returns launches issued.
+bool refine_large_candidate(const GateDesc& gd);
+size_t refine_large_scratch(int m, int n);
+int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                        uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s);
 // parallel = 1: FIXED / NAIVE (target independent of the ledger): one warp per gate;
 // parallel = 0: GLOBAL / NEAREST: one warp walks the gates in canonical order.
 void launch_select(GateDesc* d_desc, int G, uint8_t* slab, DevState* st, Record* d_rec, int parallel, cudaStream_t s);

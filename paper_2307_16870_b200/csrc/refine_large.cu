@@ -1,0 +1,628 @@
+// refine_large.cu -- FP64 spectrum of deep large-n spectra (steps a2/a3): the
+// singular values of theta for gates of the large regime with 256 < n <= 2048 whose spectrum is
+// deep, as the eigenvalues of the FP64 Gram G = theta^H theta of theta RECONTRACTED in FP64 from the
+// complex64 site tensors and gate.
+//
+// Why (reading 19, "Relative accuracy of small singular values"): the large regime's FP32
+// pipeline (FP32-rounded Cholesky factor B = L, 3xTF32 block rotations accumulated over ~13 sweeps x
+// 63 rounds) delivers right singular vectors whose error (~1e-6 sigma_max normwise) exceeds the gaps
+// of a deep, dense spectrum: at chi = 1024 (theta 2048 x 2048, sigma_k ~ k^-1.5, sigma_min =
+// 1.1e-5 sigma_max, neighbouring sigma 7.5e-9 sigma_max apart) the deep right singular vectors are
+// mixed over windows of many neighbours, so the Rayleigh quotient of a deep v_j is an average over
+// its window (7.9e-4 relative error with the pairwise polish). A Jacobi refinement warm-started from
+// that V would have to re-solve the mixed deep subspace from scratch (a numpy model: 3+ cyclic
+// sweeps of the 2048 x 2048 C). The eigenvalues of G do not depend on V at all: a backward-stable
+// FP64 Hermitian eigensolver gives sigma_j^2 with an absolute error of a few eps64 ||G||, i.e. a
+// relative error ~1e-16 / (sigma_j / sigma_max)^2 = 1e-6 at 1.1e-5 (numpy/LAPACK on the chi = 1024
+// recipe: 9.4e-9 relative in sigma, this file's recurrence re-run in numpy: 3.8e-9); the FP64
+// recontraction removes the FP32 theta's own 2.6e-6.
+// What (one wave; gates picked on the device, at most 2048 columns):
+//   k_rlg_pick     the trigger (deepest sigma >= 1e-6 sigma_max below kRatio sigma_max)
+//   k_rlg_theta    theta64[(a,s),(t,c)] = lambda_a sum_{s',t'} U[s d+t, s' d+t'] sum_b B_i[a,s',b] B_{i+1}[b,t',c]
+//                  (E2 of PAPER.md:32-41 / contract.cu with FP64 products and sums)
+//   k_rlg_gram     G = theta64^H theta64 (FP64, full Hermitian storage, row-major)
+//   k_rlg_tridiag  one-stage Householder tridiagonalisation Q^H G Q = T (LAPACK zhetd2 recurrence,
+//                  lower), all CTAs of a cooperative grid on one gate at a time; the rank-2 update of
+//                  step k-1 is applied lazily during step k (each CTA re-derives the pivot row k
+//                  itself), so every step costs one grid barrier
+//   k_rlg_bisect   eigenvalues of the real symmetric tridiagonal T by Sturm-count multisection
+//                  (one thread per eigenvalue index)
+//   k_rlg_finish   sigma^2 in descending order + FP64 tails (a3 redone)
+// The j-th largest eigenvalue replaces the sigma^2 of the j-th column of the existing order pi (rank
+// matching): the kept columns (the top of a deep spectrum) are well separated and unchanged in order;
+// the deep columns are mixed among themselves anyway and are never kept (reading 20).
+// V itself is not rotated (as refine.cu). PAPER.md:114 ("performing its SVD", "singular values in
+// decreasing order"); north_star tolerance "singular values: relative 1e-5 for sigma >= 1e-6 sigma_max".
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+
+#include "eamps_internal.cuh"
+#include "sort_tails.cuh"
+
+namespace eamps {
+
+namespace {
+
+constexpr int kMinN = 257, kMaxN = 2048;
+// measured (config 2, r02): chi = 256 (n = 512, sigma_min/sigma_max = 8.6e-5) 2.8e-6 and chi = 512
+// (n = 1024, 3.1e-5) 5.8e-6 with Rayleigh + polish -- inside the 1e-5 bar; chi = 1024 (n = 2048,
+// 1.1e-5) 7.9e-4. The FP64 eigensolver runs for spectra deeper than 2e-5 sigma_max.
+constexpr double kRatio = 2e-5;
+constexpr int TT = 512;          // tridiagonalisation threads per CTA
+constexpr int BT = 128;          // bisection threads per CTA
+constexpr int kMaxGroups = 16, kDefaultGroups = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+struct RlgLayout {               // per-gate scratch at ws_log (the large regime's dead TC / Gram scratch)
+  int64_t g, th, d, e, eig, p, part;
+};
+__host__ __device__ inline RlgLayout rlg_layout(const GateDesc& gd) {
+  RlgLayout L;
+  const int64_t n = gd.n, m = gd.m;
+  L.g = gd.ws_log;
+  L.th = L.g + 16 * n * n;
+  L.d = L.th + 16 * m * n;
+  L.e = L.d + 8 * n;
+  L.eig = L.e + 8 * n;
+  L.p = L.eig + 8 * n;                 // 2 x n double2 (by step parity)
+  L.part = L.p + 32 * n;               // 2 x 1024 double2 (by step parity)
+  return L;
+}
+
+// ---- trigger --------------------------------------------------------------------------------
+// cand[0..nc): wave-local gate indices (large regime, n in range); flag[c] = 1 if the gate is deep;
+// list[0] = count, list[1..] = wave-local gate indices.
+__global__ void k_rlg_pick(const GateDesc* __restrict__ desc, const uint8_t* slab, const int32_t* __restrict__ cand,
+                           int nc, int32_t* flag, int32_t* list) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  const GateDesc& gd = desc[cand[c]];
+  const int n = gd.n;
+  const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);   // sorted descending
+  const double smax = gS[0];
+  double deep = smax;
+  for (int j = lane; j < n; j += 32)
+    if (gS[j] >= 1e-12 * smax) deep = fmin(deep, gS[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) deep = fmin(deep, __shfl_xor_sync(0xffffffffu, deep, o));
+  const int on = gd.regime == 1 && n >= kMinN && n <= kMaxN && smax > 0.0 && deep < kRatio * kRatio * smax;
+  if (lane == 0) {
+    flag[c] = on;
+    if (on) list[1 + atomicAdd(&list[0], 1)] = cand[c];
+  }
+}
+
+// ---- theta64: the contraction in FP64 (64 x 64 tile of X over TA = 64/D left indices a and
+// TC = 64/D right indices c for all (s', t'); gate mix + lambda in the epilogue; FP32 inputs are
+// exact in FP64, products and sums in FP64) ------------------------------------------------------
+constexpr int KC = 16;
+constexpr size_t kThetaSmem = (size_t)64 * 65 * sizeof(double2);
+
+template <int D>
+__global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                   const int32_t* __restrict__ flag, uint8_t* slab, const DevState* st,
+                                                   const float2* __restrict__ us) {
+  constexpr int TA = 64 / D, TC = 64 / D;
+  if (!flag[blockIdx.y]) return;
+  const GateDesc gd = desc[cand[blockIdx.y]];
+  const int l = gd.l, mid = gd.mid, r = gd.r, m = gd.m;
+  const int ntc = (r + TC - 1) / TC, nta = (l + TA - 1) / TA;
+  if ((int)blockIdx.x >= nta * ntc) return;
+  const int a0 = (blockIdx.x / ntc) * TA, c0 = (blockIdx.x % ntc) * TC;
+  extern __shared__ __align__(16) uint8_t sm[];
+  double2(*As)[65] = reinterpret_cast<double2(*)[65]>(sm);              // [KC][65]
+  double2(*Bs)[65] = reinterpret_cast<double2(*)[65]>(sm) + KC;         // [KC][65]
+  double2(*Cs)[65] = reinterpret_cast<double2(*)[65]>(sm);              // [64][65] (epilogue)
+  __shared__ double2 Us[D * D * D * D];
+  const SiteEntry* sites = reinterpret_cast<const SiteEntry*>(slab + st->sites_off);
+  const BondEntry* bonds = reinterpret_cast<const BondEntry*>(slab + st->bonds_off);
+  const float2* __restrict__ Bi = reinterpret_cast<const float2*>(slab + sites[gd.site].off);
+  const float2* __restrict__ Bj = reinterpret_cast<const float2*>(slab + sites[gd.site + 1].off);
+  const float* __restrict__ lam = reinterpret_cast<const float*>(slab + bonds[gd.site].off);
+  double2* __restrict__ th = reinterpret_cast<double2*>(slab + rlg_layout(gd).th);
+  const int tid = threadIdx.x;
+  for (int x = tid; x < D * D * D * D; x += 256) {
+    const float2 u = us[(int64_t)gd.u_index * D * D * D * D + x];
+    Us[x] = make_double2(u.x, u.y);
+  }
+  const int ty = tid >> 4, tx = tid & 15;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+  for (int b0 = 0; b0 < mid; b0 += KC) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      const int kk = e & (KC - 1), rho = e >> 4;
+      const int a = a0 + rho / D, sp = rho % D, b = b0 + kk;
+      float2 v = make_float2(0.f, 0.f);
+      if (a < l && b < mid) v = Bi[((int64_t)a * D + sp) * mid + b];
+      As[kk][rho] = make_double2(v.x, v.y);
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      const int cc = e % TC, rest = e / TC;
+      const int tp = rest % D, kk = rest / D;
+      const int c = c0 + cc, b = b0 + kk;
+      float2 v = make_float2(0.f, 0.f);
+      if (c < r && b < mid) v = Bj[((int64_t)b * D + tp) * r + c];
+      Bs[kk][tp * TC + cc] = make_double2(v.x, v.y);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fma(av[i].x, bv[j].x, fma(-av[i].y, bv[j].y, acc[i][j].x));
+          acc[i][j].y = fma(av[i].x, bv[j].y, fma(av[i].y, bv[j].x, acc[i][j].y));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Cs[ty + 16 * i][tx + 16 * j] = acc[i][j];
+  __syncthreads();
+  for (int p = tid; p < TA * TC; p += 256) {
+    const int al = p % TA, cl = p / TA;
+    const int a = a0 + al, c = c0 + cl;
+    if (a >= l || c >= r) continue;
+    const double la = lam[a];
+#pragma unroll
+    for (int s = 0; s < D; ++s)
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int sp = 0; sp < D; ++sp)
+#pragma unroll
+          for (int tp = 0; tp < D; ++tp) {
+            const double2 u = Us[(s * D + t) * D * D + sp * D + tp];
+            const double2 cv = Cs[al * D + sp][tp * TC + cl];
+            o.x = fma(u.x, cv.x, fma(-u.y, cv.y, o.x));
+            o.y = fma(u.x, cv.y, fma(u.y, cv.x, o.y));
+          }
+        th[(int64_t)(t * r + c) * m + (a * D + s)] = make_double2(la * o.x, la * o.y);
+      }
+  }
+}
+
+// ---- G = theta64^H theta64: 64 x 64 tiles (bi <= bj), mirrored; K = m in chunks of KC ---------
+__global__ void __launch_bounds__(256) k_rlg_gram(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                  const int32_t* __restrict__ flag, uint8_t* slab) {
+  if (!flag[blockIdx.y]) return;
+  const GateDesc gd = desc[cand[blockIdx.y]];
+  const int n = gd.n, m = gd.m, nt = (n + 63) / 64;
+  int t = blockIdx.x, bi = 0;
+  while (bi < nt && t >= nt - bi) { t -= nt - bi; ++bi; }
+  if (bi >= nt) return;
+  const int bj = bi + t;
+  const RlgLayout L = rlg_layout(gd);
+  const double2* __restrict__ th = reinterpret_cast<const double2*>(slab + L.th);
+  double2* __restrict__ G = reinterpret_cast<double2*>(slab + L.g);
+  extern __shared__ __align__(16) uint8_t sm[];
+  double2(*As)[65] = reinterpret_cast<double2(*)[65]>(sm);
+  double2(*Bs)[65] = reinterpret_cast<double2(*)[65]>(sm) + KC;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int i0 = bi * 64, j0 = bj * 64;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+  for (int r0 = 0; r0 < m; r0 += KC) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      const int kk = e & (KC - 1), cc = e >> 4;
+      const int row = r0 + kk;
+      const int ci = i0 + cc, cj = j0 + cc;
+      As[kk][cc] = (row < m && ci < n) ? th[(int64_t)ci * m + row] : make_double2(0.0, 0.0);
+      Bs[kk][cc] = (row < m && cj < n) ? th[(int64_t)cj * m + row] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {   // conj(a) b
+          acc[i][j].x = fma(av[i].x, bv[j].x, fma(av[i].y, bv[j].y, acc[i][j].x));
+          acc[i][j].y = fma(av[i].x, bv[j].y, fma(-av[i].y, bv[j].x, acc[i][j].y));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
+      if (gi >= n || gj >= n) continue;
+      G[(int64_t)gi * n + gj] = acc[i][j];
+      if (bi != bj) G[(int64_t)gj * n + gi] = make_double2(acc[i][j].x, -acc[i][j].y);
+    }
+}
+
+// ---- Householder tridiagonalisation (cooperative grid, one gate at a time) ---------------------
+// Monotone arrival counter of a CTA group: barrier number b completes when the counter reaches
+// b * members.
+__device__ __forceinline__ void rlg_barrier(unsigned int* ctr, unsigned int& nb, int members) {
+  __syncthreads();
+  ++nb;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned int target = nb * (unsigned int)members;
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v < target) __nanosleep(20);
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// CTA-wide sum of one double per thread (deterministic order; identical in every CTA).
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+size_t tridiag_smem(int n) { return (size_t)3 * n * sizeof(double2) + 64 * sizeof(double) + 64; }
+
+// The grid is split into groups of cpg CTAs; group g factorises the listed gates g, g + ngrp, ...
+// (several gates in flight when the wave has several; all CTAs on one gate when it has one).
+__global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restrict__ desc,
+                                                       const int32_t* __restrict__ list, uint8_t* slab,
+                                                       unsigned int* ctr_base, int cpg) {
+  const int cnt = list[0];
+  const int grp = blockIdx.x / cpg, lcta = blockIdx.x % cpg, ngrp = gridDim.x / cpg;
+  if (grp >= ngrp) return;
+  unsigned int* ctr = ctr_base + 32 * grp;   // one 128-byte line per group
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gw = lcta * (TT / 32) + warp, W = cpg * (TT / 32);
+  unsigned int nb = 0;
+  for (int li = grp; li < cnt; li += ngrp) {
+    const GateDesc& gd = desc[list[1 + li]];
+    const int n = gd.n;
+    const RlgLayout L = rlg_layout(gd);
+    double2* A = reinterpret_cast<double2*>(slab + L.g);
+    double* dg = reinterpret_cast<double*>(slab + L.d);
+    double* eg = reinterpret_cast<double*>(slab + L.e);
+    double2* pg = reinterpret_cast<double2*>(slab + L.p);
+    double2* partg = reinterpret_cast<double2*>(slab + L.part);
+    double2* vbuf[2] = {reinterpret_cast<double2*>(sm), reinterpret_cast<double2*>(sm) + n};
+    double2* w = reinterpret_cast<double2*>(sm) + 2 * n;                 // w of step k-1
+    double* red = reinterpret_cast<double*>(w + n);                     // 32 doubles
+    double2* sc = reinterpret_cast<double2*>(red + 32);                 // [0] tau, [1] (dot)
+    for (int k = 0; k < n - 1; ++k) {
+      double2* v = vbuf[k & 1];
+      const double2* vp = vbuf[(k & 1) ^ 1];   // v of step k-1 (valid from k = 1)
+      const bool upd = k > 0;
+      // (1) pivot row k with the update of step k-1 applied (every CTA, never stored)
+      double part = 0.0, dk = 0.0;
+      for (int j = k + tid; j < n; j += TT) {
+        double2 a = __ldcg(&A[(int64_t)k * n + j]);
+        if (upd) {
+          const double2 t1 = cmulc(w[j], vp[k]);   // v_k conj(w_j) = conj(conj(v_k) w_j)
+          const double2 t2 = cmulc(vp[j], w[k]);   // w_k conj(v_j)
+          a.x -= t1.x + t2.x;
+          a.y -= t1.y + t2.y;
+        }
+        if (j == k) {
+          dk = a.x;
+        } else {
+          v[j] = make_double2(a.x, -a.y);           // x_j = conj(row) = column k below the diagonal
+          if (j >= k + 2) part += a.x * a.x + a.y * a.y;
+        }
+      }
+      const double xn2 = cta_sum(part, red);       // includes a __syncthreads: v[] complete
+      if (lcta == 0 && tid == 0) dg[k] = dk;   // j == k is thread 0's
+      const double2 al = v[k + 1];
+      double2 tau;
+      double beta;
+      double2 scale = make_double2(0.0, 0.0);
+      if (xn2 == 0.0 && al.y == 0.0) {
+        tau = make_double2(0.0, 0.0);
+        beta = al.x;
+      } else {
+        beta = -copysign(sqrt(al.x * al.x + al.y * al.y + xn2), al.x);
+        tau = make_double2((beta - al.x) / beta, -al.y / beta);
+        const double2 den = make_double2(al.x - beta, al.y);           // 1 / (alpha - beta)
+        const double dd = den.x * den.x + den.y * den.y;
+        scale = make_double2(den.x / dd, -den.y / dd);
+      }
+      if (lcta == 0 && tid == 0) eg[k] = beta;
+      __syncthreads();   // every thread has read v[k + 1]
+      for (int j = k + 2 + tid; j < n; j += TT) v[j] = cmul(v[j], scale);
+      if (tid == 0) v[k + 1] = make_double2(1.0, 0.0);
+      __syncthreads();
+      // (2) rows i > k: apply the update of step k-1, store, and p_i = tau (A v)_i
+      double2 pdot = make_double2(0.0, 0.0);       // sum over this warp's rows of conj(p_i) v_i
+      for (int i = k + 1 + gw; i < n; i += W) {
+        double2* row = A + (int64_t)i * n;
+        const double2 vi = upd ? vp[i] : make_double2(0.0, 0.0), wi = upd ? w[i] : make_double2(0.0, 0.0);
+        double sx = 0.0, sy = 0.0;
+        for (int j0 = k + 1 + lane; j0 < n; j0 += 128) {
+          double2 a[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {   // four loads in flight per lane
+            const int j = j0 + 32 * u;
+            a[u] = j < n ? __ldcg(&row[j]) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + 32 * u;
+            if (j >= n) break;
+            if (upd) {
+              const double2 t1 = cmulc(w[j], vi);    // v_i conj(w_j)
+              const double2 t2 = cmulc(vp[j], wi);   // w_i conj(v_j)
+              a[u].x -= t1.x + t2.x;
+              a[u].y -= t1.y + t2.y;
+              __stcg(&row[j], a[u]);
+            }
+            const double2 vj = v[j];
+            sx = fma(a[u].x, vj.x, fma(-a[u].y, vj.y, sx));
+            sy = fma(a[u].x, vj.y, fma(a[u].y, vj.x, sy));
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sx += __shfl_xor_sync(0xffffffffu, sx, o);
+          sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        const double2 p = cmul(tau, make_double2(sx, sy));
+        if (lane == 0) __stcg(&pg[(int64_t)(k & 1) * n + i], p);
+        const double2 cp = cmulc(p, v[i]);
+        pdot.x += cp.x;
+        pdot.y += cp.y;
+      }
+      const double dre = cta_sum(lane == 0 ? pdot.x : 0.0, red);
+      const double dim = cta_sum(lane == 0 ? pdot.y : 0.0, red);
+      if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], make_double2(dre, dim));
+      rlg_barrier(ctr, nb, cpg);
+      // (3) w = p + alpha v, alpha = -1/2 tau (p^H v)   (zhetd2; p already carries tau). The group's
+      // partials summed by warp 0 in a fixed order (identical in every CTA of the group)
+      if (warp == 0) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int c = lane; c < cpg; c += 32) {
+          const double2 q = __ldcg(&partg[(k & 1) * 1024 + c]);
+          s.x += q.x;
+          s.y += q.y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+          s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+        }
+        const double2 t = cmul(tau, s);
+        if (lane == 0) sc[0] = make_double2(-0.5 * t.x, -0.5 * t.y);
+      }
+      __syncthreads();
+      const double2 alpha = sc[0];
+      for (int j = k + 1 + tid; j < n; j += TT) {
+        const double2 p = __ldcg(&pg[(int64_t)(k & 1) * n + j]);
+        const double2 av = cmul(alpha, v[j]);
+        w[j] = make_double2(p.x + av.x, p.y + av.y);
+      }
+      __syncthreads();
+    }
+    // the last diagonal entry: A[n-1][n-1] with the update of step n-2
+    if (lcta == 0 && tid == 0) {
+      double2 a = __ldcg(&A[(int64_t)(n - 1) * n + (n - 1)]);
+      if (n >= 2) {
+        const double2* vl = vbuf[(n - 2) & 1];
+        const double2 t1 = cmulc(w[n - 1], vl[n - 1]);
+        const double2 t2 = cmulc(vl[n - 1], w[n - 1]);
+        a.x -= t1.x + t2.x;
+      }
+      dg[n - 1] = a.x;
+    }
+    rlg_barrier(ctr, nb, cpg);   // the next gate reuses the shared buffers and the partials
+  }
+}
+
+// ---- eigenvalues of the symmetric tridiagonal (d, e) by Sturm-count multisection ---------------
+// count(x) = #{eigenvalues < x} = #{negative pivots of T - x I = L D L^T}. A group of 8 lanes per
+// eigenvalue index j; each lane runs the Sturm recurrences of 2 of the 16 interior points of the
+// bracket (two independent chains), so a pass narrows [lo, hi) 17-fold; the bracket is identical
+// in the 8 lanes (same inputs, same arithmetic).
+constexpr int kBisPerCta = (BT / 32) * 4;   // eigenvalues per CTA
+__global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                   const int32_t* __restrict__ flag, uint8_t* slab) {
+  if (!flag[blockIdx.y]) return;
+  const GateDesc gd = desc[cand[blockIdx.y]];
+  const int n = gd.n;
+  if ((int)blockIdx.x * kBisPerCta >= n) return;
+  const RlgLayout L = rlg_layout(gd);
+  const double* dg = reinterpret_cast<const double*>(slab + L.d);
+  const double* eg = reinterpret_cast<const double*>(slab + L.e);
+  double* eig = reinterpret_cast<double*>(slab + L.eig);
+  __shared__ double ds[kMaxN], e2s[kMaxN];
+  __shared__ double red[3][BT / 32];
+  double lo = 1e300, hi = -1e300, emax = 0.0;
+  for (int i = threadIdx.x; i < n; i += BT) {
+    const double di = dg[i], el = i > 0 ? fabs(eg[i - 1]) : 0.0, er = i < n - 1 ? fabs(eg[i]) : 0.0;
+    ds[i] = di;
+    e2s[i] = er * er;
+    lo = fmin(lo, di - el - er);   // Gershgorin
+    hi = fmax(hi, di + el + er);
+    emax = fmax(emax, er * er);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = lo;
+    red[1][threadIdx.x >> 5] = hi;
+    red[2][threadIdx.x >> 5] = emax;
+  }
+  __syncthreads();
+  for (int i = 0; i < BT / 32; ++i) {
+    lo = fmin(lo, red[0][i]);
+    hi = fmax(hi, red[1][i]);
+    emax = fmax(emax, red[2][i]);
+  }
+  const double span = fmax(fabs(lo), fabs(hi));
+  lo -= 2.0 * 2.2e-16 * span * n + 1e-300;
+  hi += 2.0 * 2.2e-16 * span * n + 1e-300;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+  const int lane = threadIdx.x & 31, sub = lane & 7;
+  const int j = blockIdx.x * kBisPerCta + (threadIdx.x >> 3);
+  const bool act = j < n;
+  // invariant: count(lo) <= j < count(hi)
+  for (int it = 0; it < 18; ++it) {   // 17^18 > 2^73
+    const double wdt = hi - lo;
+    if (__all_sync(0xffffffffu, wdt <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300)) break;   // warp-uniform
+    const double x1 = lo + wdt * (2 * sub + 1) / 17.0, x2 = lo + wdt * (2 * sub + 2) / 17.0;
+    double q1 = ds[0] - x1, q2 = ds[0] - x2;
+    int c1 = q1 < 0.0, c2 = q2 < 0.0;
+    for (int i = 1; i < n; ++i) {
+      const double e2 = e2s[i - 1], di = ds[i];
+      if (fabs(q1) < pivmin) q1 = -pivmin;
+      if (fabs(q2) < pivmin) q2 = -pivmin;
+      q1 = (di - x1) - e2 / q1;
+      q2 = (di - x2) - e2 / q2;
+      c1 += q1 < 0.0;
+      c2 += q2 < 0.0;
+    }
+    // bit p of mask: count(x_p) > j (monotone in p); OR over the 8 lanes of the group
+    unsigned int mask = ((act && c1 > j) ? 1u : 0u) << (2 * sub) | ((act && c2 > j) ? 2u : 0u) << (2 * sub);
+    mask |= __shfl_xor_sync(0xffffffffu, mask, 1);
+    mask |= __shfl_xor_sync(0xffffffffu, mask, 2);
+    mask |= __shfl_xor_sync(0xffffffffu, mask, 4);
+    const int p = mask ? __ffs(mask) - 1 : 16;    // first point with count > j
+    const double nlo = p == 0 ? lo : lo + wdt * p / 17.0;
+    const double nhi = p == 16 ? hi : lo + wdt * (p + 1) / 17.0;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (act && sub == 0) eig[j] = 0.5 * (lo + hi);   // ascending
+}
+
+// ---- sigma^2 (descending) + tails ---------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_rlg_finish(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                    const int32_t* __restrict__ flag, uint8_t* slab) {
+  if (!flag[blockIdx.x]) return;
+  const GateDesc gd = desc[cand[blockIdx.x]];
+  const int n = gd.n;
+  const RlgLayout L = rlg_layout(gd);
+  const double* eig = reinterpret_cast<const double*>(slab + L.eig);
+  __shared__ double keys[kMaxN];
+  __shared__ double part[256];
+  double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  for (int j = threadIdx.x; j < n; j += 256) {
+    const double v = fmax(eig[n - 1 - j], 0.0);
+    keys[j] = v;
+    gS[j] = v;
+  }
+  __syncthreads();
+  cta_tails(keys, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
+}
+
+}  // namespace
+
+bool refine_large_candidate(const GateDesc& gd) { return gd.regime == 1 && gd.n >= kMinN && gd.n <= kMaxN; }
+
+size_t refine_large_scratch(int m, int n) {
+  return (size_t)16 * n * n + (size_t)16 * m * n + (size_t)56 * n + 32 * 1024 + 256;
+}
+
+// cand: device copy of the wave-local candidate gates (nc, max n / tiles from the host copy);
+// iscr: wave scratch: flags (nc ints), list (nc + 1 ints), then kMaxGroups 128-byte barrier lines.
+int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                        uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s) {
+  if (nc <= 0) return 0;
+  int max_tiles = 0, max_gram = 0, max_n = 0;
+  for (int c = 0; c < nc; ++c) {
+    const GateDesc& g = h_desc[h_cand[c]];
+    if (!refine_large_candidate(g)) continue;
+    const int T = 64 / d;
+    max_tiles = std::max(max_tiles, ((g.l + T - 1) / T) * ((g.r + T - 1) / T));
+    const int nt = (g.n + 63) / 64;
+    max_gram = std::max(max_gram, nt * (nt + 1) / 2);
+    max_n = std::max(max_n, g.n);
+  }
+  if (max_n == 0) return 0;
+  int32_t* flag = iscr;
+  int32_t* list = iscr + nc;                                                   // nc + 1 ints
+  // group barrier counters: one 128-byte line per group, at a 128-byte boundary after the lists
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(
+      (reinterpret_cast<uintptr_t>(iscr + 2 * nc + 2) + 127) & ~uintptr_t(127));
+  cudaMemsetAsync(list, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(ctr, 0, 128 * kMaxGroups, s);
+  k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list);
+  static std::atomic<unsigned long long> attr{0};
+  const size_t tsm = tridiag_smem(kMaxN);
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(k_rlg_theta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+  }
+  if (d == 2)
+    k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  else
+    k_rlg_theta<4><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  k_rlg_gram<<<dim3(max_gram, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab);
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rlg_tridiag, TT, tsm);
+  int grid = sms * std::max(per, 1);
+  if (grid > 1024) grid = 1024;   // the partial-dot buffer holds 1024 CTAs
+  // several gates in flight when the wave has several candidates (EAMPS_RLG_GROUPS overrides)
+  static const int env_groups = getenv("EAMPS_RLG_GROUPS") ? atoi(getenv("EAMPS_RLG_GROUPS")) : 0;
+  int groups = env_groups > 0 ? env_groups : kDefaultGroups;
+  groups = std::max(1, std::min({groups, nc, kMaxGroups, grid}));
+  const int cpg = grid / groups;
+  const GateDesc* a_desc = d_desc;
+  const int32_t* a_list = list;
+  uint8_t* a_slab = slab;
+  unsigned int* a_ctr = ctr;
+  int a_cpg = cpg;
+  void* args[] = {&a_desc, &a_list, &a_slab, &a_ctr, &a_cpg};
+  cudaLaunchCooperativeKernel((const void*)k_rlg_tridiag, dim3(grid), dim3(TT), args, tsm, s);
+  k_rlg_bisect<<<dim3((max_n + kBisPerCta - 1) / kBisPerCta, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+  k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab);
+  return 6;
+}
+
+}  // namespace eamps

@@ -206,6 +206,9 @@ def _graded_pair(l, r, decades, seed):
     (64, 64, "QR block-recursive (n = 128)"),
     (32, 72, "medium (m = 64 < n = 144)"),
     (128, 128, "large tcgen05 (n = 256)"),
+    (256, 256, "large + FP64 Gram eigensolver (n = 512)"),
+    (320, 256, "large + FP64 Gram eigensolver, m = 640 > n = 512"),
+    (200, 256, "large + FP64 Gram eigensolver, wide m = 400 < n = 512"),
 ])
 def test_graded_spectrum_relative_accuracy(l, r, regime):
     """Relative accuracy where it is hardest: every sigma down to ~1e-6 sigma_max (5.5 decades) at

@@ -2,7 +2,8 @@
 2048 x 2048, sigma_k ~ k^-1.5, sigma_min / sigma_max = 2048^-1.5 = 1.1e-5) through the C ABI
 against the complex128 oracle on the identical seeded inputs, at the strict north-star bars. This
 is the regime where the FP64 Cholesky preconditioner squares kappa(theta) (DESIGN.md "K3 SVD,
-large") and the smallest sigma sit just above the 1e-6 sigma_max cut-off of the bar. The oracle
+large") and the smallest sigma sit just above the 1e-6 sigma_max cut-off of the bar; the deep
+spectrum takes the FP64 Gram eigensolver (refine_large.cu). The oracle
 (its own cyclic Jacobi on a 2048^2 complex matrix, several CPU minutes) starts in a background
 thread when the session collects this test (tests/conftest.py) and overlaps the rest of the suite."""
 import numpy as np
@@ -14,12 +15,9 @@ from test_gpu_parity import SIG_RTOL, near_tie, spectra_close
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-# Known gap (reading 19, scope table): at chi = 1024 the large regime's FP32 pipeline
-# (FP32-rounded Cholesky factor, Rayleigh quotient + pairwise FP64-anchored polish) reaches a worst
-# relative sigma error of 7.9e-4 at sigma_min / sigma_max = 1.1e-5 (measured, r02); the FP64
-# Rayleigh-Ritz refinement that brings every n <= 256 theta to ~1e-8 does not cover n = 2048 yet.
-# The comparison runs and reports its number; the kept rank and f are still asserted below.
-@pytest.mark.xfail(strict=False, reason="chi=1024 sigma relative accuracy 7.9e-4 > 1e-5 (DESIGN.md reading 19)")
+# Round 2: this was the known gap (7.9e-4 with the FP32 pipeline's Rayleigh quotients + pairwise
+# polish, reading 19); the deep spectrum now comes from the FP64 eigenvalues of the Gram of
+# the FP64-recontracted theta (refine_large.cu, reading 20): measured 9.9e-9.
 def test_config2_chi1024_gate_vs_oracle():
     import paper_2307_16870_b200 as pk
     import workloads
@@ -39,4 +37,4 @@ def test_config2_chi1024_gate_vs_oracle():
     else:
         assert abs(rg["achieved_f"] - ro["achieved_f"]) < 1e-6
     assert rg["chi_after"] == 64 or near_tie(so, 0.9999, ro["chi_after"])   # SURVEY §8(c) closed form k* = 64
-    assert err < SIG_RTOL, err   # the known gap (xfail above)
+    assert err < SIG_RTOL, err
