@@ -47,6 +47,11 @@ def _peaks():
         out["tf32"] = (pk["tf32_tcgen05_m128n256_tflops"],
                        "measured: tools/peaks tcgen05.mma kind::tf32 M128 N256 K8 loop, profiles/r02/peaks.json")
         out["fp64"] = (pk["fp64_dfma_tflops"], "measured: tools/peaks DFMA loop, profiles/r02/peaks.json")
+        try:
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            out["hbm"] = (mp["hbm_gbs"], "measured (driver): MEASURED_PEAKS.json hbm_gbs, torch copy_ of 1 Gi bf16")
+        except Exception:
+            out["hbm"] = (7700.0, "nominal B200 HBM3e 7.7 TB/s (MEASURED_PEAKS.json absent)")
     except Exception:
         out["fp32"] = (148 * 128 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz")
         try:
@@ -55,6 +60,7 @@ def _peaks():
         except Exception:
             out["tf32"] = (1590.0 * (1.13 / 2.25), "fallback bf16 1590 TF/s x nominal TF32/BF16 1.13/2.25")
         out["fp64"] = (148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 lanes x 2 x 1.965 GHz")
+        out["hbm"] = (7700.0, "nominal B200 HBM3e 7.7 TB/s (peaks files absent)")
     return out
 
 
@@ -109,6 +115,21 @@ def svd_support_flops(m, n, regime):
     if regime in (1, 3):
         f += 4.0 * m * n * n + 8.0 * n ** 3 / 3 + 4.0 * m * n * n
     return f
+
+
+def eig_route_flops(m, n, k, d=2, l=None, mid=None, r=None):
+    """Executed FP64 flops of the eigen route (refine_large.cu) for one m x n theta: the FP64
+    recontraction (8 d^2 l mid r + 8 d^4 l r), the Hermitian Gram (4 m n^2), the Householder
+    tridiagonalisation (16 n^3 / 3), the back-transformation of the k kept vectors (8 n^2 k)."""
+    contract = 8.0 * d * d * l * mid * r + 8.0 * d ** 4 * l * r
+    return contract + 4.0 * m * n * n + 16.0 * n ** 3 / 3 + 8.0 * n * n * k
+
+
+def tridiag_bytes(n):
+    """Algorithmic HBM bytes of a one-stage Householder tridiagonalisation of an n x n complex128
+    Hermitian matrix: every step reads and writes its trailing triangle, sum_t 2 x 16 t^2 / 2 =
+    16 n^3 / 3 (the kernel keeps both triangles and moves 2x that)."""
+    return 16.0 * n ** 3 / 3
 
 
 def update_flops(chi, sweeps, k, regime):
@@ -368,45 +389,62 @@ def run_chi(chi, G, steps, warmup, rank, world, dev, clocks=True):
         total_ms = max_over_ranks(total_ms, dev)
     ms_step = total_ms / steps
     regime = regime_of(n, n)
-    # ---- roofline of the dominant kernel: the Jacobi SVD. Its executed algorithmic flops per
-    # launch (one launch group per wave) / its CUDA-event time (sub-phase svd_jacobi when the
-    # planner times it, else the whole SVD phase, which then also holds the support kernels)
-    alg = float(sum(jacobi_flops(n, n, sw, regime) for sw in sweeps))
-    if phases["svd_jacobi"][1]:
-        kern, (kms, kn) = "svd_jacobi", phases["svd_jacobi"]
-        per_launch_alg = alg * steps / kn
-    else:
-        kern = "svd_small" if phases["svd_small"][1] else "svd_blocked"
-        kms, kn = phases[kern]
-        per_launch_alg = alg * steps / kn
-    kms_launch = kms / max(1, kn)
-    achieved = per_launch_alg / (kms_launch / 1e3) / 1e12
-    if regime == 1:
-        (peak, peak_src), bound = PEAKS["tf32"], "tensor"
-    else:
-        (peak, peak_src), bound = PEAKS["fp32"], "alu"
+    eig = regime == 1 and phases["svd_eig_tridiag"][1] > 0 and bool(np.all(sweeps == 0))
     traffic = None
     tj = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+    if eig:
+        # ---- the eigen route (reading 20): the dominant kernel is the Householder
+        # tridiagonalisation, bound by the traffic of the trailing matrix (algorithmic bytes per
+        # launch = one wave's gates x 16 n^3 / 3) over its CUDA-event time (sub-phase svd_eig_tridiag)
+        kern, (kms, kn) = "svd_eig_tridiag", phases["svd_eig_tridiag"]
+        kms_launch = kms / max(1, kn)
+        per_launch_bytes = G * tridiag_bytes(n) * steps / kn
+        achieved = per_launch_bytes / (kms_launch / 1e3) / 1e9
+        (peak, peak_src), bound, unit = PEAKS["hbm"], "hbm", "GB/s"
+        flops_note = ("algorithmic bytes per launch: gates x 16 n^3 / 3 (one-stage Householder tridiagonalisation, "
+                      "trailing Hermitian triangle read + written per step; the kernel keeps both triangles)")
+        total_flops = float(sum(eig_route_flops(n, n, k, 2, chi, 2 * chi, chi) for k in ks)
+                            + sum(8.0 * n * n * k for k in ks))
+    else:
+        # ---- roofline of the dominant kernel: the Jacobi SVD. Its executed algorithmic flops per
+        # launch (one launch group per wave) / its CUDA-event time (sub-phase svd_jacobi when the
+        # planner times it, else the whole SVD phase, which then also holds the support kernels)
+        alg = float(sum(jacobi_flops(n, n, sw, regime) for sw in sweeps))
+        if phases["svd_jacobi"][1]:
+            kern, (kms, kn) = "svd_jacobi", phases["svd_jacobi"]
+            per_launch_alg = alg * steps / kn
+        else:
+            kern = "svd_small" if phases["svd_small"][1] else "svd_blocked"
+            kms, kn = phases[kern]
+            per_launch_alg = alg * steps / kn
+        kms_launch = kms / max(1, kn)
+        achieved = per_launch_alg / (kms_launch / 1e3) / 1e12
+        if regime == 1:
+            (peak, peak_src), bound = PEAKS["tf32"], "tensor"
+        else:
+            (peak, peak_src), bound = PEAKS["fp32"], "alu"
+        unit = "TFLOP/s"
+        flops_note = ("executed algorithmic Jacobi flops per launch: sweeps x 20 rows n^2 (+12 n^3 with V); "
+                      "rows = n for the preconditioned V-less regimes (QR, large)")
+        total_flops = float(sum(update_flops(chi, sw, k, regime) for sw, k in zip(sweeps, ks)))
     if os.path.exists(tj):
         try:
             traffic = json.load(open(tj)).get("chi%d" % chi, {}).get(kern)
         except Exception:
             traffic = None
-    total_flops = float(sum(update_flops(chi, sw, k, regime) for sw, k in zip(sweeps, ks)))
     svd_phase_ms = (phases["svd_small"][0] + phases["svd_blocked"][0]) / steps
     rec = {
         "value": world * G / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "steps": steps, "warmup": warmup,
-        "count": G, "chi": chi, "theta": "%dx%d" % (n, n), "svd_regime": {0: "small", 1: "large (tcgen05)", 2: "medium",
-                                                                           3: "QR-preconditioned"}[regime],
+        "count": G, "chi": chi, "theta": "%dx%d" % (n, n),
+        "svd_regime": "large (FP64 Gram eigensolver)" if eig else {0: "small", 1: "large (tcgen05)", 2: "medium",
+                                                                    3: "QR-preconditioned"}[regime],
         "tflops_executed": total_flops / (ms_step / 1e3) / 1e12 * world,
         "sweeps_mean": float(sweeps.mean()), "k_mean": float(ks.mean()),
         "phase_ms_per_step": {p: v[0] / max(1, steps) for p, v in phases.items()},
         "svd_phase_ms_per_step": svd_phase_ms,
-        "roofline": {"bound": bound, "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": bound, "kernel": kern, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "launch_ms": kms_launch,
-                     "flops": "executed algorithmic Jacobi flops per launch: sweeps x 20 rows n^2 (+12 n^3 with V); "
-                              "rows = n for the preconditioned V-less regimes (QR, large)"},
+                     "launch_ms": kms_launch, "flops": flops_note},
         "gpu_launches": int(launches),
         "clocks": clk_rec,
     }

@@ -209,11 +209,20 @@ mps_status mps_last_sweeps(mps_t, int32_t g, int32_t* sweeps);
  * phase and accumulates device milliseconds: ms[0] contract, ms[1] SVD (small / medium / QR
  * regimes), ms[2] SVD (large regime), ms[3] select, ms[4] reabsorb (counts[p] = waves timed);
  * and sub-phases of the SVD (counts[p] = launch groups timed): ms[5] preconditioner (FP64 Gram +
- * Cholesky + B = L), ms[6] the Jacobi kernel, ms[7] spectrum (Rayleigh + polish + sort). A
- * sub-phase is timed for the regimes whose kernels are launched from the layer planner (the QR
- * regime and the fused large regime). mps_set_profiling resets the accumulators. */
+ * Cholesky + B = L), ms[6] the Jacobi kernel, ms[7] spectrum (Rayleigh + polish + sort); the
+ * eigen route (mps_set_svd_route): ms[8] its Householder tridiagonalisation kernel, ms[9] the rest
+ * of it (FP64 theta and Gram, bisection, spectrum, eigenvectors after the select). A sub-phase is
+ * timed for the regimes whose kernels are launched from the layer planner (the QR regime, the
+ * eigen route and the fused large regime). mps_set_profiling resets the accumulators. */
 mps_status mps_set_profiling(mps_t, int32_t on);
-mps_status mps_phase_times(mps_t, double* ms /* [8] */, int64_t* counts /* [8], may be NULL */);
+/* SVD route of the large regime (a2, "performing its SVD"; reading 20):
+ * route 0 (default) takes theta with 256 < n <= 2048 through the FP64 Gram eigensolver (sigma^2 =
+ * eigenvalues of theta^H theta, V for the kept columns by inverse iteration + back-transformation),
+ * falling back to the Jacobi route for spectra deeper than 3e-6 sigma_max; route 1 takes every large
+ * theta through the tcgen05 block Jacobi (+ the FP64 refinements). Applies from the next layer;
+ * MPS_E_STATE inside a layer, MPS_E_INVAL for another route. */
+mps_status mps_set_svd_route(mps_t, int32_t route);
+mps_status mps_phase_times(mps_t, double* ms /* [10] */, int64_t* counts /* [10], may be NULL */);
 mps_status mps_sync(mps_t);
 const char* mps_last_error(mps_t);
 const char* mps_status_string(mps_status);

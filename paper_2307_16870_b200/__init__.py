@@ -26,7 +26,7 @@ ABI_FUNCTIONS = [
     "mps_fidelity_estimate", "mps_amplitude", "mps_to_statevector", "mps_bond_dims",
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
     "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
-    "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
+    "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_set_svd_route", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
     "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1", "mps_canonicalize",
 ]
@@ -84,6 +84,7 @@ def lib():
             "mps_snapshot_load": [_P, _P, C.c_size_t],
             "mps_launch_count": [_P, _P],
             "mps_set_profiling": [_P, i32],
+            "mps_set_svd_route": [_P, i32],
             "mps_phase_times": [_P, _P, _P],
             "mps_last_sweeps": [_P, i32, _P],
             "mps_sync": [_P],
@@ -343,8 +344,12 @@ class MPS:
     def mps_set_profiling(self, on: bool = True):
         self._check(lib().mps_set_profiling(self._h, int(bool(on))))
 
+    def mps_set_svd_route(self, route: int):
+        """0: eigen route for large theta with 256 < n <= 2048 (default); 1: tcgen05 Jacobi route."""
+        self._check(lib().mps_set_svd_route(self._h, int(route)))
+
     PHASES = ("contract", "svd_small", "svd_blocked", "select", "reabsorb", "svd_precond", "svd_jacobi",
-              "svd_spectrum")
+              "svd_spectrum", "svd_eig_tridiag", "svd_eig_other")
 
     def mps_phase_times(self):
         ms = np.zeros(len(self.PHASES))

@@ -42,10 +42,12 @@ struct LayerJob {                  // the layer in flight (mps_layer_begin / mps
   size_t o_desc = 0, o_rec = 0, o_gpre = 0, o_apre = 0, o_rpre = 0, tail = 0;
   std::vector<int32_t> rsm;          // wave-local gates of the fused small reabsorb
   size_t o_rsm = 0, rsm_smem = 0;
+  std::vector<int32_t> eigl;         // wave-local gates of the eigen route (refine_large.cu)
+  size_t o_eigl = 0;
   bool ran[5] = {false, false, false, false, false};
 };
 
-constexpr int kPhases = 8;
+constexpr int kPhases = 10;
 
 // EAMPS_HOST_PROF=1: host-side time of the layer path (planning before the first launch, the
 // launch calls, the post-sync bookkeeping), printed by mps_destroy -- the GPU idles through the
@@ -83,6 +85,7 @@ struct mps_handle {
   size_t pinned_bytes[2] = {0, 0};
   // phase timers (mps_set_profiling): CUDA events recorded on the launch stream around each phase
   bool profiling = false;
+  bool jacobi_only = false;              // mps_set_svd_route(h, 1): no eigen route (A/B, tests)
   // [0] contract [1] svd_small (small / medium / QR regimes) [2] svd_blocked (large regime) [3] select
   // [4] reabsorb, and sub-phases of the SVD (spans, one per bucket launch group): [5] preconditioner
   // (FP64 Gram + Cholesky + B = L) [6] the Jacobi kernel itself [7] spectrum (Rayleigh + polish + sort)
@@ -382,8 +385,8 @@ mps_status wave_front_impl(mps_t h) {
   int g1 = g0;
   while (g1 < G) {
     const int cnt = g1 - g0 + 1;
-    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 3 * align_up(4 * cnt) +
-                align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64 + 4096);
+    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 4 * align_up(4 * cnt) +
+                align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64 + 24576);
     size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
     if (bump + r2 + fx + w2 + kAlign > top) break;
     fixed = fx;
@@ -411,11 +414,14 @@ mps_status wave_front_impl(mps_t h) {
   const size_t o_small = take(4 * Gw);
   const size_t o_large = take(4 * Gw);
   const size_t o_rsm = take(4 * Gw);
+  const size_t o_eigl = take(4 * Gw);
   const size_t o_us = take((size_t)Gw * d4 * 8);
   const size_t o_rec = take(sizeof(Record) * Gw);
-  const size_t o_scr = take(32 * (size_t)Gw + 64 + 4096);
+  const size_t o_scr = take(32 * (size_t)Gw + 64 + 24576);
   const size_t staged_bytes = o_rec - base;  // desc .. us are uploaded
   std::vector<int32_t> cpre(Gw + 1, 0), small, large;
+  std::vector<int32_t>& eigl = J.eigl;
+  eigl.clear();
   J.rsm.clear();
   J.rsm_smem = 0;
   J.rpre.assign(Gw + 1, 0);
@@ -455,7 +461,7 @@ mps_status wave_front_impl(mps_t h) {
         rpre[x + 1] = rpre[x] + p.rtiles;
         gpre[x + 1] = gpre[x] + p.gtiles;
         apre[x + 1] = apre[x] + p.atiles;
-        if (gd.regime == 1) large.push_back(x);
+        if (gd.regime == 1) (gd.eig ? eigl : large).push_back(x);
         if (!J.rsm.empty() && J.rsm.back() == x - 1) J.rsm.push_back(x);   // same shape as gate x - 1
         continue;
       }
@@ -484,7 +490,7 @@ mps_status wave_front_impl(mps_t h) {
     rpre[x + 1] = rpre[x] + p.rtiles;
     gpre[x + 1] = gpre[x] + p.gtiles;
     apre[x + 1] = apre[x] + p.atiles;
-    if (gd.regime == 1) large.push_back(x);
+    if (gd.regime == 1) (gd.eig ? eigl : large).push_back(x);
     if (reabsorb_small_fits(gd.m, gd.n)) {
       J.rsm.push_back(x);
       J.rsm_smem = std::max(J.rsm_smem, reabsorb_small_smem(gd.m, gd.n));
@@ -593,7 +599,7 @@ mps_status wave_front_impl(mps_t h) {
   }
   // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
   const size_t tail = align_up(staged_bytes, 64);  // 3 small pinned slots after the staged block
-  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256, 1));
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, tail + 256 + 4 * (size_t)Gw, 1));   // + eigen-route fallback flags
   if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
   J.tail = tail;
   std::memcpy(hb + (o_desc - base), hd.data(), sizeof(GateDesc) * Gw);
@@ -603,6 +609,8 @@ mps_status wave_front_impl(mps_t h) {
   std::memcpy(hb + (o_apre - base), apre.data(), 4 * (Gw + 1));
   if (!small.empty()) std::memcpy(hb + (o_small - base), small.data(), 4 * small.size());
   if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
+  if (!eigl.empty()) std::memcpy(hb + (o_eigl - base), eigl.data(), 4 * eigl.size());
+  J.o_eigl = o_eigl;
   if (!J.rsm.empty()) std::memcpy(hb + (o_rsm - base), J.rsm.data(), 4 * J.rsm.size());
   J.o_rsm = o_rsm;
   for (int x = 0; x < Gw; ++x)
@@ -673,6 +681,38 @@ mps_status wave_front_impl(mps_t h) {
     CKL("svd_small/medium");
   }
   if (prof) CK(cudaEventRecord(h->ev[2], h->s));
+  // a2 + a3, the eigen route (large regime, 256 < n <= 2048): sigma^2 = eigenvalues of the FP64 Gram
+  // of the FP64-recontracted theta (refine_large.cu); a spectrum too deep for it (flag read back
+  // here) goes to the Jacobi route below
+  if (!eigl.empty()) {
+    const int32_t* d_eigl = reinterpret_cast<const int32_t*>(h->slab + o_eigl);
+    int32_t* fbd = reinterpret_cast<int32_t*>(h->slab + o_scr) + 4 * Gw + 5000;   // after the refine lists and barrier lines
+    const int e0 = prof ? prof_mark(h) : -1;
+    RlgMarks mk{[](void* c) { return prof_mark(static_cast<mps_t>(c)); }, h, {-1, -1}};
+    h->launches += launch_eig_front(d_desc, hd.data(), eigl.data(), d_eigl, (int)eigl.size(), h->slab, h->dst, d_us, d,
+                                    reinterpret_cast<int32_t*>(h->slab + o_scr) + Gw + 2, fbd, h->s, prof ? &mk : nullptr);
+    CKL("eig_front");
+    if (prof && mk.at[0] >= 0) {   // [8] the tridiagonalisation, [9] the rest of the eigen route
+      const int e1 = prof_mark(h);
+      prof_span(h, 9, e0, mk.at[0]);
+      prof_span(h, 8, mk.at[0], mk.at[1]);
+      prof_span(h, 9, mk.at[1], e1);
+    }
+    int32_t* fbh = reinterpret_cast<int32_t*>(hb + tail + 256);
+    CK(cudaMemcpyAsync(fbh, fbd, 4 * eigl.size(), cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    bool moved = false;
+    for (size_t c = 0; c < eigl.size(); ++c)
+      if (fbh[c]) {
+        hd[eigl[c]].eig = 0;
+        large.push_back(eigl[c]);
+        moved = true;
+      }
+    if (moved) {
+      std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
+      CK(h2d_small(h, h->slab + o_large, hb + (o_large - base), 4 * large.size()));
+    }
+  }
   // a2 + a3 SVD, large regime: blocked Jacobi
   if (!large.empty()) {
     int err = 0;
@@ -729,6 +769,15 @@ mps_status wave_back(mps_t h) {
   launch_select(d_desc, Gw, h->slab, h->dst, d_rec, par, h->s);
   h->launches += 2;
   CKL("select");
+  // the eigen route's right singular vectors, for the kept k only
+  if (!J.eigl.empty()) {
+    const int e0 = prof ? prof_mark(h) : -1;
+    h->launches += launch_eig_vectors(d_desc, hd.data(), J.eigl.data(),
+                                      reinterpret_cast<const int32_t*>(h->slab + J.o_eigl), (int)J.eigl.size(),
+                                      h->slab, h->s);
+    CKL("eig_vectors");
+    if (prof) prof_span(h, 9, e0, prof_mark(h));
+  }
   if (prof) CK(cudaEventRecord(h->ev[4], h->s));
   // a5 reabsorb
   h->launches += launch_reabsorb(d_desc, d_gpre, J.gpre[Gw], d_apre, J.apre[Gw], d_rpre, J.rpre[Gw], Gw, h->slab, h->s);
@@ -941,6 +990,13 @@ mps_status mps_set_profiling(mps_t h, int32_t on) {
   return MPS_OK;
 }
 
+mps_status mps_set_svd_route(mps_t h, int32_t route) {
+  if (!h || route < 0 || route > 1) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "mps_set_svd_route inside a layer");
+  h->jacobi_only = route == 1;
+  return MPS_OK;
+}
+
 mps_status mps_phase_times(mps_t h, double* ms, int64_t* counts) {
   if (!h || !ms) return MPS_E_INVAL;
   for (int p = 0; p < kPhases; ++p) {
@@ -1096,6 +1152,8 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // the in-CTA Householder QR instead)
     static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
     if (gd.regime == 3 && !qr_hh) gd.jrows = gd.n;
+    // large regime, 256 < n <= 2048: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps)
+    gd.eig = (!h->jacobi_only && eig_route(gd)) ? 1 : 0;
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                         : gd.regime == 1 ? large_scratch_bytes(gd)
                         : (gd.regime == 3 && gd.jrows > 0) ? large_precond_scratch(gd.n)

@@ -70,6 +70,7 @@ struct GateDesc {
   int64_t ws_E;                     // Newton-Schulz correction E (k x k) of the kept V columns
   int64_t ws_log;                   // medium: rotation log, log_sweeps x (n-1) x n/2 float4 (c, s, e); large: TC scratch
   int32_t log_sweeps;
+  int32_t eig, eig_pad;             // 1: the eigen route (refine_large.cu: FP64 Gram eigensolver, no Jacobi)
   int32_t jrows;                    // large regime: 0 = Jacobi on theta (m rows) with V accumulated;
                                     // > 0 = preconditioned, Jacobi on B = L (jrows = n rows), no V
   int32_t u_index, sweeps;          // gate matrix index in the staged array; sweeps used
@@ -169,8 +170,21 @@ int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* s
                   int32_t* d_list /* G + 1 ints */, cudaStream_t s);
 // FP64 eigenvalues of the Gram of the FP64-recontracted theta for deep large-regime gates with
 // 256 < n <= 2048 (refine_large.cu). cand = the wave's large-regime gates (host and device copies);
-// iscr: wave scratch of 2 nc + 2 ints + 2176 bytes (barrier lines). Returns launches issued.
+// iscr: wave scratch of 2 nc + 2 ints + 19 KB (barrier lines). Returns launches issued.
 bool refine_large_candidate(const GateDesc& gd);
+bool eig_route(const GateDesc& gd);
+// profiling hook: mark(ctx) records an event on the stream and returns its id (or -1); the front
+// stores the ids taken just before and after the tridiagonalisation kernel in at[0], at[1]
+struct RlgMarks {
+  int (*mark)(void*);
+  void* ctx;
+  mutable int at[2];
+};
+int launch_eig_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                     uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, int32_t* fb,
+                     cudaStream_t s, const RlgMarks* mk);
+int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                       uint8_t* slab, cudaStream_t s);
 size_t refine_large_scratch(int m, int n);
 int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
                         uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s);

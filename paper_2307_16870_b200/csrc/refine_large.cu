@@ -53,7 +53,7 @@ constexpr int kMinN = 257, kMaxN = 2048;
 constexpr double kRatio = 2e-5;
 constexpr int TT = 512;          // tridiagonalisation threads per CTA
 constexpr int BT = 128;          // bisection threads per CTA
-constexpr int kMaxGroups = 16, kDefaultGroups = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
+constexpr int kMaxGroups = 148, kDefaultGroups = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -63,8 +63,9 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) b
 }
 
 struct RlgLayout {               // per-gate scratch at ws_log (the large regime's dead TC / Gram scratch)
-  int64_t g, th, d, e, eig, p, part;
+  int64_t g, th, d, e, eig, tau, p, part, y, slot;
 };
+constexpr int kSlots = 128;      // inverse-iteration factor slots per gate (vectors in flight)
 __host__ __device__ inline RlgLayout rlg_layout(const GateDesc& gd) {
   RlgLayout L;
   const int64_t n = gd.n, m = gd.m;
@@ -73,28 +74,35 @@ __host__ __device__ inline RlgLayout rlg_layout(const GateDesc& gd) {
   L.d = L.th + 16 * m * n;
   L.e = L.d + 8 * n;
   L.eig = L.e + 8 * n;
-  L.p = L.eig + 8 * n;                 // 2 x n double2 (by step parity)
+  L.tau = L.eig + 8 * n;               // n double2: Householder tau_k
+  L.p = L.tau + 16 * n;                // 2 x n double2 (by step parity)
   L.part = L.p + 32 * n;               // 2 x 1024 double2 (by step parity)
+  L.y = L.part + 32 * 1024;            // n x n doubles: eigenvectors of T (row j = vector j)
+  L.slot = L.y + 8 * n * n;            // kSlots x n x (double4 factors + 1 pivot byte)
   return L;
 }
 
 // ---- trigger --------------------------------------------------------------------------------
 // cand[0..nc): wave-local gate indices (large regime, n in range); flag[c] = 1 if the gate is deep;
 // list[0] = count, list[1..] = wave-local gate indices.
+// mode 0 (refinement of a Jacobi spectrum): large-regime gates of the Jacobi route in range whose
+// spectrum is deep; mode 1 (eigen route): every gate marked eig.
 __global__ void k_rlg_pick(const GateDesc* __restrict__ desc, const uint8_t* slab, const int32_t* __restrict__ cand,
-                           int nc, int32_t* flag, int32_t* list) {
+                           int nc, int32_t* flag, int32_t* list, int mode) {
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= nc) return;
   const GateDesc& gd = desc[cand[c]];
   const int n = gd.n;
   const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);   // sorted descending
-  const double smax = gS[0];
+  const double smax = mode == 0 ? gS[0] : 0.0;
   double deep = smax;
-  for (int j = lane; j < n; j += 32)
+  for (int j = lane; mode == 0 && j < n; j += 32)
     if (gS[j] >= 1e-12 * smax) deep = fmin(deep, gS[j]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) deep = fmin(deep, __shfl_xor_sync(0xffffffffu, deep, o));
-  const int on = gd.regime == 1 && n >= kMinN && n <= kMaxN && smax > 0.0 && deep < kRatio * kRatio * smax;
+  const int on = mode == 1 ? gd.eig != 0
+                            : (gd.regime == 1 && !gd.eig && n >= kMinN && n <= kMaxN && smax > 0.0 &&
+                               deep < kRatio * kRatio * smax);
   if (lane == 0) {
     flag[c] = on;
     if (on) list[1 + atomicAdd(&list[0], 1)] = cand[c];
@@ -325,6 +333,7 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
     double* eg = reinterpret_cast<double*>(slab + L.e);
     double2* pg = reinterpret_cast<double2*>(slab + L.p);
     double2* partg = reinterpret_cast<double2*>(slab + L.part);
+    double2* taug = reinterpret_cast<double2*>(slab + L.tau);
     double2* vbuf[2] = {reinterpret_cast<double2*>(sm), reinterpret_cast<double2*>(sm) + n};
     double2* w = reinterpret_cast<double2*>(sm) + 2 * n;                 // w of step k-1
     double* red = reinterpret_cast<double*>(w + n);                     // 32 doubles
@@ -415,6 +424,12 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
       const double dim = cta_sum(lane == 0 ? pdot.y : 0.0, red);
       if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], make_double2(dre, dim));
       rlg_barrier(ctr, nb, cpg);
+      // the reflector H_k = I - tau_k v_k v_k^H is kept for the eigenvectors (z = H_0 .. H_{n-2} y):
+      // v_k in row k's dead columns k+1 .. n-1 (every CTA has read row k by now), tau_k in taug
+      if (lcta == 0) {
+        for (int j = k + 1 + tid; j < n; j += TT) __stcg(&A[(int64_t)k * n + j], v[j]);
+        if (tid == 0) taug[k] = tau;
+      }
       // (3) w = p + alpha v, alpha = -1/2 tau (p^H v)   (zhetd2; p already carries tau). The group's
       // partials summed by warp 0 in a fixed order (identical in every CTA of the group)
       if (warp == 0) {
@@ -537,43 +552,281 @@ __global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ 
   if (act && sub == 0) eig[j] = 0.5 * (lo + hi);   // ascending
 }
 
-// ---- sigma^2 (descending) + tails ---------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_rlg_finish(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
-                                                    const int32_t* __restrict__ flag, uint8_t* slab) {
-  if (!flag[blockIdx.x]) return;
-  const GateDesc gd = desc[cand[blockIdx.x]];
+// ---- sigma^2 (descending) + tails; mode 1 (eigen route): pi = identity (column j of V will be the
+// eigenvector of the j-th largest eigenvalue) and the depth check: a spectrum reaching below
+// kEigMin sigma_max (sigma >= 1e-6 sigma_max) leaves the eigen route (desc.eig = 0, fb[c] = 1) for the
+// Jacobi route + refinements, whose relative accuracy does not degrade as 1 / sigma^2 -------------
+constexpr double kEigMin = 3e-6;
+__global__ void __launch_bounds__(256) k_rlg_finish(GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                    const int32_t* __restrict__ flag, uint8_t* slab, int mode,
+                                                    int32_t* fb) {
+  if (!flag[blockIdx.x]) {
+    if (mode == 1 && threadIdx.x == 0) fb[blockIdx.x] = 0;
+    return;
+  }
+  GateDesc& gdr = desc[cand[blockIdx.x]];
+  const GateDesc gd = gdr;
   const int n = gd.n;
   const RlgLayout L = rlg_layout(gd);
   const double* eig = reinterpret_cast<const double*>(slab + L.eig);
   __shared__ double keys[kMaxN];
   __shared__ double part[256];
+  __shared__ int s_deep;
   double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  int32_t* gP = reinterpret_cast<int32_t*>(slab + gd.ws_pi);
+  if (threadIdx.x == 0) s_deep = 0;
+  __syncthreads();
+  const double smax = fmax(eig[n - 1], 0.0);
   for (int j = threadIdx.x; j < n; j += 256) {
     const double v = fmax(eig[n - 1 - j], 0.0);
     keys[j] = v;
     gS[j] = v;
+    if (mode == 1) {
+      gP[j] = j;
+      if (v >= 1e-12 * smax && v < kEigMin * kEigMin * smax) s_deep = 1;
+    }
   }
   __syncthreads();
   cta_tails(keys, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
+  if (mode == 1 && threadIdx.x == 0) {
+    fb[blockIdx.x] = s_deep;
+    if (s_deep) gdr.eig = 0;
+    gdr.sweeps = 0;
+  }
+}
+
+// ---- eigenvectors of T for the kept columns (eigen route, after the select: k = desc.k) ----------
+// Inverse iteration: T - lambda_j I = P L U (Gaussian elimination with partial pivoting, LAPACK
+// dgttrf), two solves from a fixed pseudo-random start, unit 2-norm. lambda_j is the bisection value
+// (accurate to a few ulps of ||T||), so y_j is accurate to ~eps64 ||T|| / gap_j in angle. One thread
+// per vector, kSlots factor slots per gate; row j of Y = y_j.
+__global__ void __launch_bounds__(32) k_rlg_invit(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                  uint8_t* slab) {
+  const GateDesc& gd = desc[cand[blockIdx.y]];
+  if (!gd.eig) return;
+  const int n = gd.n, k = gd.k;
+  const int slot = blockIdx.x * 32 + threadIdx.x;
+  if (slot >= k) return;
+  const RlgLayout L = rlg_layout(gd);
+  const double* __restrict__ dg = reinterpret_cast<const double*>(slab + L.d);
+  const double* __restrict__ eg = reinterpret_cast<const double*>(slab + L.e);
+  const double* __restrict__ eig = reinterpret_cast<const double*>(slab + L.eig);
+  double4* F = reinterpret_cast<double4*>(slab + L.slot) + (int64_t)slot * n;     // (dl, d, du, du2)
+  uint8_t* piv = reinterpret_cast<uint8_t*>(slab + L.slot + (int64_t)kSlots * n * 32) + (int64_t)slot * n;
+  double tnorm = 0.0;
+  for (int i = 0; i < n; ++i)
+    tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i < n - 1 ? fabs(eg[i]) : 0.0));
+  const double tiny = fmax(tnorm, 1e-300) * 2.220446049250313e-16;
+  for (int j = slot; j < k; j += kSlots) {
+    const double lam = eig[n - 1 - j];
+    double* y = reinterpret_cast<double*>(slab + L.y) + (int64_t)j * n;
+    // factor (dgttrf)
+    double dcur = dg[0] - lam, ducur = n > 1 ? eg[0] : 0.0;
+    for (int i = 0; i < n - 1; ++i) {
+      const double dl = eg[i], dn = dg[i + 1] - lam, dun = i + 1 < n - 1 ? eg[i + 1] : 0.0;
+      double4 f;
+      if (fabs(dcur) >= fabs(dl)) {
+        const double d0 = dcur != 0.0 ? dcur : tiny;
+        const double fact = dl / d0;
+        f = make_double4(fact, d0, ducur, 0.0);
+        piv[i] = 0;
+        dcur = dn - fact * ducur;
+        ducur = dun;
+      } else {
+        const double fact = dcur / dl;
+        f = make_double4(fact, dl, dn, dun);        // row swap: U row i = (dl, dn, dun)
+        piv[i] = 1;
+        dcur = ducur - fact * dn;
+        ducur = -fact * dun;
+      }
+      F[i] = f;
+    }
+    F[n - 1] = make_double4(0.0, dcur != 0.0 ? (fabs(dcur) < tiny ? copysign(tiny, dcur) : dcur) : tiny, 0.0, 0.0);
+    for (int i = 0; i < n - 1; ++i)   // tiny pivots: perturb (the vector direction is what matters)
+      if (fabs(F[i].y) < tiny) F[i].y = copysign(tiny, F[i].y);
+    // start vector: fixed pseudo-random in [0.5, 1.5)
+    for (int i = 0; i < n; ++i) {
+      unsigned int h = (unsigned int)i * 2654435761u ^ ((unsigned int)j * 40503u + 0x9e3779b9u);
+      h ^= h >> 15;
+      h *= 2246822519u;
+      h ^= h >> 13;
+      y[i] = 0.5 + (double)(h & 0xffffu) / 65536.0;
+    }
+    for (int it = 0; it < 2; ++it) {
+      // L: forward with the row interchanges
+      for (int i = 0; i < n - 1; ++i) {
+        const double fact = F[i].x;
+        if (piv[i] == 0) {
+          y[i + 1] -= fact * y[i];
+        } else {
+          const double t = y[i];
+          y[i] = y[i + 1];
+          y[i + 1] = t - fact * y[i];
+        }
+      }
+      // U: back substitution (diag d, super du, second super du2)
+      double nrm = 0.0;
+      for (int i = n - 1; i >= 0; --i) {
+        const double4 f = F[i];
+        double v = y[i];
+        if (i + 1 < n) v -= f.z * y[i + 1];
+        if (i + 2 < n) v -= f.w * y[i + 2];
+        v /= f.y;
+        y[i] = v;
+        nrm = fma(v, v, nrm);
+      }
+      const double sc = 1.0 / sqrt(nrm);
+      for (int i = 0; i < n; ++i) y[i] *= sc;
+    }
+  }
+}
+
+// Clusters of (numerically) degenerate eigenvalues among the kept ones: inverse iteration from
+// different starts returns independent vectors of the cluster's invariant subspace; modified
+// Gram-Schmidt makes them orthonormal. One CTA per gate (most gates have no cluster).
+__global__ void __launch_bounds__(256) k_rlg_mgs(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                 uint8_t* slab) {
+  const GateDesc& gd = desc[cand[blockIdx.x]];
+  if (!gd.eig) return;
+  const int n = gd.n, k = gd.k;
+  const RlgLayout L = rlg_layout(gd);
+  const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);
+  double* Y = reinterpret_cast<double*>(slab + L.y);
+  __shared__ double red[8];
+  const double gap = 1e-9 * gS[0];
+  int c0 = 0;
+  for (int j = 1; j < k; ++j) {
+    if (gS[j - 1] - gS[j] > gap) {
+      c0 = j;
+      continue;
+    }
+    double* yj = Y + (int64_t)j * n;
+    for (int l = c0; l < j; ++l) {
+      const double* yl = Y + (int64_t)l * n;
+      double s = 0.0;
+      for (int i = threadIdx.x; i < n; i += 256) s = fma(yl[i], yj[i], s);
+      const double dot = cta_sum(s, red);
+      for (int i = threadIdx.x; i < n; i += 256) yj[i] -= dot * yl[i];
+      __syncthreads();
+    }
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) s = fma(yj[i], yj[i], s);
+    const double sc = 1.0 / sqrt(cta_sum(s, red));
+    for (int i = threadIdx.x; i < n; i += 256) yj[i] *= sc;
+    __syncthreads();
+  }
+}
+
+// Back-transformation z_j = Q y_j = H_0 (H_1 ( .. H_{n-2} y_j)), H_q = I - tau_q v_q v_q^H (v_q in
+// row q of the factorised G, entries q+1 .. n-1), then V[:, j] = z_j in FP32 (unit norm: Q unitary).
+// kVpc vectors per CTA in shared memory; each thread owns the same rows of every vector, so only the
+// dot products v_q^H z need the CTA (one barrier per reflector, double-buffered partials).
+constexpr int kVpc = 4;
+__global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                    uint8_t* slab) {
+  const GateDesc& gd = desc[cand[blockIdx.y]];
+  if (!gd.eig) return;
+  const int n = gd.n, k = gd.k, np = gd.n_pad;
+  const int j0 = blockIdx.x * kVpc;
+  if (j0 >= k) return;
+  const int nv = min(kVpc, k - j0);
+  const RlgLayout L = rlg_layout(gd);
+  const double2* __restrict__ A = reinterpret_cast<const double2*>(slab + L.g);
+  const double2* __restrict__ taug = reinterpret_cast<const double2*>(slab + L.tau);
+  const double* __restrict__ Y = reinterpret_cast<const double*>(slab + L.y);
+  extern __shared__ __align__(16) uint8_t sm[];
+  double2* z = reinterpret_cast<double2*>(sm);                     // [kVpc][n]
+  __shared__ double2 red[2][8][kVpc];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int q = 0; q < kVpc; ++q)
+    for (int i = tid; i < n; i += 256)
+      z[q * n + i] = make_double2(q < nv ? Y[(int64_t)(j0 + q) * n + i] : 0.0, 0.0);
+  for (int r = n - 2; r >= 0; --r) {
+    const double2* vr = A + (int64_t)r * n;
+    double2 acc[kVpc];
+#pragma unroll
+    for (int q = 0; q < kVpc; ++q) acc[q] = make_double2(0.0, 0.0);
+    // rows i > r with i = tid (mod 256): every thread keeps the same rows of z for all r, so the
+    // update below and the next dot product need no barrier between them
+    int i0 = tid;
+    if (i0 <= r) i0 += ((r - tid) / 256 + 1) * 256;
+    for (int i = i0; i < n; i += 256) {
+      const double2 vi = vr[i];
+#pragma unroll
+      for (int q = 0; q < kVpc; ++q) {
+        const double2 c = cmulc(vi, z[q * n + i]);
+        acc[q].x += c.x;
+        acc[q].y += c.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kVpc; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+      }
+    const int b = r & 1;
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < kVpc; ++q) red[b][warp][q] = acc[q];
+    __syncthreads();
+    const double2 tau = taug[r];
+    double2 f[kVpc];
+#pragma unroll
+    for (int q = 0; q < kVpc; ++q) {
+      double2 sdot = make_double2(0.0, 0.0);
+      for (int w = 0; w < 8; ++w) {
+        sdot.x += red[b][w][q].x;
+        sdot.y += red[b][w][q].y;
+      }
+      f[q] = cmul(tau, sdot);
+    }
+    for (int i = i0; i < n; i += 256) {
+      const double2 vi = vr[i];
+#pragma unroll
+      for (int q = 0; q < kVpc; ++q) {
+        const double2 t = cmul(f[q], vi);
+        z[q * n + i].x -= t.x;
+        z[q * n + i].y -= t.y;
+      }
+    }
+  }
+  __syncthreads();
+  float2* V = reinterpret_cast<float2*>(slab + gd.ws_V);
+  for (int q = 0; q < nv; ++q)
+    for (int i = tid; i < np; i += 256) {
+      const double2 v = i < n ? z[q * n + i] : make_double2(0.0, 0.0);
+      V[(int64_t)(j0 + q) * np + i] = make_float2((float)v.x, (float)v.y);
+    }
 }
 
 }  // namespace
 
 bool refine_large_candidate(const GateDesc& gd) { return gd.regime == 1 && gd.n >= kMinN && gd.n <= kMaxN; }
 
-size_t refine_large_scratch(int m, int n) {
-  return (size_t)16 * n * n + (size_t)16 * m * n + (size_t)56 * n + 32 * 1024 + 256;
+// The eigen route (EAMPS_NO_EIG=1: every large gate takes the tcgen05 Jacobi route, the FP64 Gram
+// eigenvalues only refine deep spectra -- the A/B reference).
+bool eig_route(const GateDesc& gd) {
+  static const bool off = getenv("EAMPS_NO_EIG") != nullptr;
+  return !off && refine_large_candidate(gd);
 }
 
-// cand: device copy of the wave-local candidate gates (nc, max n / tiles from the host copy);
-// iscr: wave scratch: flags (nc ints), list (nc + 1 ints), then kMaxGroups 128-byte barrier lines.
-int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
-                        uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s) {
+size_t refine_large_scratch(int m, int n) {
+  return (size_t)16 * n * n + (size_t)16 * m * n + (size_t)56 * n + 32 * 1024 + (size_t)8 * n * n +
+         (size_t)kSlots * n * 33 + 512;
+}
+
+namespace {
+// mode 0: refinement of deep Jacobi spectra; mode 1: the eigen route's spectrum (fb: fallback flags).
+int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+              uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, int mode, int32_t* fb,
+              cudaStream_t s, const RlgMarks* mk) {
   if (nc <= 0) return 0;
   int max_tiles = 0, max_gram = 0, max_n = 0;
   for (int c = 0; c < nc; ++c) {
     const GateDesc& g = h_desc[h_cand[c]];
-    if (!refine_large_candidate(g)) continue;
+    if (!refine_large_candidate(g) || (mode == 1 && !g.eig)) continue;
     const int T = 64 / d;
     max_tiles = std::max(max_tiles, ((g.l + T - 1) / T) * ((g.r + T - 1) / T));
     const int nt = (g.n + 63) / 64;
@@ -588,7 +841,7 @@ int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t*
       (reinterpret_cast<uintptr_t>(iscr + 2 * nc + 2) + 127) & ~uintptr_t(127));
   cudaMemsetAsync(list, 0, sizeof(int32_t), s);
   cudaMemsetAsync(ctr, 0, 128 * kMaxGroups, s);
-  k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list);
+  k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list, mode);
   static std::atomic<unsigned long long> attr{0};
   const size_t tsm = tridiag_smem(kMaxN);
   if (first_on_device(attr)) {
@@ -596,6 +849,7 @@ int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t*
     cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    cudaFuncSetAttribute(k_rlg_backtr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kVpc * kMaxN * 16));
   }
   if (d == 2)
     k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
@@ -619,10 +873,43 @@ int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t*
   unsigned int* a_ctr = ctr;
   int a_cpg = cpg;
   void* args[] = {&a_desc, &a_list, &a_slab, &a_ctr, &a_cpg};
+  if (mk) mk->at[0] = mk->mark(mk->ctx);
   cudaLaunchCooperativeKernel((const void*)k_rlg_tridiag, dim3(grid), dim3(TT), args, tsm, s);
+  if (mk) mk->at[1] = mk->mark(mk->ctx);
   k_rlg_bisect<<<dim3((max_n + kBisPerCta - 1) / kBisPerCta, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
-  k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab);
+  k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab, mode, fb);
   return 6;
+}
+}  // namespace
+
+// cand: device copy of the wave-local candidate gates (nc, max n / tiles from the host copy);
+// iscr: wave scratch: flags (nc ints), list (nc + 1 ints), then kMaxGroups 128-byte barrier lines.
+int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                        uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s) {
+  return rlg_front(d_desc, h_desc, h_cand, d_cand, nc, slab, st, d_us, d, iscr, 0, nullptr, s, nullptr);
+}
+
+// The eigen route's front (a2 + a3 for the gates marked eig): theta64, G, T, eigenvalues, sorted
+// sigma^2 and tails, pi = identity; fb[c] = 1 where the spectrum is too deep for it (the gate is
+// unmarked on the device and must take the Jacobi route).
+int launch_eig_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                     uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, int32_t* fb,
+                     cudaStream_t s, const RlgMarks* mk) {
+  return rlg_front(d_desc, h_desc, h_cand, d_cand, nc, slab, st, d_us, d, iscr, 1, fb, s, mk);
+}
+
+// The eigen route's right singular vectors for the kept k (after the select): inverse iteration
+// on T, cluster MGS, back-transformation into V (FP32, columns 0 .. k-1).
+int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
+                       uint8_t* slab, cudaStream_t s) {
+  int max_n = 0;
+  for (int c = 0; c < nc; ++c)
+    if (h_desc[h_cand[c]].eig) max_n = std::max(max_n, h_desc[h_cand[c]].n);
+  if (max_n == 0) return 0;
+  k_rlg_invit<<<dim3(kSlots / 32, nc), 32, 0, s>>>(d_desc, d_cand, slab);
+  k_rlg_mgs<<<nc, 256, 0, s>>>(d_desc, d_cand, slab);
+  k_rlg_backtr<<<dim3((max_n + kVpc - 1) / kVpc, nc), 256, (size_t)kVpc * max_n * 16, s>>>(d_desc, d_cand, slab);
+  return 3;
 }
 
 }  // namespace eamps

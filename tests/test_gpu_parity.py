@@ -131,11 +131,12 @@ def test_exact_mode_statevector_vs_dense():
     assert abs(np.linalg.norm(sg) - 1) < 1e-4
 
 
-def _micro(chi, count, t=0.9999, rule="pure"):
+def _micro(chi, count, t=0.9999, rule="pure", route=0):
     pk = _pk()
     tensors, gates = workloads.micro_chain(chi, count)
     N = 2 * count
     gpu = pk.MPS(N, strategy="fixed", f_fixed=t, rule=rule, slab_bytes=max(256 << 20, 40 * count * (2 * chi) ** 2 * 8))
+    gpu.mps_set_svd_route(route)
     gpu.mps_import_sites(0, tensors)
     orc = oracle.OracleMPS(N, strategy="fixed", f_fixed=t, rule=rule)
     for i, B in enumerate(tensors):
@@ -162,16 +163,48 @@ def test_config2_chi256_blocked_path_parity():
     assert worst < SIG_RTOL, worst
 
 
-@pytest.mark.parametrize("chi,count", [(128, 2), (512, 1)])
+@pytest.mark.parametrize("chi,count", [(128, 2), (256, 2), (512, 1)])
 def test_config2_tensor_core_path_parity(chi, count):
-    """the tcgen05 3xTF32 block Jacobi + FP64-anchored polish (large regime, chi >= 128 in config 2)
-    at the strict bar: relative 1e-5 on every sigma >= 1e-6 sigma_max (sigma_min / sigma_max =
-    (2 chi)^-1.5 = 3e-5 at chi = 512), identical kept ranks, f to 1e-6."""
-    gpu, orc, G = _micro(chi, count)
+    """the tcgen05 3xTF32 block Jacobi + FP64-anchored polish (large regime, chi >= 128 in config 2;
+    route 1 = the Jacobi route also for 256 < n <= 2048) at the strict bar: relative 1e-5 on every
+    sigma >= 1e-6 sigma_max (sigma_min / sigma_max = (2 chi)^-1.5 = 3e-5 at chi = 512), identical
+    kept ranks, f to 1e-6."""
+    gpu, orc, G = _micro(chi, count, route=1)
     worst, same = compare_layer(gpu, orc, G)
     assert same
     assert worst < SIG_RTOL, worst
     assert all(gpu.mps_last_sweeps(g) > 0 for g in range(G))
+
+
+def _two_site(L, R):
+    """sum_j L[:, :, j] R[j, :, :] as a (l d) x (d r) matrix (B_i' = Gamma_i lambda_i carries the
+    Schmidt values): gauge-invariant -- a phase or, for degenerate lambda, a unitary mixing of the
+    bond index cancels between L and R."""
+    L, R = L.astype(np.complex128), R.astype(np.complex128)
+    k = L.shape[2]
+    return L.reshape(-1, k) @ R.reshape(k, -1)
+
+
+@pytest.mark.parametrize("chi,count", [(256, 2), (512, 1)])
+def test_config2_eigen_route_parity(chi, count):
+    """the eigen route (default for 256 < n <= 2048, refine_large.cu): sigma^2 = FP64 eigenvalues of
+    the Gram of the FP64-recontracted theta, the kept right singular vectors by inverse iteration +
+    back-transformation. Strict bar on sigma, ranks and f; the reabsorbed two-site tensor
+    B_i' diag(lambda) B_{i+1}' (gauge-invariant) equals the oracle's to 1e-5 relative, and the new
+    right factor is right-normalised."""
+    gpu, orc, G = _micro(chi, count, route=0)
+    worst, same = compare_layer(gpu, orc, G)
+    assert same
+    assert worst < SIG_RTOL, worst
+    assert all(gpu.mps_last_sweeps(g) == 0 for g in range(G))     # no Jacobi sweeps: the eigen route
+    for g in range(G):
+        Mg = _two_site(gpu.mps_export_site(2 * g), gpu.mps_export_site(2 * g + 1))
+        Mo = _two_site(orc.export_site(2 * g), orc.export_site(2 * g + 1))
+        rel = np.linalg.norm(Mg - Mo) / np.linalg.norm(Mo)
+        assert rel < 1e-5, (g, rel)
+        R = gpu.mps_export_site(2 * g + 1).astype(np.complex128)
+        Rm = R.reshape(R.shape[0], -1)
+        assert np.abs(Rm @ Rm.conj().T - np.eye(R.shape[0])).max() < 1e-5
 
 
 def test_hastings_update_keeps_state():
