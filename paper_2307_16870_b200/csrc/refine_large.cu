@@ -53,7 +53,8 @@ constexpr int kMinN = 257, kMaxN = 2048;
 constexpr double kRatio = 2e-5;
 constexpr int TT = 512;          // tridiagonalisation threads per CTA
 constexpr int BT = 128;          // bisection threads per CTA
-constexpr int kMaxGroups = 148, kDefaultGroups = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
+constexpr int kMaxGroups = 148, kDefaultGroups = 8;
+constexpr int kRowUnroll = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -296,6 +297,25 @@ __device__ __forceinline__ void rlg_barrier(unsigned int* ctr, unsigned int& nb,
   __syncthreads();
 }
 
+// CTA-wide sum of one double2 per thread (deterministic order; identical in every CTA).
+__device__ __forceinline__ double2 cta_sum2(double2 v, double2* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  for (int i = 0; i < nw; ++i) {
+    s.x += red[i].x;
+    s.y += red[i].y;
+  }
+  return s;
+}
+
 // CTA-wide sum of one double per thread (deterministic order; identical in every CTA).
 __device__ __forceinline__ double cta_sum(double v, double* red) {
 #pragma unroll
@@ -336,8 +356,8 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
     double2* taug = reinterpret_cast<double2*>(slab + L.tau);
     double2* vbuf[2] = {reinterpret_cast<double2*>(sm), reinterpret_cast<double2*>(sm) + n};
     double2* w = reinterpret_cast<double2*>(sm) + 2 * n;                 // w of step k-1
-    double* red = reinterpret_cast<double*>(w + n);                     // 32 doubles
-    double2* sc = reinterpret_cast<double2*>(red + 32);                 // [0] tau, [1] (dot)
+    double* red = reinterpret_cast<double*>(w + n);                     // 32 doubles (16 double2)
+    double2* sc = reinterpret_cast<double2*>(red + 32);                 // [0] alpha
     for (int k = 0; k < n - 1; ++k) {
       double2* v = vbuf[k & 1];
       const double2* vp = vbuf[(k & 1) ^ 1];   // v of step k-1 (valid from k = 1)
@@ -386,15 +406,16 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
         double2* row = A + (int64_t)i * n;
         const double2 vi = upd ? vp[i] : make_double2(0.0, 0.0), wi = upd ? w[i] : make_double2(0.0, 0.0);
         double sx = 0.0, sy = 0.0;
-        for (int j0 = k + 1 + lane; j0 < n; j0 += 128) {
-          double2 a[4];
+        for (int j0 = k + 1 + lane; j0 < n; j0 += 32 * kRowUnroll) {
+          double2 a[kRowUnroll];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {   // four loads in flight per lane
+          for (int u = 0; u < kRowUnroll; ++u) {   // kRowUnroll loads in flight per lane (the pass is
+                                                   // bound by the bytes in flight per SM)
             const int j = j0 + 32 * u;
             a[u] = j < n ? __ldcg(&row[j]) : make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kRowUnroll; ++u) {
             const int j = j0 + 32 * u;
             if (j >= n) break;
             if (upd) {
@@ -420,9 +441,8 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
         pdot.x += cp.x;
         pdot.y += cp.y;
       }
-      const double dre = cta_sum(lane == 0 ? pdot.x : 0.0, red);
-      const double dim = cta_sum(lane == 0 ? pdot.y : 0.0, red);
-      if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], make_double2(dre, dim));
+      const double2 dsum = cta_sum2(lane == 0 ? pdot : make_double2(0.0, 0.0), reinterpret_cast<double2*>(red));
+      if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], dsum);
       rlg_barrier(ctr, nb, cpg);
       // the reflector H_k = I - tau_k v_k v_k^H is kept for the eigenvectors (z = H_0 .. H_{n-2} y):
       // v_k in row k's dead columns k+1 .. n-1 (every CTA has read row k by now), tau_k in taug
@@ -864,7 +884,12 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   if (grid > 1024) grid = 1024;   // the partial-dot buffer holds 1024 CTAs
   // several gates in flight when the wave has several candidates (EAMPS_RLG_GROUPS overrides)
   static const int env_groups = getenv("EAMPS_RLG_GROUPS") ? atoi(getenv("EAMPS_RLG_GROUPS")) : 0;
-  int groups = env_groups > 0 ? env_groups : kDefaultGroups;
+  // measured (r02, 1 CTA per SM): n = 512: 4 / 8 / 16 / 37 / 74 groups 0.35 / 0.20 / 0.13 / 0.10 / 0.10
+  // s per 512 gates of tridiagonalisation; n = 2048: 2 / 4 / 8 / 16 groups 28 / 25 / 23 / 22 ms per
+  // gate. About n / 256 CTAs per group (>= 2): the per-step barrier and pivot latency amortised over
+  // as many gates in flight as the traffic allows.
+  int groups = env_groups > 0 ? env_groups : grid / std::max(2, max_n / 256);
+  (void)kDefaultGroups;
   groups = std::max(1, std::min({groups, nc, kMaxGroups, grid}));
   const int cpg = grid / groups;
   const GateDesc* a_desc = d_desc;
