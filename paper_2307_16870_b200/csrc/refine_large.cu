@@ -20,7 +20,7 @@
 //   k_rlg_pick     the trigger (deepest sigma >= 1e-6 sigma_max below kRatio sigma_max)
 //   k_rlg_theta    theta64[(a,s),(t,c)] = lambda_a sum_{s',t'} U[s d+t, s' d+t'] sum_b B_i[a,s',b] B_{i+1}[b,t',c]
 //                  (E2 of PAPER.md:32-41 / contract.cu with FP64 products and sums)
-//   k_rlg_gram     G = theta64^H theta64 (FP64, full Hermitian storage, row-major)
+//   k_rlg_gram     G = theta64^H theta64 (FP64, lower triangle in 32 x 32 tiles)
 //   k_rlg_tridiag  one-stage Householder tridiagonalisation Q^H G Q = T (LAPACK zhetd2 recurrence,
 //                  lower), all CTAs of a cooperative grid on one gate at a time; the rank-2 update of
 //                  step k-1 is applied lazily during step k (each CTA re-derives the pivot row k
@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 
 #include "eamps_internal.cuh"
@@ -45,6 +46,15 @@
 namespace eamps {
 
 namespace {
+
+// EAMPS_DEBUG_SYNC=1 (development): synchronise and check after every launch of this file, naming it
+void rl_dbg(cudaStream_t s, const char* what) {
+  static const bool on = getenv("EAMPS_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  const cudaError_t e = cudaGetLastError();
+  fprintf(stderr, "[eamps debug] after %s: %s\n", what, cudaGetErrorString(e));
+}
 
 constexpr int kMinN = 257, kMaxN = 2048;
 // measured (config 2, r02): chi = 256 (n = 512, sigma_min/sigma_max = 8.6e-5) 2.8e-6 and chi = 512
@@ -64,8 +74,16 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) b
 }
 
 struct RlgLayout {               // per-gate scratch at ws_log (the large regime's dead TC / Gram scratch)
-  int64_t g, th, d, e, eig, tau, p, part, y, slot;
+  int64_t g, th, d, e, eig, tau, p, part, y, slot, rs, cs;
 };
+// G in tile-major lower storage: 32 x 32 tiles (I >= J), tile (I, J) at tile index I (I + 1) / 2 + J,
+// row-major inside (diagonal tiles hold both triangles of their block).
+constexpr int TB = 32;
+__host__ __device__ inline int64_t g_tiles(int n) { const int64_t nt = (n + TB - 1) / TB; return nt * (nt + 1) / 2; }
+__device__ __forceinline__ int64_t g_at(int i, int j) {   // i >= j (or the same tile)
+  const int I = i / TB, J = j / TB;
+  return ((int64_t)I * (I + 1) / 2 + J) * (TB * TB) + (i % TB) * TB + (j % TB);
+}
 constexpr int kSlots = 128;      // inverse-iteration factor slots per gate (vectors in flight)
 __host__ __device__ inline RlgLayout rlg_layout(const GateDesc& gd) {
   RlgLayout L;
@@ -80,6 +98,8 @@ __host__ __device__ inline RlgLayout rlg_layout(const GateDesc& gd) {
   L.part = L.p + 32 * n;               // 2 x 1024 double2 (by step parity)
   L.y = L.part + 32 * 1024;            // n x n doubles: eigenvectors of T (row j = vector j)
   L.slot = L.y + 8 * n * n;            // kSlots x n x (double4 factors + 1 pivot byte)
+  L.rs = (L.slot + (int64_t)kSlots * n * 33 + 255) & ~(int64_t)255;   // tile row partials: tiles x TB double2
+  L.cs = L.rs + g_tiles(gd.n) * TB * 16;                                // tile column partials
   return L;
 }
 
@@ -271,10 +291,12 @@ __global__ void __launch_bounds__(256) k_rlg_gram(const GateDesc* __restrict__ d
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
+      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;   // G[gi][gj]
       if (gi >= n || gj >= n) continue;
-      G[(int64_t)gi * n + gj] = acc[i][j];
-      if (bi != bj) G[(int64_t)gj * n + gi] = make_double2(acc[i][j].x, -acc[i][j].y);
+      // lower tile storage: an entry is stored where its tile is lower or diagonal; the mirror
+      // G[gj][gi] = conj(G[gi][gj]) covers the other half
+      if (gi / TB >= gj / TB) G[g_at(gi, gj)] = acc[i][j];
+      if (gj / TB >= gi / TB) G[g_at(gj, gi)] = make_double2(acc[i][j].x, -acc[i][j].y);
     }
 }
 
@@ -333,6 +355,15 @@ size_t tridiag_smem(int n) { return (size_t)3 * n * sizeof(double2) + 64 * sizeo
 
 // The grid is split into groups of cpg CTAs; group g factorises the listed gates g, g + ngrp, ...
 // (several gates in flight when the wave has several; all CTAs on one gate when it has one).
+// G is the lower triangle in 32 x 32 tiles (g_at). Step k (trailing indices >= k1 = k + 1):
+//  (A) every CTA reads column k below the diagonal (x = G[k1:, k]) with the update of step k-1 applied
+//      and builds v_k, tau_k, beta_k;
+//  (B) the warps stream the trailing lower tiles once: apply the update of step k-1, store, and emit the
+//      tile's row partials (G_IJ v_J) and column partials (G_IJ^H v_I, off-diagonal tiles);
+//  barrier; (C) p_i = tau (sum of the partials of row block I), partial dots p^H v; v_k kept in
+//  column k (dead from now on); barrier; (D) w = p + alpha v, alpha = -tau (p^H v) / 2.
+// Half the bytes of full storage per step (each trailing entry read and written once) for one more
+// barrier.
 __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restrict__ desc,
                                                        const int32_t* __restrict__ list, uint8_t* slab,
                                                        unsigned int* ctr_base, int cpg) {
@@ -346,7 +377,7 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
   unsigned int nb = 0;
   for (int li = grp; li < cnt; li += ngrp) {
     const GateDesc& gd = desc[list[1 + li]];
-    const int n = gd.n;
+    const int n = gd.n, nt = (n + TB - 1) / TB;
     const RlgLayout L = rlg_layout(gd);
     double2* A = reinterpret_cast<double2*>(slab + L.g);
     double* dg = reinterpret_cast<double*>(slab + L.d);
@@ -354,34 +385,38 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
     double2* pg = reinterpret_cast<double2*>(slab + L.p);
     double2* partg = reinterpret_cast<double2*>(slab + L.part);
     double2* taug = reinterpret_cast<double2*>(slab + L.tau);
-    double2* vbuf[2] = {reinterpret_cast<double2*>(sm), reinterpret_cast<double2*>(sm) + n};
-    double2* w = reinterpret_cast<double2*>(sm) + 2 * n;                 // w of step k-1
+    double2* rsg = reinterpret_cast<double2*>(slab + L.rs);
+    double2* csg = reinterpret_cast<double2*>(slab + L.cs);
+    double2* vbuf0 = reinterpret_cast<double2*>(sm);
+    double2* vbuf1 = vbuf0 + n;
+    double2* w = vbuf0 + 2 * n;                                         // w of step k-1
     double* red = reinterpret_cast<double*>(w + n);                     // 32 doubles (16 double2)
     double2* sc = reinterpret_cast<double2*>(red + 32);                 // [0] alpha
     for (int k = 0; k < n - 1; ++k) {
-      double2* v = vbuf[k & 1];
-      const double2* vp = vbuf[(k & 1) ^ 1];   // v of step k-1 (valid from k = 1)
+      double2* v = (k & 1) ? vbuf1 : vbuf0;
+      const double2* vp = (k & 1) ? vbuf0 : vbuf1;   // v of step k-1 (valid from k = 1)
       const bool upd = k > 0;
-      // (1) pivot row k with the update of step k-1 applied (every CTA, never stored)
+      const int k1 = k + 1;
+      // (A) column k, rows k .. n-1, with the update of step k-1 (never stored)
       double part = 0.0, dk = 0.0;
-      for (int j = k + tid; j < n; j += TT) {
-        double2 a = __ldcg(&A[(int64_t)k * n + j]);
-        if (upd) {
-          const double2 t1 = cmulc(w[j], vp[k]);   // v_k conj(w_j) = conj(conj(v_k) w_j)
-          const double2 t2 = cmulc(vp[j], w[k]);   // w_k conj(v_j)
+      for (int i = k + tid; i < n; i += TT) {
+        double2 a = __ldcg(&A[g_at(i, k)]);
+        if (upd) {   // a -= v_i conj(w_k) + w_i conj(v_k)
+          const double2 t1 = cmulc(w[k], vp[i]);
+          const double2 t2 = cmulc(vp[k], w[i]);
           a.x -= t1.x + t2.x;
           a.y -= t1.y + t2.y;
         }
-        if (j == k) {
+        if (i == k) {
           dk = a.x;
         } else {
-          v[j] = make_double2(a.x, -a.y);           // x_j = conj(row) = column k below the diagonal
-          if (j >= k + 2) part += a.x * a.x + a.y * a.y;
+          v[i] = a;                                   // x_i = G[i][k]
+          if (i >= k + 2) part += a.x * a.x + a.y * a.y;
         }
       }
-      const double xn2 = cta_sum(part, red);       // includes a __syncthreads: v[] complete
-      if (lcta == 0 && tid == 0) dg[k] = dk;   // j == k is thread 0's
-      const double2 al = v[k + 1];
+      const double xn2 = cta_sum(part, red);          // includes a __syncthreads: v[] complete
+      if (lcta == 0 && tid == 0) dg[k] = dk;          // i == k is thread 0's
+      const double2 al = v[k1];
       double2 tau;
       double beta;
       double2 scale = make_double2(0.0, 0.0);
@@ -396,61 +431,126 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
         scale = make_double2(den.x / dd, -den.y / dd);
       }
       if (lcta == 0 && tid == 0) eg[k] = beta;
-      __syncthreads();   // every thread has read v[k + 1]
-      for (int j = k + 2 + tid; j < n; j += TT) v[j] = cmul(v[j], scale);
-      if (tid == 0) v[k + 1] = make_double2(1.0, 0.0);
+      __syncthreads();   // every thread has read v[k1]
+      for (int i = k + 2 + tid; i < n; i += TT) v[i] = cmul(v[i], scale);
+      if (tid == 0) v[k1] = make_double2(1.0, 0.0);
       __syncthreads();
-      // (2) rows i > k: apply the update of step k-1, store, and p_i = tau (A v)_i
-      double2 pdot = make_double2(0.0, 0.0);       // sum over this warp's rows of conj(p_i) v_i
-      for (int i = k + 1 + gw; i < n; i += W) {
-        double2* row = A + (int64_t)i * n;
-        const double2 vi = upd ? vp[i] : make_double2(0.0, 0.0), wi = upd ? w[i] : make_double2(0.0, 0.0);
-        double sx = 0.0, sy = 0.0;
-        for (int j0 = k + 1 + lane; j0 < n; j0 += 32 * kRowUnroll) {
-          double2 a[kRowUnroll];
+      // (B) trailing lower tiles (I >= J >= J0): apply update k-1, store, row / column partials
+      const int J0 = k1 / TB, m = nt - J0, ntile = m * (m + 1) / 2;
+      for (int q = gw; q < ntile; q += W) {
+        int I = 0, rem = q;                          // q -> (I, J), J0 <= J <= I, row-major over I
+        {
+          int ii = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+          while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+          while (ii * (ii + 1) / 2 > q) --ii;
+          I = ii;
+          rem = q - ii * (ii + 1) / 2;
+        }
+        const int J = J0 + rem, Ib = J0 + I;
+        const int j = J * TB + lane;
+        const bool jv = j >= k1 && j < n;
+        const double2 vj = jv ? v[j] : make_double2(0.0, 0.0);
+        const double2 vpj = (upd && jv) ? vp[j] : make_double2(0.0, 0.0);
+        const double2 wj = (upd && jv) ? w[j] : make_double2(0.0, 0.0);
+        double2* T = A + ((int64_t)Ib * (Ib + 1) / 2 + J) * (TB * TB);
+        double2 colacc = make_double2(0.0, 0.0);
+        const int64_t toff = ((int64_t)Ib * (Ib + 1) / 2 + J) * TB;
+#pragma unroll 1
+        for (int c = 0; c < TB / 8; ++c) {
+          double2 pr[8];
+          double2 a[8];
 #pragma unroll
-          for (int u = 0; u < kRowUnroll; ++u) {   // kRowUnroll loads in flight per lane (the pass is
-                                                   // bound by the bytes in flight per SM)
-            const int j = j0 + 32 * u;
-            a[u] = j < n ? __ldcg(&row[j]) : make_double2(0.0, 0.0);
+          for (int rr = 0; rr < 8; ++rr) {
+            const int i = Ib * TB + 8 * c + rr;
+            a[rr] = (jv && i >= k1 && i < n) ? __ldcg(&T[(8 * c + rr) * TB + lane]) : make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int u = 0; u < kRowUnroll; ++u) {
-            const int j = j0 + 32 * u;
-            if (j >= n) break;
-            if (upd) {
-              const double2 t1 = cmulc(w[j], vi);    // v_i conj(w_j)
-              const double2 t2 = cmulc(vp[j], wi);   // w_i conj(v_j)
-              a[u].x -= t1.x + t2.x;
-              a[u].y -= t1.y + t2.y;
-              __stcg(&row[j], a[u]);
+          for (int rr = 0; rr < 8; ++rr) {
+            const int i = Ib * TB + 8 * c + rr;
+            const bool iv = i >= k1 && i < n;
+            if (jv && iv) {
+              if (upd) {   // a -= v_i conj(w_j) + w_i conj(v_j)
+                const double2 t1 = cmulc(wj, vp[i]);
+                const double2 t2 = cmulc(vpj, w[i]);
+                a[rr].x -= t1.x + t2.x;
+                a[rr].y -= t1.y + t2.y;
+                __stcg(&T[(8 * c + rr) * TB + lane], a[rr]);
+              }
+              if (Ib != J) {   // column partial: conj(a) v_i
+                const double2 cv = cmulc(a[rr], v[i]);
+                colacc.x += cv.x;
+                colacc.y += cv.y;
+              }
             }
-            const double2 vj = v[j];
-            sx = fma(a[u].x, vj.x, fma(-a[u].y, vj.y, sx));
-            sy = fma(a[u].x, vj.y, fma(a[u].y, vj.x, sy));
+            pr[rr] = cmul(a[rr], vj);     // 0 where masked
+          }
+          // transpose-reduce the 8 row products over the 32 lanes: lane ends with the sum of row
+          // 4 b4 + 2 b3 + b2 (b_x = bit x of the lane), complete after the xor-2 / xor-1 steps
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const bool hi = lane & 16;
+            const double2 keep = hi ? pr[q4 + 4] : pr[q4], send = hi ? pr[q4] : pr[q4 + 4];
+            pr[q4].x = keep.x + __shfl_xor_sync(0xffffffffu, send.x, 16);
+            pr[q4].y = keep.y + __shfl_xor_sync(0xffffffffu, send.y, 16);
+          }
+#pragma unroll
+          for (int q2 = 0; q2 < 2; ++q2) {
+            const bool hi = lane & 8;
+            const double2 keep = hi ? pr[q2 + 2] : pr[q2], send = hi ? pr[q2] : pr[q2 + 2];
+            pr[q2].x = keep.x + __shfl_xor_sync(0xffffffffu, send.x, 8);
+            pr[q2].y = keep.y + __shfl_xor_sync(0xffffffffu, send.y, 8);
+          }
+          {
+            const bool hi = lane & 4;
+            const double2 keep = hi ? pr[1] : pr[0], send = hi ? pr[0] : pr[1];
+            pr[0].x = keep.x + __shfl_xor_sync(0xffffffffu, send.x, 4);
+            pr[0].y = keep.y + __shfl_xor_sync(0xffffffffu, send.y, 4);
+          }
+          pr[0].x += __shfl_xor_sync(0xffffffffu, pr[0].x, 2);
+          pr[0].y += __shfl_xor_sync(0xffffffffu, pr[0].y, 2);
+          pr[0].x += __shfl_xor_sync(0xffffffffu, pr[0].x, 1);
+          pr[0].y += __shfl_xor_sync(0xffffffffu, pr[0].y, 1);
+          if ((lane & 3) == 0) {
+            const int r = 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
+            __stcg(&rsg[toff + 8 * c + r], pr[0]);
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          sx += __shfl_xor_sync(0xffffffffu, sx, o);
-          sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        }
-        const double2 p = cmul(tau, make_double2(sx, sy));
-        if (lane == 0) __stcg(&pg[(int64_t)(k & 1) * n + i], p);
-        const double2 cp = cmulc(p, v[i]);
-        pdot.x += cp.x;
-        pdot.y += cp.y;
+        if (Ib != J) __stcg(&csg[toff + lane], colacc);
       }
-      const double2 dsum = cta_sum2(lane == 0 ? pdot : make_double2(0.0, 0.0), reinterpret_cast<double2*>(red));
-      if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], dsum);
       rlg_barrier(ctr, nb, cpg);
+      // (C) p_i = tau (sum_J rows(I, J) + sum_{I' > I} cols(I', I)); partial dots conj(p_i) v_i
+      double2 pdot = make_double2(0.0, 0.0);
+      for (int Ib = J0 + gw; Ib < nt; Ib += W) {
+        const int i = Ib * TB + lane;
+        double2 sacc = make_double2(0.0, 0.0);
+        for (int J = J0; J <= Ib; ++J) {
+          const double2 t = __ldcg(&rsg[((int64_t)Ib * (Ib + 1) / 2 + J) * TB + lane]);
+          sacc.x += t.x;
+          sacc.y += t.y;
+        }
+        for (int I2 = Ib + 1; I2 < nt; ++I2) {
+          const double2 t = __ldcg(&csg[((int64_t)I2 * (I2 + 1) / 2 + Ib) * TB + lane]);
+          sacc.x += t.x;
+          sacc.y += t.y;
+        }
+        if (i >= k1 && i < n) {
+          const double2 p = cmul(tau, sacc);
+          __stcg(&pg[(int64_t)(k & 1) * n + i], p);
+          const double2 cp = cmulc(p, v[i]);
+          pdot.x += cp.x;
+          pdot.y += cp.y;
+        }
+      }
       // the reflector H_k = I - tau_k v_k v_k^H is kept for the eigenvectors (z = H_0 .. H_{n-2} y):
-      // v_k in row k's dead columns k+1 .. n-1 (every CTA has read row k by now), tau_k in taug
+      // v_k in column k (dead from now on; every CTA read it in (A) before the barrier), tau_k in taug
       if (lcta == 0) {
-        for (int j = k + 1 + tid; j < n; j += TT) __stcg(&A[(int64_t)k * n + j], v[j]);
+        for (int i = k1 + tid; i < n; i += TT) __stcg(&A[g_at(i, k)], v[i]);
         if (tid == 0) taug[k] = tau;
       }
-      // (3) w = p + alpha v, alpha = -1/2 tau (p^H v)   (zhetd2; p already carries tau). The group's
+      const double2 dsum = cta_sum2(pdot, reinterpret_cast<double2*>(red));
+      if (tid == 0) __stcg(&partg[(k & 1) * 1024 + lcta], dsum);
+      rlg_barrier(ctr, nb, cpg);
+      // (D) w = p + alpha v, alpha = -1/2 tau (p^H v) (zhetd2; p already carries tau). The group's
       // partials summed by warp 0 in a fixed order (identical in every CTA of the group)
       if (warp == 0) {
         double2 s = make_double2(0.0, 0.0);
@@ -469,18 +569,18 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
       }
       __syncthreads();
       const double2 alpha = sc[0];
-      for (int j = k + 1 + tid; j < n; j += TT) {
+      for (int j = k1 + tid; j < n; j += TT) {
         const double2 p = __ldcg(&pg[(int64_t)(k & 1) * n + j]);
         const double2 av = cmul(alpha, v[j]);
         w[j] = make_double2(p.x + av.x, p.y + av.y);
       }
       __syncthreads();
     }
-    // the last diagonal entry: A[n-1][n-1] with the update of step n-2
+    // the last diagonal entry: G[n-1][n-1] with the update of step n-2
     if (lcta == 0 && tid == 0) {
-      double2 a = __ldcg(&A[(int64_t)(n - 1) * n + (n - 1)]);
+      double2 a = __ldcg(&A[g_at(n - 1, n - 1)]);
       if (n >= 2) {
-        const double2* vl = vbuf[(n - 2) & 1];
+        const double2* vl = ((n - 2) & 1) ? vbuf1 : vbuf0;
         const double2 t1 = cmulc(w[n - 1], vl[n - 1]);
         const double2 t2 = cmulc(vl[n - 1], w[n - 1]);
         a.x -= t1.x + t2.x;
@@ -738,7 +838,7 @@ __global__ void __launch_bounds__(256) k_rlg_mgs(const GateDesc* __restrict__ de
 }
 
 // Back-transformation z_j = Q y_j = H_0 (H_1 ( .. H_{n-2} y_j)), H_q = I - tau_q v_q v_q^H (v_q in
-// row q of the factorised G, entries q+1 .. n-1), then V[:, j] = z_j in FP32 (unit norm: Q unitary).
+// column q of the factorised G, entries q+1 .. n-1), then V[:, j] = z_j in FP32 (unit norm: Q unitary).
 // kVpc vectors per CTA in shared memory; each thread owns the same rows of every vector, so only the
 // dot products v_q^H z need the CTA (one barrier per reflector, double-buffered partials).
 constexpr int kVpc = 4;
@@ -762,7 +862,6 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
     for (int i = tid; i < n; i += 256)
       z[q * n + i] = make_double2(q < nv ? Y[(int64_t)(j0 + q) * n + i] : 0.0, 0.0);
   for (int r = n - 2; r >= 0; --r) {
-    const double2* vr = A + (int64_t)r * n;
     double2 acc[kVpc];
 #pragma unroll
     for (int q = 0; q < kVpc; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -771,7 +870,7 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
     int i0 = tid;
     if (i0 <= r) i0 += ((r - tid) / 256 + 1) * 256;
     for (int i = i0; i < n; i += 256) {
-      const double2 vi = vr[i];
+      const double2 vi = A[g_at(i, r)];
 #pragma unroll
       for (int q = 0; q < kVpc; ++q) {
         const double2 c = cmulc(vi, z[q * n + i]);
@@ -803,7 +902,7 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
       f[q] = cmul(tau, sdot);
     }
     for (int i = i0; i < n; i += 256) {
-      const double2 vi = vr[i];
+      const double2 vi = A[g_at(i, r)];
 #pragma unroll
       for (int q = 0; q < kVpc; ++q) {
         const double2 t = cmul(f[q], vi);
@@ -832,9 +931,11 @@ bool eig_route(const GateDesc& gd) {
   return !off && refine_large_candidate(gd);
 }
 
+// must cover rlg_layout: g 16 n^2 | th 16 m n | d, e, eig 24 n | tau 16 n | p 32 n | part 32 KB |
+// y 8 n^2 | slots kSlots 33 n | (256-byte alignment) | rs, cs 2 x tiles x TB x 16
 size_t refine_large_scratch(int m, int n) {
-  return (size_t)16 * n * n + (size_t)16 * m * n + (size_t)56 * n + 32 * 1024 + (size_t)8 * n * n +
-         (size_t)kSlots * n * 33 + 512;
+  return (size_t)16 * n * n + (size_t)16 * m * n + (size_t)72 * n + 32 * 1024 + (size_t)8 * n * n +
+         (size_t)kSlots * n * 33 + 256 + 2 * (size_t)g_tiles(n) * TB * 16 + 512;
 }
 
 namespace {
@@ -862,6 +963,7 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   cudaMemsetAsync(list, 0, sizeof(int32_t), s);
   cudaMemsetAsync(ctr, 0, 128 * kMaxGroups, s);
   k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list, mode);
+  rl_dbg(s, "k_rlg_pick");
   static std::atomic<unsigned long long> attr{0};
   const size_t tsm = tridiag_smem(kMaxN);
   if (first_on_device(attr)) {
@@ -875,7 +977,9 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
     k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
   else
     k_rlg_theta<4><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  rl_dbg(s, "k_rlg_theta");
   k_rlg_gram<<<dim3(max_gram, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab);
+  rl_dbg(s, "k_rlg_gram");
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -901,8 +1005,11 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   if (mk) mk->at[0] = mk->mark(mk->ctx);
   cudaLaunchCooperativeKernel((const void*)k_rlg_tridiag, dim3(grid), dim3(TT), args, tsm, s);
   if (mk) mk->at[1] = mk->mark(mk->ctx);
+  rl_dbg(s, "k_rlg_tridiag");
   k_rlg_bisect<<<dim3((max_n + kBisPerCta - 1) / kBisPerCta, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+  rl_dbg(s, "k_rlg_bisect");
   k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab, mode, fb);
+  rl_dbg(s, "k_rlg_finish");
   return 6;
 }
 }  // namespace
@@ -932,8 +1039,11 @@ int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* 
     if (h_desc[h_cand[c]].eig) max_n = std::max(max_n, h_desc[h_cand[c]].n);
   if (max_n == 0) return 0;
   k_rlg_invit<<<dim3(kSlots / 32, nc), 32, 0, s>>>(d_desc, d_cand, slab);
+  rl_dbg(s, "k_rlg_invit");
   k_rlg_mgs<<<nc, 256, 0, s>>>(d_desc, d_cand, slab);
+  rl_dbg(s, "k_rlg_mgs");
   k_rlg_backtr<<<dim3((max_n + kVpc - 1) / kVpc, nc), 256, (size_t)kVpc * max_n * 16, s>>>(d_desc, d_cand, slab);
+  rl_dbg(s, "k_rlg_backtr");
   return 3;
 }
 
