@@ -64,7 +64,7 @@ constexpr double kRatio = 2e-5;
 constexpr int TT = 512;          // tridiagonalisation threads per CTA
 constexpr int BT = 128;          // bisection threads per CTA
 constexpr int kMaxGroups = 148, kDefaultGroups = 8;
-constexpr int kRowUnroll = 8;   // measured (8 chi = 1024 gates): 1 / 2 / 4 / 8 groups 36 / 33 / 30 / 28 ms per gate (spectrum sub-phase)
+constexpr int kBisWide = 148 * 256;   // eigenvalues in a launch from which 1 lane per eigenvalue pays
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ 
   if ((int)blockIdx.x >= nta * ntc) return;
   const int a0 = (blockIdx.x / ntc) * TA, c0 = (blockIdx.x % ntc) * TC;
   extern __shared__ __align__(16) uint8_t sm[];
-  double2(*As)[65] = reinterpret_cast<double2(*)[65]>(sm);              // [KC][65]
-  double2(*Bs)[65] = reinterpret_cast<double2(*)[65]>(sm) + KC;         // [KC][65]
+  double2(*As)[65] = reinterpret_cast<double2(*)[65]>(sm);              // stage s: rows 2 KC s ..
+  double2(*Bs)[65] = reinterpret_cast<double2(*)[65]>(sm) + KC;         // stage s: rows 2 KC s + KC ..
   double2(*Cs)[65] = reinterpret_cast<double2(*)[65]>(sm);              // [64][65] (epilogue)
   __shared__ double2 Us[D * D * D * D];
   const SiteEntry* sites = reinterpret_cast<const SiteEntry*>(slab + st->sites_off);
@@ -169,15 +169,16 @@ __global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
-  for (int b0 = 0; b0 < mid; b0 += KC) {
+  // two shared-memory stages, the next chunk prefetched into registers during the current one's
+  // products: one barrier per chunk, the global latency under the FP64 pipe
+  float2 pa[4], pb[4];
+  auto fetch = [&](int b0) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int e = tid + it * 256;
       const int kk = e & (KC - 1), rho = e >> 4;
       const int a = a0 + rho / D, sp = rho % D, b = b0 + kk;
-      float2 v = make_float2(0.f, 0.f);
-      if (a < l && b < mid) v = Bi[((int64_t)a * D + sp) * mid + b];
-      As[kk][rho] = make_double2(v.x, v.y);
+      pa[it] = (a < l && b < mid) ? Bi[((int64_t)a * D + sp) * mid + b] : make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
@@ -185,18 +186,35 @@ __global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ 
       const int cc = e % TC, rest = e / TC;
       const int tp = rest % D, kk = rest / D;
       const int c = c0 + cc, b = b0 + kk;
-      float2 v = make_float2(0.f, 0.f);
-      if (c < r && b < mid) v = Bj[((int64_t)b * D + tp) * r + c];
-      Bs[kk][tp * TC + cc] = make_double2(v.x, v.y);
+      pb[it] = (c < r && b < mid) ? Bj[((int64_t)b * D + tp) * r + c] : make_float2(0.f, 0.f);
     }
-    __syncthreads();
+  };
+  auto stash = [&](int stg) {
+    double2(*Ad)[65] = As + stg * 2 * KC;
+    double2(*Bd)[65] = Bs + stg * 2 * KC;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      Ad[e & (KC - 1)][e >> 4] = make_double2(pa[it].x, pa[it].y);
+      const int cc = e % TC, rest = e / TC;
+      Bd[rest / D][(rest % D) * TC + cc] = make_double2(pb[it].x, pb[it].y);
+    }
+  };
+  const int nch = (mid + KC - 1) / KC;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) fetch((ch + 1) * KC);
+    double2(*Ad)[65] = As + (ch & 1) * 2 * KC;
+    double2(*Bd)[65] = Bs + (ch & 1) * 2 * KC;
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       double2 av[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) av[i] = Ad[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bv[j] = Bd[kk][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -205,6 +223,7 @@ __global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ 
           acc[i][j].y = fma(av[i].x, bv[j].y, fma(av[i].y, bv[j].x, acc[i][j].y));
         }
     }
+    if (ch + 1 < nch) stash((ch + 1) & 1);
     __syncthreads();
   }
 #pragma unroll
@@ -259,24 +278,43 @@ __global__ void __launch_bounds__(256) k_rlg_gram(const GateDesc* __restrict__ d
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
-  for (int r0 = 0; r0 < m; r0 += KC) {
+  double2 pa[4], pb[4];
+  auto fetch = [&](int r0) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int e = tid + it * 256;
       const int kk = e & (KC - 1), cc = e >> 4;
       const int row = r0 + kk;
       const int ci = i0 + cc, cj = j0 + cc;
-      As[kk][cc] = (row < m && ci < n) ? th[(int64_t)ci * m + row] : make_double2(0.0, 0.0);
-      Bs[kk][cc] = (row < m && cj < n) ? th[(int64_t)cj * m + row] : make_double2(0.0, 0.0);
+      pa[it] = (row < m && ci < n) ? th[(int64_t)ci * m + row] : make_double2(0.0, 0.0);
+      pb[it] = (row < m && cj < n) ? th[(int64_t)cj * m + row] : make_double2(0.0, 0.0);
     }
-    __syncthreads();
+  };
+  auto stash = [&](int stg) {
+    double2(*Ad)[65] = As + stg * 2 * KC;
+    double2(*Bd)[65] = Bs + stg * 2 * KC;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      Ad[e & (KC - 1)][e >> 4] = pa[it];
+      Bd[e & (KC - 1)][e >> 4] = pb[it];
+    }
+  };
+  const int nch = (m + KC - 1) / KC;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) fetch((ch + 1) * KC);
+    double2(*Ad)[65] = As + (ch & 1) * 2 * KC;
+    double2(*Bd)[65] = Bs + (ch & 1) * 2 * KC;
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       double2 av[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) av[i] = Ad[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bv[j] = Bd[kk][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -285,6 +323,7 @@ __global__ void __launch_bounds__(256) k_rlg_gram(const GateDesc* __restrict__ d
           acc[i][j].y = fma(av[i].x, bv[j].y, fma(-av[i].y, bv[j].x, acc[i][j].y));
         }
     }
+    if (ch + 1 < nch) stash((ch + 1) & 1);
     __syncthreads();
   }
 #pragma unroll
@@ -522,16 +561,24 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
       double2 pdot = make_double2(0.0, 0.0);
       for (int Ib = J0 + gw; Ib < nt; Ib += W) {
         const int i = Ib * TB + lane;
+        // up to 2 nt partials per lane: 8 independent loads in flight (a dependent chain of L2 round
+        // trips here cost ~20 us per step when one gate has the whole grid: ncu, barrier-stalled)
         double2 sacc = make_double2(0.0, 0.0);
-        for (int J = J0; J <= Ib; ++J) {
-          const double2 t = __ldcg(&rsg[((int64_t)Ib * (Ib + 1) / 2 + J) * TB + lane]);
-          sacc.x += t.x;
-          sacc.y += t.y;
-        }
-        for (int I2 = Ib + 1; I2 < nt; ++I2) {
-          const double2 t = __ldcg(&csg[((int64_t)I2 * (I2 + 1) / 2 + Ib) * TB + lane]);
-          sacc.x += t.x;
-          sacc.y += t.y;
+        const int nr = Ib - J0 + 1, ncol = nt - 1 - Ib;
+        for (int q0 = 0; q0 < nr + ncol; q0 += 8) {
+          double2 t[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u;
+            t[u] = q < nr ? __ldcg(&rsg[((int64_t)Ib * (Ib + 1) / 2 + J0 + q) * TB + lane])
+                 : q < nr + ncol ? __ldcg(&csg[((int64_t)(Ib + 1 + q - nr) * (Ib + 2 + q - nr) / 2 + Ib) * TB + lane])
+                                 : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            sacc.x += t[u].x;
+            sacc.y += t[u].y;
+          }
         }
         if (i >= k1 && i < n) {
           const double2 p = cmul(tau, sacc);
@@ -596,9 +643,14 @@ __global__ void __launch_bounds__(TT, 1) k_rlg_tridiag(const GateDesc* __restric
 // eigenvalue index j; each lane runs the Sturm recurrences of 2 of the 16 interior points of the
 // bracket (two independent chains), so a pass narrows [lo, hi) 17-fold; the bracket is identical
 // in the 8 lanes (same inputs, same arithmetic).
-constexpr int kBisPerCta = (BT / 32) * 4;   // eigenvalues per CTA
+// LPE = lanes per eigenvalue (8: a latency-bound launch with few eigenvalues; 1: a throughput-bound
+// one -- plain trisection with 2 points per thread does 4x less Sturm work per digit than the 17-way
+// multisection).
+template <int LPE>
 __global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
                                                    const int32_t* __restrict__ flag, uint8_t* slab) {
+  constexpr int kBisPerCta = BT / LPE;   // eigenvalues per CTA
+  constexpr int NP = 2 * LPE;             // points per pass
   if (!flag[blockIdx.y]) return;
   const GateDesc gd = desc[cand[blockIdx.y]];
   const int n = gd.n;
@@ -639,14 +691,14 @@ __global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ 
   lo -= 2.0 * 2.2e-16 * span * n + 1e-300;
   hi += 2.0 * 2.2e-16 * span * n + 1e-300;
   const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
-  const int lane = threadIdx.x & 31, sub = lane & 7;
-  const int j = blockIdx.x * kBisPerCta + (threadIdx.x >> 3);
+  const int lane = threadIdx.x & 31, sub = lane & (LPE - 1);
+  const int j = blockIdx.x * kBisPerCta + threadIdx.x / LPE;
   const bool act = j < n;
   // invariant: count(lo) <= j < count(hi)
-  for (int it = 0; it < 18; ++it) {   // 17^18 > 2^73
+  for (int it = 0; it < (LPE == 8 ? 18 : 48); ++it) {   // 17^18 > 2^73, 3^48 > 2^76
     const double wdt = hi - lo;
     if (__all_sync(0xffffffffu, wdt <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300)) break;   // warp-uniform
-    const double x1 = lo + wdt * (2 * sub + 1) / 17.0, x2 = lo + wdt * (2 * sub + 2) / 17.0;
+    const double x1 = lo + wdt * (2 * sub + 1) / (double)(NP + 1), x2 = lo + wdt * (2 * sub + 2) / (double)(NP + 1);
     double q1 = ds[0] - x1, q2 = ds[0] - x2;
     int c1 = q1 < 0.0, c2 = q2 < 0.0;
     for (int i = 1; i < n; ++i) {
@@ -658,14 +710,13 @@ __global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ 
       c1 += q1 < 0.0;
       c2 += q2 < 0.0;
     }
-    // bit p of mask: count(x_p) > j (monotone in p); OR over the 8 lanes of the group
+    // bit p of mask: count(x_p) > j (monotone in p); OR over the LPE lanes of the group
     unsigned int mask = ((act && c1 > j) ? 1u : 0u) << (2 * sub) | ((act && c2 > j) ? 2u : 0u) << (2 * sub);
-    mask |= __shfl_xor_sync(0xffffffffu, mask, 1);
-    mask |= __shfl_xor_sync(0xffffffffu, mask, 2);
-    mask |= __shfl_xor_sync(0xffffffffu, mask, 4);
-    const int p = mask ? __ffs(mask) - 1 : 16;    // first point with count > j
-    const double nlo = p == 0 ? lo : lo + wdt * p / 17.0;
-    const double nhi = p == 16 ? hi : lo + wdt * (p + 1) / 17.0;
+#pragma unroll
+    for (int o = 1; o < LPE; o <<= 1) mask |= __shfl_xor_sync(0xffffffffu, mask, o);
+    const int p = mask ? __ffs(mask) - 1 : NP;    // first point with count > j
+    const double nlo = p == 0 ? lo : lo + wdt * p / (double)(NP + 1);
+    const double nhi = p == NP ? hi : lo + wdt * (p + 1) / (double)(NP + 1);
     lo = nlo;
     hi = nhi;
   }
@@ -861,19 +912,31 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
   for (int q = 0; q < kVpc; ++q)
     for (int i = tid; i < n; i += 256)
       z[q * n + i] = make_double2(q < nv ? Y[(int64_t)(j0 + q) * n + i] : 0.0, 0.0);
+  // thread tid owns rows i = tid + 256 q (q < kRowsPT): the same rows of z for every r, so the update
+  // and the next dot product need no barrier between them; reflector r-1's entries of those rows are
+  // loaded while reflector r is applied (its L2 latency off the per-reflector critical path)
+  constexpr int kRowsPT = kMaxN / 256;
+  double2 cur[kRowsPT], nxt[kRowsPT];
+  auto load_col = [&](int r, double2* dst) {
+#pragma unroll
+    for (int q = 0; q < kRowsPT; ++q) {
+      const int i = tid + 256 * q;
+      dst[q] = (r >= 0 && i > r && i < n) ? __ldg(&A[g_at(i, r)]) : make_double2(0.0, 0.0);
+    }
+  };
+  load_col(n - 2, cur);
   for (int r = n - 2; r >= 0; --r) {
+    load_col(r - 1, nxt);
     double2 acc[kVpc];
 #pragma unroll
     for (int q = 0; q < kVpc; ++q) acc[q] = make_double2(0.0, 0.0);
-    // rows i > r with i = tid (mod 256): every thread keeps the same rows of z for all r, so the
-    // update below and the next dot product need no barrier between them
-    int i0 = tid;
-    if (i0 <= r) i0 += ((r - tid) / 256 + 1) * 256;
-    for (int i = i0; i < n; i += 256) {
-      const double2 vi = A[g_at(i, r)];
+#pragma unroll
+    for (int qq = 0; qq < kRowsPT; ++qq) {
+      const int i = tid + 256 * qq;
+      if (i <= r || i >= n) continue;
 #pragma unroll
       for (int q = 0; q < kVpc; ++q) {
-        const double2 c = cmulc(vi, z[q * n + i]);
+        const double2 c = cmulc(cur[qq], z[q * n + i]);
         acc[q].x += c.x;
         acc[q].y += c.y;
       }
@@ -901,15 +964,19 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
       }
       f[q] = cmul(tau, sdot);
     }
-    for (int i = i0; i < n; i += 256) {
-      const double2 vi = A[g_at(i, r)];
+#pragma unroll
+    for (int qq = 0; qq < kRowsPT; ++qq) {
+      const int i = tid + 256 * qq;
+      if (i <= r || i >= n) continue;
 #pragma unroll
       for (int q = 0; q < kVpc; ++q) {
-        const double2 t = cmul(f[q], vi);
+        const double2 t = cmul(f[q], cur[qq]);
         z[q * n + i].x -= t.x;
         z[q * n + i].y -= t.y;
       }
     }
+#pragma unroll
+    for (int qq = 0; qq < kRowsPT; ++qq) cur[qq] = nxt[qq];
   }
   __syncthreads();
   float2* V = reinterpret_cast<float2*>(slab + gd.ws_V);
@@ -1006,7 +1073,14 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   cudaLaunchCooperativeKernel((const void*)k_rlg_tridiag, dim3(grid), dim3(TT), args, tsm, s);
   if (mk) mk->at[1] = mk->mark(mk->ctx);
   rl_dbg(s, "k_rlg_tridiag");
-  k_rlg_bisect<<<dim3((max_n + kBisPerCta - 1) / kBisPerCta, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+  // the lanes per eigenvalue from the launch's parallelism (upper bound: every candidate picked)
+  int tot_n = 0;
+  for (int c = 0; c < nc; ++c)
+    if (refine_large_candidate(h_desc[h_cand[c]]) && (mode == 0 || h_desc[h_cand[c]].eig)) tot_n += h_desc[h_cand[c]].n;
+  if (tot_n >= kBisWide)
+    k_rlg_bisect<1><<<dim3((max_n + BT - 1) / BT, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+  else
+    k_rlg_bisect<8><<<dim3((max_n + BT / 8 - 1) / (BT / 8), nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
   rl_dbg(s, "k_rlg_bisect");
   k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab, mode, fb);
   rl_dbg(s, "k_rlg_finish");
