@@ -389,7 +389,7 @@ def run_chi(chi, G, steps, warmup, rank, world, dev, clocks=True):
         total_ms = max_over_ranks(total_ms, dev)
     ms_step = total_ms / steps
     regime = regime_of(n, n)
-    eig = regime == 1 and phases["svd_eig_tridiag"][1] > 0 and bool(np.all(sweeps == 0))
+    eig = regime in (1, 3) and phases["svd_eig_tridiag"][1] > 0 and bool(np.all(sweeps == 0))
     traffic = None
     tj = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
     if eig:
@@ -398,11 +398,20 @@ def run_chi(chi, G, steps, warmup, rank, world, dev, clocks=True):
         # launch = one wave's gates x 16 n^3 / 3) over its CUDA-event time (sub-phase svd_eig_tridiag)
         kern, (kms, kn) = "svd_eig_tridiag", phases["svd_eig_tridiag"]
         kms_launch = kms / max(1, kn)
-        per_launch_bytes = G * tridiag_bytes(n) * steps / kn
-        achieved = per_launch_bytes / (kms_launch / 1e3) / 1e9
-        (peak, peak_src), bound, unit = PEAKS["hbm"], "hbm", "GB/s"
-        flops_note = ("algorithmic bytes per launch: gates x 16 n^3 / 3 (one-stage Householder tridiagonalisation, "
-                      "trailing Hermitian triangle read + written per step; the kernel keeps both triangles)")
+        if regime == 1:
+            per_launch_bytes = G * tridiag_bytes(n) * steps / kn
+            achieved = per_launch_bytes / (kms_launch / 1e3) / 1e9
+            (peak, peak_src), bound, unit = PEAKS["hbm"], "hbm", "GB/s"
+            flops_note = ("algorithmic bytes per launch: gates x 16 n^3 / 3 (one-stage Householder "
+                          "tridiagonalisation, trailing Hermitian lower triangle read + written per step)")
+        else:
+            # n <= 128: one CTA per gate, G in shared memory (k_eig_cta: tridiagonalisation + bisection
+            # + spectrum); FP64 ALU-bound at best -- counted: the tridiagonalisation's 16 n^3 / 3 flops
+            per_launch_flops = G * 16.0 * n ** 3 / 3 * steps / kn
+            achieved = per_launch_flops / (kms_launch / 1e3) / 1e12
+            (peak, peak_src), bound, unit = PEAKS["fp64"], "alu", "TFLOP/s"
+            flops_note = ("algorithmic FP64 flops per launch: gates x 16 n^3 / 3 (Householder tridiagonalisation "
+                          "of the n x n Hermitian Gram; the bisection and the spectrum are not counted)")
         total_flops = float(sum(eig_route_flops(n, n, k, 2, chi, 2 * chi, chi) for k in ks)
                             + sum(8.0 * n * n * k for k in ks))
     else:
@@ -436,8 +445,8 @@ def run_chi(chi, G, steps, warmup, rank, world, dev, clocks=True):
     rec = {
         "value": world * G / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "steps": steps, "warmup": warmup,
         "count": G, "chi": chi, "theta": "%dx%d" % (n, n),
-        "svd_regime": "large (FP64 Gram eigensolver)" if eig else {0: "small", 1: "large (tcgen05)", 2: "medium",
-                                                                    3: "QR-preconditioned"}[regime],
+        "svd_regime": ({1: "large (FP64 Gram eigensolver)", 3: "QR-size (one-CTA FP64 Gram eigensolver)"}[regime] if eig
+                       else {0: "small", 1: "large (tcgen05)", 2: "medium", 3: "QR-preconditioned"}[regime]),
         "tflops_executed": total_flops / (ms_step / 1e3) / 1e12 * world,
         "sweeps_mean": float(sweeps.mean()), "k_mean": float(ks.mean()),
         "phase_ms_per_step": {p: v[0] / max(1, steps) for p, v in phases.items()},

@@ -44,6 +44,8 @@ struct LayerJob {                  // the layer in flight (mps_layer_begin / mps
   size_t o_rsm = 0, rsm_smem = 0;
   std::vector<int32_t> eigl;         // wave-local gates of the eigen route (refine_large.cu)
   size_t o_eigl = 0;
+  std::vector<int32_t> eigs;         // ... its one-CTA form for QR-regime thetas (n <= 128)
+  size_t o_eigs = 0;
   bool ran[5] = {false, false, false, false, false};
 };
 
@@ -385,7 +387,7 @@ mps_status wave_front_impl(mps_t h) {
   int g1 = g0;
   while (g1 < G) {
     const int cnt = g1 - g0 + 1;
-    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 4 * align_up(4 * cnt) +
+    size_t fx = align_up(sizeof(GateDesc) * cnt) + 4 * align_up(4 * (cnt + 1)) + 5 * align_up(4 * cnt) +
                 align_up((size_t)cnt * d4 * 8) + align_up(sizeof(Record) * cnt) + align_up(32 * (size_t)cnt + 64 + 24576);
     size_t w2 = ws + plan[g1].ws, r2 = reserve + plan[g1].reserve;
     if (bump + r2 + fx + w2 + kAlign > top) break;
@@ -415,6 +417,7 @@ mps_status wave_front_impl(mps_t h) {
   const size_t o_large = take(4 * Gw);
   const size_t o_rsm = take(4 * Gw);
   const size_t o_eigl = take(4 * Gw);
+  const size_t o_eigs = take(4 * Gw);
   const size_t o_us = take((size_t)Gw * d4 * 8);
   const size_t o_rec = take(sizeof(Record) * Gw);
   const size_t o_scr = take(32 * (size_t)Gw + 64 + 24576);
@@ -422,6 +425,8 @@ mps_status wave_front_impl(mps_t h) {
   std::vector<int32_t> cpre(Gw + 1, 0), small, large;
   std::vector<int32_t>& eigl = J.eigl;
   eigl.clear();
+  std::vector<int32_t>& eigs = J.eigs;
+  eigs.clear();
   J.rsm.clear();
   J.rsm_smem = 0;
   J.rpre.assign(Gw + 1, 0);
@@ -462,6 +467,7 @@ mps_status wave_front_impl(mps_t h) {
         gpre[x + 1] = gpre[x] + p.gtiles;
         apre[x + 1] = apre[x] + p.atiles;
         if (gd.regime == 1) (gd.eig ? eigl : large).push_back(x);
+        else if (gd.eig) eigs.push_back(x);
         if (!J.rsm.empty() && J.rsm.back() == x - 1) J.rsm.push_back(x);   // same shape as gate x - 1
         continue;
       }
@@ -481,6 +487,7 @@ mps_status wave_front_impl(mps_t h) {
     gd.ws_E = (int64_t)take(std::max(kmn * kmn * 8, (gd.regime == 1 || gd.regime == 3) ? (size_t)16 * gd.n_pad : (size_t)0));
     gd.ws_log = gd.regime == 2   ? (int64_t)take((size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16)
                 : gd.regime == 1 ? (int64_t)take(large_scratch_bytes(gd))
+                : (gd.regime == 3 && gd.eig) ? (int64_t)take(refine_large_scratch(gd.m, gd.n))
                 : (gd.regime == 3 && gd.jrows > 0) ? (int64_t)take(large_precond_scratch(gd.n))
                 : refine_scratch_bytes(gd.n) > 0 ? (int64_t)take(refine_scratch_bytes(gd.n))
                                  : 0;
@@ -491,6 +498,7 @@ mps_status wave_front_impl(mps_t h) {
     gpre[x + 1] = gpre[x] + p.gtiles;
     apre[x + 1] = apre[x] + p.atiles;
     if (gd.regime == 1) (gd.eig ? eigl : large).push_back(x);
+    else if (gd.eig) eigs.push_back(x);
     if (reabsorb_small_fits(gd.m, gd.n)) {
       J.rsm.push_back(x);
       J.rsm_smem = std::max(J.rsm_smem, reabsorb_small_smem(gd.m, gd.n));
@@ -512,7 +520,7 @@ mps_status wave_front_impl(mps_t h) {
     for (int x = 0; x < Gw; ++x) {
       const GateDesc& gd = hd[x];
       int reg = gd.regime, gt = 0, rpl = 0, pk = 0, cls = 0;
-      if (reg == 1) continue;
+      if (reg == 1 || gd.eig) continue;   // large regime / eigen route: not bucketed
       if (gd.m == last_m && gd.n == last_n && reg == last_reg) {
         keyed[last_slot].second.push_back(x);
         continue;
@@ -594,7 +602,7 @@ mps_status wave_front_impl(mps_t h) {
   if (cur > top) return set_err(h, MPS_E_NOMEM, "workspace planning overflow");
   {   // every gate of the small / medium / QR regimes must sit in exactly one bucket
     size_t want = 0;
-    for (int x = 0; x < Gw; ++x) want += hd[x].regime != 1;
+    for (int x = 0; x < Gw; ++x) want += hd[x].regime != 1 && !hd[x].eig;
     if (want != small.size()) return set_err(h, MPS_E_STATE, "internal: SVD bucketing lost a gate");
   }
   // stage desc | prefixes | lists | gates in one pinned buffer, one H2D copy
@@ -611,6 +619,8 @@ mps_status wave_front_impl(mps_t h) {
   if (!large.empty()) std::memcpy(hb + (o_large - base), large.data(), 4 * large.size());
   if (!eigl.empty()) std::memcpy(hb + (o_eigl - base), eigl.data(), 4 * eigl.size());
   J.o_eigl = o_eigl;
+  if (!eigs.empty()) std::memcpy(hb + (o_eigs - base), eigs.data(), 4 * eigs.size());
+  J.o_eigs = o_eigs;
   if (!J.rsm.empty()) std::memcpy(hb + (o_rsm - base), J.rsm.data(), 4 * J.rsm.size());
   J.o_rsm = o_rsm;
   for (int x = 0; x < Gw; ++x)
@@ -679,6 +689,25 @@ mps_status wave_front_impl(mps_t h) {
       h->launches += 2;
     }
     CKL("svd_small/medium");
+  }
+  // a2 + a3, the eigen route for QR-regime thetas (n <= 128): one CTA per gate; a spectrum deeper than
+  // 2e-4 sigma_max gets all its eigenvectors now and the FP64 Rayleigh-Ritz refinement below
+  if (!eigs.empty()) {
+    const int32_t* d_eigs = reinterpret_cast<const int32_t*>(h->slab + o_eigs);
+    const int e0 = prof ? prof_mark(h) : -1;
+    RlgMarks mk{[](void* c) { return prof_mark(static_cast<mps_t>(c)); }, h, {-1, -1}};
+    h->launches += launch_eig_small_front(d_desc, hd.data(), eigs.data(), d_eigs, (int)eigs.size(), h->slab, h->dst,
+                                          d_us, d, reinterpret_cast<int32_t*>(h->slab + o_scr) + Gw + 2, h->s,
+                                          prof ? &mk : nullptr);
+    CKL("eig_small_front");
+    h->launches += launch_eig_vectors(d_desc, hd.data(), eigs.data(), d_eigs, (int)eigs.size(), h->slab, h->s, 2);
+    CKL("eig_small_vectors_deep");
+    if (prof && mk.at[0] >= 0) {   // [8] the one-CTA eigensolver, [9] the rest
+      const int e1 = prof_mark(h);
+      prof_span(h, 9, e0, mk.at[0]);
+      prof_span(h, 8, mk.at[0], mk.at[1]);
+      prof_span(h, 9, mk.at[1], e1);
+    }
   }
   if (prof) CK(cudaEventRecord(h->ev[2], h->s));
   // a2 + a3, the eigen route (large regime, 256 < n <= 2048): sigma^2 = eigenvalues of the FP64 Gram
@@ -774,8 +803,16 @@ mps_status wave_back(mps_t h) {
     const int e0 = prof ? prof_mark(h) : -1;
     h->launches += launch_eig_vectors(d_desc, hd.data(), J.eigl.data(),
                                       reinterpret_cast<const int32_t*>(h->slab + J.o_eigl), (int)J.eigl.size(),
-                                      h->slab, h->s);
+                                      h->slab, h->s, 1);
     CKL("eig_vectors");
+    if (prof) prof_span(h, 9, e0, prof_mark(h));
+  }
+  if (!J.eigs.empty()) {
+    const int e0 = prof ? prof_mark(h) : -1;
+    h->launches += launch_eig_vectors(d_desc, hd.data(), J.eigs.data(),
+                                      reinterpret_cast<const int32_t*>(h->slab + J.o_eigs), (int)J.eigs.size(),
+                                      h->slab, h->s, 1);
+    CKL("eig_small_vectors");
     if (prof) prof_span(h, 9, e0, prof_mark(h));
   }
   if (prof) CK(cudaEventRecord(h->ev[4], h->s));
@@ -1153,9 +1190,10 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
     if (gd.regime == 3 && !qr_hh) gd.jrows = gd.n;
     // large regime, 256 < n <= 2048: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps)
-    gd.eig = (!h->jacobi_only && eig_route(gd)) ? 1 : 0;
+    gd.eig = (!h->jacobi_only && (eig_route(gd) || eig_route_small(gd))) ? 1 : 0;
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                         : gd.regime == 1 ? large_scratch_bytes(gd)
+                        : (gd.regime == 3 && gd.eig) ? refine_large_scratch(gd.m, gd.n)
                         : (gd.regime == 3 && gd.jrows > 0) ? large_precond_scratch(gd.n)
                                          : refine_scratch_bytes(gd.n);
     gd.u_index = ord[g].second;

@@ -171,8 +171,6 @@ int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* s
 // FP64 eigenvalues of the Gram of the FP64-recontracted theta for deep large-regime gates with
 // 256 < n <= 2048 (refine_large.cu). cand = the wave's large-regime gates (host and device copies);
 // iscr: wave scratch of 2 nc + 2 ints + 19 KB (barrier lines). Returns launches issued.
-bool refine_large_candidate(const GateDesc& gd);
-bool eig_route(const GateDesc& gd);
 // profiling hook: mark(ctx) records an event on the stream and returns its id (or -1); the front
 // stores the ids taken just before and after the tridiagonalisation kernel in at[0], at[1]
 struct RlgMarks {
@@ -180,11 +178,18 @@ struct RlgMarks {
   void* ctx;
   mutable int at[2];
 };
+bool refine_large_candidate(const GateDesc& gd);
+bool eig_route(const GateDesc& gd);
 int launch_eig_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
                      uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, int32_t* fb,
                      cudaStream_t s, const RlgMarks* mk);
 int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
-                       uint8_t* slab, cudaStream_t s);
+                       uint8_t* slab, cudaStream_t s, int want);
+// the eigen route for QR-regime thetas (n <= 128): one CTA per gate (refine_large.cu, k_eig_cta)
+bool eig_route_small(const GateDesc& gd);
+int launch_eig_small_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand,
+                           int nc, uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr,
+                           cudaStream_t s, const struct RlgMarks* mk);
 size_t refine_large_scratch(int m, int n);
 int launch_refine_large(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
                         uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr, cudaStream_t s);

@@ -305,6 +305,7 @@ __global__ void k_refine_pick(const GateDesc* __restrict__ desc, const uint8_t* 
   const GateDesc& gd = desc[g];
   const int n = gd.n;
   if (n > kRefineMaxN || n < 2) return;
+  if (gd.eig == 1) return;   // eigen route: V not formed yet (its too-deep gates come as eig = 2, V complete)
   const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);   // sorted descending
   const double smax = gS[0];
   // the deepest sigma^2 >= 1e-12 sigma_max^2: the last j with gS[j] >= 1e-12 smax (sorted)

@@ -772,9 +772,9 @@ __global__ void __launch_bounds__(256) k_rlg_finish(GateDesc* __restrict__ desc,
 // (accurate to a few ulps of ||T||), so y_j is accurate to ~eps64 ||T|| / gap_j in angle. One thread
 // per vector, kSlots factor slots per gate; row j of Y = y_j.
 __global__ void __launch_bounds__(32) k_rlg_invit(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
-                                                  uint8_t* slab) {
+                                                  uint8_t* slab, int want) {
   const GateDesc& gd = desc[cand[blockIdx.y]];
-  if (!gd.eig) return;
+  if (gd.eig != want) return;
   const int n = gd.n, k = gd.k;
   const int slot = blockIdx.x * 32 + threadIdx.x;
   if (slot >= k) return;
@@ -856,9 +856,9 @@ __global__ void __launch_bounds__(32) k_rlg_invit(const GateDesc* __restrict__ d
 // different starts returns independent vectors of the cluster's invariant subspace; modified
 // Gram-Schmidt makes them orthonormal. One CTA per gate (most gates have no cluster).
 __global__ void __launch_bounds__(256) k_rlg_mgs(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
-                                                 uint8_t* slab) {
+                                                 uint8_t* slab, int want) {
   const GateDesc& gd = desc[cand[blockIdx.x]];
-  if (!gd.eig) return;
+  if (gd.eig != want) return;
   const int n = gd.n, k = gd.k;
   const RlgLayout L = rlg_layout(gd);
   const double* gS = reinterpret_cast<const double*>(slab + gd.ws_sig2);
@@ -892,11 +892,16 @@ __global__ void __launch_bounds__(256) k_rlg_mgs(const GateDesc* __restrict__ de
 // column q of the factorised G, entries q+1 .. n-1), then V[:, j] = z_j in FP32 (unit norm: Q unitary).
 // kVpc vectors per CTA in shared memory; each thread owns the same rows of every vector, so only the
 // dot products v_q^H z need the CTA (one barrier per reflector, double-buffered partials).
-constexpr int kVpc = 4;
+// VPC vectors per CTA, RPT rows per thread (n <= 256 RPT): (16, 2) for n <= 512, (8, 4) for n <= 1024,
+// (4, 8) for n <= 2048 -- the shared-memory z stays <= 128 KB and each reflector's loads and barrier
+// serve as many vectors as fit.
+constexpr int kVpc = 4;   // the largest-n configuration (attribute sizing)
+template <int VPC, int RPT>
 __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
-                                                    uint8_t* slab) {
+                                                    uint8_t* slab, int want) {
+  constexpr int kVpc = VPC;
   const GateDesc& gd = desc[cand[blockIdx.y]];
-  if (!gd.eig) return;
+  if (gd.eig != want) return;
   const int n = gd.n, k = gd.k, np = gd.n_pad;
   const int j0 = blockIdx.x * kVpc;
   if (j0 >= k) return;
@@ -915,7 +920,7 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
   // thread tid owns rows i = tid + 256 q (q < kRowsPT): the same rows of z for every r, so the update
   // and the next dot product need no barrier between them; reflector r-1's entries of those rows are
   // loaded while reflector r is applied (its L2 latency off the per-reflector critical path)
-  constexpr int kRowsPT = kMaxN / 256;
+  constexpr int kRowsPT = RPT;
   double2 cur[kRowsPT], nxt[kRowsPT];
   auto load_col = [&](int r, double2* dst) {
 #pragma unroll
@@ -987,6 +992,227 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
     }
 }
 
+// ---- the eigen route for n <= 128 (QR-regime thetas, config 2 chi = 64): one CTA per gate, G in
+// shared memory (packed lower triangle, 132 KB at n = 128). Same recurrences as k_rlg_tridiag /
+// k_rlg_bisect / k_rlg_finish (zhetd2, Sturm counts), the reflectors stored to the gate's tile-layout G
+// columns and tau array exactly as k_rlg_tridiag does, so k_rlg_invit / k_rlg_mgs / k_rlg_backtr serve
+// both. Depth check: a spectrum reaching below kEigMinSmall sigma_max (sigma >= 1e-6 sigma_max) is
+// flagged (desc.eig = 2, k = n): all its eigenvectors are computed before the select and the FP64
+// Rayleigh-Ritz refinement (refine.cu, relative accuracy) replaces its sigma.
+constexpr int kSmallMaxN = 128;
+constexpr double kEigMinSmall = 2e-4;   // = refine.cu's trigger: deeper spectra get the relative-accurate RR
+__host__ __device__ inline int pk_lo(int i, int j) { return i * (i + 1) / 2 + j; }   // j <= i
+size_t eig_cta_smem(int n) {
+  return (size_t)n * (n + 1) / 2 * 16 + (size_t)3 * n * 16 + (size_t)4 * n * 8 + 64 * 8 + 256 * 8 + 128;
+}
+
+__global__ void __launch_bounds__(256, 1) k_eig_cta(GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+                                                    uint8_t* slab, int32_t* fb) {
+  GateDesc& gdr = desc[cand[blockIdx.x]];
+  if (gdr.eig != 1) return;
+  const GateDesc gd = gdr;
+  const int n = gd.n;
+  const RlgLayout L = rlg_layout(gd);
+  double2* G = reinterpret_cast<double2*>(slab + L.g);
+  double* dg = reinterpret_cast<double*>(slab + L.d);
+  double* eg = reinterpret_cast<double*>(slab + L.e);
+  double* eig = reinterpret_cast<double*>(slab + L.eig);
+  double2* taug = reinterpret_cast<double2*>(slab + L.tau);
+  extern __shared__ __align__(16) uint8_t sm[];
+  double2* A = reinterpret_cast<double2*>(sm);                         // packed lower
+  double2* v = A + n * (n + 1) / 2;
+  double2* w = v + n;
+  double2* p = w + n;
+  double* ds = reinterpret_cast<double*>(p + n);
+  double* e2 = ds + n;
+  double* keys = e2 + n;                                               // 2 n doubles (sort-free: ascending -> desc)
+  double* red = keys + 2 * n;                                          // 64
+  double* part = red + 64;                                             // 256
+  __shared__ double2 s_sc;
+  __shared__ int s_deep;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = warp; i < n; i += 8)
+    for (int j = lane; j <= i; j += 32) A[pk_lo(i, j)] = G[g_at(i, j)];
+  __syncthreads();
+  for (int k = 0; k < n - 1; ++k) {
+    const int k1 = k + 1;
+    double part2 = 0.0;
+    for (int i = k1 + tid; i < n; i += 256) {
+      const double2 x = A[pk_lo(i, k)];
+      v[i] = x;
+      if (i >= k + 2) part2 += x.x * x.x + x.y * x.y;
+    }
+    const double xn2 = cta_sum(part2, red);
+    const double2 al = v[k1];
+    double2 tau;
+    double beta;
+    double2 scale = make_double2(0.0, 0.0);
+    if (xn2 == 0.0 && al.y == 0.0) {
+      tau = make_double2(0.0, 0.0);
+      beta = al.x;
+    } else {
+      beta = -copysign(sqrt(al.x * al.x + al.y * al.y + xn2), al.x);
+      tau = make_double2((beta - al.x) / beta, -al.y / beta);
+      const double2 den = make_double2(al.x - beta, al.y);
+      const double dd = den.x * den.x + den.y * den.y;
+      scale = make_double2(den.x / dd, -den.y / dd);
+    }
+    if (tid == 0) {
+      ds[k] = A[pk_lo(k, k)].x;
+      e2[k] = beta;          // beta for now (squared below)
+      taug[k] = tau;
+    }
+    __syncthreads();
+    for (int i = k + 2 + tid; i < n; i += 256) v[i] = cmul(v[i], scale);
+    if (tid == 0) v[k1] = make_double2(1.0, 0.0);
+    __syncthreads();
+    // p = tau A22 v: two threads per row (even / odd j), A22 Hermitian from the packed lower triangle
+    {
+      const int i = k1 + (tid >> 1), h = tid & 1;
+      double2 acc = make_double2(0.0, 0.0);
+      if (i < n) {
+        for (int j = k1 + h; j < n; j += 2) {
+          const double2 a = j <= i ? A[pk_lo(i, j)] : make_double2(A[pk_lo(j, i)].x, -A[pk_lo(j, i)].y);
+          const double2 vj = v[j];
+          acc.x = fma(a.x, vj.x, fma(-a.y, vj.y, acc.x));
+          acc.y = fma(a.x, vj.y, fma(a.y, vj.x, acc.y));
+        }
+      }
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      if (i < n && h == 0) p[i] = cmul(tau, acc);
+    }
+    // the reflector for the back-transformation (column k of the tile-layout G, as k_rlg_tridiag)
+    for (int i = k1 + tid; i < n; i += 256) G[g_at(i, k)] = v[i];
+    __syncthreads();
+    double2 pd = make_double2(0.0, 0.0);
+    for (int i = k1 + tid; i < n; i += 256) {
+      const double2 c = cmulc(p[i], v[i]);
+      pd.x += c.x;
+      pd.y += c.y;
+    }
+    const double2 dot = cta_sum2(pd, reinterpret_cast<double2*>(red));
+    const double2 t = cmul(tau, dot);
+    const double2 alpha = make_double2(-0.5 * t.x, -0.5 * t.y);
+    for (int i = k1 + tid; i < n; i += 256) {
+      const double2 av = cmul(alpha, v[i]);
+      w[i] = make_double2(p[i].x + av.x, p[i].y + av.y);
+    }
+    __syncthreads();
+    // A22 -= v w^H + w v^H (packed lower)
+    for (int i = k1 + warp; i < n; i += 8) {
+      const double2 vi = v[i], wi = w[i];
+      for (int j = k1 + lane; j <= i; j += 32) {
+        const double2 t1 = cmulc(w[j], vi), t2 = cmulc(v[j], wi);
+        double2& a = A[pk_lo(i, j)];
+        a.x -= t1.x + t2.x;
+        a.y -= t1.y + t2.y;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) ds[n - 1] = A[pk_lo(n - 1, n - 1)].x;
+  __syncthreads();
+  // d, e to global (inverse iteration), e^2 for the Sturm counts
+  for (int i = tid; i < n; i += 256) {
+    dg[i] = ds[i];
+    if (i < n - 1) {
+      eg[i] = e2[i];
+      e2[i] = e2[i] * e2[i];
+    } else {
+      e2[i] = 0.0;
+    }
+  }
+  __syncthreads();
+  // Gershgorin interval
+  double lo = 1e300, hi = -1e300, emax = 0.0;
+  for (int i = tid; i < n; i += 256) {
+    const double el = i > 0 ? sqrt(e2[i - 1]) : 0.0, er = i < n - 1 ? sqrt(e2[i]) : 0.0;
+    lo = fmin(lo, ds[i] - el - er);
+    hi = fmax(hi, ds[i] + el + er);
+    emax = fmax(emax, e2[i]);
+  }
+  {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+      red[warp] = lo;
+      red[8 + warp] = hi;
+      red[16 + warp] = emax;
+    }
+    __syncthreads();
+    for (int q = 0; q < 8; ++q) {
+      lo = fmin(lo, red[q]);
+      hi = fmax(hi, red[8 + q]);
+      emax = fmax(emax, red[16 + q]);
+    }
+  }
+  const double span = fmax(fabs(lo), fabs(hi));
+  lo -= 2.0 * 2.2e-16 * span * n + 1e-300;
+  hi += 2.0 * 2.2e-16 * span * n + 1e-300;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+  // 2 lanes per eigenvalue, 2 points per lane: 5-section per pass
+  {
+    const int j = tid >> 1, sub = tid & 1;
+    const bool act = j < n;
+    for (int it = 0; it < 40; ++it) {   // 5^40 > 2^92
+      const double wdt = hi - lo;
+      if (__all_sync(0xffffffffu, wdt <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300)) break;
+      const double x1 = lo + wdt * (2 * sub + 1) / 5.0, x2 = lo + wdt * (2 * sub + 2) / 5.0;
+      double q1 = ds[0] - x1, q2 = ds[0] - x2;
+      int c1 = q1 < 0.0, c2 = q2 < 0.0;
+      for (int i = 1; i < n; ++i) {
+        const double ee = e2[i - 1], di = ds[i];
+        if (fabs(q1) < pivmin) q1 = -pivmin;
+        if (fabs(q2) < pivmin) q2 = -pivmin;
+        q1 = (di - x1) - ee / q1;
+        q2 = (di - x2) - ee / q2;
+        c1 += q1 < 0.0;
+        c2 += q2 < 0.0;
+      }
+      unsigned int mask = ((act && c1 > j) ? 1u : 0u) << (2 * sub) | ((act && c2 > j) ? 2u : 0u) << (2 * sub);
+      mask |= __shfl_xor_sync(0xffffffffu, mask, 1);
+      const int pp = mask ? __ffs(mask) - 1 : 4;
+      const double nlo = pp == 0 ? lo : lo + wdt * pp / 5.0;
+      const double nhi = pp == 4 ? hi : lo + wdt * (pp + 1) / 5.0;
+      lo = nlo;
+      hi = nhi;
+    }
+    if (act && sub == 0) keys[j] = 0.5 * (lo + hi);   // ascending
+  }
+  if (tid == 0) s_deep = 0;
+  __syncthreads();
+  // sigma^2 descending, pi = identity, tails, depth check
+  double* gS = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  int32_t* gP = reinterpret_cast<int32_t*>(slab + gd.ws_pi);
+  double* desc_keys = keys + n;
+  const double smax = fmax(keys[n - 1], 0.0);
+  for (int j = tid; j < n; j += 256) {
+    eig[j] = keys[j];
+    const double vv = fmax(keys[n - 1 - j], 0.0);
+    desc_keys[j] = vv;
+    gS[j] = vv;
+    gP[j] = j;
+    if (vv >= 1e-12 * smax && vv < kEigMinSmall * kEigMinSmall * smax) s_deep = 1;
+  }
+  __syncthreads();
+  cta_tails(desc_keys, n, reinterpret_cast<double*>(slab + gd.ws_T), part);
+  if (tid == 0) {
+    gdr.sweeps = 0;
+    if (s_deep) {          // all eigenvectors now, then the relative-accurate refinement (refine.cu)
+      gdr.eig = 2;
+      gdr.k = n;
+    }
+    if (fb) fb[blockIdx.x] = s_deep;
+  }
+  (void)s_sc;
+}
+
 }  // namespace
 
 bool refine_large_candidate(const GateDesc& gd) { return gd.regime == 1 && gd.n >= kMinN && gd.n <= kMaxN; }
@@ -1038,7 +1264,6 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
     cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    cudaFuncSetAttribute(k_rlg_backtr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kVpc * kMaxN * 16));
   }
   if (d == 2)
     k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
@@ -1106,19 +1331,82 @@ int launch_eig_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_
 
 // The eigen route's right singular vectors for the kept k (after the select): inverse iteration
 // on T, cluster MGS, back-transformation into V (FP32, columns 0 .. k-1).
+// want: the gates whose desc.eig == want (1: the kept k after the select; 2: every column, before
+// the refinement of a too-deep small spectrum). The host copy only bounds the grid.
 int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand, int nc,
-                       uint8_t* slab, cudaStream_t s) {
+                       uint8_t* slab, cudaStream_t s, int want) {
   int max_n = 0;
   for (int c = 0; c < nc; ++c)
     if (h_desc[h_cand[c]].eig) max_n = std::max(max_n, h_desc[h_cand[c]].n);
   if (max_n == 0) return 0;
-  k_rlg_invit<<<dim3(kSlots / 32, nc), 32, 0, s>>>(d_desc, d_cand, slab);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(k_rlg_backtr<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 512 * 16);
+    cudaFuncSetAttribute(k_rlg_backtr<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 1024 * 16);
+    cudaFuncSetAttribute(k_rlg_backtr<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2048 * 16);
+  }
+  k_rlg_invit<<<dim3(kSlots / 32, nc), 32, 0, s>>>(d_desc, d_cand, slab, want);
   rl_dbg(s, "k_rlg_invit");
-  k_rlg_mgs<<<nc, 256, 0, s>>>(d_desc, d_cand, slab);
+  k_rlg_mgs<<<nc, 256, 0, s>>>(d_desc, d_cand, slab, want);
   rl_dbg(s, "k_rlg_mgs");
-  k_rlg_backtr<<<dim3((max_n + kVpc - 1) / kVpc, nc), 256, (size_t)kVpc * max_n * 16, s>>>(d_desc, d_cand, slab);
+  if (max_n <= 512)
+    k_rlg_backtr<16, 2><<<dim3((max_n + 15) / 16, nc), 256, (size_t)16 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
+  else if (max_n <= 1024)
+    k_rlg_backtr<8, 4><<<dim3((max_n + 7) / 8, nc), 256, (size_t)8 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
+  else
+    k_rlg_backtr<4, 8><<<dim3((max_n + 3) / 4, nc), 256, (size_t)4 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
   rl_dbg(s, "k_rlg_backtr");
   return 3;
+}
+
+// Opt-in (EAMPS_EIG_SMALL=1): measured slower than the QR-regime Jacobi it would replace (config 2
+// chi = 64 x 4096, one B200: 40.3K vs 71.5K updates/s; k_eig_cta 17 ms per 4096 gates, the FP64
+// recontraction + Gram and the kept-vector back-transformation another ~60 ms) -- the block-recursive
+// FP32 Jacobi runs at 0.57 of the FP32 SIMT peak, the one-CTA FP64 eigensolver at 0.04 of FP64.
+bool eig_route_small(const GateDesc& gd) {
+  static const bool on = getenv("EAMPS_EIG_SMALL") != nullptr && getenv("EAMPS_NO_EIG") == nullptr;
+  return on && gd.regime == 3 && gd.n <= kSmallMaxN && gd.m >= gd.n;
+}
+
+// The eigen route's front for n <= 128 (QR-regime thetas): theta64, G (tile layout), then one CTA
+// per gate (k_eig_cta). Gates flagged too deep get eig = 2 (all vectors before the refinement).
+int launch_eig_small_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, const int32_t* d_cand,
+                           int nc, uint8_t* slab, DevState* st, const float2* d_us, int d, int32_t* iscr,
+                           cudaStream_t s, const RlgMarks* mk) {
+  int max_tiles = 0, max_gram = 0, max_n = 0;
+  for (int c = 0; c < nc; ++c) {
+    const GateDesc& g = h_desc[h_cand[c]];
+    if (!g.eig) continue;
+    const int T = 64 / d;
+    max_tiles = std::max(max_tiles, ((g.l + T - 1) / T) * ((g.r + T - 1) / T));
+    const int nt = (g.n + 63) / 64;
+    max_gram = std::max(max_gram, nt * (nt + 1) / 2);
+    max_n = std::max(max_n, g.n);
+  }
+  if (max_n == 0) return 0;
+  int32_t* flag = iscr;
+  int32_t* list = iscr + nc;
+  cudaMemsetAsync(list, 0, sizeof(int32_t), s);
+  k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list, 1);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(k_rlg_theta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_eig_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_cta_smem(kSmallMaxN));
+  }
+  if (d == 2)
+    k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  else
+    k_rlg_theta<4><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  rl_dbg(s, "k_rlg_theta (small)");
+  k_rlg_gram<<<dim3(max_gram, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab);
+  rl_dbg(s, "k_rlg_gram (small)");
+  if (mk) mk->at[0] = mk->mark(mk->ctx);
+  k_eig_cta<<<nc, 256, eig_cta_smem(max_n), s>>>(d_desc, d_cand, slab, nullptr);
+  if (mk) mk->at[1] = mk->mark(mk->ctx);
+  rl_dbg(s, "k_eig_cta");
+  return 4;
 }
 
 }  // namespace eamps

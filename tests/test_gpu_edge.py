@@ -134,6 +134,7 @@ def test_nonconvergence_is_reported_and_sticky():
     pk = _pk()
     tensors, gates = workloads.micro_chain(64, 1)
     gpu = pk.MPS(2, strategy="fixed", f_fixed=0.9999, max_sweeps=1, slab_bytes=256 << 20)
+    gpu.mps_set_svd_route(1)   # the Jacobi route (the eigen routes have no sweep limit to hit)
     gpu.mps_import_sites(0, tensors)
     with pytest.raises(pk.EampsError) as e:
         gpu.mps_apply_layer(np.zeros(1, np.int32), gates)
