@@ -351,8 +351,9 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
 // [4, 32], from the rows (small_group(m)) and the CTA width (2048 / n resp. 1024 / n lanes per pair)
 size_t large_scratch_bytes(const GateDesc& gd) {
   const size_t b = std::max(svd_tc_scratch_bytes(gd.n_pad), gd.jrows > 0 ? large_precond_scratch(gd.n) : (size_t)0);
-  // the FP64 spectrum of deep 256 < n <= 2048 gates (refine_large.cu) reuses the dead scratch
-  return refine_large_candidate(gd) ? std::max(b, refine_large_scratch(gd.m, gd.n)) : b;
+  // the eigen route (128 < n <= 2048) and the FP64 spectrum of deep 256 < n <= 2048 Jacobi-route
+  // gates (refine_large.cu) reuse the dead scratch
+  return (refine_large_candidate(gd) || eig_route(gd)) ? std::max(b, refine_large_scratch(gd.m, gd.n)) : b;
 }
 
 int lane_group(int m, int n, int reg) {
@@ -710,7 +711,7 @@ mps_status wave_front_impl(mps_t h) {
     }
   }
   if (prof) CK(cudaEventRecord(h->ev[2], h->s));
-  // a2 + a3, the eigen route (large regime, 256 < n <= 2048): sigma^2 = eigenvalues of the FP64 Gram
+  // a2 + a3, the eigen route (large regime, 128 < n <= 2048): sigma^2 = eigenvalues of the FP64 Gram
   // of the FP64-recontracted theta (refine_large.cu); a spectrum too deep for it (flag read back
   // here) goes to the Jacobi route below
   if (!eigl.empty()) {
@@ -1189,7 +1190,8 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // the in-CTA Householder QR instead)
     static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
     if (gd.regime == 3 && !qr_hh) gd.jrows = gd.n;
-    // large regime, 256 < n <= 2048: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps)
+    // large regime, 128 < n <= 2048: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps;
+    // measured 1.46x / 1.9x / 2.2x the Jacobi route at n = 256 / 512 / 2048)
     gd.eig = (!h->jacobi_only && (eig_route(gd) || eig_route_small(gd))) ? 1 : 0;
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16
                         : gd.regime == 1 ? large_scratch_bytes(gd)

@@ -56,7 +56,8 @@ void rl_dbg(cudaStream_t s, const char* what) {
   fprintf(stderr, "[eamps debug] after %s: %s\n", what, cudaGetErrorString(e));
 }
 
-constexpr int kMinN = 257, kMaxN = 2048;
+constexpr int kMinN = 257, kMaxN = 2048;   // the refinement of Jacobi spectra (n <= 256: refine.cu)
+constexpr int kEigMinN = 129;              // the eigen route
 // measured (config 2, r02): chi = 256 (n = 512, sigma_min/sigma_max = 8.6e-5) 2.8e-6 and chi = 512
 // (n = 1024, 3.1e-5) 5.8e-6 with Rayleigh + polish -- inside the 1e-5 bar; chi = 1024 (n = 2048,
 // 1.1e-5) 7.9e-4. The FP64 eigensolver runs for spectra deeper than 2e-5 sigma_max.
@@ -946,17 +947,34 @@ __global__ void __launch_bounds__(256) k_rlg_backtr(const GateDesc* __restrict__
         acc[q].y += c.y;
       }
     }
+    // transpose-reduce the kVpc per-lane partials over the warp: halving stages (offsets 16, 8, ..)
+    // leave lane L with vector q(L)'s sum over the lanes sharing its high bits, then a plain xor
+    // reduction over the remaining low bits -- kVpc - 1 + 5 - log2(kVpc) shuffle-adds instead of 5 kVpc
+    constexpr int S = kVpc >= 16 ? 4 : kVpc >= 8 ? 3 : kVpc >= 4 ? 2 : kVpc >= 2 ? 1 : 0;
 #pragma unroll
-    for (int q = 0; q < kVpc; ++q)
+    for (int st = 0; st < S; ++st) {
+      const int o = 16 >> st, half = kVpc >> (st + 1);
+      const bool hi = lane & o;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
-        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+      for (int j = 0; j < (kVpc >> 1); ++j) {
+        if (j >= half) break;
+        const double2 keep = hi ? acc[j + half] : acc[j], send = hi ? acc[j] : acc[j + half];
+        acc[j].x = keep.x + __shfl_xor_sync(0xffffffffu, send.x, o);
+        acc[j].y = keep.y + __shfl_xor_sync(0xffffffffu, send.y, o);
       }
-    const int b = r & 1;
-    if (lane == 0)
+    }
 #pragma unroll
-      for (int q = 0; q < kVpc; ++q) red[b][warp][q] = acc[q];
+    for (int o = 16 >> S; o >= 1; o >>= 1) {
+      acc[0].x += __shfl_xor_sync(0xffffffffu, acc[0].x, o);
+      acc[0].y += __shfl_xor_sync(0xffffffffu, acc[0].y, o);
+    }
+    const int b = r & 1;
+    if ((lane & ((32 >> S) - 1)) == 0) {
+      int qi = 0;
+#pragma unroll
+      for (int st = 0; st < S; ++st) qi = 2 * qi + ((lane >> (4 - st)) & 1);
+      red[b][warp][qi] = acc[0];
+    }
     __syncthreads();
     const double2 tau = taug[r];
     double2 f[kVpc];
@@ -1221,7 +1239,7 @@ bool refine_large_candidate(const GateDesc& gd) { return gd.regime == 1 && gd.n 
 // eigenvalues only refine deep spectra -- the A/B reference).
 bool eig_route(const GateDesc& gd) {
   static const bool off = getenv("EAMPS_NO_EIG") != nullptr;
-  return !off && refine_large_candidate(gd);
+  return !off && gd.regime == 1 && gd.n >= kEigMinN && gd.n <= kMaxN;
 }
 
 // must cover rlg_layout: g 16 n^2 | th 16 m n | d, e, eig 24 n | tau 16 n | p 32 n | part 32 KB |
@@ -1240,7 +1258,7 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   int max_tiles = 0, max_gram = 0, max_n = 0;
   for (int c = 0; c < nc; ++c) {
     const GateDesc& g = h_desc[h_cand[c]];
-    if (!refine_large_candidate(g) || (mode == 1 && !g.eig)) continue;
+    if (mode == 0 ? !refine_large_candidate(g) : !g.eig) continue;
     const int T = 64 / d;
     max_tiles = std::max(max_tiles, ((g.l + T - 1) / T) * ((g.r + T - 1) / T));
     const int nt = (g.n + 63) / 64;
@@ -1301,7 +1319,7 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   // the lanes per eigenvalue from the launch's parallelism (upper bound: every candidate picked)
   int tot_n = 0;
   for (int c = 0; c < nc; ++c)
-    if (refine_large_candidate(h_desc[h_cand[c]]) && (mode == 0 || h_desc[h_cand[c]].eig)) tot_n += h_desc[h_cand[c]].n;
+    if (mode == 0 ? refine_large_candidate(h_desc[h_cand[c]]) : h_desc[h_cand[c]].eig != 0) tot_n += h_desc[h_cand[c]].n;
   if (tot_n >= kBisWide)
     k_rlg_bisect<1><<<dim3((max_n + BT - 1) / BT, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
   else
