@@ -216,7 +216,7 @@ mps_status mps_last_sweeps(mps_t, int32_t g, int32_t* sweeps);
  * eigen route and the fused large regime). mps_set_profiling resets the accumulators. */
 mps_status mps_set_profiling(mps_t, int32_t on);
 /* SVD route of the large regime (a2, "performing its SVD"; reading 20):
- * route 0 (default) takes large-regime theta with 128 < n <= 2048 through the FP64 Gram eigensolver (sigma^2 =
+ * route 0 (default) takes large-regime theta with 128 < n <= 4096 through the FP64 Gram eigensolver (sigma^2 =
  * eigenvalues of theta^H theta, V for the kept columns by inverse iteration + back-transformation),
  * falling back to the Jacobi route for spectra deeper than 3e-6 sigma_max; route 1 takes every large
  * theta through the tcgen05 block Jacobi (+ the FP64 refinements). Applies from the next layer;

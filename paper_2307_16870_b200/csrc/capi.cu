@@ -351,7 +351,7 @@ mps_status put_lambda(mps_t h, int bond, const float* lam, int len, bool ones) {
 // [4, 32], from the rows (small_group(m)) and the CTA width (2048 / n resp. 1024 / n lanes per pair)
 size_t large_scratch_bytes(const GateDesc& gd) {
   const size_t b = std::max(svd_tc_scratch_bytes(gd.n_pad), gd.jrows > 0 ? large_precond_scratch(gd.n) : (size_t)0);
-  // the eigen route (128 < n <= 2048) and the FP64 spectrum of deep 256 < n <= 2048 Jacobi-route
+  // the eigen route (128 < n <= 4096) and the FP64 spectrum of deep 256 < n <= 4096 Jacobi-route
   // gates (refine_large.cu) reuse the dead scratch
   return (refine_large_candidate(gd) || eig_route(gd)) ? std::max(b, refine_large_scratch(gd.m, gd.n)) : b;
 }
@@ -711,7 +711,7 @@ mps_status wave_front_impl(mps_t h) {
     }
   }
   if (prof) CK(cudaEventRecord(h->ev[2], h->s));
-  // a2 + a3, the eigen route (large regime, 128 < n <= 2048): sigma^2 = eigenvalues of the FP64 Gram
+  // a2 + a3, the eigen route (large regime, 128 < n <= 4096): sigma^2 = eigenvalues of the FP64 Gram
   // of the FP64-recontracted theta (refine_large.cu); a spectrum too deep for it (flag read back
   // here) goes to the Jacobi route below
   if (!eigl.empty()) {
@@ -768,7 +768,7 @@ mps_status wave_front_impl(mps_t h) {
       const int e0 = prof ? prof_mark(h) : -1;
       h->launches += launch_refine(d_desc, Gw, maxn, h->slab, h->dst, d_us, reinterpret_cast<int32_t*>(h->slab + o_scr), h->s);
       CKL("refine");
-      // deep large-regime gates with 256 < n <= 2048: FP64 eigenvalues of the recontracted Gram
+      // deep large-regime gates with 256 < n <= 4096: FP64 eigenvalues of the recontracted Gram
       if (!large.empty()) {
         h->launches += launch_refine_large(d_desc, hd.data(), large.data(), d_large, (int)large.size(), h->slab, h->dst,
                                            d_us, d, reinterpret_cast<int32_t*>(h->slab + o_scr) + Gw + 2, h->s);
@@ -1190,7 +1190,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
     // the in-CTA Householder QR instead)
     static const bool qr_hh = getenv("EAMPS_QR_HOUSEHOLDER") != nullptr;
     if (gd.regime == 3 && !qr_hh) gd.jrows = gd.n;
-    // large regime, 128 < n <= 2048: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps;
+    // large regime, 128 < n <= 4096: the eigen route (FP64 Gram eigensolver, no Jacobi sweeps;
     // measured 1.46x / 1.9x / 2.2x the Jacobi route at n = 256 / 512 / 2048)
     gd.eig = (!h->jacobi_only && (eig_route(gd) || eig_route_small(gd))) ? 1 : 0;
     const size_t logb = gd.regime == 2   ? (size_t)gd.log_sweeps * (gd.n - 1) * (gd.n / 2) * 16

@@ -169,7 +169,7 @@ size_t refine_scratch_bytes(int n);
 int launch_refine(GateDesc* d_desc, int G, int max_n, uint8_t* slab, DevState* st, const float2* d_us,
                   int32_t* d_list /* G + 1 ints */, cudaStream_t s);
 // FP64 eigenvalues of the Gram of the FP64-recontracted theta for deep large-regime gates with
-// 256 < n <= 2048 (refine_large.cu). cand = the wave's large-regime gates (host and device copies);
+// 256 < n <= 4096 (refine_large.cu). cand = the wave's large-regime gates (host and device copies);
 // iscr: wave scratch of 2 nc + 2 ints + 19 KB (barrier lines). Returns launches issued.
 // profiling hook: mark(ctx) records an event on the stream and returns its id (or -1); the front
 // stores the ids taken just before and after the tridiagonalisation kernel in at[0], at[1]

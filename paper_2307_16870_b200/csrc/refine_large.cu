@@ -1,5 +1,5 @@
 // refine_large.cu -- FP64 spectrum of deep large-n spectra (steps a2/a3): the
-// singular values of theta for gates of the large regime with 256 < n <= 2048 whose spectrum is
+// singular values of theta for gates of the large regime with 256 < n <= 4096 whose spectrum is
 // deep, as the eigenvalues of the FP64 Gram G = theta^H theta of theta RECONTRACTED in FP64 from the
 // complex64 site tensors and gate.
 //
@@ -16,7 +16,7 @@
 // relative error ~1e-16 / (sigma_j / sigma_max)^2 = 1e-6 at 1.1e-5 (numpy/LAPACK on the chi = 1024
 // recipe: 9.4e-9 relative in sigma, this file's recurrence re-run in numpy: 3.8e-9); the FP64
 // recontraction removes the FP32 theta's own 2.6e-6.
-// What (one wave; gates picked on the device, at most 2048 columns):
+// What (one wave; gates picked on the device, at most 4096 columns):
 //   k_rlg_pick     the trigger (deepest sigma >= 1e-6 sigma_max below kRatio sigma_max)
 //   k_rlg_theta    theta64[(a,s),(t,c)] = lambda_a sum_{s',t'} U[s d+t, s' d+t'] sum_b B_i[a,s',b] B_{i+1}[b,t',c]
 //                  (E2 of PAPER.md:32-41 / contract.cu with FP64 products and sums)
@@ -56,7 +56,7 @@ void rl_dbg(cudaStream_t s, const char* what) {
   fprintf(stderr, "[eamps debug] after %s: %s\n", what, cudaGetErrorString(e));
 }
 
-constexpr int kMinN = 257, kMaxN = 2048;   // the refinement of Jacobi spectra (n <= 256: refine.cu)
+constexpr int kMinN = 257, kMaxN = 4096;   // the refinement of Jacobi spectra (n <= 256: refine.cu)
 constexpr int kEigMinN = 129;              // the eigen route
 // measured (config 2, r02): chi = 256 (n = 512, sigma_min/sigma_max = 8.6e-5) 2.8e-6 and chi = 512
 // (n = 1024, 3.1e-5) 5.8e-6 with Rayleigh + polish -- inside the 1e-5 bar; chi = 1024 (n = 2048,
@@ -660,7 +660,9 @@ __global__ void __launch_bounds__(BT) k_rlg_bisect(const GateDesc* __restrict__ 
   const double* dg = reinterpret_cast<const double*>(slab + L.d);
   const double* eg = reinterpret_cast<const double*>(slab + L.e);
   double* eig = reinterpret_cast<double*>(slab + L.eig);
-  __shared__ double ds[kMaxN], e2s[kMaxN];
+  extern __shared__ __align__(16) uint8_t bis_sm[];
+  double* ds = reinterpret_cast<double*>(bis_sm);     // n
+  double* e2s = ds + n;                               // n
   __shared__ double red[3][BT / 32];
   double lo = 1e300, hi = -1e300, emax = 0.0;
   for (int i = threadIdx.x; i < n; i += BT) {
@@ -1282,6 +1284,8 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
     cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    cudaFuncSetAttribute(k_rlg_bisect<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kMaxN);
+    cudaFuncSetAttribute(k_rlg_bisect<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kMaxN);
   }
   if (d == 2)
     k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
@@ -1320,10 +1324,11 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   int tot_n = 0;
   for (int c = 0; c < nc; ++c)
     if (mode == 0 ? refine_large_candidate(h_desc[h_cand[c]]) : h_desc[h_cand[c]].eig != 0) tot_n += h_desc[h_cand[c]].n;
+  const size_t bsm = (size_t)16 * max_n;
   if (tot_n >= kBisWide)
-    k_rlg_bisect<1><<<dim3((max_n + BT - 1) / BT, nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+    k_rlg_bisect<1><<<dim3((max_n + BT - 1) / BT, nc), BT, bsm, s>>>(d_desc, d_cand, flag, slab);
   else
-    k_rlg_bisect<8><<<dim3((max_n + BT / 8 - 1) / (BT / 8), nc), BT, 0, s>>>(d_desc, d_cand, flag, slab);
+    k_rlg_bisect<8><<<dim3((max_n + BT / 8 - 1) / (BT / 8), nc), BT, bsm, s>>>(d_desc, d_cand, flag, slab);
   rl_dbg(s, "k_rlg_bisect");
   k_rlg_finish<<<nc, 256, 0, s>>>(d_desc, d_cand, flag, slab, mode, fb);
   rl_dbg(s, "k_rlg_finish");
@@ -1362,6 +1367,7 @@ int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* 
     cudaFuncSetAttribute(k_rlg_backtr<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 512 * 16);
     cudaFuncSetAttribute(k_rlg_backtr<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 1024 * 16);
     cudaFuncSetAttribute(k_rlg_backtr<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2048 * 16);
+    cudaFuncSetAttribute(k_rlg_backtr<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 16);
   }
   k_rlg_invit<<<dim3(kSlots / 32, nc), 32, 0, s>>>(d_desc, d_cand, slab, want);
   rl_dbg(s, "k_rlg_invit");
@@ -1371,8 +1377,10 @@ int launch_eig_vectors(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* 
     k_rlg_backtr<16, 2><<<dim3((max_n + 15) / 16, nc), 256, (size_t)16 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
   else if (max_n <= 1024)
     k_rlg_backtr<8, 4><<<dim3((max_n + 7) / 8, nc), 256, (size_t)8 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
-  else
+  else if (max_n <= 2048)
     k_rlg_backtr<4, 8><<<dim3((max_n + 3) / 4, nc), 256, (size_t)4 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
+  else
+    k_rlg_backtr<2, 16><<<dim3((max_n + 1) / 2, nc), 256, (size_t)2 * max_n * 16, s>>>(d_desc, d_cand, slab, want);
   rl_dbg(s, "k_rlg_backtr");
   return 3;
 }

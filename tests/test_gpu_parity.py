@@ -166,7 +166,7 @@ def test_config2_chi256_blocked_path_parity():
 @pytest.mark.parametrize("chi,count", [(128, 2), (256, 2), (512, 1)])
 def test_config2_tensor_core_path_parity(chi, count):
     """the tcgen05 3xTF32 block Jacobi + FP64-anchored polish (large regime, chi >= 128 in config 2;
-    route 1 = the Jacobi route also for 128 < n <= 2048) at the strict bar: relative 1e-5 on every
+    route 1 = the Jacobi route also for 128 < n <= 4096) at the strict bar: relative 1e-5 on every
     sigma >= 1e-6 sigma_max (sigma_min / sigma_max = (2 chi)^-1.5 = 3e-5 at chi = 512), identical
     kept ranks, f to 1e-6."""
     gpu, orc, G = _micro(chi, count, route=1)
@@ -187,7 +187,7 @@ def _two_site(L, R):
 
 @pytest.mark.parametrize("chi,count", [(128, 2), (256, 2), (512, 1)])
 def test_config2_eigen_route_parity(chi, count):
-    """the eigen route (default for large-regime theta with 128 < n <= 2048, refine_large.cu): sigma^2 = FP64 eigenvalues of
+    """the eigen route (default for large-regime theta with 128 < n <= 4096, refine_large.cu): sigma^2 = FP64 eigenvalues of
     the Gram of the FP64-recontracted theta, the kept right singular vectors by inverse iteration +
     back-transformation. Strict bar on sigma, ranks and f; the reabsorbed two-site tensor
     B_i' diag(lambda) B_{i+1}' (gauge-invariant) equals the oracle's to 1e-5 relative, and the new
