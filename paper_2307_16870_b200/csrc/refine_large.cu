@@ -137,8 +137,8 @@ __global__ void k_rlg_pick(const GateDesc* __restrict__ desc, const uint8_t* sla
 constexpr int KC = 16;
 constexpr size_t kThetaSmem = (size_t)64 * 65 * sizeof(double2);
 
-template <int D>
-__global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rlg_theta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ cand,
                                                    const int32_t* __restrict__ flag, uint8_t* slab, const DevState* st,
                                                    const float2* __restrict__ us) {
   constexpr int TA = 64 / D, TC = 64 / D;
@@ -253,6 +253,21 @@ __global__ void __launch_bounds__(256) k_rlg_theta(const GateDesc* __restrict__ 
           }
         th[(int64_t)(t * r + c) * m + (a * D + s)] = make_double2(la * o.x, la * o.y);
       }
+  }
+}
+
+// EAMPS_THETA_MINB2=1: two CTAs per SM (128 registers, a few spills in the prologue) instead of one
+// (138 registers, no spills) -- A/B switch
+void launch_theta64(int d, int max_tiles, int nc, const GateDesc* d_desc, const int32_t* d_cand, const int32_t* flag,
+                    uint8_t* slab, const DevState* st, const float2* d_us, cudaStream_t s) {
+  static const bool one = getenv("EAMPS_THETA_MINB2") == nullptr;
+  const dim3 g(max_tiles, nc);
+  if (d == 2) {
+    if (one) k_rlg_theta<2, 1><<<g, 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+    else k_rlg_theta<2, 2><<<g, 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  } else {
+    if (one) k_rlg_theta<4, 1><<<g, 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+    else k_rlg_theta<4, 2><<<g, 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
   }
 }
 
@@ -1280,17 +1295,16 @@ int rlg_front(GateDesc* d_desc, const GateDesc* h_desc, const int32_t* h_cand, c
   static std::atomic<unsigned long long> attr{0};
   const size_t tsm = tridiag_smem(kMaxN);
   if (first_on_device(attr)) {
-    cudaFuncSetAttribute(k_rlg_theta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
-    cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     cudaFuncSetAttribute(k_rlg_bisect<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kMaxN);
     cudaFuncSetAttribute(k_rlg_bisect<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kMaxN);
   }
-  if (d == 2)
-    k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
-  else
-    k_rlg_theta<4><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  launch_theta64(d, max_tiles, nc, d_desc, d_cand, flag, slab, st, d_us, s);
   rl_dbg(s, "k_rlg_theta");
   k_rlg_gram<<<dim3(max_gram, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab);
   rl_dbg(s, "k_rlg_gram");
@@ -1416,15 +1430,14 @@ int launch_eig_small_front(GateDesc* d_desc, const GateDesc* h_desc, const int32
   k_rlg_pick<<<(nc + 7) / 8, 256, 0, s>>>(d_desc, slab, d_cand, nc, flag, list, 1);
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) {
-    cudaFuncSetAttribute(k_rlg_theta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
-    cudaFuncSetAttribute(k_rlg_theta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+    cudaFuncSetAttribute(k_rlg_theta<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_rlg_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
     cudaFuncSetAttribute(k_eig_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_cta_smem(kSmallMaxN));
   }
-  if (d == 2)
-    k_rlg_theta<2><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
-  else
-    k_rlg_theta<4><<<dim3(max_tiles, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab, st, d_us);
+  launch_theta64(d, max_tiles, nc, d_desc, d_cand, flag, slab, st, d_us, s);
   rl_dbg(s, "k_rlg_theta (small)");
   k_rlg_gram<<<dim3(max_gram, nc), 256, kThetaSmem, s>>>(d_desc, d_cand, flag, slab);
   rl_dbg(s, "k_rlg_gram (small)");
