@@ -50,16 +50,30 @@ __global__ void __launch_bounds__(256, 2) k_pc_gram(const GateDesc* __restrict__
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
-  for (int r0 = 0; r0 < m; r0 += 16) {
-    for (int x = tid; x < 16 * 64; x += 256) {
-      const int c = x >> 4, rr = x & 15, r = r0 + rr;
+  // the next 16-row chunk is fetched into registers while the current one multiplies (ncu r02: long
+  // scoreboard was the top stall with the fetch in front of every chunk)
+  float2 pi[4], pj[4];
+  auto fetch = [&](int r0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int x = tid + it * 256;
+      const int c = x >> 4, r = r0 + (x & 15);
       const int ci = ti * 64 + c, cj = tj * 64 + c;
-      const float2 vi = (r < m && ci < n) ? th[(int64_t)ci * m + r] : make_float2(0.f, 0.f);
-      const float2 vj = (r < m && cj < n) ? th[(int64_t)cj * m + r] : make_float2(0.f, 0.f);
-      Ai[rr][c] = make_double2(vi.x, vi.y);
-      Aj[rr][c] = make_double2(vj.x, vj.y);
+      pi[it] = (r < m && ci < n) ? th[(int64_t)ci * m + r] : make_float2(0.f, 0.f);
+      pj[it] = (r < m && cj < n) ? th[(int64_t)cj * m + r] : make_float2(0.f, 0.f);
+    }
+  };
+  fetch(0);
+  for (int r0 = 0; r0 < m; r0 += 16) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int x = tid + it * 256;
+      const int c = x >> 4, rr = x & 15;
+      Ai[rr][c] = make_double2(pi[it].x, pi[it].y);
+      Aj[rr][c] = make_double2(pj[it].x, pj[it].y);
     }
     __syncthreads();
+    if (r0 + 16 < m) fetch(r0 + 16);
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       double2 xi[4], yj[4];
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_panel(const GateDesc* __restric
 // columns: (1) every 32-row block of the panel gets G[i][panel] -= L[i][0:c0] L[panel][0:c0]^H;
 // (2) the diagonal block is factored in shared memory (pivots <= tau -> zero column) and inverted;
 // (3) the blocks below become X = G_blk L_JJ^-H = G_blk (L_JJ^-1)^H (a small GEMM, no serial solve).
-__global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(256, 3) k_pc_chol_cta(const GateDesc* __restrict__ desc, const int32_t* __restrict__ list,
                                                  uint8_t* slab) {
   const GateDesc& gd = desc[list[blockIdx.x]];
   if (gd.jrows <= 0) return;
@@ -313,7 +327,10 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
   __shared__ double s_red[8];
   __shared__ double s_rs[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rr = tid >> 3, cb = (tid & 7) * 4;    // 32 x 32 tile: row rr, columns cb .. cb+3
+  // 32 x 32 tile: row rr, columns cb + 8b (b < 4). Columns 8 apart, not 4 consecutive: the 8 threads of a
+  // shared-memory phase then read 8 consecutive rows of Bs / Mi (padded strides: distinct banks); with
+  // cb = 4 (tid & 7) they read rows 0, 4, .., 28, which share 2 bank groups (4-way conflicts, ncu r02).
+  const int rr = tid >> 3, cb = tid & 7;
   // pivot threshold tau = n eps64 max_i G_ii
   double dm = 0.0;
   for (int i = tid; i < n; i += 256) dm = fmax(dm, G[(int64_t)i * n + i].x);
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
       double2 acc[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int i = i0 + rr, j = c0 + cb + b;
+        const int i = i0 + rr, j = c0 + cb + 8 * b;
         acc[b] = (i < n && j < c0 + w) ? G[(int64_t)j * n + i] : make_double2(0.0, 0.0);
       }
       for (int k0 = 0; k0 < c0; k0 += 16) {       // k0 + 16 <= c0 (c0 is a multiple of 32)
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
           const double2 a = As[rr][kk];
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            const double2 q = Bs[cb + b][kk];   // acc -= a conj(q)
+            const double2 q = Bs[cb + 8 * b][kk];   // acc -= a conj(q)
             acc[b].x -= a.x * q.x + a.y * q.y;
             acc[b].y -= a.y * q.x - a.x * q.y;
           }
@@ -356,7 +373,7 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
       if (i0 == c0) {
         // ---- factor the diagonal block in shared memory (right-looking, unblocked)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) Lp[rr][cb + b] = acc[b];
+        for (int b = 0; b < 4; ++b) Lp[rr][cb + 8 * b] = acc[b];
         __syncthreads();
         chol32(Lp, w, tau, s_rs);
         // ---- inverse of the lower-triangular L_JJ, column by column (thread j < w owns column j)
@@ -368,21 +385,32 @@ __global__ void __launch_bounds__(256) k_pc_chol_cta(const GateDesc* __restrict_
           if (i < w && j <= i) G[(int64_t)(c0 + j) * n + c0 + i] = Lp[i][j];
         }
       } else {
-        // ---- X = T (L_JJ^-1)^H: x_j = sum_{k <= j} t_k conj(M[j][k])
+        // ---- X = T (L_JJ^-1)^H: x_j = sum_{k <= j} t_k conj(M[j][k]). The thread's 4 columns run
+        // as 4 independent accumulation chains over k <= cb + 24 (M is stored lower-triangular with
+        // zeros above the diagonal, so the extra terms add exact zeros): one T load per 4 products,
+        // no serial dependence between the columns (ncu r02: this loop was 23% of the kernel's stall
+        // samples as 4 back-to-back serial chains with 2 loads per product).
 #pragma unroll
-        for (int b = 0; b < 4; ++b) Tt[rr][cb + b] = acc[b];
+        for (int b = 0; b < 4; ++b) Tt[rr][cb + 8 * b] = acc[b];
         __syncthreads();
+        double2 x[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[b] = make_double2(0.0, 0.0);
+        const int kend = min(cb + 25, w);
+        for (int k = 0; k < kend; ++k) {
+          const double2 tk = Tt[rr][k];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double2 q = Mi[cb + 8 * b][k];
+            x[b].x += tk.x * q.x + tk.y * q.y;
+            x[b].y += tk.y * q.x - tk.x * q.y;
+          }
+        }
+        const int i = i0 + rr;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int j = cb + b;
-          double2 x = make_double2(0.0, 0.0);
-          for (int k = 0; k <= j && k < w; ++k) {
-            const double2 tk = Tt[rr][k], q = Mi[j][k];
-            x.x += tk.x * q.x + tk.y * q.y;
-            x.y += tk.y * q.x - tk.x * q.y;
-          }
-          const int i = i0 + rr;
-          if (i < n && j < w) G[(int64_t)(c0 + j) * n + i] = x;
+          const int j = cb + 8 * b;
+          if (i < n && j < w) G[(int64_t)(c0 + j) * n + i] = x[b];
         }
       }
       __syncthreads();

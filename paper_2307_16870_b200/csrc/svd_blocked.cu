@@ -446,6 +446,152 @@ __global__ void __launch_bounds__(256) k_rayleigh(const GateDesc* __restrict__ d
   }
 }
 
+// The same Rayleigh quotients and B as k_rayleigh (write_b = 1), on 64 x 64 output tiles: one CTA per
+// (64-column block, gate), a 16 x 16 thread grid with 4 rows x 4 columns of W = A V per thread (A = L^H
+// or lambda (x) Theta' as in k_rayleigh), k chunks of 16 double-buffered in shared memory (one barrier
+// per chunk, the next chunk fetched into registers while the current one multiplies). Per k step a warp
+// reads 8 shared double2 (4 rows: 16 distinct addresses, 4 columns: 2) for 16 complex FMAs (k_rayleigh:
+// 9 for 8), and the L^H chunk is fetched along k (contiguous in the column-major L; k_rayleigh strides
+// rows of L by n). Same products, different FP64 summation order (rows 4 at a time per thread, then the
+// 16 row lanes by a butterfly). ncu r02: k_rayleigh ran at 0.34 of the FP64 peak (4.16 ms per chi = 64
+// step). EAMPS_RAYLEIGH_OLD=1 keeps k_rayleigh (A/B).
+constexpr int RT_K = 16, RT_P = 65;
+constexpr size_t kRay64Half = sizeof(double2) * 2 * RT_K * RT_P;   // 33 KB per operand
+__global__ void __launch_bounds__(256, 2) k_rayleigh64(const GateDesc* __restrict__ desc, const int32_t* list,
+                                                       uint8_t* slab, const DevState* st, int use_l) {
+  const GateDesc gd = desc[list[blockIdx.y]];
+  const int j0 = blockIdx.x * 64;
+  if (j0 >= gd.n) return;
+  const int m = gd.m, n = gd.n, np = gd.n_pad, dd = st->d;
+  const bool from_l = use_l && gd.regime == 3 && gd.jrows > 0;
+  const int rows = from_l ? n : m;
+  const double2* __restrict__ Lg = reinterpret_cast<const double2*>(slab + gd.ws_log);
+  const BondEntry* bonds = reinterpret_cast<const BondEntry*>(slab + st->bonds_off);
+  const float* lam = reinterpret_cast<const float*>(slab + bonds[gd.site].off);
+  const float2* thp = reinterpret_cast<const float2*>(slab + gd.ws_thetap);
+  const float2* V = reinterpret_cast<const float2*>(slab + gd.ws_V);
+  float2* Bw = reinterpret_cast<float2*>(slab + gd.ws_theta);
+  extern __shared__ __align__(16) uint8_t r64_sm[];
+  double2 (*As)[RT_K][RT_P] = reinterpret_cast<double2 (*)[RT_K][RT_P]>(r64_sm);                   // [buf][k][row]
+  double2 (*Bs)[RT_K][RT_P] = reinterpret_cast<double2 (*)[RT_K][RT_P]>(r64_sm + kRay64Half);      // [buf][k][col]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tid & 15, ty = tid >> 4;   // rows tx + 16a, columns ty + 16b
+  double num[4] = {0.0, 0.0, 0.0, 0.0};
+  double2 ra[4];
+  float2 rb[4];
+  auto fetch = [&](int r0, int k0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;          // 1024 = 16 k x 64 rows
+      double2 v = make_double2(0.0, 0.0);
+      if (from_l) {                          // along k: (L^H)[row][k] = conj(L[k][row]) = conj(Lg[row n + k])
+        const int kk = e & 15, row = r0 + (e >> 4), k = k0 + kk;
+        if (row < n && k < n && k >= row) {
+          const double2 l = Lg[(int64_t)row * n + k];
+          v = make_double2(l.x, -l.y);
+        }
+      } else {                               // along rows: theta'[k][row], column-major ld m
+        const int row = r0 + (e & 63), k = k0 + (e >> 6);
+        if (row < m && k < n) {
+          const float2 tp = thp[(int64_t)k * m + row];
+          const float la = lam[row / dd];
+          v = make_double2(la * tp.x, la * tp.y);
+        }
+      }
+      ra[it] = v;
+      const int kk = e & 15, jj = e >> 4, k = k0 + kk, j = j0 + jj;
+      rb[it] = (k < n && j < n) ? V[(int64_t)j * np + k] : make_float2(0.f, 0.f);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      if (from_l) As[buf][e & 15][e >> 4] = ra[it];
+      else As[buf][e >> 6][e & 63] = ra[it];
+      Bs[buf][e & 15][e >> 4] = make_double2(rb[it].x, rb[it].y);
+    }
+  };
+  const int nk = (n + RT_K - 1) / RT_K;
+  for (int r0 = 0; r0 < rows; r0 += 64) {
+    double2 w[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) w[a][b] = make_double2(0.0, 0.0);
+    const int kc0 = from_l ? r0 / RT_K : 0;           // L^H: rows r0.. need k >= r0 only
+    fetch(r0, kc0 * RT_K);
+    stash(0);
+    __syncthreads();
+    for (int kc = kc0; kc < nk; ++kc) {
+      const int cur = (kc - kc0) & 1;
+      if (kc + 1 < nk) fetch(r0, (kc + 1) * RT_K);
+#pragma unroll
+      for (int kk = 0; kk < RT_K; ++kk) {
+        double2 a[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) a[p] = As[cur][kk][tx + 16 * p];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 b = Bs[cur][kk][ty + 16 * q];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            w[p][q].x = fma(a[p].x, b.x, fma(-a[p].y, b.y, w[p][q].x));
+            w[p][q].y = fma(a[p].x, b.y, fma(a[p].y, b.x, w[p][q].y));
+          }
+        }
+      }
+      if (kc + 1 < nk) stash(cur ^ 1);   // the other buffer: last read before the previous barrier
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + ty + 16 * q;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int row = r0 + tx + 16 * p;
+        num[q] += w[p][q].x * w[p][q].x + w[p][q].y * w[p][q].y;   // zero beyond rows / n
+        if (row < rows && j < n) Bw[(int64_t)j * m + row] = make_float2((float)w[p][q].x, (float)w[p][q].y);
+      }
+    }
+  }
+  if (rows < m) {   // L^H V has n rows: the polish reads m, the rest are zero
+    for (int x = tid; x < 64 * (m - rows); x += 256) {
+      const int j = j0 + x / (m - rows), row = rows + x % (m - rows);
+      if (j < n) Bw[(int64_t)j * m + row] = make_float2(0.f, 0.f);
+    }
+  }
+  // num: the 16 row lanes (tx) of each half-warp hold one column set ty; butterfly over them
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) num[q] += __shfl_xor_sync(0xffffffffu, num[q], o);
+  }
+  __shared__ double s_num[64];
+  if (tx == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s_num[ty + 16 * q] = num[q];
+  }
+  __syncthreads();
+  // den_j = |v_j|^2 and the outputs: warp w handles columns 8w .. 8w+7, lanes stride over k
+  double* sig2 = reinterpret_cast<double*>(slab + gd.ws_sig2);
+  double* shift = reinterpret_cast<double*>(slab + gd.ws_E);   // polish scratch: shift[n_pad] | den[n_pad]
+  for (int c = 0; c < 8; ++c) {
+    const int jl = warp * 8 + c, j = j0 + jl;
+    if (j >= n) break;
+    const float2* vj = V + (int64_t)j * np;
+    double d = 0.0;
+    for (int k = lane; k < n; k += 32) d += (double)vj[k].x * vj[k].x + (double)vj[k].y * vj[k].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) {
+      sig2[j] = d > 0.0 ? s_num[jl] / d : 0.0;
+      shift[j] = 0.0;
+      shift[np + j] = d;
+    }
+  }
+}
+
 __global__ void k_sort_tails_large(GateDesc* desc, const int32_t* list, uint8_t* slab, DevState* st, int polish = 0) {
   extern __shared__ __align__(16) uint8_t sm[];
   const GateDesc gd = desc[list[blockIdx.x]];
@@ -1740,7 +1886,15 @@ int launch_spectrum_polish(GateDesc* d_desc, const int32_t* d_list, int count, i
   if (count <= 0) return 0;
   // EAMPS_RAYLEIGH_THETA=1: the QR-regime Rayleigh quotients from theta V instead of L^H V (A/B)
   static const int use_l = getenv("EAMPS_RAYLEIGH_THETA") ? 0 : 1;
-  k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1, use_l);
+  static const bool old = getenv("EAMPS_RAYLEIGH_OLD") != nullptr;   // dev A/B switch
+  if (old) {
+    k_rayleigh<<<dim3((max_n + 31) / 32, count), 256, 0, s>>>(d_desc, d_list, slab, st, 1, use_l);
+  } else {
+    static std::atomic<unsigned long long> rattr{0};
+    if (first_on_device(rattr))
+      cudaFuncSetAttribute(k_rayleigh64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kRay64Half));
+    k_rayleigh64<<<dim3((max_n + 63) / 64, count), 256, 2 * kRay64Half, s>>>(d_desc, d_list, slab, st, use_l);
+  }
   static std::atomic<unsigned long long> pattr{0};
   if (first_on_device(pattr)) {
     cudaFuncSetAttribute(tcj::k_tc_polish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tcj::kGramSmem);
