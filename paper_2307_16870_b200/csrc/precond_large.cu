@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(256, 3) k_pc_chol_cta(const GateDesc* __restri
   if (gd.jrows <= 0) return;
   const int n = gd.n;
   double2* G = reinterpret_cast<double2*>(slab + gd.ws_log);
+  // B = L in FP32 (n x n_pad, ld n; the block Jacobi's working matrix, k_pc_b_from_l's layout), written
+  // as each block of L becomes final -- no separate conversion pass over L (0.47 ms per chi = 64 step)
+  float2* Bf = reinterpret_cast<float2*>(slab + gd.ws_theta);
   struct Smem {
     double2 Lp[32][33];   // factored diagonal block L_JJ; later the row block being solved
     double2 Mi[32][33];   // L_JJ^-1 (lower)
@@ -379,10 +382,14 @@ __global__ void __launch_bounds__(256, 3) k_pc_chol_cta(const GateDesc* __restri
         // ---- inverse of the lower-triangular L_JJ, column by column (thread j < w owns column j)
         tri_inv32(Lp, Mi, w);
         __syncthreads();
-        // ---- write L_JJ (lower part) back
+        // ---- write L_JJ (lower part) back, and B's diagonal block (FP32, zeros above the diagonal)
         for (int x = tid; x < 32 * 32; x += 256) {
           const int i = x >> 5, j = x & 31;
           if (i < w && j <= i) G[(int64_t)(c0 + j) * n + c0 + i] = Lp[i][j];
+          if (i < w && j < w) {
+            const double2 l = Lp[i][j];
+            Bf[(int64_t)(c0 + j) * n + c0 + i] = j <= i ? make_float2((float)l.x, (float)l.y) : make_float2(0.f, 0.f);
+          }
         }
       } else {
         // ---- X = T (L_JJ^-1)^H: x_j = sum_{k <= j} t_k conj(M[j][k]). The thread's 4 columns run
@@ -410,11 +417,20 @@ __global__ void __launch_bounds__(256, 3) k_pc_chol_cta(const GateDesc* __restri
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const int j = cb + 8 * b;
-          if (i < n && j < w) G[(int64_t)(c0 + j) * n + i] = x[b];
+          if (i < n && j < w) {
+            G[(int64_t)(c0 + j) * n + i] = x[b];
+            Bf[(int64_t)(c0 + j) * n + i] = make_float2((float)x[b].x, (float)x[b].y);
+          }
         }
       }
       __syncthreads();
     }
+  }
+  // B: zeros in the blocks above the diagonal blocks and in the pad columns
+  const int np = gd.n_pad;
+  for (int64_t x = tid; x < (int64_t)n * np; x += 256) {
+    const int j = (int)(x / n), i = (int)(x % n);
+    if (j >= n || (i >> 5) < (j >> 5)) Bf[x] = make_float2(0.f, 0.f);
   }
 }
 
@@ -676,9 +692,8 @@ int launch_precond_large(GateDesc* d_desc, const int32_t* d_list, int count, int
     if (first_on_device(attr)) {
       cudaFuncSetAttribute(k_pc_chol_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
     }
-    k_pc_chol_cta<<<count, 256, kCholSmem, s>>>(d_desc, d_list, slab);
-    k_pc_b_from_l<<<dim3(64, count), 256, 0, s>>>(d_desc, d_list, slab);
-    return 3;
+    k_pc_chol_cta<<<count, 256, kCholSmem, s>>>(d_desc, d_list, slab);   // also writes B = L
+    return 2;
   }
   for (int c0 = 0; c0 < max_n; c0 += 32) {
     k_pc_chol_diag<<<count, 256, 0, s>>>(d_desc, d_list, slab, c0);

@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(256) k_vk_gram(const GateDesc* __restrict__ de
   const float2* __restrict__ V = reinterpret_cast<const float2*>(slab + gd.ws_V);
   const int32_t* __restrict__ pi = reinterpret_cast<const int32_t*>(slab + gd.ws_pi);
   float2* E = reinterpret_cast<float2*>(slab + gd.ws_E);
-  __shared__ float2 Va[64][33], Vb[64][33];
+  // Vb rows padded to 36 float2 (16-byte aligned): a thread's 4 partner columns q4 .. q4+3 are two
+  // 16-byte loads instead of four 8-byte ones (ncu r02: short scoreboard 13 warps per issue)
+  __shared__ float2 Va[64][33];
+  __shared__ __align__(16) float2 Vb[64][36];
   __shared__ int32_t pa[32], pb[32];
   const int tid = threadIdx.x;
   if (tid < 32) pa[tid] = (a0 + tid < k) ? pi[a0 + tid] : -1;
@@ -65,13 +68,17 @@ __global__ void __launch_bounds__(256) k_vk_gram(const GateDesc* __restrict__ de
     float2 acc[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll 4
     for (int i = 0; i < 64; ++i) {
-      float2 x = Va[i][p];
+      const float2 x = Va[i][p];
+      const float4 y01 = *reinterpret_cast<const float4*>(&Vb[i][q4]);
+      const float4 y23 = *reinterpret_cast<const float4*>(&Vb[i][q4 + 2]);
+      const float2 y[4] = {make_float2(y01.x, y01.y), make_float2(y01.z, y01.w), make_float2(y23.x, y23.y),
+                           make_float2(y23.z, y23.w)};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float2 y = Vb[i][q4 + j];
-        acc[j].x = fmaf(x.x, y.x, fmaf(x.y, y.y, acc[j].x));
-        acc[j].y = fmaf(x.x, y.y, fmaf(-x.y, y.x, acc[j].y));
+        acc[j].x = fmaf(x.x, y[j].x, fmaf(x.y, y[j].y, acc[j].x));
+        acc[j].y = fmaf(x.x, y[j].y, fmaf(-x.y, y[j].x, acc[j].y));
       }
     }
 #pragma unroll
@@ -202,22 +209,29 @@ __global__ void __launch_bounds__(256) k_reabsorb(const GateDesc* __restrict__ d
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) dacc[a][b] = make_double2(0.0, 0.0);
+  // the next 16-column chunk of Theta' and V_k is fetched into registers while the current one
+  // multiplies (ncu r02: long scoreboard was the top stall with the fetch in front of every chunk)
+  float2 pa[4], pb[4];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      const int row = row0 + (e & 63), col = k0 + (e >> 6);
+      pa[it] = (row < m && col < n) ? thp[(int64_t)col * m + row] : make_float2(0.f, 0.f);
+      const int cb = k0 + (e & 15), j = j0 + (e >> 4);
+      pb[it] = (j < k && cb < n) ? Vk[(int64_t)j * n + cb] : make_float2(0.f, 0.f);
+    }
+  };
+  fetch(0);
   for (int k0 = 0; k0 < n; k0 += 16) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
-      int e = tid + it * 256;
-      int i = e & 63, kk = e >> 6;
-      int row = row0 + i, col = k0 + kk;
-      As[kk][i] = (row < m && col < n) ? thp[(int64_t)col * m + row] : make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      int e = tid + it * 256;
-      int kk = e & 15, jj = e >> 4;
-      int col = k0 + kk, j = j0 + jj;
-      Bs[kk][jj] = (j < k && col < n) ? Vk[(int64_t)j * n + col] : make_float2(0.f, 0.f);
+      const int e = tid + it * 256;
+      As[e >> 6][e & 63] = pa[it];
+      Bs[e & 15][e >> 4] = pb[it];
     }
     __syncthreads();
+    if (k0 + 16 < n) fetch(k0 + 16);
     float2 acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
