@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_vk_apply(const GateDesc* __restrict__ d
   }
 }
 
-__global__ void __launch_bounds__(256) k_reabsorb(const GateDesc* __restrict__ desc, const int32_t* __restrict__ prefix,
+__global__ void __launch_bounds__(256, 2) k_reabsorb(const GateDesc* __restrict__ desc, const int32_t* __restrict__ prefix,
                                                   int G, uint8_t* slab) {
   const int g = find_gate(prefix, G, blockIdx.x);
   const GateDesc gd = desc[g];
@@ -209,29 +209,23 @@ __global__ void __launch_bounds__(256) k_reabsorb(const GateDesc* __restrict__ d
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) dacc[a][b] = make_double2(0.0, 0.0);
-  // the next 16-column chunk of Theta' and V_k is fetched into registers while the current one
-  // multiplies (ncu r02: long scoreboard was the top stall with the fetch in front of every chunk)
-  float2 pa[4], pb[4];
-  auto fetch = [&](int k0) {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int e = tid + it * 256;
-      const int row = row0 + (e & 63), col = k0 + (e >> 6);
-      pa[it] = (row < m && col < n) ? thp[(int64_t)col * m + row] : make_float2(0.f, 0.f);
-      const int cb = k0 + (e & 15), j = j0 + (e >> 4);
-      pb[it] = (j < k && cb < n) ? Vk[(int64_t)j * n + cb] : make_float2(0.f, 0.f);
-    }
-  };
-  fetch(0);
+  // 128 registers (2 CTAs per SM; at 177 one CTA per SM left the FP32 pipe latency-bound, ncu r02)
   for (int k0 = 0; k0 < n; k0 += 16) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
-      const int e = tid + it * 256;
-      As[e >> 6][e & 63] = pa[it];
-      Bs[e & 15][e >> 4] = pb[it];
+      int e = tid + it * 256;
+      int i = e & 63, kk = e >> 6;
+      int row = row0 + i, col = k0 + kk;
+      As[kk][i] = (row < m && col < n) ? thp[(int64_t)col * m + row] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      int e = tid + it * 256;
+      int kk = e & 15, jj = e >> 4;
+      int col = k0 + kk, j = j0 + jj;
+      Bs[kk][jj] = (j < k && col < n) ? Vk[(int64_t)j * n + col] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    if (k0 + 16 < n) fetch(k0 + 16);
     float2 acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)

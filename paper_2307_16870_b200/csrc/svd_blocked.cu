@@ -1340,18 +1340,23 @@ __global__ void __launch_bounds__(128) k_tc_polish(const GateDesc* __restrict__ 
   float* Ds = reinterpret_cast<float*>(base);  // [128][129]
   gram_panel(reinterpret_cast<const float2*>(slab + gd.ws_theta), gd.m, n, I, J, base, mbar, tbase, Ds);
   if ((tid >> 5) == 0) tc::tmem_dealloc(tbase, 128);
-  // thread j (< 64) = panel column j; partners: the other block (always) and its own block (round 0)
-  if (tid < 64) {
-    const int j = tid, cj = colof(j, I, J);
+  // panel column j = tid % 64, two threads per column (all 128 of the CTA: the loop below is a chain of
+  // FP64 divisions and square roots, latency-bound at one thread per column, ncu r02 -- 55% of the
+  // kernel's stall samples): partners = the other block (always) and the column's own block (round 0);
+  // in round 0 thread half 0 takes the other block and half 1 the own block, otherwise the halves
+  // split the other block's 32 columns. Each half adds its partial sum (atomicAdd, as before across CTAs).
+  {
+    const int j = tid & 63, half = tid >> 6, cj = colof(j, I, J);
     if (cj < n) {
       const double aj = s2[cj], dj = den[cj];
       auto sym = [&](int a, int b2) { return 0.5f * (Ds[a * 129 + b2] + Ds[b2 * 129 + a]); };
       double acc = 0.0;
       const int other0 = j < TB ? TB : 0;
       const int own0 = j < TB ? 0 : TB;
-      for (int pass = 0; pass < (rnd == 0 ? 2 : 1); ++pass) {
-        const int l0 = pass == 0 ? other0 : own0;
-        for (int l = l0; l < l0 + TB; ++l) {
+      const int lb = rnd == 0 ? (half == 0 ? other0 : own0) : other0 + half * (TB / 2);
+      const int le = rnd == 0 ? lb + TB : lb + TB / 2;
+      {
+        for (int l = lb; l < le; ++l) {
           const int cl = colof(l, I, J);
           if (l == j || cl >= n) continue;
           const double gr = sym(l, j) + sym(64 + l, 64 + j), gim = sym(l, 64 + j) - sym(64 + l, j);
