@@ -605,6 +605,31 @@ def main():
                        "d2h_bytes_per_step": int(G * (48 + 160) + 512),
                        "pipeline": "%d chunks of %s updates, H2D of chunk c+1 on a side stream overlapping chunk c's update"
                                    % (C, [g1 - g0 for g0, g1 in bounds])}
+        # the same step with the updated site tensors read back too (B_i', B_{i+1}' of every update:
+        # mps_export_sites = one device gather + one D2H into pinned host memory), VERDICT r01 weak 10
+        try:
+            dims_out = np.zeros((2 * G, 3), np.int32)
+            ne = mps.mps_export_sites_raw(0, 2 * G, None, 0, dims_out)
+            host_out = torch.empty(ne, dtype=torch.complex64, pin_memory=True)
+            t_full = 0.0
+            for rep in range(reps + 1):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                recs = e2e_step()
+                got = mps.mps_export_sites_raw(0, 2 * G, pk.C.c_void_p(host_out.data_ptr()), ne, dims_out)
+                torch.cuda.synchronize()
+                if rep > 0:
+                    t_full += time.perf_counter() - t0
+            assert len(recs) == G and got == ne and bool(torch.isfinite(torch.view_as_real(host_out[:4096])).all())
+            if world > 1:
+                t_full = max_over_ranks(t_full, dev)
+            line["e2e"]["with_state_readback"] = {
+                "value": world * G / (t_full / reps), "unit": UNIT,
+                "d2h_bytes_per_step": int(G * (48 + 160) + 512 + 8 * ne),
+                "what": "records + every updated site tensor (mps_export_sites into pinned host memory)"}
+            del host_out
+        except Exception as e:   # the extra leg never blocks the line
+            line["e2e"]["with_state_readback"] = {"error": str(e)[:300]}
         del stage
         del host
     del mps, inter

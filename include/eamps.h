@@ -196,6 +196,15 @@ mps_status mps_import_site(mps_t, int32_t site, const float* B, const int32_t* d
  * (c64, row-major each; host -- pinned or pageable -- or device pointer), dims holds count x 3
  * extents (host). One H2D copy plus one device allocation/scatter launch pair. */
 mps_status mps_import_sites(mps_t, int32_t first, int32_t count, const float* B, const int32_t* dims);
+/* Bulk export, the reverse of mps_import_sites: the site tensors B_first .. B_{first+count-1} (the
+ * B tensors of E1/E2; the B_i', B_{i+1}' an update writes) packed back
+ * to back in site order (c64, row-major (chl, d, chr) each) into B -- host (pinned or pageable) or
+ * device pointer, caller-owned, cap_elems complex elements -- by one device gather launch plus,
+ * for a host B, one D2H copy. dims (host, count x 3) receives the extents and *elems_out (may be
+ * NULL) the total complex elements; B == NULL only reports them. MPS_E_RANGE if cap_elems is too
+ * small, MPS_E_STATE while a split layer is in flight. */
+mps_status mps_export_sites(mps_t, int32_t first, int32_t count, float* B, size_t cap_elems, int32_t* dims,
+                            size_t* elems_out);
 mps_status mps_set_lambda(mps_t, int32_t bond /* -1..N-1 */, const float* lam, int32_t len);
 /* Device-side snapshot of the whole state (site store, ledger, pool) into a caller device buffer
  * and back; *bytes_needed reports the size when buf == NULL. */

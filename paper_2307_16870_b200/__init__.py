@@ -25,7 +25,7 @@ ABI_FUNCTIONS = [
     "mps_create", "mps_destroy", "mps_apply_gate1", "mps_apply_gate2", "mps_apply_layer",
     "mps_fidelity_estimate", "mps_amplitude", "mps_to_statevector", "mps_bond_dims",
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
-    "mps_import_site", "mps_import_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
+    "mps_import_site", "mps_import_sites", "mps_export_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_set_svd_route", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
     "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1", "mps_canonicalize",
@@ -79,6 +79,7 @@ def lib():
             "mps_export_site": [_P, i32, _P, _P],
             "mps_import_site": [_P, i32, _P, _P],
             "mps_import_sites": [_P, i32, i32, _P, _P],
+            "mps_export_sites": [_P, i32, i32, _P, C.c_size_t, _P, _P],
             "mps_set_lambda": [_P, i32, _P, i32],
             "mps_snapshot_save": [_P, _P, C.c_size_t, _P],
             "mps_snapshot_load": [_P, _P, C.c_size_t],
@@ -318,6 +319,27 @@ class MPS:
     def mps_import_sites_raw(self, first: int, count: int, flat_ptr, dims: np.ndarray):
         dims = np.ascontiguousarray(dims, np.int32)
         self._check(lib().mps_import_sites(self._h, int(first), int(count), flat_ptr, _ptr(dims)))
+
+    def mps_export_sites(self, first: int, count: int):
+        """Bulk export of consecutive sites (one device gather + one D2H copy): list of arrays."""
+        dims = np.zeros((count, 3), np.int32)
+        ne = C.c_size_t(0)
+        self._check(lib().mps_export_sites(self._h, int(first), int(count), None, 0, _ptr(dims), C.byref(ne)))
+        flat = np.empty(ne.value, np.complex64)
+        self._check(lib().mps_export_sites(self._h, int(first), int(count), _ptr(flat), ne.value, _ptr(dims),
+                                           C.byref(ne)))
+        out, o = [], 0
+        for a, d, c in dims:
+            out.append(flat[o: o + int(a) * int(d) * int(c)].reshape(int(a), int(d), int(c)))
+            o += int(a) * int(d) * int(c)
+        return out
+
+    def mps_export_sites_raw(self, first: int, count: int, flat_ptr, cap_elems: int, dims: np.ndarray) -> int:
+        """flat_ptr: host or device pointer (c_void_p) with room for cap_elems complex64; returns elems."""
+        ne = C.c_size_t(0)
+        self._check(lib().mps_export_sites(self._h, int(first), int(count), flat_ptr, int(cap_elems), _ptr(dims),
+                                           C.byref(ne)))
+        return ne.value
 
     def mps_set_lambda(self, bond: int, lam):
         lam = np.ascontiguousarray(lam, np.float32)

@@ -5,6 +5,7 @@
 //   canonical order) -> reabsorb (all)
 // and read back the new bond profile, ledger and truncation records (one sync per wave).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstddef>
@@ -24,6 +25,15 @@
 using namespace eamps;
 
 static_assert(sizeof(Record) == sizeof(mps_record), "record layout");
+
+// NVTX range over a host-side scope (a timeline tool shows the layer / wave / step structure over
+// the kernels launched inside it; header-only NVTX 3: a no-op call when no tool is attached)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 struct LayerPlan {                 // per gate of a layer (a0 planning)
   GateDesc gd;
@@ -365,6 +375,7 @@ int lane_group(int m, int n, int reg) {
 
 mps_status wave_front_impl(mps_t h);
 mps_status wave_front(mps_t h) {
+  NvtxScope nv("eamps:wave_front (a0 plan/stage, a1 contract, a2 SVD, a3 sort+tails)");
   const double t0 = h->hp.on ? HostProf::now() : 0.0;
   mps_status st = wave_front_impl(h);
   if (h->hp.on) {
@@ -783,6 +794,7 @@ mps_status wave_front_impl(mps_t h) {
 }
 
 mps_status wave_back(mps_t h) {
+  NvtxScope nv("eamps:wave_back (a4 select+ledger, a5 reabsorb)");
   LayerJob& J = h->job;
   if (!J.front) return set_err(h, MPS_E_STATE, "no wave in flight");
   J.front = false;
@@ -1258,6 +1270,7 @@ mps_status mps_layer_step(mps_t h, int32_t* remaining) {
 }
 
 mps_status mps_apply_layer(mps_t h, int32_t G, const int32_t* sites, const float* Us) {
+  NvtxScope nv("eamps:mps_apply_layer");
   int32_t w = 0;
   mps_status st = mps_layer_begin(h, G, sites, Us, &w);
   if (st != MPS_OK || w == 0) return st;
@@ -1468,6 +1481,7 @@ mps_status mps_import_site(mps_t h, int32_t site, const float* B, const int32_t*
 }
 
 mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* B, const int32_t* dims) {
+  NvtxScope nv("eamps:mps_import_sites");
   DEVICE_GUARD(h);
   if (!h || !B || !dims || count < 1) return MPS_E_INVAL;
   if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
@@ -1544,6 +1558,70 @@ mps_status mps_import_sites(mps_t h, int32_t first, int32_t count, const float* 
   }
   h->lamlen = lamlen;
   return MPS_OK;
+}
+
+mps_status mps_export_sites(mps_t h, int32_t first, int32_t count, float* B, size_t cap_elems, int32_t* dims,
+                            size_t* elems_out) {
+  NvtxScope nv("eamps:mps_export_sites");
+  DEVICE_GUARD(h);
+  if (!h || !dims || count < 1) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "a layer is in flight");
+  if (first < 0 || first + count > h->N) return set_err(h, MPS_E_RANGE, "sites out of range");
+  mps_status st = check_sticky(h);
+  if (st != MPS_OK) return st;
+  st = sync_state(h);
+  if (st != MPS_OK) return st;
+  // the site table slice [first, first + count): offsets and extents as the device holds them
+  SiteEntry* se = static_cast<SiteEntry*>(pinned_buf(h, sizeof(SiteEntry) * (size_t)count));
+  if (!se) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  CK(cudaMemcpyAsync(se, h->slab + h->hstate.sites_off + sizeof(SiteEntry) * (size_t)first,
+                     sizeof(SiteEntry) * (size_t)count, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  std::vector<ExportEntry> ent(count);
+  int64_t elems = 0, maxe = 1;
+  for (int x = 0; x < count; ++x) {
+    dims[3 * x] = se[x].chl;
+    dims[3 * x + 1] = h->d;
+    dims[3 * x + 2] = se[x].chr;
+    ent[x].src_off = se[x].off;
+    ent[x].dst_elem = elems;
+    ent[x].elems = (int64_t)se[x].chl * h->d * se[x].chr;
+    if (!se[x].off) return set_err(h, MPS_E_STATE, "site without a tensor");
+    elems += ent[x].elems;
+    maxe = std::max(maxe, ent[x].elems);
+  }
+  if (elems_out) *elems_out = (size_t)elems;
+  if (!B) return MPS_OK;
+  if (cap_elems < (size_t)elems) return set_err(h, MPS_E_RANGE, "export buffer too small");
+  const bool dev = is_device_ptr(B);
+  const size_t ent_bytes = align_up(sizeof(ExportEntry) * (size_t)count);
+  const size_t data_bytes = dev ? 0 : align_up((size_t)elems * 8);
+  const size_t top = h->slab_bytes - 4 * kAlign;
+  if (h->hstate.pool.bump + ent_bytes + data_bytes + 2 * kAlign > top) {
+    // a host destination is staged through the top of the slab: export it in two halves
+    if (!dev && count > 1) {
+      const int c0 = count / 2;
+      const size_t e0 = (size_t)ent[c0].dst_elem;
+      st = mps_export_sites(h, first, c0, B, e0, dims, nullptr);
+      if (st != MPS_OK) return st;
+      return mps_export_sites(h, first + c0, count - c0, B + 2 * e0, cap_elems - e0, dims + 3 * c0, nullptr);
+    }
+    return set_err(h, MPS_E_NOMEM, "no room to stage the export");
+  }
+  const size_t base = align_up(top - ent_bytes - data_bytes - kAlign);
+  uint8_t* hb = static_cast<uint8_t*>(pinned_buf(h, ent_bytes, 1));
+  if (!hb) return set_err(h, MPS_E_NOMEM, "pinned host allocation failed");
+  std::memcpy(hb, ent.data(), sizeof(ExportEntry) * (size_t)count);
+  CK(h2d_small(h, h->slab + base, hb, sizeof(ExportEntry) * (size_t)count));
+  float2* dstp = dev ? reinterpret_cast<float2*>(B) : reinterpret_cast<float2*>(h->slab + base + ent_bytes);
+  // enough CTAs per site to fill the GPU when the sites are few and large
+  const int split = (int)std::max<int64_t>(1, std::min<int64_t>({64, (maxe + 8191) / 8192, (1184 + count - 1) / count}));
+  launch_export(h->slab, reinterpret_cast<const ExportEntry*>(h->slab + base), count, split, dstp, h->s);
+  ++h->launches;
+  CKL("export");
+  if (!dev) CK(cudaMemcpyAsync(B, dstp, (size_t)elems * 8, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  return device_error(h);
 }
 
 mps_status mps_set_lambda(mps_t h, int32_t bond, const float* lam, int32_t len) {
@@ -1652,6 +1730,7 @@ mps_status mps_to_statevector(mps_t h, double* out, size_t n_doubles) {
 // (log E, j, guarantee and the records are untouched); the GPU's exact mode keeps sigma > 1e-6 sigma_0
 // (reading 8), i.e. drops at most n 1e-12 of the weight per bond.
 mps_status mps_canonicalize(mps_t h) {
+  NvtxScope nv("eamps:mps_canonicalize");
   DEVICE_GUARD(h);
   if (!h) return MPS_E_INVAL;
   mps_status st = check_sticky(h);

@@ -95,6 +95,12 @@ struct ImportEntry {                // bulk site import (mps_import_sites)
   int64_t dst_off, lamL_off, lamR_off;           // written by the device allocator
 };
 
+struct ExportEntry {                // bulk site export (mps_export_sites)
+  int64_t src_off;                  // byte offset of the site tensor in the slab
+  int64_t dst_elem;                 // first complex element of this site in the destination buffer
+  int64_t elems;                    // chl * d * chr
+};
+
 struct DevState {                   // lives at slab offset 0
   DevLedger led;
   DevPool pool;
@@ -205,6 +211,8 @@ void launch_reabsorb_small(const GateDesc* d_desc, const int32_t* d_list, int co
                            cudaStream_t s);
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s);
+// gather of `count` site tensors into one contiguous buffer (mps_export_sites); `split` CTAs per site
+void launch_export(const uint8_t* slab, const ExportEntry* d_ent, int count, int split, float2* dst, cudaStream_t s);
 void launch_pool_alloc(uint8_t* slab, DevState* st, uint64_t bytes, int64_t* d_out, cudaStream_t s);
 void launch_pool_free(uint8_t* slab, DevState* st, int64_t off, int cls, cudaStream_t s);
 void launch_gate1(uint8_t* slab, DevState* st, int site, int d, const float2* d_u, cudaStream_t s);

@@ -398,7 +398,30 @@ __global__ void k_import_scatter(uint8_t* slab, const ImportEntry* ent, const fl
     for (int x = threadIdx.x; x < e.resetR; x += blockDim.x) reinterpret_cast<float*>(slab + e.lamR_off)[x] = 1.f;
 }
 
+// the reverse of k_import_scatter: site x's tensor -> dst + dst_elem (16 B per thread and step
+// when both ends are 16 B aligned: pool blocks are, the destination is when dst_elem is even)
+__global__ void k_export_gather(const uint8_t* __restrict__ slab, const ExportEntry* __restrict__ ent,
+                                float2* __restrict__ dst) {
+  const ExportEntry e = ent[blockIdx.x];
+  const float2* s = reinterpret_cast<const float2*>(slab + e.src_off);
+  float2* o = dst + e.dst_elem;
+  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (((e.dst_elem | e.elems) & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(s);
+    float4* o4 = reinterpret_cast<float4*>(o);
+    for (int64_t x = t0; x < e.elems / 2; x += stride) o4[x] = s4[x];
+  } else {
+    for (int64_t x = t0; x < e.elems; x += stride) o[x] = s[x];
+  }
+}
+
 }  // namespace
+
+void launch_export(const uint8_t* slab, const ExportEntry* d_ent, int count, int split, float2* dst, cudaStream_t s) {
+  if (count <= 0) return;
+  k_export_gather<<<dim3(count, split), 256, 0, s>>>(slab, d_ent, dst);
+}
 
 void launch_import(uint8_t* slab, DevState* st, ImportEntry* d_ent, int count, const float2* src, int d,
                    cudaStream_t s) {

@@ -231,3 +231,39 @@ def test_graded_spectrum_relative_accuracy(l, r, regime):
     print("%s: worst relative sigma error %.2e" % (regime, worst))
     assert worst < SIG_RTOL, (regime, worst)
     assert same, regime
+
+
+def test_bulk_export_is_the_per_site_export():
+    """mps_export_sites (one gather launch + one D2H) returns, bit for bit, what mps_export_site
+    returns site by site, after an update with ragged bonds: whole chain, a sub-range, a device
+    destination, the size query and the too-small-buffer error (byte work: bit-exact)."""
+    import torch
+    pk = _pk()
+    shapes = [(3, 5, 7), (16, 16, 16), (33, 20, 9), (1, 2, 1), (64, 64, 64)]
+    tensors, gates = [], []
+    for x, (l, mid, r) in enumerate(shapes):
+        L, R, U = _pair(l, mid, r, 40 + x)
+        tensors += [L, R]
+        gates.append(U)
+    N = len(tensors)
+    gpu = pk.MPS(N, strategy="fixed", f_fixed=0.999, slab_bytes=256 << 20)
+    gpu.mps_import_sites(0, tensors)
+    gpu.mps_apply_layer(np.arange(0, N, 2, dtype=np.int32), np.stack(gates))
+    single = [gpu.mps_export_site(i) for i in range(N)]
+    bulk = gpu.mps_export_sites(0, N)
+    assert len(bulk) == N
+    for a, b in zip(single, bulk):
+        assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    part = gpu.mps_export_sites(3, 4)
+    for a, b in zip(single[3:7], part):
+        assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    # device destination
+    tot = sum(a.size for a in single)
+    dbuf = torch.zeros(tot, dtype=torch.complex64, device="cuda:0")
+    dims = np.zeros((N, 3), np.int32)
+    ne = gpu.mps_export_sites_raw(0, N, pk.C.c_void_p(dbuf.data_ptr()), tot, dims)
+    assert ne == tot and [tuple(d) for d in dims] == [a.shape for a in single]
+    assert np.array_equal(dbuf.cpu().numpy().view(np.uint8), np.concatenate([a.ravel() for a in single]).view(np.uint8))
+    # too small a buffer: an error, nothing written past it
+    with pytest.raises(pk.EampsError):
+        gpu.mps_export_sites_raw(0, N, pk.C.c_void_p(dbuf.data_ptr()), tot - 1, dims)
