@@ -605,29 +605,67 @@ def main():
                        "d2h_bytes_per_step": int(G * (48 + 160) + 512),
                        "pipeline": "%d chunks of %s updates, H2D of chunk c+1 on a side stream overlapping chunk c's update"
                                    % (C, [g1 - g0 for g0, g1 in bounds])}
-        # the same step with the updated site tensors read back too (B_i', B_{i+1}' of every update:
-        # mps_export_sites = one device gather + one D2H into pinned host memory), VERDICT r01 weak 10
+        # the same step with the updated site tensors read back too (B_i', B_{i+1}' of every update),
+        # after chunk c's update, mps_export_sites gathers its sites into a device
+        # buffer (one launch) and their D2H into pinned host memory runs on a second side stream,
+        # under chunk c+1's update (PCIe is full duplex: it also overlaps chunk c+2's H2D)
         try:
             dims_out = np.zeros((2 * G, 3), np.int32)
             ne = mps.mps_export_sites_raw(0, 2 * G, None, 0, dims_out)
             host_out = torch.empty(ne, dtype=torch.complex64, pin_memory=True)
+            dev_out = torch.empty(ne, dtype=torch.complex64, device=dev)
+            side2 = torch.cuda.Stream(device=dev)
+
+            def e2e_full_step():
+                evs, off = [], 0
+
+                def issue(c):
+                    g0, g1 = bounds[c]
+                    ev = torch.cuda.Event()
+                    with torch.cuda.stream(side):
+                        stage[c % 2][: (g1 - g0) * per_el].copy_(host[g0 * per_el: g1 * per_el], non_blocking=True)
+                        ev.record(side)
+                    evs.append(ev)
+
+                issue(0)
+                for c in range(C):
+                    if c + 1 < C:
+                        issue(c + 1)
+                    g0, g1 = bounds[c]
+                    main.wait_event(evs[c])
+                    mps.mps_import_sites_raw(2 * g0, 2 * (g1 - g0), pk.C.c_void_p(stage[c % 2].data_ptr()),
+                                             dims[2 * g0: 2 * g1])
+                    mps.mps_apply_layer(sites[g0:g1], gates[g0:g1])
+                    # synchronous on the library's stream: the chunk's tensors are in dev_out on return
+                    n = mps.mps_export_sites_raw(2 * g0, 2 * (g1 - g0), pk.C.c_void_p(dev_out.data_ptr() + 8 * off),
+                                                 ne - off, dims_out[2 * g0: 2 * g1])
+                    with torch.cuda.stream(side2):
+                        host_out[off: off + n].copy_(dev_out[off: off + n], non_blocking=True)
+                    off += n
+                return mps.mps_truncation_array(last=G), off
+
             t_full = 0.0
             for rep in range(reps + 1):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                recs = e2e_step()
-                got = mps.mps_export_sites_raw(0, 2 * G, pk.C.c_void_p(host_out.data_ptr()), ne, dims_out)
+                recs, got = e2e_full_step()
                 torch.cuda.synchronize()
                 if rep > 0:
                     t_full += time.perf_counter() - t0
-            assert len(recs) == G and got == ne and bool(torch.isfinite(torch.view_as_real(host_out[:4096])).all())
+            assert len(recs) == G and got == ne
+            # the read-back is the device state, bit for bit (checked outside the timed region)
+            chk = np.zeros((2, 3), np.int32)
+            ref = torch.empty(int(dims_out[:2].prod(axis=1).sum()), dtype=torch.complex64, device=dev)
+            mps.mps_export_sites_raw(0, 2, pk.C.c_void_p(ref.data_ptr()), ref.numel(), chk)
+            assert torch.equal(torch.view_as_real(ref.cpu()), torch.view_as_real(host_out[: ref.numel()]))
             if world > 1:
                 t_full = max_over_ranks(t_full, dev)
             line["e2e"]["with_state_readback"] = {
                 "value": world * G / (t_full / reps), "unit": UNIT,
                 "d2h_bytes_per_step": int(G * (48 + 160) + 512 + 8 * ne),
-                "what": "records + every updated site tensor (mps_export_sites into pinned host memory)"}
-            del host_out
+                "what": "records + every updated site tensor (mps_export_sites per chunk, D2H into pinned host "
+                        "memory on a second side stream under the next chunk's update)"}
+            del host_out, dev_out
         except Exception as e:   # the extra leg never blocks the line
             line["e2e"]["with_state_readback"] = {"error": str(e)[:300]}
         del stage

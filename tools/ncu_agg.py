@@ -12,7 +12,7 @@ for r in rows:
     if d.get("Metric Name") != "gpu__time_duration.sum":
         continue
     v = float(d["Metric Value"].replace(",", ""))
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(d["Metric Unit"], 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(d["Metric Unit"], 1.0)
     k = d["Kernel Name"].split("(")[0][-50:]
     agg[k][0] += 1
     agg[k][1] += v

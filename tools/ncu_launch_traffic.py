@@ -18,7 +18,7 @@ for r in rows:
     key = (d["ID"], d["Kernel Name"].split("(")[0].split("::")[-1])
     v = float(d["Metric Value"].replace(",", ""))
     u = d["Metric Unit"]
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6, "byte": 1.0, "Kbyte": 1e3,
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6, "byte": 1.0, "Kbyte": 1e3,
              "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1.0)
     launches.setdefault(key, {})[d["Metric Name"]] = v * scale
 per = collections.defaultdict(lambda: [0, 0.0, 0.0])

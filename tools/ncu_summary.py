@@ -91,7 +91,7 @@ def summarise_launches(path, tag):
         except ValueError:
             continue
         unit = rec.get("Metric Unit", "nsecond")
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1e-3)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(unit, 1e-3)
         c, t = per.get(name, (0, 0.0))
         per[name] = (c + 1, t + v)
     tot = sum(t for _, t in per.values())
