@@ -274,7 +274,7 @@ def run_reference(args, rank, world):
     import workloads  # noqa: F401
     per_step = max(2.0, 150.0 / (args.steps + args.warmup))
     cb = cpu_sample(args.chi, per_step)
-    G = int(round(cb["value"] * per_step)) or 1
+    G = min(int(round(cb["value"] * per_step)) or 1, args.count)   # never more than the workload's layer
     import oracle
     times = []
     for step in range(args.warmup + args.steps):

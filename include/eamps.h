@@ -186,6 +186,11 @@ mps_status mps_truncation_log(mps_t, mps_record* rows, int64_t cap, int64_t* len
  * layer's final wave (a layer larger than the slab's workspace runs in waves); MPS_E_STATE for
  * earlier waves, whose workspace was reused. */
 mps_status mps_last_spectrum(mps_t, int32_t g, double* out, int32_t cap, int32_t* len);
+/* Parity switch for layers that run in several waves: with on != 0 every wave copies its gates'
+ * sorted sigma^2 (the SVD step's output) to host memory before its workspace is
+ * reused, and mps_last_spectrum then serves every gate of the last layer (one small D2H copy per
+ * gate and wave: tests only, off by default). MPS_E_STATE inside a split layer. */
+mps_status mps_keep_spectra(mps_t, int32_t on);
 /* Site tensors for tests / checkpoints. dims3 = {chi_l, d, chi_r}. B: c64 row-major. The
  * pointer kind (host or device) is detected with cudaPointerGetAttributes. lam (float32, may be
  * NULL) = Schmidt vector of the bond right of `site`. Import resets the lambda of a bond whose

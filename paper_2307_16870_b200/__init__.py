@@ -25,7 +25,7 @@ ABI_FUNCTIONS = [
     "mps_create", "mps_destroy", "mps_apply_gate1", "mps_apply_gate2", "mps_apply_layer",
     "mps_fidelity_estimate", "mps_amplitude", "mps_to_statevector", "mps_bond_dims",
     "mps_schmidt_values", "mps_truncation_log", "mps_last_spectrum", "mps_export_site",
-    "mps_import_site", "mps_import_sites", "mps_export_sites", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
+    "mps_import_site", "mps_import_sites", "mps_export_sites", "mps_keep_spectra", "mps_set_lambda", "mps_snapshot_save", "mps_snapshot_load",
     "mps_launch_count", "mps_last_sweeps", "mps_set_profiling", "mps_set_svd_route", "mps_phase_times", "mps_sync", "mps_last_error", "mps_status_string",
     "mps_layer_begin", "mps_layer_step", "mps_ledger_get", "mps_ledger_set", "mps_plan_regime",
     "mps_overlap", "mps_trace", "mps_expectation2", "mps_apply_layer1", "mps_canonicalize",
@@ -80,6 +80,7 @@ def lib():
             "mps_import_site": [_P, i32, _P, _P],
             "mps_import_sites": [_P, i32, i32, _P, _P],
             "mps_export_sites": [_P, i32, i32, _P, C.c_size_t, _P, _P],
+            "mps_keep_spectra": [_P, i32],
             "mps_set_lambda": [_P, i32, _P, i32],
             "mps_snapshot_save": [_P, _P, C.c_size_t, _P],
             "mps_snapshot_load": [_P, _P, C.c_size_t],
@@ -288,6 +289,10 @@ class MPS:
         out = np.zeros(ln.value)
         self._check(lib().mps_last_spectrum(self._h, int(g), _ptr(out), ln.value, C.byref(ln)))
         return out
+
+    def mps_keep_spectra(self, on: bool = True):
+        """Keep every wave's spectra readable through mps_last_spectrum (tests of multi-wave layers)."""
+        self._check(lib().mps_keep_spectra(self._h, int(bool(on))))
 
     def mps_last_sweeps(self, g: int) -> int:
         s = C.c_int32(0)

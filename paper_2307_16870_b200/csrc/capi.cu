@@ -87,7 +87,9 @@ struct mps_handle {
   std::vector<mps_record> records;
   std::vector<GateDesc> last_desc;         // every wave of the last layer (k, sweeps)
   LayerJob job;
-  int last_wave_begin = 0;                 // spectra are readable for the final wave only
+  int last_wave_begin = 0;                 // spectra are readable for the final wave only ...
+  bool keep_spectra = false;               // ... unless mps_keep_spectra: a host copy per gate, every wave
+  std::vector<std::vector<double>> spectra;   // parallel to last_desc (sigma^2, sorted), when kept
   bool poisoned = false;
   int sticky = 0;
   std::string err;
@@ -878,6 +880,17 @@ mps_status wave_back(mps_t h) {
     std::memcpy(&rec, &rr[x], sizeof(rec));
     h->records.push_back(rec);
   }
+  if (h->keep_spectra && de == MPS_OK) {
+    // parity export of multi-wave layers: this wave's workspace is reused by the next front
+    h->spectra.resize(h->last_desc.size());
+    for (int x = 0; x < Gw; ++x) {
+      h->spectra.emplace_back((size_t)std::max(hd[x].n, 0));
+      if (hd[x].n > 0)
+        CK(cudaMemcpyAsync(h->spectra.back().data(), h->slab + hd[x].ws_sig2, 8 * (size_t)hd[x].n,
+                           cudaMemcpyDeviceToHost, h->s));
+    }
+    CK(cudaStreamSynchronize(h->s));
+  }
   h->last_wave_begin = (int)h->last_desc.size();
   h->last_desc.insert(h->last_desc.end(), hd.begin(), hd.end());
   if (h->hp.on && h->hp.layers > 3) h->hp.post += HostProf::now() - hw1;
@@ -1037,6 +1050,14 @@ mps_status mps_set_profiling(mps_t h, int32_t on) {
     for (int e = 0; e < 6; ++e) CK(cudaEventCreate(&h->ev[e]));
   h->profiling = on != 0;
   for (int p = 0; p < kPhases; ++p) { h->phase_ms[p] = 0; h->phase_n[p] = 0; }
+  return MPS_OK;
+}
+
+mps_status mps_keep_spectra(mps_t h, int32_t on) {
+  if (!h) return MPS_E_INVAL;
+  if (h->job.active) return set_err(h, MPS_E_STATE, "mps_keep_spectra inside a layer");
+  h->keep_spectra = on != 0;
+  h->spectra.clear();
   return MPS_OK;
 }
 
@@ -1238,6 +1259,7 @@ mps_status mps_layer_begin(mps_t h, int32_t G, const int32_t* sites, const float
   J.front = false;
   J.active = true;
   h->last_desc.clear();
+  h->spectra.clear();
   h->last_wave_begin = 0;
   if (h->hp.on && h->hp.layers > 3) h->hp.plan += HostProf::now() - hp0;
   mps_status fs = wave_front(h);
@@ -1399,8 +1421,14 @@ mps_status mps_truncation_log(mps_t h, mps_record* rows, int64_t cap, int64_t* l
 mps_status mps_last_spectrum(mps_t h, int32_t g, double* out, int32_t cap, int32_t* len) {
   if (!h || !len) return MPS_E_INVAL;
   if (g < 0 || g >= (int)h->last_desc.size()) return set_err(h, MPS_E_RANGE, "gate index out of range");
-  if (g < h->last_wave_begin) return set_err(h, MPS_E_STATE, "spectrum of an earlier wave (workspace reused)");
   const GateDesc& gd = h->last_desc[g];
+  if (g < (int)h->spectra.size() && (int)h->spectra[g].size() == gd.n && h->keep_spectra) {   // kept host copy
+    *len = gd.n;
+    if (out)
+      for (int j = 0; j < std::min(cap, gd.n); ++j) out[j] = std::sqrt(std::max(h->spectra[g][j], 0.0));
+    return MPS_OK;
+  }
+  if (g < h->last_wave_begin) return set_err(h, MPS_E_STATE, "spectrum of an earlier wave (workspace reused)");
   *len = gd.n;
   if (out && cap > 0) {
     CK(cudaMemcpyAsync(out, h->slab + gd.ws_sig2, 8 * (size_t)std::min(cap, gd.n), cudaMemcpyDeviceToHost, h->s));

@@ -145,7 +145,8 @@ def test_nonconvergence_is_reported_and_sticky():
 
 def test_multiwave_layer_matches_oracle():
     """a slab too small for one wave: the layer runs in several waves (workspace reused between
-    them); every kept rank and fidelity matches the oracle, and the last wave's spectra too."""
+    them); every kept rank and fidelity matches the oracle, the last wave's spectra too, and with
+    mps_keep_spectra the spectra of every wave."""
     pk = _pk()
     chi, G = 64, 12
     tensors, gates = workloads.micro_chain(chi, G)
@@ -172,6 +173,15 @@ def test_multiwave_layer_matches_oracle():
             assert spectra_close(gpu.mps_last_spectrum(g), orc.last_spectrum(g)) < SIG_RTOL
         if 0 < len(readable) < G:
             multi = True
+            # the same multi-wave layer with mps_keep_spectra: every wave's spectra, all at the bar
+            gpu2 = pk.MPS(2 * G, strategy="fixed", f_fixed=0.9999, slab_bytes=mb << 20)
+            gpu2.mps_keep_spectra(True)
+            gpu2.mps_import_sites(0, tensors)
+            gpu2.mps_apply_layer(sites, gates)
+            for g in range(G):
+                assert spectra_close(gpu2.mps_last_spectrum(g), orc.last_spectrum(g)) < SIG_RTOL, g
+            for g in readable:   # and the kept copy is the workspace's
+                assert np.array_equal(gpu2.mps_last_spectrum(g), gpu.mps_last_spectrum(g))
             break
     assert multi, "no slab size produced a multi-wave layer"
 
